@@ -1,0 +1,264 @@
+/*
+ * tvegpu.h — C ABI of the B200-native TLED thermo-visco-elastodynamic step.
+ *
+ * This is the drop-in boundary for the reference's `tve::Engine`
+ * (/root/reference/proj/include/tve/engine.hpp:83-143).  The reference is a C++20
+ * API (headers only, no bodies); this header is what a C++ host (or any FFI)
+ * binds instead.  Plain pointers and sizes only: no exceptions, no Eigen, no STL,
+ * no torch types cross it.  A header-only C++ facade with the reference's
+ * class shape lives in include/tve_gpu.hpp.
+ *
+ * Conventions
+ *   - All indices are 0-based ORIGINAL ids (the caller's numbering).  Internal
+ *     Morton/first-touch permutations and partitions never leak out.
+ *   - Every input buffer is caller-owned and copied inside tvegpu_create
+ *     (the reference keeps references to mesh/pre/material, engine.hpp:122-124;
+ *     copying is strictly safer and observably equivalent).
+ *   - Errors map to the reference exception taxonomy (errors.hpp:8-33) by
+ *     status code; tvegpu_last_error() returns the message and, for
+ *     InstabilityError, the (step, node) payload (errors.hpp:21-27).
+ *   - One handle is not thread-safe; distinct handles are independent.
+ *   - tvegpu_step() is synchronous: it returns after the device finite check.
+ */
+#ifndef TVEGPU_H
+#define TVEGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TVEGPU_ABI_VERSION 1
+
+/* errors.hpp:8-33 — ParseError, ValidationError, InstabilityError, IoError,
+ * plus device-side failures the reference (CPU-only) never had. */
+typedef enum tvegpu_status {
+    TVEGPU_OK = 0,
+    TVEGPU_E_PARSE = 1,        /* tve::ParseError        (errors.hpp:9)  */
+    TVEGPU_E_VALIDATION = 2,   /* tve::ValidationError   (errors.hpp:15) */
+    TVEGPU_E_INSTABILITY = 3,  /* tve::InstabilityError  (errors.hpp:21) */
+    TVEGPU_E_IO = 4,           /* tve::IoError           (errors.hpp:30) */
+    TVEGPU_E_CUDA = 5,         /* CUDA runtime failure / no device       */
+    TVEGPU_E_NCCL = 6,         /* NCCL failure (multi-GPU halo)           */
+    TVEGPU_E_ARG = 7           /* NULL handle / bad size / bad option     */
+} tvegpu_status;
+
+/* mesh.hpp:15 ElementKind */
+enum { TVEGPU_T4 = 0, TVEGPU_H8 = 1 };
+/* engine.hpp:16 CouplingMode */
+enum { TVEGPU_COUPLED = 0, TVEGPU_THERMAL_ONLY = 1, TVEGPU_MECHANICAL_ONLY = 2 };
+/* materials.hpp:77 ExpansionKind */
+enum { TVEGPU_EXP_ISOTROPIC = 0, TVEGPU_EXP_TRANSVERSELY_ISOTROPIC = 1, TVEGPU_EXP_ORTHOTROPIC = 2 };
+
+/* mechanics.hpp:25-35 PrescribedDisplacement */
+typedef struct tvegpu_prescribed {
+    int32_t num_nodes;
+    const int32_t* nodes;
+    int32_t component;   /* 0,1,2 */
+    double target;       /* [m] */
+    double ramp_time;    /* [s]; <= 0 means step load (value_at, mechanics.hpp:31-34) */
+} tvegpu_prescribed;
+
+/* bioheat.hpp:19-26 SourceRegion */
+typedef struct tvegpu_source {
+    int32_t num_elements;
+    const int32_t* elements;
+    double q_r;          /* [W/m^3] */
+    double t_start;      /* [s] */
+    double t_end;        /* [s]; +inf allowed */
+} tvegpu_source;
+
+/*
+ * Flat mirror of everything tve::Engine's constructor receives
+ * (engine.hpp:85-87): Mesh (mesh.hpp:22-37), the precompute inputs
+ * (density, ref_specific_heat; mesh.hpp:83), MaterialModel
+ * (materials.hpp:89-97), MechBCs (mechanics.hpp:37-47, without the host
+ * std::function motion_override), ThermalBCs (bioheat.hpp:32-35),
+ * HeatSourceSet (bioheat.hpp:28-30) and SimulationConfig (engine.hpp:28-39,
+ * without the OutputSpec, which is run-level).
+ */
+typedef struct tvegpu_problem {
+    /* ---- Mesh (mesh.hpp:22-37) ---- */
+    int32_t kind;                   /* TVEGPU_T4 | TVEGPU_H8 */
+    int32_t num_nodes;
+    int32_t num_elements;
+    const double* nodes;            /* 3*num_nodes, xyz interleaved [m] */
+    const int32_t* elements;        /* nn*num_elements, element-major, 0-based */
+    const double* fiber_dirs;       /* 3*num_elements or NULL (mesh.hpp:28) */
+    const double* expansion_axes;   /* 6*num_elements (m then n) or NULL (mesh.hpp:29) */
+
+    /* ---- precompute(mesh, density, ref_specific_heat) (mesh.hpp:83) ---- */
+    double ref_specific_heat;       /* [J/(kg degC)] */
+
+    /* ---- HyperelasticParams (materials.hpp:15-19) ---- */
+    double mu, kappa, eta_a;
+    /* ---- PronySeries::from_terms (materials.hpp:27-36) ---- */
+    int32_t prony_count;
+    const double* prony_phi;        /* prony_count */
+    const double* prony_tau;        /* prony_count */
+    /* ---- ThermalProps (materials.hpp:67-75) ---- */
+    double density;
+    int32_t c_table_len;            /* ScalarTable specific_heat (materials.hpp:39-49) */
+    const double* c_table_T;
+    const double* c_table_value;
+    int32_t k_table_len;            /* ConductivityTable (materials.hpp:53-65) */
+    const double* k_table_T;
+    const double* k_table_tensor;   /* 9 per entry, row-major (symmetric) */
+    double perfusion_rate;          /* w_b */
+    double blood_specific_heat;     /* c_b */
+    double arterial_temperature;    /* T_a */
+    double metabolic_rate;          /* Q_m */
+    /* ---- optional<ExpansionSpec> (materials.hpp:80-86, 93) ---- */
+    int32_t has_expansion;
+    int32_t expansion_kind;
+    double alpha_i, alpha_m, alpha_n, reference_temperature;
+    /* ---- optional<Vector3d> fiber, axis_m, axis_n (materials.hpp:94-96) ---- */
+    int32_t has_fiber;
+    double fiber[3];
+    double axis_m[3];
+    double axis_n[3];
+
+    /* ---- MechBCs (mechanics.hpp:37-47) ---- */
+    int32_t num_fixed_nodes;
+    const int32_t* fixed_nodes;
+    int32_t num_prescribed;
+    const tvegpu_prescribed* prescribed;
+    const double* external_force;   /* 3*num_nodes or NULL */
+    double body_force[3];           /* [N/m^3] */
+
+    /* ---- ThermalBCs (bioheat.hpp:32-35) ---- */
+    int32_t num_fixed_temperatures;
+    const int32_t* fixed_temperature_nodes;
+    const double* fixed_temperature_values;
+    double initial_temperature;
+
+    /* ---- HeatSourceSet (bioheat.hpp:28-30) ---- */
+    int32_t num_sources;
+    const tvegpu_source* sources;
+
+    /* ---- SimulationConfig (engine.hpp:28-39) ---- */
+    double dt;
+    double duration;
+    int32_t mode;                   /* TVEGPU_COUPLED | _THERMAL_ONLY | _MECHANICAL_ONLY */
+    int32_t expansion_enabled;
+    int32_t temperature_dependent;
+    double damping_gamma;
+    double hourglass_stiffness;
+    int32_t allow_unstable_dt;
+    int32_t workers;                /* ignored on the GPU; kept for layout parity */
+} tvegpu_problem;
+
+/* Device / decomposition options (no reference counterpart). */
+typedef struct tvegpu_options {
+    int32_t device;                 /* CUDA ordinal; -1 = current */
+    int32_t nranks;                 /* 1 = single GPU; >1 = this handle is one RCB partition */
+    int32_t rank;
+    const void* nccl_unique_id;     /* 128 bytes from tvegpu_nccl_unique_id() when nranks > 1 */
+    int32_t reorder;                /* 1 (default) = Morton elements + first-touch nodes; 0 = identity */
+    int32_t diagnostics;            /* 1 = keep F, S_tilde, assembled forces (engine.hpp:101-105) */
+    int32_t steps_per_graph;        /* CUDA-graph chunk length; 0 = default (64) */
+} tvegpu_options;
+
+typedef struct tvegpu_engine tvegpu_engine;
+
+/* Fill *opt with defaults (single GPU, reorder on, no diagnostics). */
+void tvegpu_default_options(tvegpu_options* opt);
+
+/* Engine(mesh, pre, material, mech_bcs, thermal_bcs, sources, config)
+ * (engine.hpp:85-87) fused with precompute() (mesh.hpp:83): validates inputs
+ * (ValidationError as the reference: degenerate elements mesh.hpp:81-82,
+ * Prony weights materials.hpp:33-35, axes materials.hpp:112, dt above critical
+ * engine.hpp:36), builds the device layout and uploads it. */
+tvegpu_status tvegpu_create(const tvegpu_problem* problem, const tvegpu_options* options,
+                            tvegpu_engine** out);
+void tvegpu_destroy(tvegpu_engine* h);
+
+/* nsteps x Engine::step() (engine.hpp:89-90).  Returns TVEGPU_E_INSTABILITY
+ * at the first step that produced a non-finite T or u; the state is then the
+ * state the reference leaves behind when step() throws (that step applied,
+ * time and step counter not advanced). */
+tvegpu_status tvegpu_step(tvegpu_engine* h, int64_t nsteps);
+
+/* Readback of SimulationState (engine.hpp:41-45, 95-97) in original numbering. */
+tvegpu_status tvegpu_get_temperatures(tvegpu_engine* h, double* T /* num_nodes */);
+tvegpu_status tvegpu_get_displacements(tvegpu_engine* h, double* disp /* 3N */,
+                                       double* disp_prev /* 3N or NULL */);
+/* Viscous history, MechState::viscous (mechanics.hpp:20): (e*P + p)*9, row-major. */
+tvegpu_status tvegpu_get_viscous(tvegpu_engine* h, double* viscous);
+double  tvegpu_time(const tvegpu_engine* h);
+int64_t tvegpu_step_count(const tvegpu_engine* h);
+
+/* Write access to state() between steps (engine.hpp:95): any pointer may be
+ * NULL to leave that field unchanged. */
+tvegpu_status tvegpu_set_state(tvegpu_engine* h, const double* T, const double* disp,
+                               const double* disp_prev, const double* viscous,
+                               double time, int64_t step);
+
+/* Override the lumped nodal source vector (bioheat.hpp:57 nodal_source_power,
+ * engine.hpp:138) with caller-supplied powers [W] per node (original ids);
+ * NULL restores the regional HeatSourceSet schedule. */
+tvegpu_status tvegpu_set_nodal_sources(tvegpu_engine* h, const double* power);
+
+/* Diagnostics of the last mechanics phase (engine.hpp:101-105); requires
+ * options.diagnostics = 1.  f_int: assembled internal force 3N; F, S: 9 per
+ * element (row-major) deformation gradients and S_tilde.  Any may be NULL. */
+tvegpu_status tvegpu_get_diagnostics(tvegpu_engine* h, double* f_int, double* F, double* S);
+
+/* Message of the last failure; for TVEGPU_E_INSTABILITY also the step index and
+ * the lowest original node id holding a non-finite value (errors.hpp:21-27). */
+tvegpu_status tvegpu_last_error(const tvegpu_engine* h, char* msg, size_t cap,
+                                int64_t* step, int32_t* node);
+const char* tvegpu_status_string(tvegpu_status s);
+
+/* Host-only helpers (no device needed). */
+/* critical_timestep(mesh, material) (mesh.hpp:92-97). */
+tvegpu_status tvegpu_critical_timestep(const tvegpu_problem* problem, double* thermal,
+                                       double* mechanical);
+/* Library-owned error text for failures before a handle exists. */
+const char* tvegpu_create_error(void);
+int32_t tvegpu_abi_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Decomposition plan (host-only; exposes the integer maps for bit-exact tests).
+ * For nranks == 1 this is the single-GPU layout: Morton element order,
+ * first-touch node order and the node -> slot CSR in canonical
+ * (ascending original element id, then local index) order (mesh.hpp:58-61).
+ * For nranks > 1, elements are split by recursive coordinate bisection and
+ * each rank's CSR addresses local slots [0, nn*E_local) followed by the
+ * receive area of its halo exchange.
+ * ------------------------------------------------------------------------- */
+typedef struct tvegpu_plan tvegpu_plan;
+
+typedef struct tvegpu_plan_view {
+    int32_t nranks, rank, nn;
+    int32_t num_elements;           /* local (owned) elements */
+    int32_t num_boundary_elements;  /* the first ones in local order touch a shared node */
+    int32_t num_nodes;              /* local nodes (owned + replicated) */
+    const int32_t* element_orig;    /* num_elements: local -> original element id */
+    const int32_t* node_orig;       /* num_nodes: local -> original node id */
+    const int32_t* conn;            /* nn*num_elements, element-major, local node ids */
+    const int32_t* csr_offsets;     /* num_nodes + 1 */
+    const int32_t* csr_slots;       /* slot ids: e*nn + a (local) or nn*E + k (receive slot k) */
+    int32_t num_neighbors;
+    const int32_t* neighbor_ranks;  /* ascending */
+    const int32_t* send_offsets;    /* num_neighbors + 1, into send_slots */
+    const int32_t* send_slots;      /* local slot ids sent to each neighbour, canonical order */
+    const int32_t* recv_offsets;    /* num_neighbors + 1; receive slot k of neighbour j at recv_offsets[j] + k */
+    const int32_t* element_owner;   /* GLOBAL: num_elements_global owner ranks (original ids) */
+    int32_t num_elements_global;
+} tvegpu_plan_view;
+
+tvegpu_status tvegpu_plan_create(const tvegpu_problem* problem, int32_t nranks, int32_t rank,
+                                 int32_t reorder, tvegpu_plan** out);
+tvegpu_status tvegpu_plan_get(const tvegpu_plan* plan, tvegpu_plan_view* view);
+void tvegpu_plan_destroy(tvegpu_plan* plan);
+
+/* ncclGetUniqueId for the multi-GPU halo communicator (128 bytes). */
+tvegpu_status tvegpu_nccl_unique_id(void* out128);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TVEGPU_H */
