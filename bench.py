@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark of the coupled TLED time step (BASELINE.json metric: element-steps/s,
+achieved HBM GB/s, ms per explicit step).
+
+Workload at N=1: cfg4 (BASELINE configs[3]) — H8 block 100^3 = 1,000,000 elements,
+1,030,301 nodes, coupled TherMechExpanTD (temperature-dependent c/k, isotropic
+thermal expansion), hourglass control, one Prony term, central RFA source.  It is
+the configuration the north_star's >= 60 % HBM-roofline target is stated on.
+At N>1 (torchrun, one rank per GPU): weak scaling, a 100a x 100b x 100c block with
+a*b*c = N, split by RCB into one 1M-element partition per GPU with the NCCL halo.
+
+--impl reference: the reference's algorithm on the host CPU (the fp64 oracle,
+OpenMP over all host threads) on the same workload — the reference ships no
+runnable code, so the oracle restatement is its CPU implementation.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2009_10400_b200 import configs  # noqa: E402
+from paper_2009_10400_b200.problem import H8  # noqa: E402
+
+METRIC = "element-steps/s"
+
+
+def weak_block(nranks, steps):
+    """cfg4 physics on a (100a, 100b, 100c) block, a*b*c = nranks, h = 1 mm."""
+    f = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}.get(nranks)
+    if f is None:
+        a = nranks
+        f = (a, 1, 1)
+    from paper_2009_10400_b200 import meshgen
+    from paper_2009_10400_b200.problem import Prescribed, SourceRegion
+    nx, ny, nz = 100 * f[0], 100 * f[1], 100 * f[2]
+    if f == (1, 1, 1):
+        return configs.cfg4(steps=steps), "cfg4: H8 100^3 (1,000,000 el) TherMechExpanTD, hourglass, Prony P=1"
+    nodes, el = meshgen.structured_h8(100, 0.1, nx=nx, ny=ny, nz=nz)
+    p = configs._base(H8, nodes, el, 1e-4, steps)
+    top = nodes[:, 2].max()
+    p.fixed_nodes = np.nonzero(nodes[:, 2] <= 1e-12)[0].astype(np.int32)
+    p.prescribed = [Prescribed(np.nonzero(np.abs(nodes[:, 2] - top) <= 1e-9)[0].astype(np.int32), 2, 1e-2,
+                               1e-4 * steps)]
+    c = 0.5 * np.array([nx, ny, nz]) * 1e-3
+    p.sources = [SourceRegion(meshgen.elements_in_sphere(nodes, el, c, 0.01), configs.Q_R_TABLE5)]
+    return p, f"cfg4 physics, H8 {nx}x{ny}x{nz} ({nx*ny*nz:,} el), RCB into {nranks} x 1M partitions"
+
+
+def canonical_bytes(p):
+    """SURVEY.md §8(d) algorithmic bytes per launch of each kernel (fp64 values, int32 indices)."""
+    E, N, nn, P = p.num_elements, p.num_nodes, p.nn, p.prony_count
+    fib = 24 if p.fiber_dirs is not None else 0
+    axes = 48 if p.expansion_axes is not None else 0
+    hasR = p.external_force is not None or any(b != 0 for b in p.body_force)
+    return {
+        "thermal_element": E * (12 * nn + 80) + N * 32,
+        "thermal_node": E * 12 * nn + N * 37,
+        "mech_element": E * (28 * nn + 80 + 96 * P + fib + axes) + N * (32 + (24 if p.kind == H8 else 0)),
+        "mech_node": E * 28 * nn + N * (85 + (24 if hasR else 0)),
+    }
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload_key, kernel):
+    """dram bytes per launch from a committed `ncu --set full` capture (profiles/ncu_dram_bytes.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_dram_bytes.json")) as f:
+            return json.load(f).get(workload_key, {}).get(kernel)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 100 ms while the bench runs."""
+
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id):
+        self.rows = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(gpu_id)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sel = [r for t, r in self.rows if t0 - 0.15 <= t <= t1 + 0.15] or [r for _, r in self.rows[-5:]]
+        sm, smax, reasons = [], [], set()
+        for r in sel:
+            parts = [x.strip() for x in r.split(",")]
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+                for n, v in zip(names, parts[4:8]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+            except Exception:
+                continue
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_oracle_rate(problem, budget_s, max_steps, warmup=1):
+    """Element-steps/s of the fp64 oracle (OpenMP, all host threads) on the same problem."""
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    o = O.OracleEngine(problem, workers=threads)
+    o.step(warmup)
+    t0 = time.perf_counter()
+    n = 0
+    while n < max_steps:
+        o.step(1)
+        n += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return problem.num_elements * n / dt, n, dt, threads
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    p, workload = weak_block(world, args.steps)
+    rate, n, dt, threads = cpu_oracle_rate(p, budget_s=args.ref_budget, max_steps=args.steps,
+                                           warmup=min(args.warmup, 1))
+    sample = (f"{n} of {args.steps} requested steps of the full {p.num_elements:,}-element workload "
+              f"({dt:.1f} s, fp64 oracle, OpenMP {threads} threads on {cpu_model()})")
+    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": METRIC, "n_gpus": world,
+            "steps": n, "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * dt / n, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload, "elements": p.num_elements, "nodes": p.num_nodes},
+            "cpu_baseline": {"value": rate, "unit": METRIC, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": rate, "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import paper_2009_10400_b200 as tg
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    p, workload = weak_block(world, args.steps + args.warmup + 64)
+    nccl_id = None
+    if world > 1:
+        obj = [tg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    eng = tg.Engine(p, device=local, nranks=world, rank=rank, nccl_id=nccl_id, steps_per_graph=args.graph_steps)
+    stream = torch.cuda.ExternalStream(eng.stream, device=local)
+    props = torch.cuda.get_device_properties(local)
+    sampler = ClockSampler(getattr(props, "uuid", None) and f"GPU-{props.uuid}" or local)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up: W steps, then keep the GPU busy ~0.5 s so clocks settle (untimed)
+    eng.step(args.warmup)
+    t_soak = time.time()
+    while time.time() - t_soak < args.soak:
+        eng.step(args.graph_steps)
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    wall0 = time.time()
+    ev0.record(stream)
+    eng.enqueue(args.steps)
+    ev1.record(stream)
+    ev1.synchronize()
+    wall1 = time.time()
+    eng.sync()  # finite check of the timed steps (raises on instability)
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    clocks = sampler.summary(wall0, wall1)
+    sampler.stop()
+    E_total = p.num_elements  # weak scaling: the global mesh holds all ranks' elements
+    value = E_total * args.steps / (ms / 1e3)
+    ms_step = ms / args.steps
+
+    # per-kernel durations (CUDA events on the engine stream, direct launches)
+    prof = eng.profile_kernels(min(args.steps, 50))
+    local_bytes = canonical_bytes(p)
+    kname = {"thermal_element": "k_thermal_element", "thermal_node": "k_thermal_node",
+             "mech_element": "k_mech_element", "mech_node": "k_mech_node"}
+    per_kernel = {}
+    for k, b in local_bytes.items():
+        for n, t in prof.items():
+            if n.startswith(kname[k]):
+                per_kernel[k] = (b / world, t)
+    dom = max(per_kernel, key=lambda k: per_kernel[k][1])
+    b_dom, t_dom = per_kernel[dom]
+    peak, peak_src = load_peaks()
+    ach = b_dom / (t_dom / 1e3) / 1e9
+    step_bytes = sum(local_bytes.values())
+    step_gbs = step_bytes * args.steps / (ms / 1e3) / 1e9
+    wkey = f"cfg4_n{world}" if world > 1 else "cfg4"
+    roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": ncu_traffic(wkey, dom), "kernel": dom, "kernel_ms": t_dom,
+                "algorithmic_bytes_per_launch": b_dom, "peak_source": peak_src}
+
+    # end to end through the public API with host buffers: per step upload this step's
+    # nodal source powers (pinned H2D, bioheat.hpp:57), step (finite check D2H), read T and u (D2H)
+    e2e_steps = max(3, min(args.steps, args.e2e_steps))
+    power = np.zeros(p.num_nodes)
+    Th = np.empty(p.num_nodes)
+    uh = np.empty(3 * p.num_nodes)
+    barrier()
+    t0 = time.perf_counter()
+    for k in range(e2e_steps):
+        power[:] = 0.0
+        eng.set_nodal_sources(power)
+        eng.step(1)
+        eng.make_snapshot(Th, uh)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": E_total * e2e_steps / e2e_s, "unit": METRIC, "ms_per_step": 1e3 * e2e_s / e2e_steps,
+           "h2d_bytes_per_step": 8 * p.num_nodes, "d2h_bytes_per_step": 32 * p.num_nodes + 40,
+           "steps": e2e_steps,
+           "calls": "tvegpu_set_nodal_sources + tvegpu_step(1) + tvegpu_make_snapshot (C ABI, host buffers)"}
+
+    line = {"metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload, "elements": p.num_elements, "nodes": p.num_nodes,
+                       "parallelism": f"rcb{world}" if world > 1 else "single",
+                       "l2": "working set > 1 GB per GPU vs 126 MB L2: no flush needed",
+                       "graph_steps": args.graph_steps},
+            "achieved_hbm_gbs_step": step_gbs, "canonical_bytes_per_element_step": step_bytes / p.num_elements,
+            "step_roofline_frac": step_gbs / peak,
+            "kernel_ms": prof, "roofline": roofline, "e2e": e2e,
+            "gpu_launches": eng.kernels_per_step() * args.steps, "clocks": clocks}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, n, dt, threads = cpu_oracle_rate(p, budget_s=args.cpu_budget, max_steps=1000)
+        line["cpu_baseline"] = {"value": rate, "unit": METRIC, "cores": threads, "kind": "port",
+                                "sample": f"{n} steps of the full cfg4 mesh in {dt:.1f} s (fp64 oracle, OpenMP "
+                                          f"{threads} threads, {cpu_model()})"}
+    if rank == 0 and world == 1 and not args.no_extras:
+        # the real-time target: cfg3 liver-shaped T4 (~100k el), ms per step (L2-resident regime)
+        p3 = configs.cfg3(steps=100000)
+        e3 = tg.Engine(p3, device=local, steps_per_graph=args.graph_steps)
+        e3.step(200)
+        s3 = torch.cuda.ExternalStream(e3.stream, device=local)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n3 = 2000
+        a.record(s3)
+        e3.enqueue(n3)
+        b.record(s3)
+        b.synchronize()
+        e3.sync()
+        t3 = a.elapsed_time(b) / n3
+        line["cfg3_liver"] = {"elements": p3.num_elements, "nodes": p3.num_nodes, "ms_per_step": t3,
+                              "element_steps_per_s": p3.num_elements / (t3 / 1e3),
+                              "realtime_dt_ms": 1e3 * p3.dt, "steps": n3}
+        e3.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--graph-steps", type=int, default=64)
+    ap.add_argument("--soak", type=float, default=0.5)
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-budget", type=float, default=90.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    return run_reference(args) if args.impl == "reference" else run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

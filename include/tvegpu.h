@@ -185,6 +185,9 @@ tvegpu_status tvegpu_step(tvegpu_engine* h, int64_t nsteps);
 tvegpu_status tvegpu_get_temperatures(tvegpu_engine* h, double* T /* num_nodes */);
 tvegpu_status tvegpu_get_displacements(tvegpu_engine* h, double* disp /* 3N */,
                                        double* disp_prev /* 3N or NULL */);
+/* Engine::make_snapshot() (engine.hpp:47-55, 99): T and u of the current state in
+ * one device read (either pointer may be NULL). */
+tvegpu_status tvegpu_make_snapshot(tvegpu_engine* h, double* T /* N */, double* disp /* 3N */);
 /* Viscous history, MechState::viscous (mechanics.hpp:20): (e*P + p)*9, row-major. */
 tvegpu_status tvegpu_get_viscous(tvegpu_engine* h, double* viscous);
 double  tvegpu_time(const tvegpu_engine* h);
@@ -257,6 +260,23 @@ void tvegpu_plan_destroy(tvegpu_plan* plan);
 
 /* ncclGetUniqueId for the multi-GPU halo communicator (128 bytes). */
 tvegpu_status tvegpu_nccl_unique_id(void* out128);
+
+/* ---------------------------------------------------------------------------
+ * Measurement hooks (no reference counterpart; used by bench.py).
+ * ------------------------------------------------------------------------- */
+/* cudaStream_t (as void*) every step kernel is launched on. */
+void* tvegpu_stream(tvegpu_engine* h);
+/* Kernel launches per step (K1..K5, plus halo packs when nranks > 1). */
+int32_t tvegpu_kernels_per_step(const tvegpu_engine* h);
+/* Enqueue nsteps on the stream without waiting or reading back the finite
+ * check; tvegpu_sync() waits and applies it.  tvegpu_step == enqueue + sync. */
+tvegpu_status tvegpu_enqueue_steps(tvegpu_engine* h, int64_t nsteps);
+tvegpu_status tvegpu_sync(tvegpu_engine* h);
+/* Time each kernel of the step with CUDA events over nsteps direct (un-graphed)
+ * steps; ms_per_kernel[k] = mean duration of kernel k per step (up to 8 kinds),
+ * names = ';'-separated kernel names.  Returns the number of kinds in *count. */
+tvegpu_status tvegpu_profile_kernels(tvegpu_engine* h, int32_t nsteps, double* ms_per_kernel, int32_t* count,
+                                     char* names, size_t cap);
 
 #ifdef __cplusplus
 }

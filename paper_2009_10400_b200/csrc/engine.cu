@@ -1,0 +1,1095 @@
+// engine.cu — the device engine behind the C ABI of include/tvegpu.h.
+//
+// Replaces tve::Engine (engine.hpp:83-143).  The constructor's work
+// (engine.hpp:85-87) plus precompute() (mesh.hpp:81-83) happens once in
+// tvegpu_create: validation, the compressed precompute, Morton/first-touch
+// reordering and (nranks > 1) the RCB partition run on the host (plan.cpp),
+// then everything is uploaded and stays resident in HBM.  Engine::step()
+// (engine.hpp:89-90) becomes K1..K5 on one stream, replayed as CUDA graphs of
+// `steps_per_graph` steps; time, step counter, BC ramps and the finite check
+// live on the device so a graph replay needs no host work.  The only per-call
+// host work is the regional-source refresh when the active-source mask changes
+// (engine.hpp:119, 140), predicted from the same fp64 time sequence.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <nccl.h>
+
+#include "kernels.cuh"
+#include "plan.hpp"
+
+using namespace tvegpu;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+#define CU(x)                                                                                      \
+    do {                                                                                           \
+        cudaError_t _e = (x);                                                                      \
+        if (_e != cudaSuccess)                                                                     \
+            throw Error(TVEGPU_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(_e));           \
+    } while (0)
+
+// ---------------------------------------------------------------- NCCL, loaded lazily (multi-GPU only)
+struct NcclApi {
+    void* lib = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    if (!api.lib) {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) throw Error(TVEGPU_E_NCCL, std::string("cannot load libnccl.so.2: ") + dlerror());
+        auto sym = [&](const char* n) {
+            void* p = dlsym(h, n);
+            if (!p) throw Error(TVEGPU_E_NCCL, std::string("libnccl.so.2 lacks ") + n);
+            return p;
+        };
+        api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
+        api.CommInitRank = (decltype(api.CommInitRank))sym("ncclCommInitRank");
+        api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
+        api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
+        api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
+        api.Send = (decltype(api.Send))sym("ncclSend");
+        api.Recv = (decltype(api.Recv))sym("ncclRecv");
+        api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+        api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
+        api.lib = h;
+    }
+    return api;
+}
+
+#define NC(x)                                                                                      \
+    do {                                                                                           \
+        ncclResult_t _r = (x);                                                                     \
+        if (_r != ncclSuccess) throw Error(TVEGPU_E_NCCL, std::string(#x) + ": " + nccl().GetErrorString(_r)); \
+    } while (0)
+
+template <class T>
+T* dalloc(std::vector<void*>& owned, size_t n) {
+    if (n == 0) n = 1;
+    void* p = nullptr;
+    CU(cudaMalloc(&p, n * sizeof(T)));
+    owned.push_back(p);
+    return static_cast<T*>(p);
+}
+template <class T>
+T* dupload(std::vector<void*>& owned, const std::vector<T>& v, cudaStream_t s) {
+    T* p = dalloc<T>(owned, v.size());
+    if (!v.empty()) CU(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return p;
+}
+
+struct Region {
+    double q_r, t_start, t_end;
+    std::vector<int32_t> nodes;  // nn per element, original ids
+    std::vector<double> vol;
+    bool active_at(double t) const { return t >= t_start && t < t_end; }
+};
+
+}  // namespace
+
+struct tvegpu_engine {
+    int device = 0, nn = 4, kind = 0, mode = 0, N_global = 0, E_global = 0, P = 0;
+    double dt = 0;
+    RankPlan plan;
+    DevParams prm{};
+    DevPtrs ptr{};
+    std::vector<void*> owned;
+    cudaStream_t s = nullptr, sc = nullptr;
+    cudaEvent_t ev_pack = nullptr, ev_comm = nullptr;
+    int cur = 0;
+    double host_time = 0;
+    long long host_step = 0;
+    bool halted = false;
+    // sources
+    std::vector<Region> regions;
+    std::vector<char> active;
+    bool sources_init = false, source_override = false;
+    double* qr_host = nullptr;  // pinned staging of the nodal source vector (local order)
+    // multi-GPU
+    ncclComm_t comm = nullptr;
+    double* send_th = nullptr;
+    double* send_m = nullptr;
+    const int32_t* d_send_slot = nullptr;
+    // graphs keyed by (parity, nsteps)
+    std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
+    int steps_per_graph = 64;
+    // errors
+    std::string err;
+    long long err_step = -1;
+    int err_node = -1;
+    tvegpu_status last_status = TVEGPU_OK;
+    bool pending = false;  // steps enqueued whose finite check has not been read back
+    long long pend_step = 0;
+    int pend_cur = 0;
+    unsigned long long* h_words = nullptr;  // pinned: clock (3 words) + err_inst + err_elem
+    double4* stage = nullptr;               // pinned readback staging (N records)
+};
+
+namespace {
+
+int blocks(int n, int t) { return (n + t - 1) / t; }
+
+void refresh_sources_if_needed(tvegpu_engine* h, double t) {
+    if (h->source_override) return;
+    bool changed = !h->sources_init;
+    for (size_t r = 0; r < h->regions.size(); ++r) {
+        const char a = h->regions[r].active_at(t) ? 1 : 0;
+        if (a != h->active[r]) changed = true;
+        h->active[r] = a;
+    }
+    h->sources_init = true;
+    if (!changed) return;
+    // accumulate_nodal_sources (bioheat.hpp:65-69): region order, element order, local order
+    std::vector<double> q(h->N_global, 0.0);
+    for (size_t r = 0; r < h->regions.size(); ++r) {
+        if (!h->active[r]) continue;
+        const Region& g = h->regions[r];
+        for (size_t e = 0; e < g.vol.size(); ++e)
+            for (int a = 0; a < h->nn; ++a) q[g.nodes[e * h->nn + a]] += g.q_r * g.vol[e] / h->nn;
+    }
+    for (int li = 0; li < h->plan.N; ++li) h->qr_host[li] = q[h->plan.node_orig[li]];
+    CU(cudaMemcpyAsync(const_cast<double*>(h->ptr.qr), h->qr_host, (size_t)h->plan.N * 8,
+                       cudaMemcpyHostToDevice, h->s));
+    CU(cudaStreamSynchronize(h->s));  // qr_host is reused
+}
+
+bool sources_stable(tvegpu_engine* h, double t) {
+    if (h->source_override) return true;
+    for (size_t r = 0; r < h->regions.size(); ++r)
+        if ((h->regions[r].active_at(t) ? 1 : 0) != h->active[r]) return false;
+    return true;
+}
+
+void exchange(tvegpu_engine* h, double* slots, double* sendbuf, int width) {
+    const RankPlan& pl = h->plan;
+    const int ns = pl.send_off.back();
+    if (ns > 0) k_pack<<<blocks(ns, 256), 256, 0, h->s>>>(slots, h->d_send_slot, ns, width, sendbuf, h->ptr.clock);
+    CU(cudaEventRecord(h->ev_pack, h->s));
+    CU(cudaStreamWaitEvent(h->sc, h->ev_pack, 0));
+    auto& api = nccl();
+    NC(api.GroupStart());
+    for (size_t j = 0; j < pl.neighbors.size(); ++j) {
+        const int peer = pl.neighbors[j];
+        const size_t so = pl.send_off[j], sn = pl.send_off[j + 1] - so;
+        const size_t ro = pl.recv_off[j], rn = pl.recv_off[j + 1] - ro;
+        if (sn) NC(api.Send(sendbuf + so * width, sn * width, ncclFloat64, peer, h->comm, h->sc));
+        if (rn) NC(api.Recv(slots + ((size_t)pl.E * pl.nn + ro) * width, rn * width, ncclFloat64, peer, h->comm, h->sc));
+    }
+    NC(api.GroupEnd());
+    CU(cudaEventRecord(h->ev_comm, h->sc));
+}
+
+template <int NN>
+void launch_mech_element(tvegpu_engine* h, int e0, int e1) {
+    if (e1 <= e0) return;
+    const int T = 128;
+    const int g = blocks(e1 - e0, T);
+    switch (h->prm.exp_kind < 0 ? 0 : (h->prm.exp_kind == 0 ? 1 : 2)) {
+        case 0: k_mech_element<NN, 0><<<g, T, 0, h->s>>>(h->prm, h->ptr, h->cur, e0, e1); break;
+        case 1: k_mech_element<NN, 1><<<g, T, 0, h->s>>>(h->prm, h->ptr, h->cur, e0, e1); break;
+        default: k_mech_element<NN, 2><<<g, T, 0, h->s>>>(h->prm, h->ptr, h->cur, e0, e1); break;
+    }
+}
+
+template <int NN>
+void launch_thermal_element(tvegpu_engine* h, int e0, int e1) {
+    if (e1 <= e0) return;
+    k_thermal_element<NN><<<blocks(e1 - e0, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur, e0, e1);
+}
+
+// One Engine::step() (engine.hpp:70-82): K1 K2 [K3 K4] K5, with the halo
+// exchange of boundary-element slots overlapped with interior elements.
+void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr) {
+    const int E = h->plan.E, Eb = h->plan.Eb, N = h->plan.N;
+    const bool multi = h->plan.nranks > 1;
+    int ev = 0;
+    auto mark = [&]() {
+        if (evs) CU(cudaEventRecord(evs[ev++], h->s));
+    };
+    mark();
+    if (h->mode != TVEGPU_MECHANICAL_ONLY) {
+        if (multi) {
+            h->nn == 4 ? launch_thermal_element<4>(h, 0, Eb) : launch_thermal_element<8>(h, 0, Eb);
+            exchange(h, h->ptr.slot_th, h->send_th, 1);
+            h->nn == 4 ? launch_thermal_element<4>(h, Eb, E) : launch_thermal_element<8>(h, Eb, E);
+            CU(cudaStreamWaitEvent(h->s, h->ev_comm, 0));
+        } else {
+            h->nn == 4 ? launch_thermal_element<4>(h, 0, E) : launch_thermal_element<8>(h, 0, E);
+        }
+        mark();
+        k_thermal_node<<<blocks(N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur);
+        mark();
+    }
+    if (h->mode != TVEGPU_THERMAL_ONLY) {
+        if (multi) {
+            h->nn == 4 ? launch_mech_element<4>(h, 0, Eb) : launch_mech_element<8>(h, 0, Eb);
+            exchange(h, h->ptr.slot_m, h->send_m, 3);
+            h->nn == 4 ? launch_mech_element<4>(h, Eb, E) : launch_mech_element<8>(h, Eb, E);
+            CU(cudaStreamWaitEvent(h->s, h->ev_comm, 0));
+        } else {
+            h->nn == 4 ? launch_mech_element<4>(h, 0, E) : launch_mech_element<8>(h, 0, E);
+        }
+        mark();
+        k_mech_node<<<blocks(N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur);
+        mark();
+        h->cur ^= 1;
+    }
+    k_finish_step<<<1, 32, 0, h->s>>>(h->ptr.clock, h->ptr.err_inst, h->ptr.err_elem, h->dt);
+    mark();
+    CU(cudaGetLastError());
+}
+
+cudaGraphExec_t get_graph(tvegpu_engine* h, int nsteps) {
+    auto key = std::make_pair(h->cur, nsteps);
+    auto it = h->graphs.find(key);
+    if (it != h->graphs.end()) return it->second;
+    const int cur0 = h->cur;
+    cudaGraph_t g;
+    CU(cudaStreamBeginCapture(h->s, cudaStreamCaptureModeThreadLocal));
+    try {
+        for (int k = 0; k < nsteps; ++k) enqueue_one_step(h);
+    } catch (...) {
+        cudaStreamEndCapture(h->s, &g);
+        h->cur = cur0;
+        throw;
+    }
+    CU(cudaStreamEndCapture(h->s, &g));
+    h->cur = cur0;
+    cudaGraphExec_t ex;
+    CU(cudaGraphInstantiate(&ex, g, 0));
+    CU(cudaGraphDestroy(g));
+    h->graphs[key] = ex;
+    return ex;
+}
+
+bool flips(const tvegpu_engine* h) { return h->mode != TVEGPU_THERMAL_ONLY; }
+
+// Enqueue nsteps: graph chunks, split where the active-source mask changes.
+void enqueue_steps(tvegpu_engine* h, long long nsteps) {
+    if (h->halted) return;
+    if (!h->pending) {
+        h->pending = true;
+        h->pend_step = h->host_step;
+        h->pend_cur = h->cur;
+    }
+    long long done = 0;
+    while (done < nsteps) {
+        refresh_sources_if_needed(h, h->host_time);
+        // how many steps keep the same source mask?
+        long long k = 0;
+        double t = h->host_time;
+        const long long cap = std::min<long long>(nsteps - done, h->steps_per_graph);
+        while (k < cap) {
+            if (k > 0 && !sources_stable(h, t)) break;
+            t += h->dt;
+            ++k;
+        }
+        if (k == h->steps_per_graph) {
+            CU(cudaGraphLaunch(get_graph(h, (int)k), h->s));
+            if (flips(h) && (k & 1)) h->cur ^= 1;
+        } else {
+            for (long long j = 0; j < k; ++j) enqueue_one_step(h);
+        }
+        h->host_time = t;
+        h->host_step += k;
+        done += k;
+    }
+}
+
+tvegpu_status sync_and_check(tvegpu_engine* h, long long step_at_start, int cur_at_start) {
+    CU(cudaMemcpyAsync(h->h_words, h->ptr.clock, sizeof(Clock), cudaMemcpyDeviceToHost, h->s));
+    CU(cudaMemcpyAsync(h->h_words + 3, h->ptr.err_inst, 8, cudaMemcpyDeviceToHost, h->s));
+    CU(cudaMemcpyAsync(h->h_words + 4, h->ptr.err_elem, 8, cudaMemcpyDeviceToHost, h->s));
+    CU(cudaStreamSynchronize(h->s));
+    Clock c;
+    std::memcpy(&c, h->h_words, sizeof(Clock));
+    unsigned long long wi = h->h_words[3], we = h->h_words[4];
+    if (h->plan.nranks > 1) {
+        // agree on the first failure across ranks
+        unsigned long long* dw = reinterpret_cast<unsigned long long*>(h->ptr.err_inst);
+        auto& api = nccl();
+        NC(api.AllReduce(dw, dw, 1, ncclUint64, ncclMin, h->comm, h->s));
+        NC(api.AllReduce(h->ptr.err_elem, h->ptr.err_elem, 1, ncclUint64, ncclMin, h->comm, h->s));
+        CU(cudaMemcpyAsync(h->h_words + 3, h->ptr.err_inst, 8, cudaMemcpyDeviceToHost, h->s));
+        CU(cudaMemcpyAsync(h->h_words + 4, h->ptr.err_elem, 8, cudaMemcpyDeviceToHost, h->s));
+        CU(cudaStreamSynchronize(h->s));
+        wi = h->h_words[3];
+        we = h->h_words[4];
+    }
+    if (!c.halted && wi == ~0ULL && we == ~0ULL) {
+        if (c.step != h->host_step) throw Error(TVEGPU_E_CUDA, "internal: device/host step mismatch");
+        h->host_time = c.time;
+        return TVEGPU_OK;
+    }
+    // A step failed: the device halted right after it (state = the reference's state
+    // when step() throws: that step applied, time/step not advanced).
+    h->halted = true;
+    h->host_time = c.time;
+    const long long executed = c.step - step_at_start + (c.halted ? 1 : 0);
+    h->host_step = c.step;
+    h->cur = flips(h) ? (cur_at_start ^ (int)(executed & 1)) : cur_at_start;
+    char buf[256];
+    if (we != ~0ULL && (wi == ~0ULL || (long long)(we >> 32) <= (long long)(wi >> 33))) {
+        h->err_step = (long long)(we >> 32);
+        h->err_node = (int)(we & 0xffffffffu);
+        std::snprintf(buf, sizeof buf, "non-SPD C or singular F in element %d at step %lld", h->err_node, h->err_step);
+        h->err = buf;
+        return TVEGPU_E_VALIDATION;
+    }
+    h->err_step = (long long)(wi >> 33);
+    h->err_node = (int)(wi & 0xffffffffu);
+    std::snprintf(buf, sizeof buf, "non-finite %s at step %lld, node %d", ((wi >> 32) & 1) ? "displacement" : "temperature",
+                  h->err_step, h->err_node);
+    h->err = buf;
+    return TVEGPU_E_INSTABILITY;
+}
+
+void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_options& o) {
+    if (o.device >= 0) CU(cudaSetDevice(o.device));
+    CU(cudaGetDevice(&h->device));
+    const int nranks = o.nranks > 0 ? o.nranks : 1;
+    if (!p.allow_unstable_dt) {
+        double th, me;
+        critical_timestep(p, &th, &me);
+        if (p.dt > std::min(th, me)) {
+            char buf[200];
+            std::snprintf(buf, sizeof buf, "dt %.6g above critical timestep (thermal %.6g, mechanical %.6g)", p.dt, th, me);
+            throw Error(TVEGPU_E_VALIDATION, buf);
+        }
+    }
+    GlobalMesh g = build_global(p);
+    h->plan = build_rank_plan(p, g, nranks, o.rank, o.reorder);
+    const RankPlan& pl = h->plan;
+    h->nn = g.nn;
+    h->kind = p.kind;
+    h->mode = p.mode;
+    h->dt = p.dt;
+    h->N_global = g.N;
+    h->E_global = g.E;
+    h->P = p.prony_count;
+    if (o.steps_per_graph > 0) h->steps_per_graph = o.steps_per_graph;
+    const int nn = g.nn, E = pl.E, N = pl.N, P = p.prony_count;
+    // ---- params
+    DevParams& m = h->prm;
+    m.nn = nn;
+    m.E = E;
+    m.N = N;
+    m.P = P;
+    m.mode = p.mode;
+    m.td = p.temperature_dependent ? 1 : 0;
+    m.dt = p.dt;
+    m.mu = p.mu;
+    m.kappa = p.kappa;
+    m.eta_a = p.eta_a;
+    m.kh = p.hourglass_stiffness * p.mu;
+    m.rho = p.density;
+    m.wbcb = p.perfusion_rate * p.blood_specific_heat;
+    m.Ta = p.arterial_temperature;
+    m.Qm = p.metabolic_rate;
+    m.gamma = p.damping_gamma;
+    m.c_len = p.c_table_len;
+    m.k_len = p.k_table_len;
+    for (int i = 0; i < p.c_table_len; ++i) {
+        m.cT[i] = p.c_table_T[i];
+        m.cV[i] = p.c_table_value[i];
+    }
+    for (int i = 0; i < p.k_table_len; ++i) {
+        m.kT[i] = p.k_table_T[i];
+        for (int q = 0; q < 9; ++q) m.kK[i][q] = p.k_table_tensor[9 * i + q];
+    }
+    // fixed-property temperature 37 degC (engine.hpp:141)
+    {
+        auto interp = [&](const double* Ts, const double* Vs, int n, double T) {
+            if (n == 1 || T <= Ts[0]) return Vs[0];
+            if (T >= Ts[n - 1]) return Vs[n - 1];
+            int j = 0;
+            while (j + 2 < n && T >= Ts[j + 1]) ++j;
+            const double w = (T - Ts[j]) / (Ts[j + 1] - Ts[j]);
+            return Vs[j] + (Vs[j + 1] - Vs[j]) * w;
+        };
+        m.c_fixed = interp(m.cT, m.cV, m.c_len, 37.0);
+        for (int q = 0; q < 9; ++q) {
+            double col[kMaxTable];
+            for (int i = 0; i < m.k_len; ++i) col[i] = m.kK[i][q];
+            m.k_fixed[q] = interp(m.kT, col, m.k_len, 37.0);
+        }
+    }
+    const bool expansion = p.mode == TVEGPU_COUPLED && p.expansion_enabled && p.has_expansion;
+    m.exp_kind = expansion ? p.expansion_kind : -1;
+    m.alpha_i = p.alpha_i;
+    m.alpha_m = p.alpha_m;
+    m.alpha_n = p.alpha_n;
+    m.Tref = p.reference_temperature;
+    for (int k = 0; k < 3; ++k) {
+        m.axis_m[k] = p.axis_m[k];
+        m.axis_n[k] = p.axis_n[k];
+        m.fiber[k] = p.fiber[k];
+    }
+    m.axes_per_elem = p.expansion_axes ? 1 : 0;
+    m.fiber_mode = p.eta_a > 0 ? (p.fiber_dirs ? 2 : 1) : 0;
+    for (int i = 0; i < P; ++i) {
+        const double phi = p.prony_phi[i], tau = p.prony_tau[i];
+        m.pa[i] = p.dt * phi / (p.dt + tau);
+        m.pb[i] = tau / (p.dt + tau);
+    }
+    m.diag = o.diagnostics ? 1 : 0;
+    // ---- streams
+    CU(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&h->sc, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&h->ev_pack, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&h->ev_comm, cudaEventDisableTiming));
+    CU(cudaMallocHost(&h->h_words, 8 * sizeof(unsigned long long)));
+    cudaStream_t s = h->s;
+    auto& own = h->owned;
+    // ---- element arrays (SoA)
+    {
+        std::vector<int32_t> conn((size_t)nn * E);
+        std::vector<double> A((size_t)9 * E), vol(E);
+        for (int e = 0; e < E; ++e) {
+            const int oe = pl.elem_orig[e];
+            for (int a = 0; a < nn; ++a) conn[(size_t)a * E + e] = pl.conn[(size_t)e * nn + a];
+            for (int q = 0; q < 9; ++q) A[(size_t)q * E + e] = g.A[(size_t)9 * oe + q];
+            vol[e] = g.vol[oe];
+        }
+        h->ptr.conn = dupload(own, conn, s);
+        h->ptr.A = dupload(own, A, s);
+        h->ptr.vol = dupload(own, vol, s);
+        CU(cudaStreamSynchronize(s));
+    }
+    h->ptr.elem_orig = dupload(own, pl.elem_orig, s);
+    h->ptr.theta = dalloc<double>(own, (size_t)6 * P * E);
+    CU(cudaMemsetAsync(h->ptr.theta, 0, std::max<size_t>(1, (size_t)6 * P * E) * 8, s));
+    if (p.fiber_dirs && m.fiber_mode == 2) {
+        std::vector<double> f((size_t)3 * E);
+        for (int e = 0; e < E; ++e)
+            for (int k = 0; k < 3; ++k) f[(size_t)k * E + e] = p.fiber_dirs[3 * (size_t)pl.elem_orig[e] + k];
+        h->ptr.fiber = dupload(own, f, s);
+        CU(cudaStreamSynchronize(s));
+    }
+    if (p.expansion_axes && expansion) {
+        std::vector<double> f((size_t)6 * E);
+        for (int e = 0; e < E; ++e)
+            for (int k = 0; k < 6; ++k) f[(size_t)k * E + e] = p.expansion_axes[6 * (size_t)pl.elem_orig[e] + k];
+        h->ptr.axes = dupload(own, f, s);
+        CU(cudaStreamSynchronize(s));
+    }
+    // ---- node arrays
+    {
+        std::vector<double4> rec(N), X(nn == 8 ? N : 0);
+        std::vector<double> mass(N), vn(N);
+        for (int i = 0; i < N; ++i) {
+            const int oi = pl.node_orig[i];
+            rec[i] = make_double4(0.0, 0.0, 0.0, p.initial_temperature);
+            if (nn == 8) X[i] = make_double4(p.nodes[3 * (size_t)oi], p.nodes[3 * (size_t)oi + 1], p.nodes[3 * (size_t)oi + 2], 0.0);
+            mass[i] = g.mass[oi];
+            vn[i] = g.vnode[oi];
+        }
+        h->ptr.rec0 = dupload(own, rec, s);
+        h->ptr.rec1 = dupload(own, rec, s);
+        if (nn == 8) h->ptr.X = dupload(own, X, s);
+        h->ptr.mass = dupload(own, mass, s);
+        h->ptr.vnode = dupload(own, vn, s);
+        CU(cudaStreamSynchronize(s));
+    }
+    h->ptr.node_orig = dupload(own, pl.node_orig, s);
+    CU(cudaMallocHost(&h->qr_host, std::max(1, N) * sizeof(double)));
+    std::memset(h->qr_host, 0, std::max(1, N) * sizeof(double));
+    h->ptr.qr = dalloc<double>(own, N);
+    CU(cudaMemsetAsync(const_cast<double*>(h->ptr.qr), 0, std::max(1, N) * sizeof(double), s));
+    // ---- boundary conditions (mechanics.hpp:37-47, bioheat.hpp:32-35)
+    {
+        std::vector<int32_t> local(g.N, -1);
+        for (int i = 0; i < N; ++i) local[pl.node_orig[i]] = i;
+        std::vector<uint8_t> mask(N, 0);
+        std::vector<int32_t> row(N, -1);
+        std::vector<int32_t> presc;  // [nbc][3]
+        std::vector<double> tfix;
+        auto get_row = [&](int li) {
+            if (row[li] < 0) {
+                row[li] = (int32_t)tfix.size();
+                tfix.push_back(0.0);
+                presc.insert(presc.end(), {-1, -1, -1});
+            }
+            return row[li];
+        };
+        for (int k = 0; k < p.num_fixed_nodes; ++k) {
+            const int li = local[p.fixed_nodes[k]];
+            if (li >= 0) mask[li] |= BC_FIXED;
+        }
+        std::vector<double> tg(std::max(1, p.num_prescribed)), rt(std::max(1, p.num_prescribed));
+        for (int q = 0; q < p.num_prescribed; ++q) {
+            const auto& d = p.prescribed[q];
+            tg[q] = d.target;
+            rt[q] = d.ramp_time;
+            for (int k = 0; k < d.num_nodes; ++k) {
+                const int li = local[d.nodes[k]];
+                if (li < 0) continue;
+                mask[li] |= (uint8_t)(BC_PX << d.component);
+                presc[3 * get_row(li) + d.component] = q;  // list order: last wins (C9)
+            }
+        }
+        for (int k = 0; k < p.num_fixed_temperatures; ++k) {
+            const int li = local[p.fixed_temperature_nodes[k]];
+            if (li < 0) continue;
+            mask[li] |= BC_TFIX;
+            tfix[get_row(li)] = p.fixed_temperature_values[k];  // last wins
+        }
+        for (int i = 0; i < N; ++i)
+            if (row[i] < 0) row[i] = 0;
+        if (tfix.empty()) {
+            tfix.push_back(0.0);
+            presc.insert(presc.end(), {-1, -1, -1});
+        }
+        h->ptr.mask = dupload(own, mask, s);
+        h->ptr.bc_index = dupload(own, row, s);
+        h->ptr.bc_presc = dupload(own, presc, s);
+        h->ptr.bc_tfix = dupload(own, tfix, s);
+        h->ptr.presc_target = dupload(own, tg, s);
+        h->ptr.presc_ramp = dupload(own, rt, s);
+        CU(cudaStreamSynchronize(s));
+        // external + body force R (engine.hpp:139)
+        bool anyR = p.body_force[0] != 0 || p.body_force[1] != 0 || p.body_force[2] != 0;
+        if (p.external_force)
+            for (int64_t k = 0; k < 3 * (int64_t)g.N && !anyR; ++k) anyR = p.external_force[k] != 0;
+        m.has_R = anyR ? 1 : 0;
+        if (anyR) {
+            std::vector<double> R((size_t)3 * N);
+            for (int i = 0; i < N; ++i)
+                for (int c = 0; c < 3; ++c) {
+                    const int oi = pl.node_orig[i];
+                    const double ext = p.external_force ? p.external_force[3 * (size_t)oi + c] : 0.0;
+                    R[(size_t)3 * i + c] = ext + p.body_force[c] * g.vnode[oi];
+                }
+            h->ptr.R = dupload(own, R, s);
+            CU(cudaStreamSynchronize(s));
+        }
+    }
+    // ---- gather CSR and slot buffers
+    h->ptr.csr_off = dupload(own, pl.csr_off, s);
+    h->ptr.csr_slot = dupload(own, pl.csr_slot, s);
+    const size_t nrecv = pl.recv_off.empty() ? 0 : pl.recv_off.back();
+    const size_t nslots = (size_t)nn * E + nrecv;
+    m.nslots = (int)nslots;
+    h->ptr.slot_th = dalloc<double>(own, nslots);
+    h->ptr.slot_m = dalloc<double>(own, 3 * nslots);
+    CU(cudaMemsetAsync(h->ptr.slot_th, 0, nslots * 8, s));
+    CU(cudaMemsetAsync(h->ptr.slot_m, 0, 3 * nslots * 8, s));
+    // ---- clock and error words
+    h->ptr.clock = dalloc<Clock>(own, 1);
+    h->ptr.err_inst = dalloc<unsigned long long>(own, 1);
+    h->ptr.err_elem = dalloc<unsigned long long>(own, 1);
+    {
+        Clock c{0.0, 0, 0, 0};
+        CU(cudaMemcpyAsync(h->ptr.clock, &c, sizeof c, cudaMemcpyHostToDevice, s));
+        CU(cudaMemsetAsync(h->ptr.err_inst, 0xff, 8, s));
+        CU(cudaMemsetAsync(h->ptr.err_elem, 0xff, 8, s));
+        CU(cudaStreamSynchronize(s));
+    }
+    if (m.diag) {
+        h->ptr.diag_F = dalloc<double>(own, (size_t)9 * E);
+        h->ptr.diag_S = dalloc<double>(own, (size_t)9 * E);
+        h->ptr.diag_f = dalloc<double>(own, (size_t)3 * N);
+        CU(cudaMemsetAsync(h->ptr.diag_F, 0, (size_t)9 * E * 8, s));
+        CU(cudaMemsetAsync(h->ptr.diag_S, 0, (size_t)9 * E * 8, s));
+        CU(cudaMemsetAsync(h->ptr.diag_f, 0, (size_t)3 * N * 8, s));
+    }
+    // ---- sources
+    for (int r = 0; r < p.num_sources; ++r) {
+        Region reg;
+        reg.q_r = p.sources[r].q_r;
+        reg.t_start = p.sources[r].t_start;
+        reg.t_end = p.sources[r].t_end;
+        for (int k = 0; k < p.sources[r].num_elements; ++k) {
+            const int e = p.sources[r].elements[k];
+            for (int a = 0; a < nn; ++a) reg.nodes.push_back(p.elements[(size_t)e * nn + a]);
+            reg.vol.push_back(g.vol[e]);
+        }
+        h->regions.push_back(std::move(reg));
+    }
+    h->active.assign(h->regions.size(), 0);
+    // ---- multi-GPU halo
+    if (nranks > 1) {
+        if (!o.nccl_unique_id) throw Error(TVEGPU_E_ARG, "nranks > 1 needs options.nccl_unique_id");
+        ncclUniqueId id;
+        std::memcpy(&id, o.nccl_unique_id, sizeof id);
+        NC(nccl().CommInitRank(&h->comm, nranks, id, o.rank));
+        const size_t ns = pl.send_off.back();
+        h->d_send_slot = dupload(own, pl.send_slot, s);
+        h->send_th = dalloc<double>(own, ns);
+        h->send_m = dalloc<double>(own, 3 * ns);
+        CU(cudaStreamSynchronize(s));
+    }
+    CU(cudaStreamSynchronize(s));
+}
+
+std::string status_name(tvegpu_status st) { return tvegpu_status_string(st); }
+
+template <class F>
+tvegpu_status guard(tvegpu_engine* h, F&& f) {
+    try {
+        return f();
+    } catch (const Error& e) {
+        if (h) {
+            h->err = e.what();
+            h->last_status = e.status;
+        }
+        return e.status;
+    } catch (const std::exception& e) {
+        if (h) h->err = e.what();
+        return TVEGPU_E_ARG;
+    }
+}
+
+void to_local_rec(tvegpu_engine* h, std::vector<double4>& r0, std::vector<double4>& r1) {
+    const int N = h->plan.N;
+    r0.resize(N);
+    r1.resize(N);
+    CU(cudaMemcpyAsync(r0.data(), h->ptr.rec0, N * sizeof(double4), cudaMemcpyDeviceToHost, h->s));
+    CU(cudaMemcpyAsync(r1.data(), h->ptr.rec1, N * sizeof(double4), cudaMemcpyDeviceToHost, h->s));
+    CU(cudaStreamSynchronize(h->s));
+}
+
+// One D2H copy of the current node record (u, T) into pinned staging, scattered to
+// original numbering; the previous record is copied only when u_prev is wanted.
+void read_fields(tvegpu_engine* h, double* T, double* u, double* up) {
+    const int N = h->plan.N;
+    if (!h->stage) CU(cudaMallocHost(&h->stage, (size_t)N * sizeof(double4)));
+    const double4* rc = h->cur ? h->ptr.rec1 : h->ptr.rec0;
+    const double4* rp = h->cur ? h->ptr.rec0 : h->ptr.rec1;
+    CU(cudaMemcpyAsync(h->stage, rc, N * sizeof(double4), cudaMemcpyDeviceToHost, h->s));
+    CU(cudaStreamSynchronize(h->s));
+    const int32_t* no = h->plan.node_orig.data();
+    for (int i = 0; i < N; ++i) {
+        const double4 r = h->stage[i];
+        const size_t o = (size_t)no[i];
+        if (T) T[o] = r.w;
+        if (u) {
+            u[3 * o] = r.x;
+            u[3 * o + 1] = r.y;
+            u[3 * o + 2] = r.z;
+        }
+    }
+    if (up) {
+        CU(cudaMemcpyAsync(h->stage, rp, N * sizeof(double4), cudaMemcpyDeviceToHost, h->s));
+        CU(cudaStreamSynchronize(h->s));
+        for (int i = 0; i < N; ++i) {
+            const size_t o = 3 * (size_t)no[i];
+            up[o] = h->stage[i].x;
+            up[o + 1] = h->stage[i].y;
+            up[o + 2] = h->stage[i].z;
+        }
+    }
+}
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+int32_t tvegpu_abi_version(void) { return TVEGPU_ABI_VERSION; }
+
+const char* tvegpu_status_string(tvegpu_status s) {
+    switch (s) {
+        case TVEGPU_OK: return "ok";
+        case TVEGPU_E_PARSE: return "ParseError";
+        case TVEGPU_E_VALIDATION: return "ValidationError";
+        case TVEGPU_E_INSTABILITY: return "InstabilityError";
+        case TVEGPU_E_IO: return "IoError";
+        case TVEGPU_E_CUDA: return "CudaError";
+        case TVEGPU_E_NCCL: return "NcclError";
+        case TVEGPU_E_ARG: return "ArgumentError";
+    }
+    return "unknown";
+}
+
+const char* tvegpu_create_error(void) { return g_create_error.c_str(); }
+
+void tvegpu_default_options(tvegpu_options* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof *o);
+    o->device = -1;
+    o->nranks = 1;
+    o->rank = 0;
+    o->reorder = 1;
+    o->steps_per_graph = 64;
+}
+
+tvegpu_status tvegpu_create(const tvegpu_problem* p, const tvegpu_options* o, tvegpu_engine** out) {
+    if (!p || !out) {
+        g_create_error = "NULL argument";
+        return TVEGPU_E_ARG;
+    }
+    *out = nullptr;
+    tvegpu_options def;
+    tvegpu_default_options(&def);
+    if (!o) o = &def;
+    auto* h = new tvegpu_engine();
+    try {
+        build_engine(h, *p, *o);
+    } catch (const Error& e) {
+        g_create_error = e.what();
+        tvegpu_destroy(h);
+        return e.status;
+    } catch (const std::exception& e) {
+        g_create_error = e.what();
+        tvegpu_destroy(h);
+        return TVEGPU_E_ARG;
+    }
+    g_create_error.clear();
+    *out = h;
+    return TVEGPU_OK;
+}
+
+void tvegpu_destroy(tvegpu_engine* h) {
+    if (!h) return;
+    for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+    if (h->s) cudaStreamSynchronize(h->s);
+    if (h->comm) nccl().CommDestroy(h->comm);
+    for (void* p : h->owned) cudaFree(p);
+    if (h->h_words) cudaFreeHost(h->h_words);
+    if (h->stage) cudaFreeHost(h->stage);
+    if (h->qr_host) cudaFreeHost(h->qr_host);
+    if (h->ev_pack) cudaEventDestroy(h->ev_pack);
+    if (h->ev_comm) cudaEventDestroy(h->ev_comm);
+    if (h->s) cudaStreamDestroy(h->s);
+    if (h->sc) cudaStreamDestroy(h->sc);
+    delete h;
+}
+
+tvegpu_status tvegpu_enqueue_steps(tvegpu_engine* h, int64_t n) {
+    if (!h || n < 0) return TVEGPU_E_ARG;
+    return guard(h, [&] {
+        enqueue_steps(h, n);
+        return TVEGPU_OK;
+    });
+}
+
+tvegpu_status tvegpu_sync(tvegpu_engine* h) {
+    if (!h) return TVEGPU_E_ARG;
+    return guard(h, [&] {
+        if (h->halted) return h->last_status;
+        if (!h->pending) {
+            CU(cudaStreamSynchronize(h->s));
+            return TVEGPU_OK;
+        }
+        h->pending = false;
+        h->last_status = sync_and_check(h, h->pend_step, h->pend_cur);
+        return h->last_status;
+    });
+}
+
+tvegpu_status tvegpu_step(tvegpu_engine* h, int64_t n) {
+    if (!h || n < 0) return TVEGPU_E_ARG;
+    return guard(h, [&] {
+        if (h->halted) {
+            h->err = "engine halted by an earlier failure; reset the state with tvegpu_set_state";
+            return h->last_status;
+        }
+        enqueue_steps(h, n);
+        h->pending = false;
+        h->last_status = sync_and_check(h, h->pend_step, h->pend_cur);
+        return h->last_status;
+    });
+}
+
+double tvegpu_time(const tvegpu_engine* h) { return h ? h->host_time : 0.0; }
+int64_t tvegpu_step_count(const tvegpu_engine* h) { return h ? h->host_step : 0; }
+
+tvegpu_status tvegpu_get_temperatures(tvegpu_engine* h, double* T) {
+    if (!h || !T) return TVEGPU_E_ARG;
+    return guard(h, [&] {
+        read_fields(h, T, nullptr, nullptr);
+        return TVEGPU_OK;
+    });
+}
+
+tvegpu_status tvegpu_get_displacements(tvegpu_engine* h, double* u, double* up) {
+    if (!h || !u) return TVEGPU_E_ARG;
+    return guard(h, [&] {
+        read_fields(h, nullptr, u, up);
+        return TVEGPU_OK;
+    });
+}
+
+tvegpu_status tvegpu_make_snapshot(tvegpu_engine* h, double* T, double* u) {
+    if (!h || (!T && !u)) return TVEGPU_E_ARG;
+    return guard(h, [&] {
+        read_fields(h, T, u, nullptr);
+        return TVEGPU_OK;
+    });
+}
+
+tvegpu_status tvegpu_get_viscous(tvegpu_engine* h, double* v) {
+    if (!h || !v) return TVEGPU_E_ARG;
+    return guard(h, [&] {
+        const int E = h->plan.E, P = h->P;
+        std::vector<double> th((size_t)6 * P * E);
+        if (!th.empty()) {
+            CU(cudaMemcpyAsync(th.data(), h->ptr.theta, th.size() * 8, cudaMemcpyDeviceToHost, h->s));
+            CU(cudaStreamSynchronize(h->s));
+        }
+        static const int map9[9] = {0, 3, 5, 3, 1, 4, 5, 4, 2};
+        for (int e = 0; e < E; ++e)
+            for (int p = 0; p < P; ++p) {
+                double* o = v + ((size_t)h->plan.elem_orig[e] * P + p) * 9;
+                for (int q = 0; q < 9; ++q) o[q] = th[((size_t)p * 6 + map9[q]) * E + e];
+            }
+        return TVEGPU_OK;
+    });
+}
+
+tvegpu_status tvegpu_set_state(tvegpu_engine* h, const double* T, const double* u, const double* up,
+                               const double* viscous, double time, int64_t step) {
+    if (!h) return TVEGPU_E_ARG;
+    return guard(h, [&] {
+        std::vector<double4> r0, r1;
+        to_local_rec(h, r0, r1);
+        auto& rc = h->cur ? r1 : r0;
+        auto& rp = h->cur ? r0 : r1;
+        for (int i = 0; i < h->plan.N; ++i) {
+            const size_t o = (size_t)h->plan.node_orig[i];
+            if (T) rc[i].w = rp[i].w = T[o];
+            if (u) rc[i] = make_double4(u[3 * o], u[3 * o + 1], u[3 * o + 2], rc[i].w);
+            if (up) rp[i] = make_double4(up[3 * o], up[3 * o + 1], up[3 * o + 2], rp[i].w);
+        }
+        const int N = h->plan.N;
+        CU(cudaMemcpyAsync(h->ptr.rec0, r0.data(), N * sizeof(double4), cudaMemcpyHostToDevice, h->s));
+        CU(cudaMemcpyAsync(h->ptr.rec1, r1.data(), N * sizeof(double4), cudaMemcpyHostToDevice, h->s));
+        if (viscous && h->P) {
+            const int E = h->plan.E, P = h->P;
+            std::vector<double> th((size_t)6 * P * E);
+            static const int pick[6] = {0, 4, 8, 1, 5, 2};  // xx yy zz xy yz xz from row-major 3x3
+            for (int e = 0; e < E; ++e)
+                for (int p = 0; p < P; ++p) {
+                    const double* iv = viscous + ((size_t)h->plan.elem_orig[e] * P + p) * 9;
+                    for (int q = 0; q < 6; ++q) th[((size_t)p * 6 + q) * E + e] = iv[pick[q]];
+                }
+            CU(cudaMemcpyAsync(h->ptr.theta, th.data(), th.size() * 8, cudaMemcpyHostToDevice, h->s));
+            CU(cudaStreamSynchronize(h->s));
+        }
+        Clock c{time, (long long)step, 0, 0};
+        CU(cudaMemcpyAsync(h->ptr.clock, &c, sizeof c, cudaMemcpyHostToDevice, h->s));
+        CU(cudaMemsetAsync(h->ptr.err_inst, 0xff, 8, h->s));
+        CU(cudaMemsetAsync(h->ptr.err_elem, 0xff, 8, h->s));
+        CU(cudaStreamSynchronize(h->s));
+        h->host_time = time;
+        h->host_step = step;
+        h->halted = false;
+        h->last_status = TVEGPU_OK;
+        return TVEGPU_OK;
+    });
+}
+
+tvegpu_status tvegpu_set_nodal_sources(tvegpu_engine* h, const double* power) {
+    if (!h) return TVEGPU_E_ARG;
+    return guard(h, [&] {
+        if (!power) {
+            h->source_override = false;
+            h->sources_init = false;
+            return TVEGPU_OK;
+        }
+        h->source_override = true;
+        for (int li = 0; li < h->plan.N; ++li) h->qr_host[li] = power[h->plan.node_orig[li]];
+        CU(cudaMemcpyAsync(const_cast<double*>(h->ptr.qr), h->qr_host, (size_t)h->plan.N * 8,
+                           cudaMemcpyHostToDevice, h->s));
+        CU(cudaStreamSynchronize(h->s));
+        return TVEGPU_OK;
+    });
+}
+
+tvegpu_status tvegpu_get_diagnostics(tvegpu_engine* h, double* f_int, double* F, double* S) {
+    if (!h) return TVEGPU_E_ARG;
+    if (!h->prm.diag) {
+        h->err = "diagnostics need options.diagnostics = 1";
+        return TVEGPU_E_ARG;
+    }
+    return guard(h, [&] {
+        const int E = h->plan.E, N = h->plan.N;
+        std::vector<double> buf((size_t)9 * std::max(E, N));
+        if (f_int) {
+            CU(cudaMemcpy(buf.data(), h->ptr.diag_f, (size_t)3 * N * 8, cudaMemcpyDeviceToHost));
+            for (int i = 0; i < N; ++i)
+                for (int c = 0; c < 3; ++c) f_int[3 * (size_t)h->plan.node_orig[i] + c] = buf[3 * (size_t)i + c];
+        }
+        for (int k = 0; k < 2; ++k) {
+            double* dst = k == 0 ? F : S;
+            if (!dst) continue;
+            CU(cudaMemcpy(buf.data(), k == 0 ? h->ptr.diag_F : h->ptr.diag_S, (size_t)9 * E * 8, cudaMemcpyDeviceToHost));
+            for (int e = 0; e < E; ++e)
+                for (int q = 0; q < 9; ++q) dst[9 * (size_t)h->plan.elem_orig[e] + q] = buf[9 * (size_t)e + q];
+        }
+        return TVEGPU_OK;
+    });
+}
+
+tvegpu_status tvegpu_last_error(const tvegpu_engine* h, char* msg, size_t cap, int64_t* step, int32_t* node) {
+    if (!h) return TVEGPU_E_ARG;
+    if (msg && cap) {
+        std::strncpy(msg, h->err.c_str(), cap - 1);
+        msg[cap - 1] = 0;
+    }
+    if (step) *step = h->err_step;
+    if (node) *node = h->err_node;
+    return h->last_status;
+}
+
+tvegpu_status tvegpu_critical_timestep(const tvegpu_problem* p, double* thermal, double* mechanical) {
+    if (!p || !thermal || !mechanical) return TVEGPU_E_ARG;
+    try {
+        validate_problem(*p);
+        critical_timestep(*p, thermal, mechanical);
+    } catch (const Error& e) {
+        g_create_error = e.what();
+        return e.status;
+    }
+    return TVEGPU_OK;
+}
+
+// ---------------------------------------------------------------- plan (host only)
+struct tvegpu_plan {
+    RankPlan r;
+};
+
+tvegpu_status tvegpu_plan_create(const tvegpu_problem* p, int32_t nranks, int32_t rank, int32_t reorder,
+                                 tvegpu_plan** out) {
+    if (!p || !out) return TVEGPU_E_ARG;
+    try {
+        GlobalMesh g = build_global(*p);
+        auto* pl = new tvegpu_plan();
+        pl->r = build_rank_plan(*p, g, nranks, rank, reorder);
+        *out = pl;
+    } catch (const Error& e) {
+        g_create_error = e.what();
+        return e.status;
+    } catch (const std::exception& e) {
+        g_create_error = e.what();
+        return TVEGPU_E_ARG;
+    }
+    return TVEGPU_OK;
+}
+
+tvegpu_status tvegpu_plan_get(const tvegpu_plan* pl, tvegpu_plan_view* v) {
+    if (!pl || !v) return TVEGPU_E_ARG;
+    const RankPlan& r = pl->r;
+    v->nranks = r.nranks;
+    v->rank = r.rank;
+    v->nn = r.nn;
+    v->num_elements = r.E;
+    v->num_boundary_elements = r.Eb;
+    v->num_nodes = r.N;
+    v->element_orig = r.elem_orig.data();
+    v->node_orig = r.node_orig.data();
+    v->conn = r.conn.data();
+    v->csr_offsets = r.csr_off.data();
+    v->csr_slots = r.csr_slot.data();
+    v->num_neighbors = (int32_t)r.neighbors.size();
+    v->neighbor_ranks = r.neighbors.data();
+    v->send_offsets = r.send_off.data();
+    v->send_slots = r.send_slot.data();
+    v->recv_offsets = r.recv_off.data();
+    v->element_owner = r.owner.data();
+    v->num_elements_global = (int32_t)r.owner.size();
+    return TVEGPU_OK;
+}
+
+void tvegpu_plan_destroy(tvegpu_plan* p) { delete p; }
+
+tvegpu_status tvegpu_nccl_unique_id(void* out128) {
+    if (!out128) return TVEGPU_E_ARG;
+    try {
+        ncclUniqueId id;
+        NC(nccl().GetUniqueId(&id));
+        std::memcpy(out128, &id, sizeof id);
+    } catch (const Error& e) {
+        g_create_error = e.what();
+        return e.status;
+    }
+    return TVEGPU_OK;
+}
+
+void* tvegpu_stream(tvegpu_engine* h) { return h ? (void*)h->s : nullptr; }
+
+int32_t tvegpu_kernels_per_step(const tvegpu_engine* h) {
+    if (!h) return 0;
+    const bool multi = h->plan.nranks > 1;
+    int k = 1;  // K5
+    if (h->mode != TVEGPU_MECHANICAL_ONLY) k += multi ? 4 : 2;  // K1 (x2 + pack) + K2
+    if (h->mode != TVEGPU_THERMAL_ONLY) k += multi ? 4 : 2;
+    return k;
+}
+
+tvegpu_status tvegpu_profile_kernels(tvegpu_engine* h, int32_t nsteps, double* ms, int32_t* count, char* names,
+                                     size_t cap) {
+    if (!h || nsteps <= 0 || !ms || !count) return TVEGPU_E_ARG;
+    return guard(h, [&] {
+        if (h->halted) return h->last_status;
+        if (h->pending) {
+            h->pending = false;
+            h->last_status = sync_and_check(h, h->pend_step, h->pend_cur);
+            if (h->last_status != TVEGPU_OK) return h->last_status;
+        }
+        std::vector<std::string> nm;
+        if (h->mode != TVEGPU_MECHANICAL_ONLY) {
+            nm.push_back(h->nn == 4 ? "k_thermal_element<4>" : "k_thermal_element<8>");
+            nm.push_back("k_thermal_node");
+        }
+        if (h->mode != TVEGPU_THERMAL_ONLY) {
+            nm.push_back(h->nn == 4 ? "k_mech_element<4>" : "k_mech_element<8>");
+            nm.push_back("k_mech_node");
+        }
+        nm.push_back("k_finish_step");
+        const int nk = (int)nm.size();
+        std::vector<cudaEvent_t> ev((size_t)(nk + 1) * nsteps);
+        for (auto& e : ev) CU(cudaEventCreate(&e));
+        const long long s0 = h->host_step;
+        const int c0 = h->cur;
+        for (int k = 0; k < nsteps; ++k) {
+            refresh_sources_if_needed(h, h->host_time);
+            enqueue_one_step(h, ev.data() + (size_t)k * (nk + 1));
+            h->host_time += h->dt;
+            h->host_step += 1;
+        }
+        tvegpu_status st = sync_and_check(h, s0, c0);
+        std::vector<double> acc(nk, 0.0);
+        for (int k = 0; k < nsteps; ++k)
+            for (int j = 0; j < nk; ++j) {
+                float t = 0;
+                CU(cudaEventElapsedTime(&t, ev[(size_t)k * (nk + 1) + j], ev[(size_t)k * (nk + 1) + j + 1]));
+                acc[j] += t;
+            }
+        for (auto& e : ev) cudaEventDestroy(e);
+        *count = nk;
+        std::string all;
+        for (int j = 0; j < nk; ++j) {
+            ms[j] = acc[j] / nsteps;
+            all += (j ? ";" : "") + nm[j];
+        }
+        if (names && cap) {
+            std::strncpy(names, all.c_str(), cap - 1);
+            names[cap - 1] = 0;
+        }
+        return st;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,612 @@
+// kernels.cuh — the sm_100a kernels of one TLED step.
+//
+//   K1 k_thermal_element<NN>   F from u^n, element-mean T^n -> D(T), conduction load
+//                              V det F B^T D B T_e (Eqs. 16/18/19; bioheat.hpp:37-47)
+//   K2 k_thermal_node          deterministic CSR gather + Eq. 20 (bioheat.hpp:49-63)
+//   K3 k_mech_element<NN,EXP>  F_ther (Eq. 11), total PK2 (Eqs. 8-10), Prony (Eq. 28),
+//                              f = V F S~ G plus closed-form H8 hourglass
+//                              (materials.hpp:99-127; mechanics.hpp:55-84)
+//   K4 k_mech_node             CSR gather + Eq. 22 central difference + BCs
+//                              (mechanics.hpp:86-97)
+//   K5 k_finish_step           finite check verdict, t += dt, step++ (engine.hpp:89-90, 120)
+//
+// fp64 throughout (north_star parity <= 1e-10).  One thread per element / node;
+// element data is SoA ([component][E], coalesced), node state is a packed
+// 32-byte record (ux, uy, uz, T) so every element gathers one sector per node.
+// Assembly is a gather in canonical (original element, local) order: no float
+// atomics, results bit-identical at any partition count.  The only atomics are
+// integer atomicMin on the error words (lowest step, then T before u, then node).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tvegpu {
+
+constexpr int kMaxTable = 16;
+constexpr int kMaxProny = 4;
+
+struct Clock {
+    double time;
+    long long step;
+    int halted;
+    int pad;
+};
+
+struct DevParams {
+    int nn, E, N, P, mode, td, exp_kind, fiber_mode, axes_per_elem, has_R, diag, nslots;
+    double dt, mu, kappa, eta_a, kh, rho, wbcb, Ta, Qm, gamma;
+    double fiber[3];
+    double c_fixed;
+    double k_fixed[9];
+    int c_len, k_len;
+    double cT[kMaxTable], cV[kMaxTable], kT[kMaxTable], kK[kMaxTable][9];
+    double alpha_i, alpha_m, alpha_n, Tref;
+    double axis_m[3], axis_n[3];
+    double pa[kMaxProny], pb[kMaxProny];
+};
+
+struct DevPtrs {
+    const int32_t* conn;       // [nn][E]
+    const double* A;           // [9][E]
+    const double* vol;         // [E]
+    double* theta;             // [P][6][E]   (xx, yy, zz, xy, yz, xz)
+    const double* fiber;       // [3][E] or null
+    const double* axes;        // [6][E] or null
+    const int32_t* elem_orig;  // [E]
+    double4* rec0;             // node record (ux, uy, uz, T), two rotating buffers
+    double4* rec1;
+    const double4* X;          // [N] (x, y, z, 0), H8 only
+    const double* mass;        // [N]
+    const double* vnode;       // [N]
+    const double* qr;          // [N] lumped nodal source power
+    const uint8_t* mask;       // [N] bit0 fixed, bit1..3 prescribed x/y/z, bit4 fixed T
+    const int32_t* bc_index;   // [N] -> row of the BC tables (masked nodes only)
+    const int32_t* bc_presc;   // [nbc][3] prescribed entry id or -1
+    const double* bc_tfix;     // [nbc]
+    const double* presc_target;
+    const double* presc_ramp;
+    const double* R;           // [N][3] external + body force, or null
+    const int32_t* csr_off;    // [N+1]
+    const int32_t* csr_slot;   // gather list: slot ids
+    const int32_t* node_orig;  // [N]
+    double* slot_th;           // [nslots]
+    double* slot_m;            // [nslots][3]
+    Clock* clock;
+    unsigned long long* err_inst;  // (step << 33) | (field << 32) | orig node
+    unsigned long long* err_elem;  // (step << 32) | orig element
+    double* diag_F;            // [E][9] or null
+    double* diag_S;            // [E][9] or null
+    double* diag_f;            // [N][3] or null
+};
+
+enum : uint8_t { BC_FIXED = 1, BC_PX = 2, BC_PY = 4, BC_PZ = 8, BC_TFIX = 16 };
+
+// ------------------------------------------------------------------ small fp64 algebra
+__device__ __forceinline__ double interp1(const double* Ts, const double* Vs, int n, double T) {
+    if (n == 1 || T <= Ts[0]) return Vs[0];
+    if (T >= Ts[n - 1]) return Vs[n - 1];
+    int j = 0;
+    while (j + 2 < n && T >= Ts[j + 1]) ++j;
+    const double w = (T - Ts[j]) / (Ts[j + 1] - Ts[j]);
+    return Vs[j] + (Vs[j + 1] - Vs[j]) * w;
+}
+
+__device__ __forceinline__ void conductivity_at(const DevParams& P, double T, double D[9]) {
+    const int n = P.k_len;
+    if (n == 1 || T <= P.kT[0]) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) D[q] = P.kK[0][q];
+        return;
+    }
+    if (T >= P.kT[n - 1]) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) D[q] = P.kK[n - 1][q];
+        return;
+    }
+    int j = 0;
+    while (j + 2 < n && T >= P.kT[j + 1]) ++j;
+    const double w = (T - P.kT[j]) / (P.kT[j + 1] - P.kT[j]);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) D[q] = P.kK[j][q] + (P.kK[j + 1][q] - P.kK[j][q]) * w;
+}
+
+// adjugate (transpose of cofactors) of a row-major 3x3, returns det
+__device__ __forceinline__ double adj3(const double m[9], double a[9]) {
+    a[0] = m[4] * m[8] - m[5] * m[7];
+    a[1] = m[2] * m[7] - m[1] * m[8];
+    a[2] = m[1] * m[5] - m[2] * m[4];
+    a[3] = m[5] * m[6] - m[3] * m[8];
+    a[4] = m[0] * m[8] - m[2] * m[6];
+    a[5] = m[2] * m[3] - m[0] * m[5];
+    a[6] = m[3] * m[7] - m[4] * m[6];
+    a[7] = m[1] * m[6] - m[0] * m[7];
+    a[8] = m[0] * m[4] - m[1] * m[3];
+    return m[0] * a[0] + m[1] * a[3] + m[2] * a[6];
+}
+
+__device__ __forceinline__ unsigned long long pack_inst(long long step, int field, int node) {
+    return ((unsigned long long)step << 33) | ((unsigned long long)field << 32) | (unsigned)node;
+}
+__device__ __forceinline__ unsigned long long pack_elem(long long step, int elem) {
+    return ((unsigned long long)step << 32) | (unsigned)elem;
+}
+
+__device__ __forceinline__ double4 ldg4(const double4* p) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    return make_double4(a.x, a.y, b.x, b.y);
+}
+
+// H8 corner signs (standard brick order) and hourglass vectors.
+__device__ __forceinline__ constexpr int h8s(int a, int j) {
+    return ((j == 0) ? ((a == 1 || a == 2 || a == 5 || a == 6) ? 1 : -1)
+                     : (j == 1) ? ((a == 2 || a == 3 || a == 6 || a == 7) ? 1 : -1) : (a >= 4 ? 1 : -1));
+}
+__device__ __forceinline__ constexpr int h8h(int al, int a) {
+    // h1 = eta*zeta, h2 = zeta*xi, h3 = xi*eta, h4 = xi*eta*zeta
+    return al == 0 ? h8s(a, 1) * h8s(a, 2)
+                   : al == 1 ? h8s(a, 2) * h8s(a, 0) : al == 2 ? h8s(a, 0) * h8s(a, 1) : h8s(a, 0) * h8s(a, 1) * h8s(a, 2);
+}
+
+// ------------------------------------------------------------------ K1: thermal element
+template <int NN>
+__global__ void __launch_bounds__(256) k_thermal_element(const DevParams P, const DevPtrs D, int cur, int e0,
+                                                         int e1) {
+    const int e = e0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= e1 || D.clock->halted) return;
+    const int E = P.E;
+    const double4* __restrict__ R = cur ? D.rec1 : D.rec0;
+    double H[9], gT[3], Ts;
+    if constexpr (NN == 4) {
+        const double4 r0 = ldg4(R + __ldg(D.conn + e));
+        Ts = r0.w;
+#pragma unroll
+        for (int a = 1; a < 4; ++a) {
+            const double4 r = ldg4(R + __ldg(D.conn + a * E + e));
+            H[0 * 3 + a - 1] = r.x - r0.x;
+            H[1 * 3 + a - 1] = r.y - r0.y;
+            H[2 * 3 + a - 1] = r.z - r0.z;
+            gT[a - 1] = r.w - r0.w;
+            Ts += r.w;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) H[q] = 0.0;
+        gT[0] = gT[1] = gT[2] = 0.0;
+        Ts = 0.0;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const double4 r = ldg4(R + __ldg(D.conn + a * E + e));
+            Ts += r.w;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const double s = (double)h8s(a, j);
+                H[0 * 3 + j] += s * r.x;
+                H[1 * 3 + j] += s * r.y;
+                H[2 * 3 + j] += s * r.z;
+                gT[j] += s * r.w;
+            }
+        }
+    }
+    double A[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) A[q] = __ldg(D.A + q * E + e);
+    const double V = __ldg(D.vol + e);
+    // F = I + H A^T
+    double F[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            F[i * 3 + j] = (i == j ? 1.0 : 0.0) + H[i * 3 + 0] * A[j * 3 + 0] + H[i * 3 + 1] * A[j * 3 + 1] +
+                           H[i * 3 + 2] * A[j * 3 + 2];
+    double Dk[9];
+    if (P.td) conductivity_at(P, Ts / NN, Dk);
+    else {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) Dk[q] = P.k_fixed[q];
+    }
+    // g = G T_e = A (Xi T_e);  w = adj(F)^T g;  q = (V / det F) adj(F) D w;  f_a = xi_a . (A^T q)
+    double g[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) g[i] = A[i * 3 + 0] * gT[0] + A[i * 3 + 1] * gT[1] + A[i * 3 + 2] * gT[2];
+    double Ad[9];
+    const double dF = adj3(F, Ad);
+    double w[3], dw[3], q[3], r[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) w[i] = Ad[0 * 3 + i] * g[0] + Ad[1 * 3 + i] * g[1] + Ad[2 * 3 + i] * g[2];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) dw[i] = Dk[i * 3 + 0] * w[0] + Dk[i * 3 + 1] * w[1] + Dk[i * 3 + 2] * w[2];
+    const double sc = V / dF;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) q[i] = sc * (Ad[i * 3 + 0] * dw[0] + Ad[i * 3 + 1] * dw[1] + Ad[i * 3 + 2] * dw[2]);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) r[j] = A[0 * 3 + j] * q[0] + A[1 * 3 + j] * q[1] + A[2 * 3 + j] * q[2];
+    double* out = D.slot_th + (size_t)e * NN;
+    if constexpr (NN == 4) {
+        const double f0 = -(r[0] + r[1] + r[2]);
+        reinterpret_cast<double2*>(out)[0] = make_double2(f0, r[0]);
+        reinterpret_cast<double2*>(out)[1] = make_double2(r[1], r[2]);
+    } else {
+        double f[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) f[a] = h8s(a, 0) * r[0] + h8s(a, 1) * r[1] + h8s(a, 2) * r[2];
+#pragma unroll
+        for (int a = 0; a < 8; a += 2) reinterpret_cast<double2*>(out)[a / 2] = make_double2(f[a], f[a + 1]);
+    }
+    if (dF == 0.0) atomicMin(D.err_elem, pack_elem(D.clock->step, D.elem_orig[e]));
+}
+
+// ------------------------------------------------------------------ K2: thermal node
+__global__ void __launch_bounds__(256) k_thermal_node(const DevParams P, const DevPtrs D, int cur) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.N || D.clock->halted) return;
+    double4* R = cur ? D.rec1 : D.rec0;
+    const int k0 = __ldg(D.csr_off + i), k1 = __ldg(D.csr_off + i + 1);
+    double s = 0.0;
+    for (int k = k0; k < k1; ++k) s += __ldg(D.slot_th + __ldg(D.csr_slot + k));
+    const double T = R[i].w;
+    const double V = __ldg(D.vnode + i);
+    const double c = P.td ? interp1(P.cT, P.cV, P.c_len, T) : P.c_fixed;
+    const double C = P.rho * c * V;
+    double Tn = T + P.dt / C * (-s - P.wbcb * V * (T - P.Ta) + P.Qm * V + __ldg(D.qr + i));
+    const uint8_t m = __ldg(D.mask + i);
+    if (m & BC_TFIX) Tn = __ldg(D.bc_tfix + __ldg(D.bc_index + i));
+    if (!isfinite(Tn)) atomicMin(D.err_inst, pack_inst(D.clock->step, 0, D.node_orig[i]));
+    R[i].w = Tn;
+}
+
+// ------------------------------------------------------------------ K3: mechanical element
+// EXP: 0 = F_ther = I, 1 = isotropic lambda I, 2 = general (transversely isotropic / orthotropic)
+template <int NN, int EXP>
+__global__ void __launch_bounds__(128) k_mech_element(const DevParams P, const DevPtrs D, int cur, int e0,
+                                                      int e1) {
+    const int e = e0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= e1 || D.clock->halted) return;
+    const int E = P.E;
+    const double4* __restrict__ R = cur ? D.rec1 : D.rec0;
+    double H[9], Ts;
+    double Uh[4][3], cX[4][3];  // H8 only: U h_alpha and X h_alpha
+    if constexpr (NN == 4) {
+        const double4 r0 = ldg4(R + __ldg(D.conn + e));
+        Ts = r0.w;
+#pragma unroll
+        for (int a = 1; a < 4; ++a) {
+            const double4 r = ldg4(R + __ldg(D.conn + a * E + e));
+            H[0 * 3 + a - 1] = r.x - r0.x;
+            H[1 * 3 + a - 1] = r.y - r0.y;
+            H[2 * 3 + a - 1] = r.z - r0.z;
+            Ts += r.w;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) H[q] = 0.0;
+#pragma unroll
+        for (int al = 0; al < 4; ++al)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) Uh[al][i] = cX[al][i] = 0.0;
+        Ts = 0.0;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const int n = __ldg(D.conn + a * E + e);
+            const double4 r = ldg4(R + n);
+            const double4 x = ldg4(D.X + n);
+            Ts += r.w;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const double s = (double)h8s(a, j);
+                H[0 * 3 + j] += s * r.x;
+                H[1 * 3 + j] += s * r.y;
+                H[2 * 3 + j] += s * r.z;
+            }
+#pragma unroll
+            for (int al = 0; al < 4; ++al) {
+                const double h = (double)h8h(al, a);
+                Uh[al][0] += h * r.x;
+                Uh[al][1] += h * r.y;
+                Uh[al][2] += h * r.z;
+                cX[al][0] += h * x.x;
+                cX[al][1] += h * x.y;
+                cX[al][2] += h * x.z;
+            }
+        }
+    }
+    double A[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) A[q] = __ldg(D.A + q * E + e);
+    const double V = __ldg(D.vol + e);
+    double F[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            F[i * 3 + j] = (i == j ? 1.0 : 0.0) + H[i * 3 + 0] * A[j * 3 + 0] + H[i * 3 + 1] * A[j * 3 + 1] +
+                           H[i * 3 + 2] * A[j * 3 + 2];
+    // ---- elastic right Cauchy-Green C (symmetric: 00 11 22 01 12 02)
+    double Fel[9];
+    double lam = 1.0, Fi[9], detFth = 1.0;
+    if constexpr (EXP == 0) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) Fel[q] = F[q];
+    } else if constexpr (EXP == 1) {
+        lam = 1.0 + P.alpha_i * (Ts / NN - P.Tref);
+        const double il = 1.0 / lam;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) Fel[q] = F[q] * il;
+    } else {
+        const double dT = Ts / NN - P.Tref;
+        const double li = 1.0 + P.alpha_i * dT;
+        double m[3], n[3];
+        if (P.axes_per_elem) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                m[k] = __ldg(D.axes + k * E + e);
+                n[k] = __ldg(D.axes + (3 + k) * E + e);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                m[k] = P.axis_m[k];
+                n[k] = P.axis_n[k];
+            }
+        }
+        const double dm = (1.0 + P.alpha_m * dT) - li;
+        const double dn = P.exp_kind == 2 ? (1.0 + P.alpha_n * dT) - li : 0.0;
+        double Fth[9];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) Fth[i * 3 + j] = (i == j ? li : 0.0) + dm * m[i] * m[j] + dn * n[i] * n[j];
+        double Ad[9];
+        detFth = adj3(Fth, Ad);
+        const double idt = 1.0 / detFth;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) Fi[q] = Ad[q] * idt;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+                Fel[i * 3 + j] = F[i * 3 + 0] * Fi[0 * 3 + j] + F[i * 3 + 1] * Fi[1 * 3 + j] + F[i * 3 + 2] * Fi[2 * 3 + j];
+    }
+    double c00 = Fel[0] * Fel[0] + Fel[3] * Fel[3] + Fel[6] * Fel[6];
+    double c11 = Fel[1] * Fel[1] + Fel[4] * Fel[4] + Fel[7] * Fel[7];
+    double c22 = Fel[2] * Fel[2] + Fel[5] * Fel[5] + Fel[8] * Fel[8];
+    double c01 = Fel[0] * Fel[1] + Fel[3] * Fel[4] + Fel[6] * Fel[7];
+    double c12 = Fel[1] * Fel[2] + Fel[4] * Fel[5] + Fel[7] * Fel[8];
+    double c02 = Fel[0] * Fel[2] + Fel[3] * Fel[5] + Fel[6] * Fel[8];
+    // ---- S_int = mu J^-2/3 (I - I1/3 C^-1) + 2 eta (I4b - 1) J^-2/3 (a(x)a - I4/3 C^-1) + kappa J (J-1) C^-1
+    const double a00 = c11 * c22 - c12 * c12, a11 = c00 * c22 - c02 * c02, a22 = c00 * c11 - c01 * c01;
+    const double a01 = c02 * c12 - c01 * c22, a12 = c01 * c02 - c00 * c12, a02 = c01 * c12 - c02 * c11;
+    const double detC = c00 * a00 + c01 * a01 + c02 * a02;
+    if (!(detC > 0.0)) atomicMin(D.err_elem, pack_elem(D.clock->step, D.elem_orig[e]));
+    const double J = sqrt(detC);
+    const double Jm23 = rcbrt(detC);
+    const double idC = 1.0 / detC;
+    const double I1 = c00 + c11 + c22;
+    const double iso = P.mu * Jm23, vol = P.kappa * J * (J - 1.0);
+    double ciw = vol - iso * (I1 / 3.0);  // coefficient of C^-1
+    double S[6];                           // 00 11 22 01 12 02
+    S[0] = iso;
+    S[1] = iso;
+    S[2] = iso;
+    S[3] = S[4] = S[5] = 0.0;
+    if (P.fiber_mode) {
+        double fa[3];
+        if (P.fiber_mode == 2) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) fa[k] = __ldg(D.fiber + k * E + e);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) fa[k] = P.fiber[k];
+        }
+        const double Ca0 = c00 * fa[0] + c01 * fa[1] + c02 * fa[2];
+        const double Ca1 = c01 * fa[0] + c11 * fa[1] + c12 * fa[2];
+        const double Ca2 = c02 * fa[0] + c12 * fa[1] + c22 * fa[2];
+        const double I4 = fa[0] * Ca0 + fa[1] * Ca1 + fa[2] * Ca2;
+        const double an = 2.0 * P.eta_a * (Jm23 * I4 - 1.0) * Jm23;
+        S[0] += an * fa[0] * fa[0];
+        S[1] += an * fa[1] * fa[1];
+        S[2] += an * fa[2] * fa[2];
+        S[3] += an * fa[0] * fa[1];
+        S[4] += an * fa[1] * fa[2];
+        S[5] += an * fa[0] * fa[2];
+        ciw -= an * (I4 / 3.0);
+    }
+    const double cw = ciw * idC;
+    S[0] += cw * a00;
+    S[1] += cw * a11;
+    S[2] += cw * a22;
+    S[3] += cw * a01;
+    S[4] += cw * a12;
+    S[5] += cw * a02;
+    // ---- pull back to the reference configuration: det(F_th) F_th^-1 S F_th^-T
+    if constexpr (EXP == 1) {
+#pragma unroll
+        for (int q = 0; q < 6; ++q) S[q] *= lam;
+    } else if constexpr (EXP == 2) {
+        const double Sm[9] = {S[0], S[3], S[5], S[3], S[1], S[4], S[5], S[4], S[2]};
+        double T1[9];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+                T1[i * 3 + j] = Fi[i * 3 + 0] * Sm[0 * 3 + j] + Fi[i * 3 + 1] * Sm[1 * 3 + j] + Fi[i * 3 + 2] * Sm[2 * 3 + j];
+        auto pb = [&](int i, int j) {
+            return detFth * (T1[i * 3 + 0] * Fi[j * 3 + 0] + T1[i * 3 + 1] * Fi[j * 3 + 1] + T1[i * 3 + 2] * Fi[j * 3 + 2]);
+        };
+        S[0] = pb(0, 0);
+        S[1] = pb(1, 1);
+        S[2] = pb(2, 2);
+        S[3] = pb(0, 1);
+        S[4] = pb(1, 2);
+        S[5] = pb(0, 2);
+    }
+    // ---- Prony recurrence (Eq. 28): theta_i <- a_i S + b_i theta_i ;  S~ = S - sum theta_i
+    double St[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) St[q] = S[q];
+    for (int p = 0; p < P.P; ++p) {
+        double* th = D.theta + (size_t)p * 6 * E + e;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            const double t = P.pa[p] * S[q] + P.pb[p] * th[(size_t)q * E];
+            th[(size_t)q * E] = t;
+            St[q] -= t;
+        }
+    }
+    // ---- P = V F S~ ;  PA = P A  (f_a = PA xi_a)
+    const double Sm[9] = {St[0], St[3], St[5], St[3], St[1], St[4], St[5], St[4], St[2]};
+    double Pm[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            Pm[i * 3 + j] = V * (F[i * 3 + 0] * Sm[0 * 3 + j] + F[i * 3 + 1] * Sm[1 * 3 + j] + F[i * 3 + 2] * Sm[2 * 3 + j]);
+    double Q[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            Q[i * 3 + j] = Pm[i * 3 + 0] * A[0 * 3 + j] + Pm[i * 3 + 1] * A[1 * 3 + j] + Pm[i * 3 + 2] * A[2 * 3 + j];
+    double* out = D.slot_m + (size_t)e * NN * 3;
+    if constexpr (NN == 4) {
+        double f[12];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            f[0 * 3 + i] = -(Q[i * 3 + 0] + Q[i * 3 + 1] + Q[i * 3 + 2]);
+            f[1 * 3 + i] = Q[i * 3 + 0];
+            f[2 * 3 + i] = Q[i * 3 + 1];
+            f[3 * 3 + i] = Q[i * 3 + 2];
+        }
+#pragma unroll
+        for (int k = 0; k < 12; k += 2) reinterpret_cast<double2*>(out)[k / 2] = make_double2(f[k], f[k + 1]);
+    } else {
+        // ---- closed-form hourglass: g_al = (U h_al - (F - I) c_al) / (8 + 8 |A^T c_al|^2)
+        const double k = P.kh * cbrt(V);
+        double W[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) W[q] = 0.0;
+#pragma unroll
+        for (int al = 0; al < 4; ++al) {
+            double atc[3], fc[3];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) atc[j] = A[0 * 3 + j] * cX[al][0] + A[1 * 3 + j] * cX[al][1] + A[2 * 3 + j] * cX[al][2];
+            const double n2 = 8.0 + 8.0 * (atc[0] * atc[0] + atc[1] * atc[1] + atc[2] * atc[2]);
+            // (F - I) c = H A^T c = H atc
+#pragma unroll
+            for (int i = 0; i < 3; ++i) fc[i] = H[i * 3 + 0] * atc[0] + H[i * 3 + 1] * atc[1] + H[i * 3 + 2] * atc[2];
+            const double in2 = 1.0 / n2;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                Uh[al][i] = (Uh[al][i] - fc[i]) * in2;  // g_al, in place
+#pragma unroll
+                for (int j = 0; j < 3; ++j) W[i * 3 + j] += Uh[al][i] * atc[j];  // W A = sum g c^T A
+            }
+        }
+        // Q <- Q - k (sum_al g_al c_al^T) A = Q - k W'  where W' = sum g (A^T c)^T
+#pragma unroll
+        for (int q = 0; q < 9; ++q) Q[q] -= k * W[q];
+#pragma unroll
+        for (int a = 0; a < 8; a += 2) {
+            double f[6];
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const int aa = a + b;
+                    double v = h8s(aa, 0) * Q[i * 3 + 0] + h8s(aa, 1) * Q[i * 3 + 1] + h8s(aa, 2) * Q[i * 3 + 2];
+                    double hg = h8h(0, aa) * Uh[0][i] + h8h(1, aa) * Uh[1][i] + h8h(2, aa) * Uh[2][i] + h8h(3, aa) * Uh[3][i];
+                    f[b * 3 + i] = v + k * hg;
+                }
+            double2* o = reinterpret_cast<double2*>(out + a * 3);
+            o[0] = make_double2(f[0], f[1]);
+            o[1] = make_double2(f[2], f[3]);
+            o[2] = make_double2(f[4], f[5]);
+        }
+    }
+    if (P.diag) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) D.diag_F[(size_t)e * 9 + q] = F[q];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) D.diag_S[(size_t)e * 9 + q] = Sm[q];
+    }
+}
+
+// ------------------------------------------------------------------ K4: mechanical node
+__global__ void __launch_bounds__(256) k_mech_node(const DevParams P, const DevPtrs D, int cur) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.N || D.clock->halted) return;
+    const double4* Rc = cur ? D.rec1 : D.rec0;
+    double4* Rn = cur ? D.rec0 : D.rec1;  // holds u^{n-1}; receives u^{n+1}
+    const int k0 = __ldg(D.csr_off + i), k1 = __ldg(D.csr_off + i + 1);
+    double f0 = 0.0, f1 = 0.0, f2 = 0.0;
+    for (int k = k0; k < k1; ++k) {
+        const double* s = D.slot_m + (size_t)__ldg(D.csr_slot + k) * 3;
+        f0 += __ldg(s);
+        f1 += __ldg(s + 1);
+        f2 += __ldg(s + 2);
+    }
+    const double4 u = Rc[i];
+    const double4 up = Rn[i];
+    const double m = __ldg(D.mass + i);
+    const double Dm = P.gamma * m;
+    const double a = Dm / (2.0 * P.dt), b = m / (P.dt * P.dt);
+    double R0 = 0.0, R1 = 0.0, R2 = 0.0;
+    if (P.has_R) {
+        R0 = __ldg(D.R + 3 * (size_t)i);
+        R1 = __ldg(D.R + 3 * (size_t)i + 1);
+        R2 = __ldg(D.R + 3 * (size_t)i + 2);
+    }
+    double x = (R0 - f0 + 2.0 * b * u.x + (a - b) * up.x) / (a + b);
+    double y = (R1 - f1 + 2.0 * b * u.y + (a - b) * up.y) / (a + b);
+    double z = (R2 - f2 + 2.0 * b * u.z + (a - b) * up.z) / (a + b);
+    const uint8_t msk = __ldg(D.mask + i);
+    if (msk & (BC_FIXED | BC_PX | BC_PY | BC_PZ)) {
+        if (msk & BC_FIXED) x = y = z = 0.0;
+        if (msk & (BC_PX | BC_PY | BC_PZ)) {
+            const double tn = D.clock->time + P.dt;  // value_at(t + dt), mechanics.hpp:89
+            const int row = __ldg(D.bc_index + i);
+            auto value_at = [&](int q) {
+                const int id = __ldg(D.bc_presc + 3 * row + q);
+                const double tg = D.presc_target[id], rt = D.presc_ramp[id];
+                return rt <= 0.0 ? tg : tg * fmin(tn / rt, 1.0);
+            };
+            if (msk & BC_PX) x = value_at(0);
+            if (msk & BC_PY) y = value_at(1);
+            if (msk & BC_PZ) z = value_at(2);
+        }
+    }
+    if (!(isfinite(x) && isfinite(y) && isfinite(z))) atomicMin(D.err_inst, pack_inst(D.clock->step, 1, D.node_orig[i]));
+    Rn[i] = make_double4(x, y, z, u.w);
+    if (P.diag) {
+        D.diag_f[3 * (size_t)i] = f0;
+        D.diag_f[3 * (size_t)i + 1] = f1;
+        D.diag_f[3 * (size_t)i + 2] = f2;
+    }
+}
+
+// ------------------------------------------------------------------ K5: end of step
+__global__ void k_finish_step(Clock* clock, const unsigned long long* err_inst, const unsigned long long* err_elem,
+                              double dt) {
+    if (threadIdx.x != 0 || clock->halted) return;
+    const unsigned long long s = (unsigned long long)clock->step;
+    const bool bad = (*err_elem != ~0ULL && (*err_elem >> 32) == s) || (*err_inst != ~0ULL && (*err_inst >> 33) == s);
+    if (bad) {
+        clock->halted = 1;  // the reference throws before advancing time/step (engine.hpp:89-90)
+        return;
+    }
+    clock->time += dt;
+    clock->step += 1;
+}
+
+// ------------------------------------------------------------------ halo pack (nranks > 1)
+__global__ void k_pack(const double* __restrict__ slots, const int32_t* __restrict__ idx, int n, int width,
+                       double* __restrict__ out, const Clock* clock) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int s = idx[k];
+    for (int c = 0; c < width; ++c) out[(size_t)k * width + c] = slots[(size_t)s * width + c];
+}
+
+}  // namespace tvegpu

@@ -1,0 +1,441 @@
+// plan.cpp — host setup for the device path (see plan.hpp).
+#include "plan.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <numeric>
+
+namespace tvegpu {
+
+const int kH8Sign[8][3] = {{-1, -1, -1}, {1, -1, -1}, {1, 1, -1}, {-1, 1, -1},
+                           {-1, -1, 1},  {1, -1, 1},  {1, 1, 1},  {-1, 1, 1}};
+const int kT4Xi[4][3] = {{-1, -1, -1}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+const int kHg[4][8] = {{1, 1, -1, -1, -1, -1, 1, 1},
+                       {1, -1, -1, 1, -1, 1, 1, -1},
+                       {1, -1, 1, -1, 1, -1, 1, -1},
+                       {-1, 1, -1, 1, 1, -1, 1, -1}};
+
+namespace {
+
+[[noreturn]] void invalid(const std::string& m) { throw Error(TVEGPU_E_VALIDATION, m); }
+
+double det3(const double m[3][3]) {
+    return m[0][0] * (m[1][1] * m[2][2] - m[1][2] * m[2][1]) - m[0][1] * (m[1][0] * m[2][2] - m[1][2] * m[2][0]) +
+           m[0][2] * (m[1][0] * m[2][1] - m[1][1] * m[2][0]);
+}
+
+// inverse-transpose via the adjugate: (J^-1)^T = cof(J) / det J
+void inv_transpose(const double J[3][3], double d, double out[3][3]) {
+    out[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) / d;
+    out[0][1] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) / d;
+    out[0][2] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) / d;
+    out[1][0] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / d;
+    out[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / d;
+    out[1][2] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / d;
+    out[2][0] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / d;
+    out[2][1] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / d;
+    out[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / d;
+}
+
+double sym_max_eig(const double* t) {
+    double a[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) a[i][j] = 0.5 * (t[i * 3 + j] + t[j * 3 + i]);
+    // closed-form eigenvalues of a symmetric 3x3 (trigonometric method)
+    const double p1 = a[0][1] * a[0][1] + a[0][2] * a[0][2] + a[1][2] * a[1][2];
+    if (p1 == 0) return std::max(a[0][0], std::max(a[1][1], a[2][2]));
+    const double q = (a[0][0] + a[1][1] + a[2][2]) / 3;
+    const double p2 = (a[0][0] - q) * (a[0][0] - q) + (a[1][1] - q) * (a[1][1] - q) + (a[2][2] - q) * (a[2][2] - q) +
+                      2 * p1;
+    const double p = std::sqrt(p2 / 6);
+    double B[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) B[i][j] = (a[i][j] - (i == j ? q : 0)) / p;
+    double r = det3(B) / 2;
+    r = std::max(-1.0, std::min(1.0, r));
+    const double phi = std::acos(r) / 3;
+    return q + 2 * p * std::cos(phi);
+}
+
+uint64_t spread21(uint64_t v) {
+    v &= 0x1fffff;
+    v = (v | (v << 32)) & 0x1f00000000ffffULL;
+    v = (v | (v << 16)) & 0x1f0000ff0000ffULL;
+    v = (v | (v << 8)) & 0x100f00f00f00f00fULL;
+    v = (v | (v << 4)) & 0x10c30c30c30c30c3ULL;
+    v = (v | (v << 2)) & 0x1249249249249249ULL;
+    return v;
+}
+
+}  // namespace
+
+uint64_t morton_key(const double* c, const double* lo, const double* hi) {
+    uint64_t q[3];
+    for (int k = 0; k < 3; ++k) {
+        const double ext = hi[k] - lo[k];
+        const double s = ext > 0 ? 2097151.0 / ext : 0.0;
+        double v = std::floor((c[k] - lo[k]) * s);
+        v = std::min(2097151.0, std::max(0.0, v));
+        q[k] = (uint64_t)v;
+    }
+    return spread21(q[0]) | (spread21(q[1]) << 1) | (spread21(q[2]) << 2);
+}
+
+void validate_problem(const tvegpu_problem& p) {
+    if (p.kind != TVEGPU_T4 && p.kind != TVEGPU_H8) invalid("unknown element kind");
+    if (p.num_nodes <= 0 || p.num_elements <= 0 || !p.nodes || !p.elements) invalid("empty mesh");
+    const int nn = p.kind == TVEGPU_T4 ? 4 : 8;
+    for (int64_t k = 0; k < (int64_t)p.num_elements * nn; ++k) {
+        const int v = p.elements[k];
+        if (v < 0 || v >= p.num_nodes)
+            invalid("element " + std::to_string(k / nn + 1) + " references out-of-range node " + std::to_string(v + 1));
+    }
+    if (!(p.mu > 0) || !(p.kappa > 0) || p.eta_a < 0) invalid("hyperelastic parameters need mu > 0, kappa > 0, eta_a >= 0");
+    double sphi = 0;
+    for (int i = 0; i < p.prony_count; ++i) {
+        if (!(p.prony_phi[i] > 0) || !(p.prony_tau[i] > 0)) invalid("Prony terms need phi > 0 and tau > 0");
+        sphi += p.prony_phi[i];
+    }
+    if (p.prony_count > 0 && !(sphi < 1.0)) invalid("Prony weights must sum to < 1");
+    if (p.prony_count > 4) invalid("at most 4 Prony terms are supported on the device");
+    if (!(p.density > 0)) invalid("density must be > 0");
+    if (p.c_table_len < 1 || p.c_table_len > 16 || p.k_table_len < 1 || p.k_table_len > 16)
+        invalid("property tables need 1..16 entries");
+    for (int i = 0; i < p.c_table_len; ++i)
+        if (!(p.c_table_value[i] > 0)) invalid("specific heat must be > 0");
+    for (int i = 1; i < p.c_table_len; ++i)
+        if (!(p.c_table_T[i] > p.c_table_T[i - 1])) invalid("specific heat table must be sorted by T");
+    for (int i = 1; i < p.k_table_len; ++i)
+        if (!(p.k_table_T[i] > p.k_table_T[i - 1])) invalid("conductivity table must be sorted by T");
+    if (!(p.dt > 0)) invalid("dt must be > 0");
+    if (p.mode < 0 || p.mode > 2) invalid("unknown coupling mode");
+    if (p.eta_a > 0 && !p.has_fiber && !p.fiber_dirs) invalid("eta_a > 0 requires a fiber direction");
+    auto unit = [](const double* v) { return std::fabs(v[0] * v[0] + v[1] * v[1] + v[2] * v[2] - 1.0) <= 1e-6; };
+    if (p.has_expansion) {
+        if (p.expansion_kind < 0 || p.expansion_kind > 2) invalid("unknown expansion kind");
+        auto check_axes = [&](const double* m, const double* n) {
+            if (p.expansion_kind >= TVEGPU_EXP_TRANSVERSELY_ISOTROPIC && !unit(m)) invalid("expansion axis m not unit");
+            if (p.expansion_kind == TVEGPU_EXP_ORTHOTROPIC &&
+                (!unit(n) || std::fabs(m[0] * n[0] + m[1] * n[1] + m[2] * n[2]) > 1e-6))
+                invalid("expansion axes not orthonormal");
+        };
+        if (p.expansion_axes)
+            for (int e = 0; e < p.num_elements; ++e) check_axes(p.expansion_axes + 6 * (size_t)e, p.expansion_axes + 6 * (size_t)e + 3);
+        else
+            check_axes(p.axis_m, p.axis_n);
+    }
+    for (int i = 0; i < p.num_prescribed; ++i) {
+        const auto& q = p.prescribed[i];
+        if (q.component < 0 || q.component > 2) invalid("prescribed component must be 0..2");
+        for (int k = 0; k < q.num_nodes; ++k)
+            if (q.nodes[k] < 0 || q.nodes[k] >= p.num_nodes) invalid("prescribed node out of range");
+    }
+    for (int i = 0; i < p.num_fixed_nodes; ++i)
+        if (p.fixed_nodes[i] < 0 || p.fixed_nodes[i] >= p.num_nodes) invalid("fixed node out of range");
+    for (int i = 0; i < p.num_fixed_temperatures; ++i)
+        if (p.fixed_temperature_nodes[i] < 0 || p.fixed_temperature_nodes[i] >= p.num_nodes)
+            invalid("fixed-temperature node out of range");
+    for (int i = 0; i < p.num_sources; ++i)
+        for (int k = 0; k < p.sources[i].num_elements; ++k)
+            if (p.sources[i].elements[k] < 0 || p.sources[i].elements[k] >= p.num_elements)
+                invalid("source element out of range");
+}
+
+GlobalMesh build_global(const tvegpu_problem& p) {
+    validate_problem(p);
+    GlobalMesh g;
+    g.kind = p.kind;
+    g.nn = p.kind == TVEGPU_T4 ? 4 : 8;
+    g.N = p.num_nodes;
+    g.E = p.num_elements;
+    const int nn = g.nn, E = g.E, N = g.N;
+    g.A.resize((size_t)9 * E);
+    g.vol.resize(E);
+    g.centroid.resize((size_t)3 * E);
+    for (int k = 0; k < 3; ++k) {
+        g.lo[k] = std::numeric_limits<double>::infinity();
+        g.hi[k] = -std::numeric_limits<double>::infinity();
+    }
+    int bad = -1;
+#pragma omp parallel for schedule(static) reduction(max : bad)
+    for (int e = 0; e < E; ++e) {
+        const int32_t* el = p.elements + (size_t)e * nn;
+        double J[3][3];
+        if (nn == 4) {
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) J[i][j] = p.nodes[3 * (size_t)el[j + 1] + i] - p.nodes[3 * (size_t)el[0] + i];
+        } else {
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) {
+                    double s = 0;
+                    for (int a = 0; a < 8; ++a) s += p.nodes[3 * (size_t)el[a] + i] * kH8Sign[a][j];
+                    J[i][j] = s / 8.0;
+                }
+        }
+        const double d = det3(J);
+        const double V = nn == 4 ? d / 6.0 : 8.0 * d;
+        if (!(V > 0)) {
+            bad = std::max(bad, E - e);  // keep the LOWEST failing element
+            continue;
+        }
+        double Ai[3][3];
+        inv_transpose(J, d, Ai);
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) g.A[(size_t)9 * e + i * 3 + j] = nn == 4 ? Ai[i][j] : Ai[i][j] / 8.0;
+        g.vol[e] = V;
+        for (int k = 0; k < 3; ++k) {
+            double s = 0;
+            for (int a = 0; a < nn; ++a) s += p.nodes[3 * (size_t)el[a] + k];
+            g.centroid[(size_t)3 * e + k] = s / nn;
+        }
+    }
+    if (bad >= 0) invalid("degenerate or inverted element " + std::to_string(E - bad + 1));
+    for (int e = 0; e < E; ++e)
+        for (int k = 0; k < 3; ++k) {
+            g.lo[k] = std::min(g.lo[k], g.centroid[(size_t)3 * e + k]);
+            g.hi[k] = std::max(g.hi[k], g.centroid[(size_t)3 * e + k]);
+        }
+    // canonical adjacency over original ids
+    g.adj_off.assign(N + 1, 0);
+    for (int64_t k = 0; k < (int64_t)E * nn; ++k) g.adj_off[p.elements[k] + 1]++;
+    for (int i = 0; i < N; ++i) g.adj_off[i + 1] += g.adj_off[i];
+    g.adj_elem.resize((size_t)E * nn);
+    g.adj_local.resize((size_t)E * nn);
+    {
+        std::vector<int32_t> fill(g.adj_off.begin(), g.adj_off.end() - 1);
+        for (int e = 0; e < E; ++e)
+            for (int a = 0; a < nn; ++a) {
+                const int i = p.elements[(size_t)e * nn + a];
+                g.adj_elem[fill[i]] = e;
+                g.adj_local[fill[i]] = a;
+                fill[i]++;
+            }
+    }
+    g.mass.assign(N, 0.0);
+    g.vnode.assign(N, 0.0);
+    int orphan = -1;
+#pragma omp parallel for schedule(static) reduction(max : orphan)
+    for (int i = 0; i < N; ++i) {
+        if (g.adj_off[i] == g.adj_off[i + 1]) orphan = std::max(orphan, N - i);
+        double m = 0, v = 0;
+        for (int k = g.adj_off[i]; k < g.adj_off[i + 1]; ++k) {
+            const double V = g.vol[g.adj_elem[k]];
+            m += p.density * V / nn;
+            v += V / nn;
+        }
+        g.mass[i] = m;
+        g.vnode[i] = v;
+    }
+    if (orphan >= 0) invalid("node " + std::to_string(N - orphan) + " is not attached to any element (zero lumped mass)");
+    return g;
+}
+
+// ---------------------------------------------------------------- RCB
+static void rcb_rec(const GlobalMesh& g, std::vector<int32_t>& ids, size_t b, size_t e, int parts, int first,
+                    std::vector<int32_t>& owner) {
+    if (parts == 1) {
+        for (size_t k = b; k < e; ++k) owner[ids[k]] = first;
+        return;
+    }
+    double lo[3], hi[3];
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = std::numeric_limits<double>::infinity();
+        hi[k] = -lo[k];
+    }
+    for (size_t k = b; k < e; ++k)
+        for (int c = 0; c < 3; ++c) {
+            lo[c] = std::min(lo[c], g.centroid[(size_t)3 * ids[k] + c]);
+            hi[c] = std::max(hi[c], g.centroid[(size_t)3 * ids[k] + c]);
+        }
+    int ax = 0;
+    for (int c = 1; c < 3; ++c)
+        if (hi[c] - lo[c] > hi[ax] - lo[ax]) ax = c;
+    const int left_parts = parts / 2;
+    const size_t n = e - b;
+    const size_t nl = (size_t)((n * (uint64_t)left_parts) / parts);
+    auto less = [&](int32_t x, int32_t y) {
+        const double cx = g.centroid[(size_t)3 * x + ax], cy = g.centroid[(size_t)3 * y + ax];
+        return cx < cy || (cx == cy && x < y);
+    };
+    std::nth_element(ids.begin() + b, ids.begin() + b + nl, ids.begin() + e, less);
+    std::sort(ids.begin() + b, ids.begin() + b + nl);
+    std::sort(ids.begin() + b + nl, ids.begin() + e);
+    rcb_rec(g, ids, b, b + nl, left_parts, first, owner);
+    rcb_rec(g, ids, b + nl, e, parts - left_parts, first + left_parts, owner);
+}
+
+std::vector<int32_t> rcb_partition(const GlobalMesh& g, int nranks) {
+    std::vector<int32_t> owner(g.E, 0);
+    if (nranks <= 1) return owner;
+    std::vector<int32_t> ids(g.E);
+    std::iota(ids.begin(), ids.end(), 0);
+    rcb_rec(g, ids, 0, ids.size(), nranks, 0, owner);
+    return owner;
+}
+
+// ---------------------------------------------------------------- rank plan
+RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nranks, int rank, int reorder) {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(TVEGPU_E_ARG, "bad rank / nranks");
+    if (nranks > 1 && !reorder) throw Error(TVEGPU_E_ARG, "reorder = 0 needs nranks = 1");
+    RankPlan r;
+    r.nranks = nranks;
+    r.rank = rank;
+    r.nn = g.nn;
+    const int nn = g.nn, N = g.N, E = g.E;
+    r.owner = rcb_partition(g, nranks);
+    // sharers of each node: bitmask of ranks touching it (nranks <= 64)
+    if (nranks > 64) throw Error(TVEGPU_E_ARG, "at most 64 ranks");
+    std::vector<uint64_t> touch(N, 0);
+    for (int e = 0; e < E; ++e)
+        for (int a = 0; a < nn; ++a) touch[p.elements[(size_t)e * nn + a]] |= 1ULL << r.owner[e];
+    const uint64_t me = 1ULL << rank;
+    // owned elements, split into boundary (touches a shared node) and interior
+    std::vector<int32_t> bnd, inr;
+    for (int e = 0; e < E; ++e) {
+        if (r.owner[e] != rank) continue;
+        bool b = false;
+        for (int a = 0; a < nn && !b; ++a) b = (touch[p.elements[(size_t)e * nn + a]] & ~me) != 0;
+        (b ? bnd : inr).push_back(e);
+    }
+    if (reorder) {
+        std::vector<uint64_t> key(E);
+        auto sort_group = [&](std::vector<int32_t>& v) {
+            for (int32_t e : v) key[e] = morton_key(&g.centroid[(size_t)3 * e], g.lo, g.hi);
+            std::sort(v.begin(), v.end(), [&](int32_t x, int32_t y) { return key[x] < key[y] || (key[x] == key[y] && x < y); });
+        };
+        sort_group(bnd);
+        sort_group(inr);
+    }
+    r.Eb = (int)bnd.size();
+    r.elem_orig = bnd;
+    r.elem_orig.insert(r.elem_orig.end(), inr.begin(), inr.end());
+    r.E = (int)r.elem_orig.size();
+    // first-touch node numbering (identity when reorder = 0, nranks = 1)
+    std::vector<int32_t> local(N, -1);
+    if (reorder) {
+        for (int le = 0; le < r.E; ++le)
+            for (int a = 0; a < nn; ++a) {
+                const int i = p.elements[(size_t)r.elem_orig[le] * nn + a];
+                if (local[i] < 0) {
+                    local[i] = (int)r.node_orig.size();
+                    r.node_orig.push_back(i);
+                }
+            }
+    } else {
+        r.node_orig.resize(N);
+        std::iota(r.node_orig.begin(), r.node_orig.end(), 0);
+        std::iota(local.begin(), local.end(), 0);
+    }
+    r.N = (int)r.node_orig.size();
+    r.conn.resize((size_t)r.E * nn);
+    std::vector<int32_t> elem_local(E, -1);
+    for (int le = 0; le < r.E; ++le) {
+        elem_local[r.elem_orig[le]] = le;
+        for (int a = 0; a < nn; ++a) r.conn[(size_t)le * nn + a] = local[p.elements[(size_t)r.elem_orig[le] * nn + a]];
+    }
+    // neighbours and halo lists: for each neighbour s, the (orig e, a) contributions of
+    // elements owned by the SENDER to nodes shared with the receiver, canonical order.
+    std::vector<std::vector<int32_t>> send(nranks), recv_keys(nranks);  // recv: global adjacency index k
+    for (int i = 0; i < N; ++i) {
+        const uint64_t t = touch[i];
+        if (!(t & me) || (t & (t - 1)) == 0) continue;  // not local or not shared
+        for (int k = g.adj_off[i]; k < g.adj_off[i + 1]; ++k) {
+            const int e = g.adj_elem[k], a = g.adj_local[k];
+            const int o = r.owner[e];
+            if (o == rank) {
+                for (int s = 0; s < nranks; ++s)
+                    if (s != rank && (t >> s & 1)) send[s].push_back(elem_local[e] * nn + a);
+            } else {
+                recv_keys[o].push_back(k);
+            }
+        }
+    }
+    // send lists must be in canonical (orig e, a) order per neighbour: sort by (orig e, a)
+    for (int s = 0; s < nranks; ++s) {
+        auto& v = send[s];
+        std::sort(v.begin(), v.end(), [&](int32_t x, int32_t y) {
+            const int ex = r.elem_orig[x / nn], ey = r.elem_orig[y / nn];
+            return ex < ey || (ex == ey && x % nn < y % nn);
+        });
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+        auto& w = recv_keys[s];
+        std::sort(w.begin(), w.end(), [&](int32_t x, int32_t y) {
+            return g.adj_elem[x] < g.adj_elem[y] || (g.adj_elem[x] == g.adj_elem[y] && g.adj_local[x] < g.adj_local[y]);
+        });
+        w.erase(std::unique(w.begin(), w.end(), [&](int32_t x, int32_t y) {
+                    return g.adj_elem[x] == g.adj_elem[y] && g.adj_local[x] == g.adj_local[y];
+                }), w.end());
+    }
+    r.send_off.push_back(0);
+    r.recv_off.push_back(0);
+    // receive index of global adjacency entry k (only for remote contributions)
+    std::vector<std::pair<int64_t, int32_t>> recv_index;  // key = e*nn + a -> receive slot
+    for (int s = 0; s < nranks; ++s) {
+        if (s == rank || (send[s].empty() && recv_keys[s].empty())) continue;
+        r.neighbors.push_back(s);
+        r.send_slot.insert(r.send_slot.end(), send[s].begin(), send[s].end());
+        r.send_off.push_back((int32_t)r.send_slot.size());
+        for (size_t q = 0; q < recv_keys[s].size(); ++q) {
+            const int32_t k = recv_keys[s][q];
+            recv_index.push_back({(int64_t)g.adj_elem[k] * nn + g.adj_local[k], r.recv_off.back() + (int32_t)q});
+        }
+        r.recv_off.push_back(r.recv_off.back() + (int32_t)recv_keys[s].size());
+    }
+    std::sort(recv_index.begin(), recv_index.end());
+    // CSR per local node in canonical order: local slots and receive slots interleaved
+    r.csr_off.assign(r.N + 1, 0);
+    for (int li = 0; li < r.N; ++li) {
+        const int i = r.node_orig[li];
+        r.csr_off[li + 1] = r.csr_off[li] + (g.adj_off[i + 1] - g.adj_off[i]);
+    }
+    r.csr_slot.resize(r.csr_off[r.N]);
+    const int32_t base = r.E * nn;
+    for (int li = 0; li < r.N; ++li) {
+        const int i = r.node_orig[li];
+        int32_t pos = r.csr_off[li];
+        for (int k = g.adj_off[i]; k < g.adj_off[i + 1]; ++k) {
+            const int e = g.adj_elem[k], a = g.adj_local[k];
+            if (r.owner[e] == rank) {
+                r.csr_slot[pos++] = elem_local[e] * nn + a;
+            } else {
+                const int64_t key = (int64_t)e * nn + a;
+                auto it = std::lower_bound(recv_index.begin(), recv_index.end(), std::make_pair(key, (int32_t)-1));
+                if (it == recv_index.end() || it->first != key) throw Error(TVEGPU_E_ARG, "internal: halo map");
+                r.csr_slot[pos++] = base + it->second;
+            }
+        }
+    }
+    return r;
+}
+
+void critical_timestep(const tvegpu_problem& p, double* thermal, double* mechanical) {
+    static const int t4e[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+    static const int h8e[12][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 0}, {4, 5}, {5, 6},
+                                   {6, 7}, {7, 4}, {0, 4}, {1, 5}, {2, 6}, {3, 7}};
+    const bool t4 = p.kind == TVEGPU_T4;
+    const int nn = t4 ? 4 : 8, ne = t4 ? 6 : 12;
+    double L = std::numeric_limits<double>::infinity();
+#pragma omp parallel for schedule(static) reduction(min : L)
+    for (int e = 0; e < p.num_elements; ++e) {
+        const int32_t* el = p.elements + (size_t)e * nn;
+        for (int k = 0; k < ne; ++k) {
+            const int a = t4 ? t4e[k][0] : h8e[k][0], b = t4 ? t4e[k][1] : h8e[k][1];
+            double d2 = 0;
+            for (int i = 0; i < 3; ++i) {
+                const double d = p.nodes[3 * (size_t)el[a] + i] - p.nodes[3 * (size_t)el[b] + i];
+                d2 += d * d;
+            }
+            L = std::min(L, std::sqrt(d2));
+        }
+    }
+    const double cd = std::sqrt((p.kappa + 4.0 * p.mu / 3.0) / p.density);
+    double cmin = std::numeric_limits<double>::infinity(), kmax = -std::numeric_limits<double>::infinity();
+    for (int i = 0; i < p.c_table_len; ++i) cmin = std::min(cmin, p.c_table_value[i]);
+    for (int i = 0; i < p.k_table_len; ++i) kmax = std::max(kmax, sym_max_eig(p.k_table_tensor + 9 * (size_t)i));
+    *mechanical = 0.9 * L / cd;
+    *thermal = 0.9 * (p.density * cmin * L * L) / (2.0 * kmax * 3.0);
+}
+
+}  // namespace tvegpu

@@ -1,0 +1,77 @@
+// plan.hpp — host-side setup for the B200 TLED step: validation, the
+// compressed precompute, element/node reordering, the deterministic gather CSR
+// and (for nranks > 1) the RCB partition with its halo lists.
+//
+// Replaces the reference's precompute() (mesh.hpp:81-83) for the device path.
+// Unlike the reference layout (3 x nn gradients per element, stored 4 x 8
+// hourglass basis), the device keeps only A_e (G_e = A_e Xi, 9 doubles) and V_e
+// per element; per-node sums (lumped mass, volume) are
+// accumulated once on the GLOBAL mesh in canonical adjacency order (ascending
+// original element, then local index; mesh.hpp:58-61) so every partition sees
+// bit-identical node constants.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tvegpu.h"
+
+namespace tvegpu {
+
+struct Error : std::runtime_error {
+    Error(tvegpu_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+    tvegpu_status status;
+};
+
+// Reference corner signs (H8 brick order) and T4 reference gradients.
+extern const int kH8Sign[8][3];
+extern const int kT4Xi[4][3];
+extern const int kHg[4][8];
+
+struct GlobalMesh {
+    int kind = TVEGPU_T4, nn = 4, N = 0, E = 0;
+    std::vector<double> A;         // 9 per element (row-major), G_e = A_e Xi
+    std::vector<double> vol;       // per element (T4: V; H8: 8 det J0)
+    std::vector<double> centroid;  // 3 per element
+    std::vector<double> mass;      // per node: sum rho V_e / nn (canonical order)
+    std::vector<double> vnode;     // per node: sum V_e / nn (canonical order)
+    std::vector<int32_t> adj_off;  // node -> (element, local): canonical CSR over original ids
+    std::vector<int32_t> adj_elem, adj_local;
+    double lo[3], hi[3];           // bounding box of element centroids
+};
+
+// Validates the problem (the reference's ValidationError cases) and builds the
+// global compressed precompute.  Throws Error.
+void validate_problem(const tvegpu_problem& p);
+GlobalMesh build_global(const tvegpu_problem& p);
+
+// Morton key of a centroid: 21-bit quantisation per axis over [lo, hi].
+uint64_t morton_key(const double* c, const double* lo, const double* hi);
+
+// Deterministic recursive coordinate bisection of element centroids into nranks parts.
+std::vector<int32_t> rcb_partition(const GlobalMesh& g, int nranks);
+
+struct RankPlan {
+    int nranks = 1, rank = 0, nn = 4;
+    int E = 0, Eb = 0, N = 0;
+    std::vector<int32_t> elem_orig;   // local -> original element
+    std::vector<int32_t> node_orig;   // local -> original node
+    std::vector<int32_t> conn;        // nn * E, element-major, local node ids
+    std::vector<int32_t> csr_off;     // N + 1
+    std::vector<int32_t> csr_slot;    // local slot (e*nn + a) or nn*E + receive index
+    std::vector<int32_t> neighbors;
+    std::vector<int32_t> send_off, send_slot, recv_off;
+    std::vector<int32_t> owner;       // global element -> rank
+};
+
+// Builds one rank's plan.  reorder = 0 keeps the original element and node order
+// (single rank only); otherwise Morton element order (boundary elements first)
+// and first-touch node order.
+RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nranks, int rank, int reorder);
+
+// Critical timestep (mesh.hpp:92-97).
+void critical_timestep(const tvegpu_problem& p, double* thermal, double* mechanical);
+
+}  // namespace tvegpu

@@ -1,0 +1,329 @@
+"""Python mirror of the reference's ``tve::Engine`` over the C ABI (include/tvegpu.h).
+
+Same names, argument meaning and error behaviour as engine.hpp:83-143:
+``Engine(problem)`` ~ ``Engine(mesh, pre, material, mech_bcs, thermal_bcs,
+sources, config)``; ``step()`` raises :class:`InstabilityError` carrying
+``step`` and ``node`` (errors.hpp:21-27); ``state()`` returns T, u, u_prev and
+the viscous history in original numbering.  Every call goes through
+``libtvegpu.so`` (hand-written sm_100a kernels); there is no CPU fallback — a
+missing library or device raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+from .problem import Problem
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIBPATH = os.path.join(_HERE, "lib", "libtvegpu.so")
+_LIB = None
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int32)
+
+
+# errors.hpp:8-33
+class TveError(RuntimeError):
+    status = 7
+
+
+class ParseError(TveError):
+    status = 1
+
+
+class ValidationError(TveError):
+    status = 2
+
+    def __init__(self, msg, step=-1, element=-1):
+        super().__init__(msg)
+        self.step, self.element = step, element
+
+
+class InstabilityError(TveError):
+    status = 3
+
+    def __init__(self, msg, step=-1, node=-1):
+        super().__init__(msg)
+        self.step, self.node = step, node
+
+
+class IoError(TveError):
+    status = 4
+
+
+class CudaError(TveError):
+    status = 5
+
+
+class NcclError(TveError):
+    status = 6
+
+
+_BY_STATUS = {1: ParseError, 2: ValidationError, 3: InstabilityError, 4: IoError, 5: CudaError, 6: NcclError}
+
+
+class COptions(C.Structure):
+    _fields_ = [("device", C.c_int32), ("nranks", C.c_int32), ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p),
+                ("reorder", C.c_int32), ("diagnostics", C.c_int32), ("steps_per_graph", C.c_int32)]
+
+
+class CPlanView(C.Structure):
+    _fields_ = [("nranks", C.c_int32), ("rank", C.c_int32), ("nn", C.c_int32), ("num_elements", C.c_int32),
+                ("num_boundary_elements", C.c_int32), ("num_nodes", C.c_int32), ("element_orig", _ip),
+                ("node_orig", _ip), ("conn", _ip), ("csr_offsets", _ip), ("csr_slots", _ip),
+                ("num_neighbors", C.c_int32), ("neighbor_ranks", _ip), ("send_offsets", _ip), ("send_slots", _ip),
+                ("recv_offsets", _ip), ("element_owner", _ip), ("num_elements_global", C.c_int32)]
+
+
+EXPORTS = {
+    "tvegpu_abi_version": (C.c_int32, []),
+    "tvegpu_status_string": (C.c_char_p, [C.c_int]),
+    "tvegpu_create_error": (C.c_char_p, []),
+    "tvegpu_default_options": (None, [C.c_void_p]),
+    "tvegpu_create": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "tvegpu_destroy": (None, [C.c_void_p]),
+    "tvegpu_step": (C.c_int, [C.c_void_p, C.c_int64]),
+    "tvegpu_get_temperatures": (C.c_int, [C.c_void_p, _dp]),
+    "tvegpu_get_displacements": (C.c_int, [C.c_void_p, _dp, _dp]),
+    "tvegpu_get_viscous": (C.c_int, [C.c_void_p, _dp]),
+    "tvegpu_make_snapshot": (C.c_int, [C.c_void_p, _dp, _dp]),
+    "tvegpu_time": (C.c_double, [C.c_void_p]),
+    "tvegpu_step_count": (C.c_int64, [C.c_void_p]),
+    "tvegpu_set_state": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp, C.c_double, C.c_int64]),
+    "tvegpu_set_nodal_sources": (C.c_int, [C.c_void_p, _dp]),
+    "tvegpu_get_diagnostics": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
+    "tvegpu_last_error": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_int64),
+                                    C.POINTER(C.c_int32)]),
+    "tvegpu_critical_timestep": (C.c_int, [C.c_void_p, _dp, _dp]),
+    "tvegpu_plan_create": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "tvegpu_plan_get": (C.c_int, [C.c_void_p, C.POINTER(CPlanView)]),
+    "tvegpu_plan_destroy": (None, [C.c_void_p]),
+    "tvegpu_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "tvegpu_stream": (C.c_void_p, [C.c_void_p]),
+    "tvegpu_kernels_per_step": (C.c_int32, [C.c_void_p]),
+    "tvegpu_enqueue_steps": (C.c_int, [C.c_void_p, C.c_int64]),
+    "tvegpu_sync": (C.c_int, [C.c_void_p]),
+    "tvegpu_profile_kernels": (C.c_int, [C.c_void_p, C.c_int32, _dp, C.POINTER(C.c_int32), C.c_char_p,
+                                         C.c_size_t]),
+}
+
+
+def build(force=False):
+    """Compile csrc/ for sm_100a into lib/libtvegpu.so (nvcc cross-compiles without a GPU)."""
+    cmd = ["make", "-s", "-C", os.path.join(_HERE, "csrc")]
+    if force:
+        subprocess.run(cmd + ["clean"], check=True)
+    subprocess.run(cmd, check=True)
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(_LIBPATH):
+            raise CudaError(f"{_LIBPATH} missing: run paper_2009_10400_b200.build() (no CPU fallback exists)")
+        L = C.CDLL(_LIBPATH)
+        for name, (res, args) in EXPORTS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _LIB = L
+    return _LIB
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _P(a):
+    return None if a is None else a.ctypes.data_as(_dp)
+
+
+def critical_timestep(problem: Problem):
+    """critical_timestep(mesh, material) (mesh.hpp:92-97) -> (thermal, mechanical)."""
+    c, keep = problem.to_c()
+    th, me = C.c_double(), C.c_double()
+    rc = lib().tvegpu_critical_timestep(C.byref(c), C.byref(th), C.byref(me))
+    if rc:
+        raise _BY_STATUS.get(rc, TveError)(lib().tvegpu_create_error().decode())
+    return th.value, me.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    rc = lib().tvegpu_nccl_unique_id(buf)
+    if rc:
+        raise NcclError(lib().tvegpu_create_error().decode())
+    return buf.raw
+
+
+def plan(problem: Problem, nranks=1, rank=0, reorder=True):
+    """The integer maps of one rank's layout (host-only; no GPU needed)."""
+    c, keep = problem.to_c()
+    h = C.c_void_p()
+    rc = lib().tvegpu_plan_create(C.byref(c), nranks, rank, int(reorder), C.byref(h))
+    if rc:
+        raise _BY_STATUS.get(rc, TveError)(lib().tvegpu_create_error().decode())
+    try:
+        v = CPlanView()
+        lib().tvegpu_plan_get(h, C.byref(v))
+
+        def arr(ptr, n):
+            return np.ctypeslib.as_array(ptr, shape=(n,)).copy() if n else np.zeros(0, np.int32)
+
+        E, N, nn, nb = v.num_elements, v.num_nodes, v.nn, v.num_neighbors
+        off = arr(v.csr_offsets, N + 1)
+        send_off = arr(v.send_offsets, nb + 1)
+        recv_off = arr(v.recv_offsets, nb + 1)
+        return dict(nranks=v.nranks, rank=v.rank, nn=nn, num_elements=E, num_boundary_elements=v.num_boundary_elements,
+                    num_nodes=N, element_orig=arr(v.element_orig, E), node_orig=arr(v.node_orig, N),
+                    conn=arr(v.conn, E * nn).reshape(E, nn), csr_offsets=off, csr_slots=arr(v.csr_slots, int(off[-1])),
+                    neighbors=arr(v.neighbor_ranks, nb), send_offsets=send_off,
+                    send_slots=arr(v.send_slots, int(send_off[-1])), recv_offsets=recv_off,
+                    element_owner=arr(v.element_owner, v.num_elements_global))
+    finally:
+        lib().tvegpu_plan_destroy(h)
+
+
+class Engine:
+    """tve::Engine on a B200 (engine.hpp:83-143)."""
+
+    def __init__(self, problem: Problem, *, device: int = -1, nranks: int = 1, rank: int = 0,
+                 nccl_id: bytes | None = None, reorder: bool = True, diagnostics: bool = False,
+                 steps_per_graph: int = 64):
+        L = lib()
+        self.problem = problem
+        self._c, self._keep = problem.to_c()
+        o = COptions()
+        L.tvegpu_default_options(C.byref(o))
+        o.device, o.nranks, o.rank = device, nranks, rank
+        self._id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        o.nccl_unique_id = C.cast(self._id, C.c_void_p) if self._id is not None else None
+        o.reorder, o.diagnostics, o.steps_per_graph = int(reorder), int(diagnostics), steps_per_graph
+        self._opt = o
+        h = C.c_void_p()
+        rc = L.tvegpu_create(C.byref(self._c), C.byref(o), C.byref(h))
+        if rc:
+            raise _BY_STATUS.get(rc, TveError)(L.tvegpu_create_error().decode())
+        self._h = h
+        self.N, self.E, self.P = problem.num_nodes, problem.num_elements, problem.prony_count
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tvegpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _raise(self, rc):
+        msg = C.create_string_buffer(512)
+        st, nd = C.c_int64(-1), C.c_int32(-1)
+        lib().tvegpu_last_error(self._h, msg, 512, C.byref(st), C.byref(nd))
+        text = msg.value.decode()
+        if rc == 3:
+            raise InstabilityError(text, st.value, nd.value)
+        if rc == 2:
+            raise ValidationError(text, st.value, nd.value)
+        raise _BY_STATUS.get(rc, TveError)(text)
+
+    # ---- engine.hpp:89-97
+    def step(self, n: int = 1):
+        rc = lib().tvegpu_step(self._h, n)
+        if rc:
+            self._raise(rc)
+
+    def enqueue(self, n: int):
+        rc = lib().tvegpu_enqueue_steps(self._h, n)
+        if rc:
+            self._raise(rc)
+
+    def sync(self):
+        rc = lib().tvegpu_sync(self._h)
+        if rc:
+            self._raise(rc)
+
+    def time(self) -> float:
+        return lib().tvegpu_time(self._h)
+
+    def step_count(self) -> int:
+        return lib().tvegpu_step_count(self._h)
+
+    def temperatures(self, out=None):
+        T = np.empty(self.N) if out is None else out
+        rc = lib().tvegpu_get_temperatures(self._h, _P(T))
+        if rc:
+            self._raise(rc)
+        return T
+
+    def displacements(self, out=None, out_prev=None):
+        u = np.empty(3 * self.N) if out is None else out
+        rc = lib().tvegpu_get_displacements(self._h, _P(u), _P(out_prev))
+        if rc:
+            self._raise(rc)
+        return u
+
+    def make_snapshot(self, T=None, u=None):
+        """Engine::make_snapshot (engine.hpp:99): T and u in one device read."""
+        T = np.empty(self.N) if T is None else T
+        u = np.empty(3 * self.N) if u is None else u
+        rc = lib().tvegpu_make_snapshot(self._h, _P(T), _P(u))
+        if rc:
+            self._raise(rc)
+        return T, u
+
+    def state(self):
+        T = self.temperatures()
+        u = np.empty(3 * self.N)
+        up = np.empty(3 * self.N)
+        self.displacements(u, up)
+        th = np.empty(9 * self.E * self.P)
+        if th.size:
+            rc = lib().tvegpu_get_viscous(self._h, _P(th))
+            if rc:
+                self._raise(rc)
+        return dict(T=T, u=u, u_prev=up, viscous=th, time=self.time(), step=self.step_count())
+
+    def set_state(self, T=None, u=None, u_prev=None, viscous=None, time=0.0, step=0):
+        arrs = [None if a is None else _f64(a).reshape(-1) for a in (T, u, u_prev, viscous)]
+        rc = lib().tvegpu_set_state(self._h, *(_P(a) for a in arrs), time, step)
+        if rc:
+            self._raise(rc)
+
+    def set_nodal_sources(self, power):
+        self._src = None if power is None else _f64(power)
+        rc = lib().tvegpu_set_nodal_sources(self._h, _P(self._src))
+        if rc:
+            self._raise(rc)
+
+    # ---- engine.hpp:101-105
+    def diagnostics(self):
+        f = np.empty(3 * self.N)
+        F = np.empty(9 * self.E)
+        S = np.empty(9 * self.E)
+        rc = lib().tvegpu_get_diagnostics(self._h, _P(f), _P(F), _P(S))
+        if rc:
+            self._raise(rc)
+        return dict(f_int=f, F=F, S=S)
+
+    # ---- measurement hooks
+    @property
+    def stream(self) -> int:
+        return lib().tvegpu_stream(self._h) or 0
+
+    def kernels_per_step(self) -> int:
+        return lib().tvegpu_kernels_per_step(self._h)
+
+    def profile_kernels(self, nsteps: int):
+        ms = np.zeros(8)
+        cnt = C.c_int32(0)
+        names = C.create_string_buffer(512)
+        rc = lib().tvegpu_profile_kernels(self._h, nsteps, _P(ms), C.byref(cnt), names, 512)
+        if rc:
+            self._raise(rc)
+        return dict(zip(names.value.decode().split(";"), ms[:cnt.value].tolist()))

@@ -1,0 +1,215 @@
+"""GPU parity: the sm_100a engine (through the C ABI) against the CPU oracle.
+
+Tolerance (north_star): fp64 path, after N steps,
+    ||x_gpu - x_cpu||_inf / max(||x_cpu - x0||_inf, 1e-300) <= 1e-10
+for u (x0 = 0) and T (x0 = initial temperature); integer maps bit-exact
+(tests/test_abi_and_maps.py).  Partition / reorder invariance and determinism
+are bit-exact by construction and tested as such.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import paper_2009_10400_b200 as tg
+from oracle import oracle as O
+from paper_2009_10400_b200 import configs
+from paper_2009_10400_b200.problem import (COUPLED, EXP_ISOTROPIC, EXP_ORTHOTROPIC, EXP_TRANSVERSELY_ISOTROPIC, H8,
+                                           MECHANICAL_ONLY, T4, THERMAL_ONLY)
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def inc_err(x, ref, x0):
+    return float(np.abs(x - ref).max() / max(np.abs(ref - x0).max(), 1e-300))
+
+
+def compare(p, steps, tol=TOL, check_viscous=True, **kw):
+    g = tg.Engine(p, **kw)
+    o = O.OracleEngine(p)
+    g.step(steps)
+    o.step(steps)
+    a, b = g.state(), o.state()
+    eT = inc_err(a["T"], b["T"], p.initial_temperature)
+    eu = inc_err(a["u"], b["u"], 0.0)
+    eup = inc_err(a["u_prev"], b["u_prev"], 0.0)
+    assert a["step"] == b["step"] == steps
+    assert a["time"] == b["time"]  # same fp64 accumulation t += dt
+    assert eT <= tol, f"T err {eT:.3e}"
+    assert eu <= tol, f"u err {eu:.3e}"
+    assert eup <= tol, f"u_prev err {eup:.3e}"
+    if check_viscous and p.prony_count:
+        ev = inc_err(a["viscous"], b["viscous"], 0.0)
+        assert ev <= tol, f"viscous err {ev:.3e}"
+    return g, o, dict(T=eT, u=eu)
+
+
+@pytest.mark.parametrize("kind", [T4, H8])
+@pytest.mark.parametrize("variant", ["base", "global_fiber", "no_prony", "prony2", "iso_noTD", "no_expansion"])
+def test_small_coupled(kind, variant):
+    p = configs.small_problem(kind=kind, n=4, steps=60)
+    if variant == "global_fiber":
+        p.fiber_dirs = None
+        p.fiber = (0.6, 0.8, 0.0)
+    elif variant == "no_prony":
+        p.prony_phi, p.prony_tau = [], []
+    elif variant == "prony2":
+        p.prony_phi, p.prony_tau = [0.3, 0.2], [0.58, 0.0058]
+    elif variant == "iso_noTD":
+        p.temperature_dependent = False
+        p.eta_a = 0.0
+        p.fiber_dirs = None
+    elif variant == "no_expansion":
+        p.expansion_enabled = False
+    compare(p, 60)
+
+
+@pytest.mark.parametrize("kind", [T4, H8])
+@pytest.mark.parametrize("exp_kind", [EXP_TRANSVERSELY_ISOTROPIC, EXP_ORTHOTROPIC])
+@pytest.mark.parametrize("per_element_axes", [False, True])
+def test_anisotropic_expansion(kind, exp_kind, per_element_axes):
+    p = configs.small_problem(kind=kind, n=3, steps=40)
+    p.expansion = dict(kind=exp_kind, alpha_i=1e-4, alpha_m=3e-4, alpha_n=-2e-4, reference_temperature=37.0)
+    p.initial_temperature = 45.0
+    if per_element_axes:
+        rng = np.random.default_rng(11)
+        Q = np.linalg.qr(rng.normal(size=(p.num_elements, 3, 3)))[0]
+        p.expansion_axes = np.concatenate([Q[:, :, 0], Q[:, :, 1]], axis=1)
+    else:
+        s = 1 / math.sqrt(2)
+        p.axis_m, p.axis_n = (s, s, 0.0), (-s, s, 0.0)
+    compare(p, 40)
+
+
+@pytest.mark.parametrize("kind", [T4, H8])
+@pytest.mark.parametrize("mode", [THERMAL_ONLY, MECHANICAL_ONLY])
+def test_modes(kind, mode):
+    p = configs.small_problem(kind=kind, n=4, steps=50)
+    p.mode = mode
+    if mode == THERMAL_ONLY:
+        p.initial_temperature = 40.0
+    compare(p, 50)
+
+
+def test_bcs_forces_and_fixed_temperatures():
+    p = configs.small_problem(kind=H8, n=4, steps=40)
+    rng = np.random.default_rng(5)
+    p.external_force = rng.normal(scale=1e-6, size=(p.num_nodes, 3))
+    p.body_force = (0.0, 0.0, -9.81 * p.density)
+    p.fixed_temperatures = [(int(i), 37.0 + 10 * k) for k, i in enumerate(range(0, p.num_nodes, 7))]
+    p.sources[0].t_start, p.sources[0].t_end = 5 * p.dt, 25.5 * p.dt  # window switches mid-run
+    compare(p, 40)
+
+
+def test_cfg1_reference_run():
+    """configs[0]: H8 10^3, central source, 1000 steps — the reference CPU run."""
+    p = configs.cfg1()
+    _, _, err = compare(p, 1000)
+    print("cfg1 increment-relative errors", err)
+
+
+def test_cfg2_t4_anisotropic():
+    p = configs.cfg2(steps=200)
+    compare(p, 200)
+
+
+def test_cfg3_liver():
+    p = configs.cfg3(steps=100)
+    compare(p, 100)
+
+
+@pytest.mark.slow
+def test_cfg4_1m_h8_parity():
+    p = configs.cfg4(steps=20)
+    compare(p, 20)
+
+
+def test_reorder_and_determinism_bit_exact():
+    p = configs.small_problem(kind=H8, n=6, steps=30)
+    a = tg.Engine(p)
+    b = tg.Engine(p, reorder=False)
+    c = tg.Engine(p, steps_per_graph=7)
+    for e in (a, b, c):
+        e.step(30)
+    sa, sb, sc = a.state(), b.state(), c.state()
+    for k in ("T", "u", "u_prev", "viscous"):
+        np.testing.assert_array_equal(sa[k], sb[k], err_msg=k)
+        np.testing.assert_array_equal(sa[k], sc[k], err_msg=k)
+
+
+def test_restart_bit_exact():
+    p = configs.small_problem(kind=T4, n=4, steps=40)
+    a = tg.Engine(p)
+    a.step(40)
+    b = tg.Engine(p)
+    b.step(15)
+    s = b.state()
+    c = tg.Engine(p)
+    c.set_state(s["T"], s["u"], s["u_prev"], s["viscous"], s["time"], s["step"])
+    c.step(25)
+    for k in ("T", "u", "u_prev", "viscous"):
+        np.testing.assert_array_equal(a.state()[k], c.state()[k], err_msg=k)
+    assert a.time() == c.time() and c.step_count() == 40
+
+
+def test_diagnostics_match_oracle():
+    p = configs.small_problem(kind=H8, n=3, steps=10)
+    g = tg.Engine(p, diagnostics=True)
+    o = O.OracleEngine(p)
+    g.step(10)
+    o.step(10)
+    dg, do = g.diagnostics(), o.diagnostics()
+    for k in ("f_int", "F", "S"):
+        scale = np.abs(do[k]).max()
+        assert np.abs(dg[k] - do[k]).max() <= 1e-10 * scale, k
+
+
+def test_nodal_source_override():
+    p = configs.small_problem(kind=T4, n=3, steps=20)
+    q = np.random.default_rng(1).uniform(0, 1e-3, p.num_nodes)
+    g = tg.Engine(p)
+    o = O.OracleEngine(p)
+    g.set_nodal_sources(q)
+    o.set_nodal_sources(q)
+    g.step(20)
+    o.step(20)
+    assert inc_err(g.temperatures(), o.state()["T"], 37.0) <= TOL
+
+
+def test_instability_matches_oracle():
+    p = configs.small_problem(kind=T4, n=2, steps=10)
+    p.mode = THERMAL_ONLY
+    p.dt *= 3e5
+    p.allow_unstable_dt = True
+    g = tg.Engine(p)
+    o = O.OracleEngine(p)
+    with pytest.raises(O.OracleError) as eo:
+        o.step(5000)
+    with pytest.raises(tg.InstabilityError) as eg:
+        g.step(5000)
+    assert (eg.value.step, eg.value.node) == (eo.value.step, eo.value.node)
+    assert g.step_count() == o.step_count() and g.time() == o.time()
+    sg, so = g.temperatures(), o.state()["T"]
+    np.testing.assert_array_equal(np.isfinite(sg), np.isfinite(so))
+
+
+def test_mechanical_blowup_matches_oracle():
+    p = configs.small_problem(kind=T4, n=2, steps=10)
+    p.dt *= 40
+    p.allow_unstable_dt = True
+    g = tg.Engine(p)
+    o = O.OracleEngine(p)
+    with pytest.raises(O.OracleError) as eo:
+        o.step(5000)
+    with pytest.raises(tg.TveError) as eg:
+        g.step(5000)
+    assert eg.value.status == eo.value.status
+    assert eg.value.step == eo.value.step
+
+
+def test_unstable_dt_refused():
+    p = configs.small_problem(kind=H8, n=2)
+    p.dt *= 10
+    with pytest.raises(tg.ValidationError, match="critical"):
+        tg.Engine(p)
