@@ -355,29 +355,49 @@ double strain_energy(const Mat3& C, const HyperelasticParams& p, const Vec3* fib
 // materials.hpp:104-106: S = 2 dPsi/dC (checked against FD in tests).
 // Non-throwing core: a non-SPD (or non-finite) C yields NaN and sets *bad, which
 // the engine turns into a ValidationError after completing the step (C25).
-static Mat3 pk2_core(const Mat3& C, const HyperelasticParams& p, const Vec3* fiber, bool* bad) {
-    const double dC = det(C);
-    if (!(dC > 0)) {
+//
+// Evaluated from the strain X = C - I rather than from C: with soft tissue near
+// its reference state (strains 1e-6..1e-2) every O(1) difference in the textbook
+// form (I - I1/3 C^-1, J - 1, I4b - 1) loses ~|log10 strain| digits, and those
+// rounding errors, not the physics, would then dominate an fp64 comparison of two
+// implementations.  The identities used are exact:
+//   det C - 1 = tr X + (tr^2 X - tr X^2)/2 + det X,
+//   I - (I1/3) C^-1 = C^-1 dev(X),   J - 1 = (det C - 1)/(J + 1),
+//   J^-2/3 - 1 = -(det C - 1) / (c (c^2 + c + 1)),  c = (det C)^(1/3).
+static Mat3 pk2_from_strain(const Mat3& X, const HyperelasticParams& p, const Vec3* fiber, bool* bad) {
+    const double i1 = trace(X);
+    const double i2 = 0.5 * (i1 * i1 - trace(X * X));
+    const double d1 = i1 + i2 + det(X);  // det C - 1
+    if (!(d1 > -1.0)) {
         *bad = true;
         Mat3 r;
         for (int i = 0; i < 3; ++i)
             for (int j = 0; j < 3; ++j) r.m[i][j] = std::numeric_limits<double>::quiet_NaN();
         return r;
     }
-    const double J = std::sqrt(dC);
-    const double Jm23 = std::pow(J, -2.0 / 3.0);
-    const Mat3 Ci = inverse(C);
-    const double I1 = trace(C);
-    Mat3 S = (p.mu * Jm23) * (Mat3::identity() - (I1 / 3.0) * Ci);
+    const double J = std::sqrt(1.0 + d1);
+    const double Jm1 = d1 / (J + 1.0);
+    const double c = std::cbrt(1.0 + d1);
+    const double Jm23m1 = -d1 / (c * (c * c + c + 1.0));
+    const double Jm23 = 1.0 + Jm23m1;
+    const Mat3 Ci = inverse(Mat3::identity() + X);
+    const Mat3 M = Ci * (X - (i1 / 3.0) * Mat3::identity());
+    Mat3 S = (0.5 * p.mu * Jm23) * (M + transpose(M));
     if (p.eta_a > 0) {
         if (!fiber) throw ValidationError("fiber required when eta_a > 0");
         const Vec3& a = *fiber;
-        const Vec3 Ca = C * a;
-        const double I4 = a[0] * Ca[0] + a[1] * Ca[1] + a[2] * Ca[2];
-        S = S + (2.0 * p.eta_a * (Jm23 * I4 - 1.0) * Jm23) * (outer(a, a) - (I4 / 3.0) * Ci);
+        const Vec3 Xa = X * a;
+        const double aa = a[0] * a[0] + a[1] * a[1] + a[2] * a[2];
+        const double aXa = a[0] * Xa[0] + a[1] * Xa[1] + a[2] * Xa[2];
+        const double I4 = aa + aXa;
+        const double I4bm1 = Jm23m1 + Jm23 * ((aa - 1.0) + aXa);  // J^-2/3 I4 - 1
+        S = S + (2.0 * p.eta_a * I4bm1 * Jm23) * (outer(a, a) - (I4 / 3.0) * Ci);
     }
-    S = S + (p.kappa * J * (J - 1.0)) * Ci;
+    S = S + (p.kappa * J * Jm1) * Ci;
     return S;
+}
+static Mat3 pk2_core(const Mat3& C, const HyperelasticParams& p, const Vec3* fiber, bool* bad) {
+    return pk2_from_strain(C - Mat3::identity(), p, fiber, bad);
 }
 Mat3 pk2_stress(const Mat3& C, const HyperelasticParams& p, const Vec3* fiber) {
     bool bad = false;
@@ -386,34 +406,43 @@ Mat3 pk2_stress(const Mat3& C, const HyperelasticParams& p, const Vec3* fiber) {
     return S;
 }
 
-// materials.hpp:108-114; Eq. 11.
-Mat3 thermal_deformation_gradient(double T, const ExpansionSpec& s, const Vec3& m, const Vec3& n) {
+// materials.hpp:108-114; Eq. 11.  F_ther - I, formed from the
+// stretch increments alpha dT directly (see pk2_from_strain on why not 1 + alpha dT - 1).
+static Mat3 thermal_deformation_delta(double T, const ExpansionSpec& s, const Vec3& m, const Vec3& n) {
     auto dot = [](const Vec3& a, const Vec3& b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; };
     const double dT = T - s.reference_temperature;
-    const double li = 1.0 + s.alpha_i * dT;
-    Mat3 F = li * Mat3::identity();
+    const double ei = s.alpha_i * dT;
+    Mat3 D = ei * Mat3::identity();
     if (s.kind != ExpansionKind::Isotropic) {
         if (std::fabs(dot(m, m) - 1.0) > 1e-6) throw ValidationError("expansion axis m not unit");
-        const double lm = 1.0 + s.alpha_m * dT;
-        F = F + (lm - li) * outer(m, m);
+        D = D + (s.alpha_m * dT - ei) * outer(m, m);
     }
     if (s.kind == ExpansionKind::Orthotropic) {
         if (std::fabs(dot(n, n) - 1.0) > 1e-6 || std::fabs(dot(m, n)) > 1e-6)
             throw ValidationError("expansion axes not orthonormal");
-        const double ln = 1.0 + s.alpha_n * dT;
-        F = F + (ln - li) * outer(n, n);
+        D = D + (s.alpha_n * dT - ei) * outer(n, n);
     }
-    return F;
+    return D;
+}
+Mat3 thermal_deformation_gradient(double T, const ExpansionSpec& s, const Vec3& m, const Vec3& n) {
+    return Mat3::identity() + thermal_deformation_delta(T, s, m, n);
 }
 
-// materials.hpp:116-120; Eq. 8-10.
+// materials.hpp:116-120; Eq. 8-10, from the displacement gradient
+// Hd = F - I and Delta = F_ther - I:  F_elas - I = (Hd - Delta) F_ther^-1,
+// C_elas - I = Hel + Hel^T + Hel^T Hel.
+static Mat3 total_pk2_from_grad(const Mat3& Hd, const Mat3& Delta, const HyperelasticParams& p, const Vec3* fiber,
+                                bool* bad) {
+    const Mat3 Fth = Mat3::identity() + Delta;
+    const Mat3 Fi = inverse(Fth);
+    const Mat3 Hel = (Hd - Delta) * Fi;
+    const Mat3 X = Hel + transpose(Hel) + transpose(Hel) * Hel;
+    const Mat3 Sint = pk2_from_strain(X, p, fiber, bad);
+    return det(Fth) * (Fi * Sint * transpose(Fi));
+}
 static Mat3 total_pk2_core(const Mat3& F, const Mat3& Fth, const HyperelasticParams& p, const Vec3* fiber,
                            bool* bad) {
-    const Mat3 Fi = inverse(Fth);
-    const Mat3 Fel = F * Fi;
-    const Mat3 C = transpose(Fel) * Fel;
-    const Mat3 Sint = pk2_core(C, p, fiber, bad);
-    return det(Fth) * (Fi * Sint * transpose(Fi));
+    return total_pk2_from_grad(F - Mat3::identity(), Fth - Mat3::identity(), p, fiber, bad);
 }
 Mat3 total_pk2_stress(const Mat3& F, const Mat3& Fth, const HyperelasticParams& p, const Vec3* fiber) {
     bool bad = false;
@@ -529,16 +558,28 @@ Mat3 deformation_gradient(const double* U, const double* G) {
 }
 template Mat3 deformation_gradient<4>(const double*, const double*);
 template Mat3 deformation_gradient<8>(const double*, const double*);
+// U G^T alone: the mechanics phase keeps F - I at full relative precision.
+template <int NN>
+static Mat3 displacement_gradient(const double* U, const double* G) {
+    Mat3 H;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = 0;
+            for (int a = 0; a < NN; ++a) s += U[a * 3 + i] * G[a * 3 + j];
+            H.m[i][j] = s;
+        }
+    return H;
+}
 
 // mechanics.hpp:55-69; Eqs. 25/26/28.
 template <int NN>
-static void internal_force_core(const Mat3& F, const double* G, const HyperelasticParams& params,
-                                const Vec3* fiber, const Mat3& Fth, std::span<Mat3> hist, double dt,
+static void internal_force_core(const Mat3& Hd, const double* G, const HyperelasticParams& params,
+                                const Vec3* fiber, const Mat3& Delta, std::span<Mat3> hist, double dt,
                                 const PronySeries& prony, double V, double* out, Mat3* S_tilde_out, bool* bad) {
-    const Mat3 S = total_pk2_core(F, Fth, params, fiber, bad);
+    const Mat3 S = total_pk2_from_grad(Hd, Delta, params, fiber, bad);
     const Mat3 St = prony.empty() ? S : prony_update(S, hist, dt, prony);
     if (S_tilde_out) *S_tilde_out = St;
-    const Mat3 P = V * (F * St);
+    const Mat3 P = V * (St + Hd * St);  // V F S~ with F = I + Hd
     for (int a = 0; a < NN; ++a)
         for (int i = 0; i < 3; ++i)
             out[a * 3 + i] = P.m[i][0] * G[a * 3 + 0] + P.m[i][1] * G[a * 3 + 1] + P.m[i][2] * G[a * 3 + 2];
@@ -548,7 +589,8 @@ void element_internal_force(const Mat3& F, const double* G, const HyperelasticPa
                             const Mat3& Fth, std::span<Mat3> hist, double dt, const PronySeries& prony, double V,
                             double* out, Mat3* S_tilde_out) {
     bool bad = false;
-    internal_force_core<NN>(F, G, params, fiber, Fth, hist, dt, prony, V, out, S_tilde_out, &bad);
+    internal_force_core<NN>(F - Mat3::identity(), G, params, fiber, Fth - Mat3::identity(), hist, dt, prony, V, out,
+                            S_tilde_out, &bad);
     if (bad) throw ValidationError("non-SPD C");
 }
 template void element_internal_force<4>(const Mat3&, const double*, const HyperelasticParams&, const Vec3*,
@@ -625,6 +667,7 @@ Engine::Engine(const Mesh& mesh, const PrecomputedMesh& pre, const MaterialModel
     state_.mech = MechState::zero(N, E, P);
     f_cache_.assign(E, Mat3::identity());
     f_ther_cache_.assign(E, Mat3::identity());
+    f_ther_delta_.assign(E, Mat3{});
     stress_cache_.assign(E, Mat3{});
     element_thermal_loads_.assign((size_t)E * nn, 0.0);
     element_forces_.assign((size_t)E * 3 * nn, 0.0);
@@ -730,14 +773,15 @@ void Engine::mechanics_element_phase(bool compute_f) {
         double U[3 * NN];
         for (int a = 0; a < NN; ++a)
             for (int i = 0; i < 3; ++i) U[a * 3 + i] = u[(size_t)3 * el[a] + i];
-        if (compute_f) f_cache_[e] = deformation_gradient<NN>(U, G);
+        const Mat3 Hd = displacement_gradient<NN>(U, G);
+        if (compute_f) f_cache_[e] = Mat3::identity() + Hd;
         const Vec3* fiber = nullptr;
         if (!mesh_.fiber_dirs.empty()) fiber = &mesh_.fiber_dirs[e];
         else if (material_.fiber) fiber = &*material_.fiber;
         double f[3 * NN];
         std::span<Mat3> hist(state_.mech.viscous.data() + (size_t)e * P, P);
         bool bad = false;
-        internal_force_core<NN>(f_cache_[e], G, material_.hyperelastic, fiber, f_ther_cache_[e], hist, config_.dt,
+        internal_force_core<NN>(Hd, G, material_.hyperelastic, fiber, f_ther_delta_[e], hist, config_.dt,
                                 material_.prony, pre_.geometry_factor(e), f, &stress_cache_[e], &bad);
         if (bad) bad_elem = std::min(bad_elem, e);
         if constexpr (NN == 8) {
@@ -796,7 +840,8 @@ void Engine::step_impl() {
                 const double Tbar = Ts / NN;
                 const Vec3& m = mesh_.expansion_axes.empty() ? material_.axis_m : mesh_.expansion_axes[e][0];
                 const Vec3& n = mesh_.expansion_axes.empty() ? material_.axis_n : mesh_.expansion_axes[e][1];
-                f_ther_cache_[e] = thermal_deformation_gradient(Tbar, *material_.expansion, m, n);
+                f_ther_delta_[e] = thermal_deformation_delta(Tbar, *material_.expansion, m, n);
+                f_ther_cache_[e] = Mat3::identity() + f_ther_delta_[e];
             }
         }
         mechanics_element_phase<NN>(!coupled);

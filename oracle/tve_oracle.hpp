@@ -269,6 +269,7 @@ private:
 
     SimulationState state_;
     std::vector<Mat3> f_cache_, f_ther_cache_, stress_cache_;
+    std::vector<Mat3> f_ther_delta_;  // F_ther - I (exact small-strain form, see pk2_from_strain)
     std::vector<double> element_thermal_loads_, element_forces_;
     std::vector<double> assembled_load_, assembled_force_;
     std::vector<double> nodal_source_, external_force_total_;

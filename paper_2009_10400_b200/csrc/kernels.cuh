@@ -316,27 +316,30 @@ __global__ void __launch_bounds__(128) k_mech_element(const DevParams P, const D
 #pragma unroll
     for (int q = 0; q < 9; ++q) A[q] = __ldg(D.A + q * E + e);
     const double V = __ldg(D.vol + e);
-    double F[9];
+    // ---- displacement gradient Hd = F - I = H A^T, kept separate from I (small-strain accuracy)
+    double Hd[9];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-            F[i * 3 + j] = (i == j ? 1.0 : 0.0) + H[i * 3 + 0] * A[j * 3 + 0] + H[i * 3 + 1] * A[j * 3 + 1] +
-                           H[i * 3 + 2] * A[j * 3 + 2];
-    // ---- elastic right Cauchy-Green C (symmetric: 00 11 22 01 12 02)
-    double Fel[9];
+            Hd[i * 3 + j] = H[i * 3 + 0] * A[j * 3 + 0] + H[i * 3 + 1] * A[j * 3 + 1] + H[i * 3 + 2] * A[j * 3 + 2];
+    // ---- elastic part: F_el - I = (Hd - Delta) F_ther^-1, Delta = F_ther - I (Eqs. 8, 11)
+    double Hel[9];
     double lam = 1.0, Fi[9], detFth = 1.0;
     if constexpr (EXP == 0) {
 #pragma unroll
-        for (int q = 0; q < 9; ++q) Fel[q] = F[q];
+        for (int q = 0; q < 9; ++q) Hel[q] = Hd[q];
     } else if constexpr (EXP == 1) {
-        lam = 1.0 + P.alpha_i * (Ts / NN - P.Tref);
+        const double e1 = P.alpha_i * (Ts / NN - P.Tref);
+        lam = 1.0 + e1;
         const double il = 1.0 / lam;
 #pragma unroll
-        for (int q = 0; q < 9; ++q) Fel[q] = F[q] * il;
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) Hel[i * 3 + j] = (Hd[i * 3 + j] - (i == j ? e1 : 0.0)) * il;
     } else {
         const double dT = Ts / NN - P.Tref;
-        const double li = 1.0 + P.alpha_i * dT;
+        const double ei = P.alpha_i * dT;
         double m[3], n[3];
         if (P.axes_per_elem) {
 #pragma unroll
@@ -351,13 +354,16 @@ __global__ void __launch_bounds__(128) k_mech_element(const DevParams P, const D
                 n[k] = P.axis_n[k];
             }
         }
-        const double dm = (1.0 + P.alpha_m * dT) - li;
-        const double dn = P.exp_kind == 2 ? (1.0 + P.alpha_n * dT) - li : 0.0;
-        double Fth[9];
+        const double dm = P.alpha_m * dT - ei;
+        const double dn = P.exp_kind == 2 ? P.alpha_n * dT - ei : 0.0;
+        double Dl[9], Fth[9];
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
-            for (int j = 0; j < 3; ++j) Fth[i * 3 + j] = (i == j ? li : 0.0) + dm * m[i] * m[j] + dn * n[i] * n[j];
+            for (int j = 0; j < 3; ++j) {
+                Dl[i * 3 + j] = (i == j ? ei : 0.0) + dm * m[i] * m[j] + dn * n[i] * n[j];
+                Fth[i * 3 + j] = (i == j ? 1.0 : 0.0) + Dl[i * 3 + j];
+            }
         double Ad[9];
         detFth = adj3(Fth, Ad);
         const double idt = 1.0 / detFth;
@@ -367,30 +373,47 @@ __global__ void __launch_bounds__(128) k_mech_element(const DevParams P, const D
         for (int i = 0; i < 3; ++i)
 #pragma unroll
             for (int j = 0; j < 3; ++j)
-                Fel[i * 3 + j] = F[i * 3 + 0] * Fi[0 * 3 + j] + F[i * 3 + 1] * Fi[1 * 3 + j] + F[i * 3 + 2] * Fi[2 * 3 + j];
+                Hel[i * 3 + j] = (Hd[i * 3 + 0] - Dl[i * 3 + 0]) * Fi[0 * 3 + j] +
+                                 (Hd[i * 3 + 1] - Dl[i * 3 + 1]) * Fi[1 * 3 + j] +
+                                 (Hd[i * 3 + 2] - Dl[i * 3 + 2]) * Fi[2 * 3 + j];
     }
-    double c00 = Fel[0] * Fel[0] + Fel[3] * Fel[3] + Fel[6] * Fel[6];
-    double c11 = Fel[1] * Fel[1] + Fel[4] * Fel[4] + Fel[7] * Fel[7];
-    double c22 = Fel[2] * Fel[2] + Fel[5] * Fel[5] + Fel[8] * Fel[8];
-    double c01 = Fel[0] * Fel[1] + Fel[3] * Fel[4] + Fel[6] * Fel[7];
-    double c12 = Fel[1] * Fel[2] + Fel[4] * Fel[5] + Fel[7] * Fel[8];
-    double c02 = Fel[0] * Fel[2] + Fel[3] * Fel[5] + Fel[6] * Fel[8];
-    // ---- S_int = mu J^-2/3 (I - I1/3 C^-1) + 2 eta (I4b - 1) J^-2/3 (a(x)a - I4/3 C^-1) + kappa J (J-1) C^-1
-    const double a00 = c11 * c22 - c12 * c12, a11 = c00 * c22 - c02 * c02, a22 = c00 * c11 - c01 * c01;
-    const double a01 = c02 * c12 - c01 * c22, a12 = c01 * c02 - c00 * c12, a02 = c01 * c12 - c02 * c11;
-    const double detC = c00 * a00 + c01 * a01 + c02 * a02;
-    if (!(detC > 0.0)) atomicMin(D.err_elem, pack_elem(D.clock->step, D.elem_orig[e]));
+    // ---- strain X = C_el - I = Hel + Hel^T + Hel^T Hel  (symmetric: 00 11 22 01 12 02)
+    auto hh = [&](int i, int j) {
+        return Hel[0 * 3 + i] * Hel[0 * 3 + j] + Hel[1 * 3 + i] * Hel[1 * 3 + j] + Hel[2 * 3 + i] * Hel[2 * 3 + j];
+    };
+    const double x00 = 2.0 * Hel[0] + hh(0, 0), x11 = 2.0 * Hel[4] + hh(1, 1), x22 = 2.0 * Hel[8] + hh(2, 2);
+    const double x01 = Hel[1] + Hel[3] + hh(0, 1), x12 = Hel[5] + Hel[7] + hh(1, 2), x02 = Hel[2] + Hel[6] + hh(0, 2);
+    // ---- S_int = 2 dPsi/dC from X without O(1) cancellation (identities in oracle pk2_from_strain):
+    //   det C - 1 = i1 + i2 + det X;  I - I1/3 C^-1 = C^-1 dev X;  J - 1 = (det C - 1)/(J + 1);
+    //   J^-2/3 - 1 = -(det C - 1)/(c (c^2 + c + 1)), c = cbrt(det C)
+    const double i1 = x00 + x11 + x22;
+    const double trX2 = x00 * x00 + x11 * x11 + x22 * x22 + 2.0 * (x01 * x01 + x12 * x12 + x02 * x02);
+    const double detX = x00 * (x11 * x22 - x12 * x12) - x01 * (x01 * x22 - x12 * x02) + x02 * (x01 * x12 - x11 * x02);
+    const double d1 = i1 + 0.5 * (i1 * i1 - trX2) + detX;
+    if (!(d1 > -1.0)) atomicMin(D.err_elem, pack_elem(D.clock->step, D.elem_orig[e]));
+    const double detC = 1.0 + d1;
     const double J = sqrt(detC);
-    const double Jm23 = rcbrt(detC);
+    const double Jm1 = d1 / (J + 1.0);
+    const double cb = cbrt(detC);
+    const double Jm23m1 = -d1 / (cb * (cb * cb + cb + 1.0));
+    const double Jm23 = 1.0 + Jm23m1;
+    const double c00 = 1.0 + x00, c11 = 1.0 + x11, c22 = 1.0 + x22;
     const double idC = 1.0 / detC;
-    const double I1 = c00 + c11 + c22;
-    const double iso = P.mu * Jm23, vol = P.kappa * J * (J - 1.0);
-    double ciw = vol - iso * (I1 / 3.0);  // coefficient of C^-1
-    double S[6];                           // 00 11 22 01 12 02
-    S[0] = iso;
-    S[1] = iso;
-    S[2] = iso;
-    S[3] = S[4] = S[5] = 0.0;
+    const double k00 = (c11 * c22 - x12 * x12) * idC, k11 = (c00 * c22 - x02 * x02) * idC,
+                 k22 = (c00 * c11 - x01 * x01) * idC;  // C^-1
+    const double k01 = (x02 * x12 - x01 * c22) * idC, k12 = (x01 * x02 - c00 * x12) * idC,
+                 k02 = (x01 * x12 - x02 * c11) * idC;
+    const double t3 = i1 / 3.0;
+    const double v00 = x00 - t3, v11 = x11 - t3, v22 = x22 - t3;  // dev X
+    const double iso = 0.5 * P.mu * Jm23;
+    double S[6];  // sym(C^-1 dev X) scaled
+    S[0] = iso * 2.0 * (k00 * v00 + k01 * x01 + k02 * x02);
+    S[1] = iso * 2.0 * (k01 * x01 + k11 * v11 + k12 * x12);
+    S[2] = iso * 2.0 * (k02 * x02 + k12 * x12 + k22 * v22);
+    S[3] = iso * ((k00 * x01 + k01 * v11 + k02 * x12) + (k01 * v00 + k11 * x01 + k12 * x02));
+    S[4] = iso * ((k01 * x02 + k11 * x12 + k12 * v22) + (k02 * x01 + k12 * v11 + k22 * x12));
+    S[5] = iso * ((k00 * x02 + k01 * x12 + k02 * v22) + (k02 * v00 + k12 * x01 + k22 * x02));
+    double ciw = P.kappa * J * Jm1;  // coefficient of C^-1
     if (P.fiber_mode) {
         double fa[3];
         if (P.fiber_mode == 2) {
@@ -400,11 +423,13 @@ __global__ void __launch_bounds__(128) k_mech_element(const DevParams P, const D
 #pragma unroll
             for (int k = 0; k < 3; ++k) fa[k] = P.fiber[k];
         }
-        const double Ca0 = c00 * fa[0] + c01 * fa[1] + c02 * fa[2];
-        const double Ca1 = c01 * fa[0] + c11 * fa[1] + c12 * fa[2];
-        const double Ca2 = c02 * fa[0] + c12 * fa[1] + c22 * fa[2];
-        const double I4 = fa[0] * Ca0 + fa[1] * Ca1 + fa[2] * Ca2;
-        const double an = 2.0 * P.eta_a * (Jm23 * I4 - 1.0) * Jm23;
+        const double Xa0 = x00 * fa[0] + x01 * fa[1] + x02 * fa[2];
+        const double Xa1 = x01 * fa[0] + x11 * fa[1] + x12 * fa[2];
+        const double Xa2 = x02 * fa[0] + x12 * fa[1] + x22 * fa[2];
+        const double aa = fa[0] * fa[0] + fa[1] * fa[1] + fa[2] * fa[2];
+        const double aXa = fa[0] * Xa0 + fa[1] * Xa1 + fa[2] * Xa2;
+        const double I4 = aa + aXa;
+        const double an = 2.0 * P.eta_a * (Jm23m1 + Jm23 * ((aa - 1.0) + aXa)) * Jm23;
         S[0] += an * fa[0] * fa[0];
         S[1] += an * fa[1] * fa[1];
         S[2] += an * fa[2] * fa[2];
@@ -413,13 +438,12 @@ __global__ void __launch_bounds__(128) k_mech_element(const DevParams P, const D
         S[5] += an * fa[0] * fa[2];
         ciw -= an * (I4 / 3.0);
     }
-    const double cw = ciw * idC;
-    S[0] += cw * a00;
-    S[1] += cw * a11;
-    S[2] += cw * a22;
-    S[3] += cw * a01;
-    S[4] += cw * a12;
-    S[5] += cw * a02;
+    S[0] += ciw * k00;
+    S[1] += ciw * k11;
+    S[2] += ciw * k22;
+    S[3] += ciw * k01;
+    S[4] += ciw * k12;
+    S[5] += ciw * k02;
     // ---- pull back to the reference configuration: det(F_th) F_th^-1 S F_th^-T
     if constexpr (EXP == 1) {
 #pragma unroll
@@ -455,14 +479,15 @@ __global__ void __launch_bounds__(128) k_mech_element(const DevParams P, const D
             St[q] -= t;
         }
     }
-    // ---- P = V F S~ ;  PA = P A  (f_a = PA xi_a)
+    // ---- P = V F S~ = V (S~ + Hd S~) ;  PA = P A  (f_a = PA xi_a)
     const double Sm[9] = {St[0], St[3], St[5], St[3], St[1], St[4], St[5], St[4], St[2]};
     double Pm[9];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-            Pm[i * 3 + j] = V * (F[i * 3 + 0] * Sm[0 * 3 + j] + F[i * 3 + 1] * Sm[1 * 3 + j] + F[i * 3 + 2] * Sm[2 * 3 + j]);
+            Pm[i * 3 + j] = V * (Sm[i * 3 + j] + (Hd[i * 3 + 0] * Sm[0 * 3 + j] + Hd[i * 3 + 1] * Sm[1 * 3 + j] +
+                                                  Hd[i * 3 + 2] * Sm[2 * 3 + j]));
     double Q[9];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
@@ -527,7 +552,7 @@ __global__ void __launch_bounds__(128) k_mech_element(const DevParams P, const D
     }
     if (P.diag) {
 #pragma unroll
-        for (int q = 0; q < 9; ++q) D.diag_F[(size_t)e * 9 + q] = F[q];
+        for (int q = 0; q < 9; ++q) D.diag_F[(size_t)e * 9 + q] = Hd[q] + ((q == 0 || q == 4 || q == 8) ? 1.0 : 0.0);
 #pragma unroll
         for (int q = 0; q < 9; ++q) D.diag_S[(size_t)e * 9 + q] = Sm[q];
     }
