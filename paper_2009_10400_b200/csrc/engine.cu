@@ -183,7 +183,7 @@ bool sources_stable(tvegpu_engine* h, double t) {
 void exchange(tvegpu_engine* h, double* slots, double* sendbuf, int width) {
     const RankPlan& pl = h->plan;
     const int ns = pl.send_off.back();
-    if (ns > 0) k_pack<<<blocks(ns, 256), 256, 0, h->s>>>(slots, h->d_send_slot, ns, width, sendbuf, h->ptr.clock);
+    if (ns > 0) k_pack<<<blocks(ns, 256), 256, 0, h->s>>>(slots, h->d_send_slot, ns, width, sendbuf);
     CU(cudaEventRecord(h->ev_pack, h->s));
     CU(cudaStreamWaitEvent(h->sc, h->ev_pack, 0));
     auto& api = nccl();
@@ -237,7 +237,7 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr) {
             h->nn == 4 ? launch_thermal_element<4>(h, 0, E) : launch_thermal_element<8>(h, 0, E);
         }
         mark();
-        k_thermal_node<<<blocks(N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur);
+        k_thermal_node<<<blocks(N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur, h->mode == TVEGPU_THERMAL_ONLY);
         mark();
     }
     if (h->mode != TVEGPU_THERMAL_ONLY) {
@@ -250,12 +250,11 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr) {
             h->nn == 4 ? launch_mech_element<4>(h, 0, E) : launch_mech_element<8>(h, 0, E);
         }
         mark();
-        k_mech_node<<<blocks(N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur);
+        k_mech_node<<<blocks(N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur, 1);
         mark();
         h->cur ^= 1;
     }
-    k_finish_step<<<1, 32, 0, h->s>>>(h->ptr.clock, h->ptr.err_inst, h->ptr.err_elem, h->dt);
-    mark();
+    // the closing node kernel (K2 in ThermalOnly, else K4) ends the step: verdict, t += dt, step++
     CU(cudaGetLastError());
 }
 
@@ -407,6 +406,8 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     m.Ta = p.arterial_temperature;
     m.Qm = p.metabolic_rate;
     m.gamma = p.damping_gamma;
+    m.inv_2dt = 1.0 / (2.0 * p.dt);
+    m.inv_dt2 = 1.0 / (p.dt * p.dt);
     m.c_len = p.c_table_len;
     m.k_len = p.k_table_len;
     for (int i = 0; i < p.c_table_len; ++i) {
@@ -461,19 +462,13 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     CU(cudaMallocHost(&h->h_words, 8 * sizeof(unsigned long long)));
     cudaStream_t s = h->s;
     auto& own = h->owned;
-    // ---- element arrays (SoA)
+    // ---- element arrays (SoA).  Geometry (A_e, V_e) is recomputed in-kernel from the
+    // node coordinates, so only the connectivity is element data.
     {
         std::vector<int32_t> conn((size_t)nn * E);
-        std::vector<double> A((size_t)9 * E), vol(E);
-        for (int e = 0; e < E; ++e) {
-            const int oe = pl.elem_orig[e];
+        for (int e = 0; e < E; ++e)
             for (int a = 0; a < nn; ++a) conn[(size_t)a * E + e] = pl.conn[(size_t)e * nn + a];
-            for (int q = 0; q < 9; ++q) A[(size_t)q * E + e] = g.A[(size_t)9 * oe + q];
-            vol[e] = g.vol[oe];
-        }
         h->ptr.conn = dupload(own, conn, s);
-        h->ptr.A = dupload(own, A, s);
-        h->ptr.vol = dupload(own, vol, s);
         CU(cudaStreamSynchronize(s));
     }
     h->ptr.elem_orig = dupload(own, pl.elem_orig, s);
@@ -495,18 +490,18 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     }
     // ---- node arrays
     {
-        std::vector<double4> rec(N), X(nn == 8 ? N : 0);
+        std::vector<double4> rec(N), X(N);
         std::vector<double> mass(N), vn(N);
         for (int i = 0; i < N; ++i) {
             const int oi = pl.node_orig[i];
             rec[i] = make_double4(0.0, 0.0, 0.0, p.initial_temperature);
-            if (nn == 8) X[i] = make_double4(p.nodes[3 * (size_t)oi], p.nodes[3 * (size_t)oi + 1], p.nodes[3 * (size_t)oi + 2], 0.0);
+            X[i] = make_double4(p.nodes[3 * (size_t)oi], p.nodes[3 * (size_t)oi + 1], p.nodes[3 * (size_t)oi + 2], 0.0);
             mass[i] = g.mass[oi];
             vn[i] = g.vnode[oi];
         }
         h->ptr.rec0 = dupload(own, rec, s);
         h->ptr.rec1 = dupload(own, rec, s);
-        if (nn == 8) h->ptr.X = dupload(own, X, s);
+        h->ptr.X = dupload(own, X, s);
         h->ptr.mass = dupload(own, mass, s);
         h->ptr.vnode = dupload(own, vn, s);
         CU(cudaStreamSynchronize(s));
@@ -1032,7 +1027,7 @@ void* tvegpu_stream(tvegpu_engine* h) { return h ? (void*)h->s : nullptr; }
 int32_t tvegpu_kernels_per_step(const tvegpu_engine* h) {
     if (!h) return 0;
     const bool multi = h->plan.nranks > 1;
-    int k = 1;  // K5
+    int k = 0;
     if (h->mode != TVEGPU_MECHANICAL_ONLY) k += multi ? 4 : 2;  // K1 (x2 + pack) + K2
     if (h->mode != TVEGPU_THERMAL_ONLY) k += multi ? 4 : 2;
     return k;
@@ -1057,7 +1052,7 @@ tvegpu_status tvegpu_profile_kernels(tvegpu_engine* h, int32_t nsteps, double* m
             nm.push_back(h->nn == 4 ? "k_mech_element<4>" : "k_mech_element<8>");
             nm.push_back("k_mech_node");
         }
-        nm.push_back("k_finish_step");
+        // (the end-of-step verdict runs inside the last node kernel)
         const int nk = (int)nm.size();
         std::vector<cudaEvent_t> ev((size_t)(nk + 1) * nsteps);
         for (auto& e : ev) CU(cudaEventCreate(&e));

@@ -8,14 +8,19 @@
 //                              (materials.hpp:99-127; mechanics.hpp:55-84)
 //   K4 k_mech_node             CSR gather + Eq. 22 central difference + BCs
 //                              (mechanics.hpp:86-97)
-//   K5 k_finish_step           finite check verdict, t += dt, step++ (engine.hpp:89-90, 120)
+//   The last node kernel of the step also closes it: the last block to finish
+//   applies the finite-check verdict and advances t and the step counter
+//   (engine.hpp:89-90, 120), so a step is 4 launches.
 //
-// fp64 throughout (north_star parity <= 1e-10).  One thread per element / node;
-// element data is SoA ([component][E], coalesced), node state is a packed
-// 32-byte record (ux, uy, uz, T) so every element gathers one sector per node.
-// Assembly is a gather in canonical (original element, local) order: no float
-// atomics, results bit-identical at any partition count.  The only atomics are
-// integer atomicMin on the error words (lowest step, then T before u, then node).
+// fp64 throughout (north_star parity <= 1e-10).  One thread per element / node.
+// Node state is a packed 32-byte record (ux, uy, uz, T) and reference
+// coordinates a 32-byte record (x, y, z, -), so an element gathers one sector
+// per node and per field.  The element geometry (A_e with G_e = A_e Xi, and
+// V_e) is recomputed from the gathered coordinates instead of being streamed
+// (80 B/element saved per element kernel).  Assembly is a gather in
+// canonical (original element, local) order: no float atomics, results
+// bit-identical at any partition count.  The only atomics are integer
+// atomicMin on the error words and the end-of-step ticket.
 #pragma once
 
 #include <cstdint>
@@ -25,17 +30,19 @@ namespace tvegpu {
 
 constexpr int kMaxTable = 16;
 constexpr int kMaxProny = 4;
+constexpr int kGather = 8;  // node-kernel gather batch (loads in flight per thread)
 
 struct Clock {
     double time;
     long long step;
     int halted;
-    int pad;
+    unsigned ticket;  // end-of-step block counter of the closing node kernel
 };
 
 struct DevParams {
     int nn, E, N, P, mode, td, exp_kind, fiber_mode, axes_per_elem, has_R, diag, nslots;
     double dt, mu, kappa, eta_a, kh, rho, wbcb, Ta, Qm, gamma;
+    double inv_2dt, inv_dt2;  // 1/(2 dt), 1/dt^2 (Eq. 22 coefficients)
     double fiber[3];
     double c_fixed;
     double k_fixed[9];
@@ -48,15 +55,13 @@ struct DevParams {
 
 struct DevPtrs {
     const int32_t* conn;       // [nn][E]
-    const double* A;           // [9][E]
-    const double* vol;         // [E]
     double* theta;             // [P][6][E]   (xx, yy, zz, xy, yz, xz)
     const double* fiber;       // [3][E] or null
     const double* axes;        // [6][E] or null
     const int32_t* elem_orig;  // [E]
     double4* rec0;             // node record (ux, uy, uz, T), two rotating buffers
     double4* rec1;
-    const double4* X;          // [N] (x, y, z, 0), H8 only
+    const double4* X;          // [N] reference coordinates (x, y, z, 0)
     const double* mass;        // [N]
     const double* vnode;       // [N]
     const double* qr;          // [N] lumped nodal source power
@@ -149,6 +154,66 @@ __device__ __forceinline__ constexpr int h8h(int al, int a) {
                    : al == 1 ? h8s(a, 2) * h8s(a, 0) : al == 2 ? h8s(a, 0) * h8s(a, 1) : h8s(a, 0) * h8s(a, 1) * h8s(a, 2);
 }
 
+// Element kinematics from one pass over the element's nodes:
+//   H = U Xi^T (displacement sums), J = X Xi^T (T4: edge matrix; H8: 8 J0), Ts = sum T,
+//   gT = Xi T_e (thermal only).  Then A = J^-T (T4) or J0^-T / 8 (H8) and V (mesh.hpp:44).
+template <int NN, bool WANT_GT>
+__device__ __forceinline__ void element_pass(const DevPtrs& D, const double4* __restrict__ R, const int (&n)[NN],
+                                             double H[9], double A[9], double& V, double& Ts, double gT[3]) {
+    double J[9];
+    if constexpr (NN == 4) {
+        const double4 r0 = ldg4(R + n[0]);
+        const double4 x0 = ldg4(D.X + n[0]);
+        Ts = r0.w;
+#pragma unroll
+        for (int a = 1; a < 4; ++a) {
+            const double4 r = ldg4(R + n[a]);
+            const double4 x = ldg4(D.X + n[a]);
+            H[0 * 3 + a - 1] = r.x - r0.x;
+            H[1 * 3 + a - 1] = r.y - r0.y;
+            H[2 * 3 + a - 1] = r.z - r0.z;
+            J[0 * 3 + a - 1] = x.x - x0.x;
+            J[1 * 3 + a - 1] = x.y - x0.y;
+            J[2 * 3 + a - 1] = x.z - x0.z;
+            if constexpr (WANT_GT) gT[a - 1] = r.w - r0.w;
+            Ts += r.w;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) H[q] = J[q] = 0.0;
+        if constexpr (WANT_GT) gT[0] = gT[1] = gT[2] = 0.0;
+        Ts = 0.0;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const double4 r = ldg4(R + n[a]);
+            const double4 x = ldg4(D.X + n[a]);
+            Ts += r.w;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const double s = (double)h8s(a, j);
+                H[0 * 3 + j] += s * r.x;
+                H[1 * 3 + j] += s * r.y;
+                H[2 * 3 + j] += s * r.z;
+                J[0 * 3 + j] += s * x.x;
+                J[1 * 3 + j] += s * x.y;
+                J[2 * 3 + j] += s * x.z;
+                if constexpr (WANT_GT) gT[j] += s * r.w;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 9; ++q) J[q] = J[q] / 8.0;  // J0 = X Xi^T / 8
+    }
+    double Ad[9];
+    const double dJ = adj3(J, Ad);
+    // A = (J^-1)^T = Ad^T / det   (H8: / 8 more); one reciprocal, fp64 division is ~15 instructions
+    const double s = (NN == 4 ? 1.0 : 0.125) / dJ;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) A[i * 3 + j] = Ad[j * 3 + i] * s;
+    V = NN == 4 ? dJ * (1.0 / 6.0) : 8.0 * dJ;
+}
+
 // ------------------------------------------------------------------ K1: thermal element
 template <int NN>
 __global__ void __launch_bounds__(256) k_thermal_element(const DevParams P, const DevPtrs D, int cur, int e0,
@@ -157,42 +222,11 @@ __global__ void __launch_bounds__(256) k_thermal_element(const DevParams P, cons
     if (e >= e1 || D.clock->halted) return;
     const int E = P.E;
     const double4* __restrict__ R = cur ? D.rec1 : D.rec0;
-    double H[9], gT[3], Ts;
-    if constexpr (NN == 4) {
-        const double4 r0 = ldg4(R + __ldg(D.conn + e));
-        Ts = r0.w;
+    int n[NN];
 #pragma unroll
-        for (int a = 1; a < 4; ++a) {
-            const double4 r = ldg4(R + __ldg(D.conn + a * E + e));
-            H[0 * 3 + a - 1] = r.x - r0.x;
-            H[1 * 3 + a - 1] = r.y - r0.y;
-            H[2 * 3 + a - 1] = r.z - r0.z;
-            gT[a - 1] = r.w - r0.w;
-            Ts += r.w;
-        }
-    } else {
-#pragma unroll
-        for (int q = 0; q < 9; ++q) H[q] = 0.0;
-        gT[0] = gT[1] = gT[2] = 0.0;
-        Ts = 0.0;
-#pragma unroll
-        for (int a = 0; a < 8; ++a) {
-            const double4 r = ldg4(R + __ldg(D.conn + a * E + e));
-            Ts += r.w;
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                const double s = (double)h8s(a, j);
-                H[0 * 3 + j] += s * r.x;
-                H[1 * 3 + j] += s * r.y;
-                H[2 * 3 + j] += s * r.z;
-                gT[j] += s * r.w;
-            }
-        }
-    }
-    double A[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) A[q] = __ldg(D.A + q * E + e);
-    const double V = __ldg(D.vol + e);
+    for (int a = 0; a < NN; ++a) n[a] = __ldg(D.conn + a * E + e);
+    double H[9], A[9], gT[3], V, Ts;
+    element_pass<NN, true>(D, R, n, H, A, V, Ts, gT);
     // F = I + H A^T
     double F[9];
 #pragma unroll
@@ -238,91 +272,98 @@ __global__ void __launch_bounds__(256) k_thermal_element(const DevParams P, cons
     if (dF == 0.0) atomicMin(D.err_elem, pack_elem(D.clock->step, D.elem_orig[e]));
 }
 
-// ------------------------------------------------------------------ K2: thermal node
-__global__ void __launch_bounds__(256) k_thermal_node(const DevParams P, const DevPtrs D, int cur) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= P.N || D.clock->halted) return;
-    double4* R = cur ? D.rec1 : D.rec0;
-    const int k0 = __ldg(D.csr_off + i), k1 = __ldg(D.csr_off + i + 1);
+// ------------------------------------------------------------------ end of step (last block)
+// Applies the finite-check verdict of the step and advances time/step
+// (engine.hpp:89-90: the reference throws before advancing).  Called by every
+// block of the closing node kernel after its body; the last block to arrive acts.
+__device__ __forceinline__ void close_step(const DevPtrs& D, double dt) {
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    __threadfence();
+    const unsigned t = atomicAdd(&D.clock->ticket, 1u);
+    if (t != gridDim.x - 1) return;
+    __threadfence();
+    Clock* c = D.clock;
+    volatile unsigned long long* wi = D.err_inst;
+    volatile unsigned long long* we = D.err_elem;
+    if (!c->halted) {
+        const unsigned long long s = (unsigned long long)c->step;
+        const bool bad = (*we != ~0ULL && (*we >> 32) == s) || (*wi != ~0ULL && (*wi >> 33) == s);
+        if (bad) c->halted = 1;
+        else {
+            c->time += dt;
+            c->step += 1;
+        }
+    }
+    c->ticket = 0;
+    __threadfence();
+}
+
+// Sum of gathered slots in list order (canonical).  (A batched variant with 8
+// loads in flight per thread measured slower: it raised K4 to 80 registers.)
+__device__ __forceinline__ double gather1(const double* __restrict__ slots, const int32_t* __restrict__ idx, int k0,
+                                         int k1) {
     double s = 0.0;
-    for (int k = k0; k < k1; ++k) s += __ldg(D.slot_th + __ldg(D.csr_slot + k));
-    const double T = R[i].w;
-    const double V = __ldg(D.vnode + i);
-    const double c = P.td ? interp1(P.cT, P.cV, P.c_len, T) : P.c_fixed;
-    const double C = P.rho * c * V;
-    double Tn = T + P.dt / C * (-s - P.wbcb * V * (T - P.Ta) + P.Qm * V + __ldg(D.qr + i));
-    const uint8_t m = __ldg(D.mask + i);
-    if (m & BC_TFIX) Tn = __ldg(D.bc_tfix + __ldg(D.bc_index + i));
-    if (!isfinite(Tn)) atomicMin(D.err_inst, pack_inst(D.clock->step, 0, D.node_orig[i]));
-    R[i].w = Tn;
+    for (int k = k0; k < k1; ++k) s += __ldg(slots + __ldg(idx + k));
+    return s;
+}
+
+__device__ __forceinline__ void gather3(const double* __restrict__ slots, const int32_t* __restrict__ idx, int k0,
+                                        int k1, double& f0, double& f1, double& f2) {
+    f0 = f1 = f2 = 0.0;
+    for (int k = k0; k < k1; ++k) {
+        const double* s = slots + (size_t)__ldg(idx + k) * 3;
+        f0 += __ldg(s);
+        f1 += __ldg(s + 1);
+        f2 += __ldg(s + 2);
+    }
+}
+
+// ------------------------------------------------------------------ K2: thermal node
+__global__ void __launch_bounds__(256) k_thermal_node(const DevParams P, const DevPtrs D, int cur, int closes) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < P.N && !D.clock->halted) {
+        double4* R = cur ? D.rec1 : D.rec0;
+        const double s = gather1(D.slot_th, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1));
+        const double T = R[i].w;
+        const double V = __ldg(D.vnode + i);
+        const double c = P.td ? interp1(P.cT, P.cV, P.c_len, T) : P.c_fixed;
+        const double C = P.rho * c * V;
+        double Tn = T + P.dt / C * (-s - P.wbcb * V * (T - P.Ta) + P.Qm * V + __ldg(D.qr + i));
+        const uint8_t m = __ldg(D.mask + i);
+        if (m & BC_TFIX) Tn = __ldg(D.bc_tfix + __ldg(D.bc_index + i));
+        if (!isfinite(Tn)) atomicMin(D.err_inst, pack_inst(D.clock->step, 0, D.node_orig[i]));
+        R[i].w = Tn;
+    }
+    if (closes) close_step(D, P.dt);
 }
 
 // ------------------------------------------------------------------ K3: mechanical element
 // EXP: 0 = F_ther = I, 1 = isotropic lambda I, 2 = general (transversely isotropic / orthotropic)
 template <int NN, int EXP>
-__global__ void __launch_bounds__(128) k_mech_element(const DevParams P, const DevPtrs D, int cur, int e0,
+#ifndef TVEGPU_K3_MINBLOCKS
+#define TVEGPU_K3_MINBLOCKS 4  // 128 registers: 16 warps/SM (168 unbounded -> 8 warps, latency-bound)
+#endif
+__global__ void __launch_bounds__(128, TVEGPU_K3_MINBLOCKS) k_mech_element(const DevParams P, const DevPtrs D, int cur, int e0,
                                                       int e1) {
     const int e = e0 + blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= e1 || D.clock->halted) return;
     const int E = P.E;
     const double4* __restrict__ R = cur ? D.rec1 : D.rec0;
-    double H[9], Ts;
-    double Uh[4][3], cX[4][3];  // H8 only: U h_alpha and X h_alpha
-    if constexpr (NN == 4) {
-        const double4 r0 = ldg4(R + __ldg(D.conn + e));
-        Ts = r0.w;
+    int n[NN];
 #pragma unroll
-        for (int a = 1; a < 4; ++a) {
-            const double4 r = ldg4(R + __ldg(D.conn + a * E + e));
-            H[0 * 3 + a - 1] = r.x - r0.x;
-            H[1 * 3 + a - 1] = r.y - r0.y;
-            H[2 * 3 + a - 1] = r.z - r0.z;
-            Ts += r.w;
-        }
-    } else {
+    for (int a = 0; a < NN; ++a) n[a] = __ldg(D.conn + a * E + e);
+    double Hd[9], A[9], V, Ts;
+    {
+        double H[9], gT[3];
+        element_pass<NN, false>(D, R, n, H, A, V, Ts, gT);
+        // displacement gradient Hd = F - I = H A^T, kept separate from I (small-strain accuracy)
 #pragma unroll
-        for (int q = 0; q < 9; ++q) H[q] = 0.0;
+        for (int i = 0; i < 3; ++i)
 #pragma unroll
-        for (int al = 0; al < 4; ++al)
-#pragma unroll
-            for (int i = 0; i < 3; ++i) Uh[al][i] = cX[al][i] = 0.0;
-        Ts = 0.0;
-#pragma unroll
-        for (int a = 0; a < 8; ++a) {
-            const int n = __ldg(D.conn + a * E + e);
-            const double4 r = ldg4(R + n);
-            const double4 x = ldg4(D.X + n);
-            Ts += r.w;
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                const double s = (double)h8s(a, j);
-                H[0 * 3 + j] += s * r.x;
-                H[1 * 3 + j] += s * r.y;
-                H[2 * 3 + j] += s * r.z;
-            }
-#pragma unroll
-            for (int al = 0; al < 4; ++al) {
-                const double h = (double)h8h(al, a);
-                Uh[al][0] += h * r.x;
-                Uh[al][1] += h * r.y;
-                Uh[al][2] += h * r.z;
-                cX[al][0] += h * x.x;
-                cX[al][1] += h * x.y;
-                cX[al][2] += h * x.z;
-            }
-        }
+            for (int j = 0; j < 3; ++j)
+                Hd[i * 3 + j] = H[i * 3 + 0] * A[j * 3 + 0] + H[i * 3 + 1] * A[j * 3 + 1] + H[i * 3 + 2] * A[j * 3 + 2];
     }
-    double A[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) A[q] = __ldg(D.A + q * E + e);
-    const double V = __ldg(D.vol + e);
-    // ---- displacement gradient Hd = F - I = H A^T, kept separate from I (small-strain accuracy)
-    double Hd[9];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-            Hd[i * 3 + j] = H[i * 3 + 0] * A[j * 3 + 0] + H[i * 3 + 1] * A[j * 3 + 1] + H[i * 3 + 2] * A[j * 3 + 2];
     // ---- elastic part: F_el - I = (Hd - Delta) F_ther^-1, Delta = F_ther - I (Eqs. 8, 11)
     double Hel[9];
     double lam = 1.0, Fi[9], detFth = 1.0;
@@ -330,28 +371,28 @@ __global__ void __launch_bounds__(128) k_mech_element(const DevParams P, const D
 #pragma unroll
         for (int q = 0; q < 9; ++q) Hel[q] = Hd[q];
     } else if constexpr (EXP == 1) {
-        const double e1 = P.alpha_i * (Ts / NN - P.Tref);
-        lam = 1.0 + e1;
+        const double e1v = P.alpha_i * (Ts / NN - P.Tref);
+        lam = 1.0 + e1v;
         const double il = 1.0 / lam;
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
-            for (int j = 0; j < 3; ++j) Hel[i * 3 + j] = (Hd[i * 3 + j] - (i == j ? e1 : 0.0)) * il;
+            for (int j = 0; j < 3; ++j) Hel[i * 3 + j] = (Hd[i * 3 + j] - (i == j ? e1v : 0.0)) * il;
     } else {
         const double dT = Ts / NN - P.Tref;
         const double ei = P.alpha_i * dT;
-        double m[3], n[3];
+        double m[3], nn_[3];
         if (P.axes_per_elem) {
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 m[k] = __ldg(D.axes + k * E + e);
-                n[k] = __ldg(D.axes + (3 + k) * E + e);
+                nn_[k] = __ldg(D.axes + (3 + k) * E + e);
             }
         } else {
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 m[k] = P.axis_m[k];
-                n[k] = P.axis_n[k];
+                nn_[k] = P.axis_n[k];
             }
         }
         const double dm = P.alpha_m * dT - ei;
@@ -361,7 +402,7 @@ __global__ void __launch_bounds__(128) k_mech_element(const DevParams P, const D
         for (int i = 0; i < 3; ++i)
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
-                Dl[i * 3 + j] = (i == j ? ei : 0.0) + dm * m[i] * m[j] + dn * n[i] * n[j];
+                Dl[i * 3 + j] = (i == j ? ei : 0.0) + dm * m[i] * m[j] + dn * nn_[i] * nn_[j];
                 Fth[i * 3 + j] = (i == j ? 1.0 : 0.0) + Dl[i * 3 + j];
             }
         double Ad[9];
@@ -393,20 +434,23 @@ __global__ void __launch_bounds__(128) k_mech_element(const DevParams P, const D
     if (!(d1 > -1.0)) atomicMin(D.err_elem, pack_elem(D.clock->step, D.elem_orig[e]));
     const double detC = 1.0 + d1;
     const double J = sqrt(detC);
-    const double Jm1 = d1 / (J + 1.0);
     const double cb = cbrt(detC);
-    const double Jm23m1 = -d1 / (cb * (cb * cb + cb + 1.0));
+    // one reciprocal for 1/detC, 1/(J+1) and 1/(cb (cb^2 + cb + 1))
+    const double qa = J + 1.0, qb = cb * (cb * cb + cb + 1.0);
+    const double rq = 1.0 / (detC * qa * qb);
+    const double idC = qa * qb * rq;
+    const double Jm1 = d1 * (detC * qb * rq);
+    const double Jm23m1 = -d1 * (detC * qa * rq);
     const double Jm23 = 1.0 + Jm23m1;
     const double c00 = 1.0 + x00, c11 = 1.0 + x11, c22 = 1.0 + x22;
-    const double idC = 1.0 / detC;
     const double k00 = (c11 * c22 - x12 * x12) * idC, k11 = (c00 * c22 - x02 * x02) * idC,
                  k22 = (c00 * c11 - x01 * x01) * idC;  // C^-1
     const double k01 = (x02 * x12 - x01 * c22) * idC, k12 = (x01 * x02 - c00 * x12) * idC,
                  k02 = (x01 * x12 - x02 * c11) * idC;
-    const double t3 = i1 / 3.0;
+    const double t3 = i1 * (1.0 / 3.0);
     const double v00 = x00 - t3, v11 = x11 - t3, v22 = x22 - t3;  // dev X
     const double iso = 0.5 * P.mu * Jm23;
-    double S[6];  // sym(C^-1 dev X) scaled
+    double S[6];  // mu J^-2/3 sym(C^-1 dev X)
     S[0] = iso * 2.0 * (k00 * v00 + k01 * x01 + k02 * x02);
     S[1] = iso * 2.0 * (k01 * x01 + k11 * v11 + k12 * x12);
     S[2] = iso * 2.0 * (k02 * x02 + k12 * x12 + k22 * v22);
@@ -470,30 +514,36 @@ __global__ void __launch_bounds__(128) k_mech_element(const DevParams P, const D
     double St[6];
 #pragma unroll
     for (int q = 0; q < 6; ++q) St[q] = S[q];
+#pragma unroll 1
     for (int p = 0; p < P.P; ++p) {
         double* th = D.theta + (size_t)p * 6 * E + e;
+        double t[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) t[q] = th[(size_t)q * E];
 #pragma unroll
         for (int q = 0; q < 6; ++q) {
-            const double t = P.pa[p] * S[q] + P.pb[p] * th[(size_t)q * E];
-            th[(size_t)q * E] = t;
-            St[q] -= t;
+            t[q] = P.pa[p] * S[q] + P.pb[p] * t[q];
+            th[(size_t)q * E] = t[q];
+            St[q] -= t[q];
         }
     }
-    // ---- P = V F S~ = V (S~ + Hd S~) ;  PA = P A  (f_a = PA xi_a)
+    // ---- P = V F S~ = V (S~ + Hd S~) ;  Q = P A  (f_a = Q xi_a)
     const double Sm[9] = {St[0], St[3], St[5], St[3], St[1], St[4], St[5], St[4], St[2]};
-    double Pm[9];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-            Pm[i * 3 + j] = V * (Sm[i * 3 + j] + (Hd[i * 3 + 0] * Sm[0 * 3 + j] + Hd[i * 3 + 1] * Sm[1 * 3 + j] +
-                                                  Hd[i * 3 + 2] * Sm[2 * 3 + j]));
     double Q[9];
+    {
+        double Pm[9];
 #pragma unroll
-    for (int i = 0; i < 3; ++i)
+        for (int i = 0; i < 3; ++i)
 #pragma unroll
-        for (int j = 0; j < 3; ++j)
-            Q[i * 3 + j] = Pm[i * 3 + 0] * A[0 * 3 + j] + Pm[i * 3 + 1] * A[1 * 3 + j] + Pm[i * 3 + 2] * A[2 * 3 + j];
+            for (int j = 0; j < 3; ++j)
+                Pm[i * 3 + j] = V * (Sm[i * 3 + j] + (Hd[i * 3 + 0] * Sm[0 * 3 + j] + Hd[i * 3 + 1] * Sm[1 * 3 + j] +
+                                                      Hd[i * 3 + 2] * Sm[2 * 3 + j]));
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+                Q[i * 3 + j] = Pm[i * 3 + 0] * A[0 * 3 + j] + Pm[i * 3 + 1] * A[1 * 3 + j] + Pm[i * 3 + 2] * A[2 * 3 + j];
+    }
     double* out = D.slot_m + (size_t)e * NN * 3;
     if constexpr (NN == 4) {
         double f[12];
@@ -507,31 +557,47 @@ __global__ void __launch_bounds__(128) k_mech_element(const DevParams P, const D
 #pragma unroll
         for (int k = 0; k < 12; k += 2) reinterpret_cast<double2*>(out)[k / 2] = make_double2(f[k], f[k + 1]);
     } else {
-        // ---- closed-form hourglass: g_al = (U h_al - (F - I) c_al) / (8 + 8 |A^T c_al|^2)
-        const double k = P.kh * cbrt(V);
-        double W[9];
+        // ---- closed-form hourglass, second pass over the element's nodes (L1-hot):
+        //   U gamma_hat_al = U h_al - Hd c_al,  |gamma_hat_al|^2 = 8 + 8 |A^T c_al|^2,  c_al = X h_al
+        //   f_hg[:, a] = k sum_al g_al gamma_hat_al[a] = k (sum_al h_al[a] g_al - W A xi_a),
+        //   g_al = U gamma_hat_al / |gamma_hat_al|^2,  W A = sum_al g_al (A^T c_al)^T
+        double Uh[4][3], cX[4][3];
 #pragma unroll
-        for (int q = 0; q < 9; ++q) W[q] = 0.0;
+        for (int al = 0; al < 4; ++al)
 #pragma unroll
-        for (int al = 0; al < 4; ++al) {
-            double atc[3], fc[3];
+            for (int i = 0; i < 3; ++i) Uh[al][i] = cX[al][i] = 0.0;
 #pragma unroll
-            for (int j = 0; j < 3; ++j) atc[j] = A[0 * 3 + j] * cX[al][0] + A[1 * 3 + j] * cX[al][1] + A[2 * 3 + j] * cX[al][2];
-            const double n2 = 8.0 + 8.0 * (atc[0] * atc[0] + atc[1] * atc[1] + atc[2] * atc[2]);
-            // (F - I) c = H A^T c = H atc
+        for (int a = 0; a < 8; ++a) {
+            const double4 r = ldg4(R + n[a]);
+            const double4 x = ldg4(D.X + n[a]);
 #pragma unroll
-            for (int i = 0; i < 3; ++i) fc[i] = H[i * 3 + 0] * atc[0] + H[i * 3 + 1] * atc[1] + H[i * 3 + 2] * atc[2];
-            const double in2 = 1.0 / n2;
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                Uh[al][i] = (Uh[al][i] - fc[i]) * in2;  // g_al, in place
-#pragma unroll
-                for (int j = 0; j < 3; ++j) W[i * 3 + j] += Uh[al][i] * atc[j];  // W A = sum g c^T A
+            for (int al = 0; al < 4; ++al) {
+                const double h = (double)h8h(al, a);
+                Uh[al][0] += h * r.x;
+                Uh[al][1] += h * r.y;
+                Uh[al][2] += h * r.z;
+                cX[al][0] += h * x.x;
+                cX[al][1] += h * x.y;
+                cX[al][2] += h * x.z;
             }
         }
-        // Q <- Q - k (sum_al g_al c_al^T) A = Q - k W'  where W' = sum g (A^T c)^T
+        const double k = P.kh * cbrt(V);
 #pragma unroll
-        for (int q = 0; q < 9; ++q) Q[q] -= k * W[q];
+        for (int al = 0; al < 4; ++al) {
+            double atc[3];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) atc[j] = A[0 * 3 + j] * cX[al][0] + A[1 * 3 + j] * cX[al][1] + A[2 * 3 + j] * cX[al][2];
+            const double in2 = 1.0 / (8.0 + 8.0 * (atc[0] * atc[0] + atc[1] * atc[1] + atc[2] * atc[2]));
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const double hc = Hd[i * 3 + 0] * cX[al][0] + Hd[i * 3 + 1] * cX[al][1] + Hd[i * 3 + 2] * cX[al][2];
+                Uh[al][i] = (Uh[al][i] - hc) * in2;  // g_al, in place
+            }
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+                for (int j = 0; j < 3; ++j) Q[i * 3 + j] -= k * Uh[al][i] * atc[j];
+        }
 #pragma unroll
         for (int a = 0; a < 8; a += 2) {
             double f[6];
@@ -540,8 +606,9 @@ __global__ void __launch_bounds__(128) k_mech_element(const DevParams P, const D
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
                     const int aa = a + b;
-                    double v = h8s(aa, 0) * Q[i * 3 + 0] + h8s(aa, 1) * Q[i * 3 + 1] + h8s(aa, 2) * Q[i * 3 + 2];
-                    double hg = h8h(0, aa) * Uh[0][i] + h8h(1, aa) * Uh[1][i] + h8h(2, aa) * Uh[2][i] + h8h(3, aa) * Uh[3][i];
+                    const double v = h8s(aa, 0) * Q[i * 3 + 0] + h8s(aa, 1) * Q[i * 3 + 1] + h8s(aa, 2) * Q[i * 3 + 2];
+                    const double hg = h8h(0, aa) * Uh[0][i] + h8h(1, aa) * Uh[1][i] + h8h(2, aa) * Uh[2][i] +
+                                      h8h(3, aa) * Uh[3][i];
                     f[b * 3 + i] = v + k * hg;
                 }
             double2* o = reinterpret_cast<double2*>(out + a * 3);
@@ -559,75 +626,59 @@ __global__ void __launch_bounds__(128) k_mech_element(const DevParams P, const D
 }
 
 // ------------------------------------------------------------------ K4: mechanical node
-__global__ void __launch_bounds__(256) k_mech_node(const DevParams P, const DevPtrs D, int cur) {
+__global__ void __launch_bounds__(256) k_mech_node(const DevParams P, const DevPtrs D, int cur, int closes) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= P.N || D.clock->halted) return;
-    const double4* Rc = cur ? D.rec1 : D.rec0;
-    double4* Rn = cur ? D.rec0 : D.rec1;  // holds u^{n-1}; receives u^{n+1}
-    const int k0 = __ldg(D.csr_off + i), k1 = __ldg(D.csr_off + i + 1);
-    double f0 = 0.0, f1 = 0.0, f2 = 0.0;
-    for (int k = k0; k < k1; ++k) {
-        const double* s = D.slot_m + (size_t)__ldg(D.csr_slot + k) * 3;
-        f0 += __ldg(s);
-        f1 += __ldg(s + 1);
-        f2 += __ldg(s + 2);
-    }
-    const double4 u = Rc[i];
-    const double4 up = Rn[i];
-    const double m = __ldg(D.mass + i);
-    const double Dm = P.gamma * m;
-    const double a = Dm / (2.0 * P.dt), b = m / (P.dt * P.dt);
-    double R0 = 0.0, R1 = 0.0, R2 = 0.0;
-    if (P.has_R) {
-        R0 = __ldg(D.R + 3 * (size_t)i);
-        R1 = __ldg(D.R + 3 * (size_t)i + 1);
-        R2 = __ldg(D.R + 3 * (size_t)i + 2);
-    }
-    double x = (R0 - f0 + 2.0 * b * u.x + (a - b) * up.x) / (a + b);
-    double y = (R1 - f1 + 2.0 * b * u.y + (a - b) * up.y) / (a + b);
-    double z = (R2 - f2 + 2.0 * b * u.z + (a - b) * up.z) / (a + b);
-    const uint8_t msk = __ldg(D.mask + i);
-    if (msk & (BC_FIXED | BC_PX | BC_PY | BC_PZ)) {
-        if (msk & BC_FIXED) x = y = z = 0.0;
-        if (msk & (BC_PX | BC_PY | BC_PZ)) {
-            const double tn = D.clock->time + P.dt;  // value_at(t + dt), mechanics.hpp:89
-            const int row = __ldg(D.bc_index + i);
-            auto value_at = [&](int q) {
-                const int id = __ldg(D.bc_presc + 3 * row + q);
-                const double tg = D.presc_target[id], rt = D.presc_ramp[id];
-                return rt <= 0.0 ? tg : tg * fmin(tn / rt, 1.0);
-            };
-            if (msk & BC_PX) x = value_at(0);
-            if (msk & BC_PY) y = value_at(1);
-            if (msk & BC_PZ) z = value_at(2);
+    if (i < P.N && !D.clock->halted) {
+        const double4* Rc = cur ? D.rec1 : D.rec0;
+        double4* Rn = cur ? D.rec0 : D.rec1;  // holds u^{n-1}; receives u^{n+1}
+        double f0, f1, f2;
+        gather3(D.slot_m, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1), f0, f1, f2);
+        const double4 u = Rc[i];
+        const double4 up = Rn[i];
+        const double m = __ldg(D.mass + i);
+        const double Dm = P.gamma * m;
+        const double a = Dm * P.inv_2dt, b = m * P.inv_dt2;
+        const double iab = 1.0 / (a + b);
+        double R0 = 0.0, R1 = 0.0, R2 = 0.0;
+        if (P.has_R) {
+            R0 = __ldg(D.R + 3 * (size_t)i);
+            R1 = __ldg(D.R + 3 * (size_t)i + 1);
+            R2 = __ldg(D.R + 3 * (size_t)i + 2);
+        }
+        double x = (R0 - f0 + 2.0 * b * u.x + (a - b) * up.x) * iab;
+        double y = (R1 - f1 + 2.0 * b * u.y + (a - b) * up.y) * iab;
+        double z = (R2 - f2 + 2.0 * b * u.z + (a - b) * up.z) * iab;
+        const uint8_t msk = __ldg(D.mask + i);
+        if (msk & (BC_FIXED | BC_PX | BC_PY | BC_PZ)) {
+            if (msk & BC_FIXED) x = y = z = 0.0;
+            if (msk & (BC_PX | BC_PY | BC_PZ)) {
+                const double tn = D.clock->time + P.dt;  // value_at(t + dt), mechanics.hpp:89
+                const int row = __ldg(D.bc_index + i);
+                auto value_at = [&](int q) {
+                    const int id = __ldg(D.bc_presc + 3 * row + q);
+                    const double tg = D.presc_target[id], rt = D.presc_ramp[id];
+                    return rt <= 0.0 ? tg : tg * fmin(tn / rt, 1.0);
+                };
+                if (msk & BC_PX) x = value_at(0);
+                if (msk & BC_PY) y = value_at(1);
+                if (msk & BC_PZ) z = value_at(2);
+            }
+        }
+        if (!(isfinite(x) && isfinite(y) && isfinite(z)))
+            atomicMin(D.err_inst, pack_inst(D.clock->step, 1, D.node_orig[i]));
+        Rn[i] = make_double4(x, y, z, u.w);
+        if (P.diag) {
+            D.diag_f[3 * (size_t)i] = f0;
+            D.diag_f[3 * (size_t)i + 1] = f1;
+            D.diag_f[3 * (size_t)i + 2] = f2;
         }
     }
-    if (!(isfinite(x) && isfinite(y) && isfinite(z))) atomicMin(D.err_inst, pack_inst(D.clock->step, 1, D.node_orig[i]));
-    Rn[i] = make_double4(x, y, z, u.w);
-    if (P.diag) {
-        D.diag_f[3 * (size_t)i] = f0;
-        D.diag_f[3 * (size_t)i + 1] = f1;
-        D.diag_f[3 * (size_t)i + 2] = f2;
-    }
-}
-
-// ------------------------------------------------------------------ K5: end of step
-__global__ void k_finish_step(Clock* clock, const unsigned long long* err_inst, const unsigned long long* err_elem,
-                              double dt) {
-    if (threadIdx.x != 0 || clock->halted) return;
-    const unsigned long long s = (unsigned long long)clock->step;
-    const bool bad = (*err_elem != ~0ULL && (*err_elem >> 32) == s) || (*err_inst != ~0ULL && (*err_inst >> 33) == s);
-    if (bad) {
-        clock->halted = 1;  // the reference throws before advancing time/step (engine.hpp:89-90)
-        return;
-    }
-    clock->time += dt;
-    clock->step += 1;
+    if (closes) close_step(D, P.dt);
 }
 
 // ------------------------------------------------------------------ halo pack (nranks > 1)
 __global__ void k_pack(const double* __restrict__ slots, const int32_t* __restrict__ idx, int n, int width,
-                       double* __restrict__ out, const Clock* clock) {
+                       double* __restrict__ out) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int s = idx[k];

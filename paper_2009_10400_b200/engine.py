@@ -19,7 +19,8 @@ import numpy as np
 from .problem import Problem
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIBPATH = os.path.join(_HERE, "lib", "libtvegpu.so")
+# TVEGPU_LIB selects an experimental build variant (csrc/Makefile `variant` target).
+_LIBPATH = os.environ.get("TVEGPU_LIB") or os.path.join(_HERE, "lib", "libtvegpu.so")
 _LIB = None
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int32)
