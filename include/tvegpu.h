@@ -251,6 +251,14 @@ typedef struct tvegpu_plan_view {
     const int32_t* recv_offsets;    /* num_neighbors + 1; receive slot k of neighbour j at recv_offsets[j] + k */
     const int32_t* element_owner;   /* GLOBAL: num_elements_global owner ranks (original ids) */
     int32_t num_elements_global;
+    /* element-kernel chunks (one CTA each): nodes staged in shared memory */
+    int32_t num_chunks;
+    const int32_t* chunk_start;     /* num_chunks + 1 */
+    const int32_t* chunk_node_off;  /* num_chunks + 1 */
+    const int32_t* chunk_nodes;     /* unique local node ids of each chunk, ascending */
+    const uint16_t* chunk_node_slot;/* shared-memory slot of each chunk_nodes entry */
+    const uint16_t* chunk_conn;     /* nn*num_elements: slot of node (e, a) in its chunk */
+    int32_t max_chunk_slots;
 } tvegpu_plan_view;
 
 tvegpu_status tvegpu_plan_create(const tvegpu_problem* problem, int32_t nranks, int32_t rank,

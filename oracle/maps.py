@@ -30,12 +30,33 @@ def _spread21(v):
     return v
 
 
-def morton_keys(c, lo, hi):
+_T4E = [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)]
+_H8E = [(0, 1), (1, 2), (2, 3), (3, 0), (4, 5), (5, 6), (6, 7), (7, 4), (0, 4), (1, 5), (2, 6), (3, 7)]
+
+
+def min_edge(nodes, el):
+    edges = _T4E if el.shape[1] == 4 else _H8E
+    L = np.inf
+    for a, b in edges:
+        d = nodes[el[:, a]] - nodes[el[:, b]]
+        d2 = d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1] + d[:, 2] * d[:, 2]  # same summation order as C++
+        L = min(L, float(np.sqrt(d2).min()))
+    return L
+
+
+def morton_scale(c, lo, hi, lmin):
+    ext = float((hi - lo).max())
+    s = 1.0 / lmin if lmin > 0 else 0.0
+    if ext > 0 and ext * s > 2097151.0:
+        s = 2097151.0 / ext
+    return s
+
+
+def morton_keys(c, lo, scale):
+    """round((c - lo) * scale) per axis on the element lattice, 21 bits each, bit-interleaved."""
     q = []
     for k in range(3):
-        ext = hi[k] - lo[k]
-        s = 2097151.0 / ext if ext > 0 else 0.0
-        v = np.floor((c[:, k] - lo[k]) * s)
+        v = np.floor((c[:, k] - lo[k]) * scale + 0.5)
         v = np.clip(v, 0.0, 2097151.0)
         q.append(v.astype(np.uint64))
     return _spread21(q[0]) | (_spread21(q[1]) << np.uint64(1)) | (_spread21(q[2]) << np.uint64(2))
@@ -87,7 +108,7 @@ def rank_plan(nodes, el, nranks=1, rank=0, reorder=True):
     bnd = mine[shared_other.any(axis=1)]
     inr = mine[~shared_other.any(axis=1)]
     if reorder:
-        keys = morton_keys(c, lo, hi)
+        keys = morton_keys(c, lo, morton_scale(c, lo, hi, min_edge(nodes, el)))
         bnd = bnd[np.lexsort((bnd, keys[bnd]))]
         inr = inr[np.lexsort((inr, keys[inr]))]
         elem_orig = np.concatenate([bnd, inr]).astype(np.int32)

@@ -129,7 +129,9 @@ struct tvegpu_engine {
     ncclComm_t comm = nullptr;
     double* send_th = nullptr;
     double* send_m = nullptr;
-    const int32_t* d_send_slot = nullptr;
+    double* recv_th = nullptr;
+    double* recv_m = nullptr;
+    const int32_t* d_send_pos = nullptr;
     // graphs keyed by (parity, nsteps)
     std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
     int steps_per_graph = 64;
@@ -180,10 +182,16 @@ bool sources_stable(tvegpu_engine* h, double t) {
     return true;
 }
 
-void exchange(tvegpu_engine* h, double* slots, double* sendbuf, int width) {
+// Halo exchange of interface contributions: pack the boundary
+// elements' contributions on the compute stream, then on the comm stream one
+// grouped ncclSend/ncclRecv per neighbour straight into the receive area that
+// follows the local slots (the gather lists index it).  The node kernel waits on
+// ev_comm; the interior elements run meanwhile.
+void exchange(tvegpu_engine* h, double* slots, double* sendbuf, double* /*recvbuf*/, int width) {
     const RankPlan& pl = h->plan;
     const int ns = pl.send_off.back();
-    if (ns > 0) k_pack<<<blocks(ns, 256), 256, 0, h->s>>>(slots, h->d_send_slot, ns, width, sendbuf);
+    double* recvbuf = slots + (size_t)pl.E * pl.nn * width;
+    if (ns > 0) k_pack<<<blocks(ns, 256), 256, 0, h->s>>>(slots, h->d_send_pos, ns, width, sendbuf);
     CU(cudaEventRecord(h->ev_pack, h->s));
     CU(cudaStreamWaitEvent(h->sc, h->ev_pack, 0));
     auto& api = nccl();
@@ -193,34 +201,51 @@ void exchange(tvegpu_engine* h, double* slots, double* sendbuf, int width) {
         const size_t so = pl.send_off[j], sn = pl.send_off[j + 1] - so;
         const size_t ro = pl.recv_off[j], rn = pl.recv_off[j + 1] - ro;
         if (sn) NC(api.Send(sendbuf + so * width, sn * width, ncclFloat64, peer, h->comm, h->sc));
-        if (rn) NC(api.Recv(slots + ((size_t)pl.E * pl.nn + ro) * width, rn * width, ncclFloat64, peer, h->comm, h->sc));
+        if (rn) NC(api.Recv(recvbuf + ro * width, rn * width, ncclFloat64, peer, h->comm, h->sc));
     }
     NC(api.GroupEnd());
     CU(cudaEventRecord(h->ev_comm, h->sc));
 }
 
+size_t chunk_smem(const tvegpu_engine* h) { return (size_t)4 * h->prm.max_chunk_nodes * sizeof(double2); }
+
+// Element kernels run one CTA per 128-element chunk over chunk range [c0, c1).
 template <int NN>
-void launch_mech_element(tvegpu_engine* h, int e0, int e1) {
-    if (e1 <= e0) return;
-    const int T = 128;
-    const int g = blocks(e1 - e0, T);
+void launch_mech_element(tvegpu_engine* h, int c0, int c1) {
+    if (c1 <= c0) return;
+    const size_t sm = chunk_smem(h);
     switch (h->prm.exp_kind < 0 ? 0 : (h->prm.exp_kind == 0 ? 1 : 2)) {
-        case 0: k_mech_element<NN, 0><<<g, T, 0, h->s>>>(h->prm, h->ptr, h->cur, e0, e1); break;
-        case 1: k_mech_element<NN, 1><<<g, T, 0, h->s>>>(h->prm, h->ptr, h->cur, e0, e1); break;
-        default: k_mech_element<NN, 2><<<g, T, 0, h->s>>>(h->prm, h->ptr, h->cur, e0, e1); break;
+        case 0: k_mech_element<NN, 0><<<c1 - c0, kChunkThreads, sm, h->s>>>(h->prm, h->ptr, h->cur, c0, c1); break;
+        case 1: k_mech_element<NN, 1><<<c1 - c0, kChunkThreads, sm, h->s>>>(h->prm, h->ptr, h->cur, c0, c1); break;
+        default: k_mech_element<NN, 2><<<c1 - c0, kChunkThreads, sm, h->s>>>(h->prm, h->ptr, h->cur, c0, c1); break;
     }
 }
 
 template <int NN>
-void launch_thermal_element(tvegpu_engine* h, int e0, int e1) {
-    if (e1 <= e0) return;
-    k_thermal_element<NN><<<blocks(e1 - e0, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur, e0, e1);
+void launch_thermal_element(tvegpu_engine* h, int c0, int c1) {
+    if (c1 <= c0) return;
+    k_thermal_element<NN><<<c1 - c0, kChunkThreads, chunk_smem(h), h->s>>>(h->prm, h->ptr, h->cur, c0, c1);
 }
 
-// One Engine::step() (engine.hpp:70-82): K1 K2 [K3 K4] K5, with the halo
-// exchange of boundary-element slots overlapped with interior elements.
+void set_smem_limits(tvegpu_engine* h) {
+    const int sm = (int)chunk_smem(h);
+    if (sm <= 48 * 1024) return;
+    auto attr = [&](const void* f) { CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); };
+    attr((const void*)k_thermal_element<4>);
+    attr((const void*)k_thermal_element<8>);
+    attr((const void*)k_mech_element<4, 0>);
+    attr((const void*)k_mech_element<4, 1>);
+    attr((const void*)k_mech_element<4, 2>);
+    attr((const void*)k_mech_element<8, 0>);
+    attr((const void*)k_mech_element<8, 1>);
+    attr((const void*)k_mech_element<8, 2>);
+}
+
+// One Engine::step() (engine.hpp:70-82): K1 K2 [K3 K4], with the halo exchange of
+// boundary-element slots overlapped with the interior elements.
 void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr) {
-    const int E = h->plan.E, Eb = h->plan.Eb, N = h->plan.N;
+    const int N = h->plan.N;
+    const int nc = (int)h->plan.chunk_start.size() - 1, ncb = h->plan.nchunks_boundary;
     const bool multi = h->plan.nranks > 1;
     int ev = 0;
     auto mark = [&]() {
@@ -229,12 +254,12 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr) {
     mark();
     if (h->mode != TVEGPU_MECHANICAL_ONLY) {
         if (multi) {
-            h->nn == 4 ? launch_thermal_element<4>(h, 0, Eb) : launch_thermal_element<8>(h, 0, Eb);
-            exchange(h, h->ptr.slot_th, h->send_th, 1);
-            h->nn == 4 ? launch_thermal_element<4>(h, Eb, E) : launch_thermal_element<8>(h, Eb, E);
+            h->nn == 4 ? launch_thermal_element<4>(h, 0, ncb) : launch_thermal_element<8>(h, 0, ncb);
+            exchange(h, h->ptr.slot_th, h->send_th, h->recv_th, 1);
+            h->nn == 4 ? launch_thermal_element<4>(h, ncb, nc) : launch_thermal_element<8>(h, ncb, nc);
             CU(cudaStreamWaitEvent(h->s, h->ev_comm, 0));
         } else {
-            h->nn == 4 ? launch_thermal_element<4>(h, 0, E) : launch_thermal_element<8>(h, 0, E);
+            h->nn == 4 ? launch_thermal_element<4>(h, 0, nc) : launch_thermal_element<8>(h, 0, nc);
         }
         mark();
         k_thermal_node<<<blocks(N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur, h->mode == TVEGPU_THERMAL_ONLY);
@@ -242,12 +267,12 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr) {
     }
     if (h->mode != TVEGPU_THERMAL_ONLY) {
         if (multi) {
-            h->nn == 4 ? launch_mech_element<4>(h, 0, Eb) : launch_mech_element<8>(h, 0, Eb);
-            exchange(h, h->ptr.slot_m, h->send_m, 3);
-            h->nn == 4 ? launch_mech_element<4>(h, Eb, E) : launch_mech_element<8>(h, Eb, E);
+            h->nn == 4 ? launch_mech_element<4>(h, 0, ncb) : launch_mech_element<8>(h, 0, ncb);
+            exchange(h, h->ptr.slot_m, h->send_m, h->recv_m, 3);
+            h->nn == 4 ? launch_mech_element<4>(h, ncb, nc) : launch_mech_element<8>(h, ncb, nc);
             CU(cudaStreamWaitEvent(h->s, h->ev_comm, 0));
         } else {
-            h->nn == 4 ? launch_mech_element<4>(h, 0, E) : launch_mech_element<8>(h, 0, E);
+            h->nn == 4 ? launch_mech_element<4>(h, 0, nc) : launch_mech_element<8>(h, 0, nc);
         }
         mark();
         k_mech_node<<<blocks(N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur, 1);
@@ -462,15 +487,17 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     CU(cudaMallocHost(&h->h_words, 8 * sizeof(unsigned long long)));
     cudaStream_t s = h->s;
     auto& own = h->owned;
-    // ---- element arrays (SoA).  Geometry (A_e, V_e) is recomputed in-kernel from the
-    // node coordinates, so only the connectivity is element data.
-    {
-        std::vector<int32_t> conn((size_t)nn * E);
-        for (int e = 0; e < E; ++e)
-            for (int a = 0; a < nn; ++a) conn[(size_t)a * E + e] = pl.conn[(size_t)e * nn + a];
-        h->ptr.conn = dupload(own, conn, s);
-        CU(cudaStreamSynchronize(s));
-    }
+    // ---- element arrays.  Geometry (A_e, V_e) is recomputed in-kernel from the node
+    // coordinates, so the element data is the chunked connectivity: per 128-element
+    // chunk its unique node list, per element 16-bit indices into that list.
+    h->ptr.chunk_start = dupload(own, pl.chunk_start, s);
+    h->ptr.chunk_node_off = dupload(own, pl.chunk_node_off, s);
+    h->ptr.chunk_nodes = dupload(own, pl.chunk_nodes, s);
+    h->ptr.chunk_node_slot = dupload(own, pl.chunk_node_slot, s);
+    h->ptr.lconn = dupload(own, pl.lconn, s);
+    m.max_chunk_nodes = std::max(1, pl.max_chunk_nodes);
+    CU(cudaStreamSynchronize(s));
+    set_smem_limits(h);
     h->ptr.elem_orig = dupload(own, pl.elem_orig, s);
     h->ptr.theta = dalloc<double>(own, (size_t)6 * P * E);
     CU(cudaMemsetAsync(h->ptr.theta, 0, std::max<size_t>(1, (size_t)6 * P * E) * 8, s));
@@ -629,7 +656,9 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
         std::memcpy(&id, o.nccl_unique_id, sizeof id);
         NC(nccl().CommInitRank(&h->comm, nranks, id, o.rank));
         const size_t ns = pl.send_off.back();
-        h->d_send_slot = dupload(own, pl.send_slot, s);
+        const size_t nr = pl.recv_off.back();
+        (void)nr;
+        h->d_send_pos = dupload(own, pl.send_slot, s);  // element-major slot ids
         h->send_th = dalloc<double>(own, ns);
         h->send_m = dalloc<double>(own, 3 * ns);
         CU(cudaStreamSynchronize(s));
@@ -1004,6 +1033,13 @@ tvegpu_status tvegpu_plan_get(const tvegpu_plan* pl, tvegpu_plan_view* v) {
     v->recv_offsets = r.recv_off.data();
     v->element_owner = r.owner.data();
     v->num_elements_global = (int32_t)r.owner.size();
+    v->num_chunks = (int32_t)r.chunk_start.size() - 1;
+    v->chunk_start = r.chunk_start.data();
+    v->chunk_node_off = r.chunk_node_off.data();
+    v->chunk_nodes = r.chunk_nodes.data();
+    v->chunk_node_slot = r.chunk_node_slot.data();
+    v->chunk_conn = r.lconn.data();
+    v->max_chunk_slots = r.max_chunk_nodes;
     return TVEGPU_OK;
 }
 

@@ -30,7 +30,7 @@ namespace tvegpu {
 
 constexpr int kMaxTable = 16;
 constexpr int kMaxProny = 4;
-constexpr int kGather = 8;  // node-kernel gather batch (loads in flight per thread)
+constexpr int kChunkThreads = 128;  // element kernels: one thread per element of a 128-element chunk
 
 struct Clock {
     double time;
@@ -41,6 +41,7 @@ struct Clock {
 
 struct DevParams {
     int nn, E, N, P, mode, td, exp_kind, fiber_mode, axes_per_elem, has_R, diag, nslots;
+    int max_chunk_nodes;  // shared-memory stride of the staged node records
     double dt, mu, kappa, eta_a, kh, rho, wbcb, Ta, Qm, gamma;
     double inv_2dt, inv_dt2;  // 1/(2 dt), 1/dt^2 (Eq. 22 coefficients)
     double fiber[3];
@@ -54,7 +55,11 @@ struct DevParams {
 };
 
 struct DevPtrs {
-    const int32_t* conn;       // [nn][E]
+    const int32_t* chunk_start;     // [nchunks + 1] first local element of each 128-element chunk
+    const int32_t* chunk_node_off;  // [nchunks + 1]
+    const int32_t* chunk_nodes;     // unique local nodes of each chunk (ascending)
+    const uint16_t* chunk_node_slot;  // their shared-memory slots
+    const uint16_t* lconn;          // [E][nn] index of node (e, a) in its chunk's node list
     double* theta;             // [P][6][E]   (xx, yy, zz, xy, yz, xz)
     const double* fiber;       // [3][E] or null
     const double* axes;        // [6][E] or null
@@ -73,7 +78,7 @@ struct DevPtrs {
     const double* presc_ramp;
     const double* R;           // [N][3] external + body force, or null
     const int32_t* csr_off;    // [N+1]
-    const int32_t* csr_slot;   // gather list: slot ids
+    const int32_t* csr_slot;   // gather list: element-major slot ids (e*nn + a, or receive area)
     const int32_t* node_orig;  // [N]
     double* slot_th;           // [nslots]
     double* slot_m;            // [nslots][3]
@@ -157,18 +162,37 @@ __device__ __forceinline__ constexpr int h8h(int al, int a) {
 // Element kinematics from one pass over the element's nodes:
 //   H = U Xi^T (displacement sums), J = X Xi^T (T4: edge matrix; H8: 8 J0), Ts = sum T,
 //   gT = Xi T_e (thermal only).  Then A = J^-T (T4) or J0^-T / 8 (H8) and V (mesh.hpp:44).
+//   R and Xs point to the chunk's node records staged in shared memory.
+// A chunk's nodes staged in shared memory as four 16-byte planes, (ux, uy),
+// (uz, T), (x, y), (z, -), indexed by colour-assigned slot (plan.cpp colour_slots):
+// each quarter-warp's 16-byte reads of node a hit 8 distinct bank groups.
+struct NodeStage {
+    double2* a;
+    double2* b;
+    double2* c;
+    double2* d;
+    __device__ __forceinline__ double4 rec(int n) const {
+        const double2 p = a[n], q = b[n];
+        return make_double4(p.x, p.y, q.x, q.y);
+    }
+    __device__ __forceinline__ double4 X(int n) const {
+        const double2 p = c[n], q = d[n];
+        return make_double4(p.x, p.y, q.x, 0.0);
+    }
+};
+
 template <int NN, bool WANT_GT>
-__device__ __forceinline__ void element_pass(const DevPtrs& D, const double4* __restrict__ R, const int (&n)[NN],
-                                             double H[9], double A[9], double& V, double& Ts, double gT[3]) {
+__device__ __forceinline__ void element_pass(const NodeStage& S, const int (&n)[NN], double H[9], double A[9],
+                                             double& V, double& Ts, double gT[3]) {
     double J[9];
     if constexpr (NN == 4) {
-        const double4 r0 = ldg4(R + n[0]);
-        const double4 x0 = ldg4(D.X + n[0]);
+        const double4 r0 = S.rec(n[0]);
+        const double4 x0 = S.X(n[0]);
         Ts = r0.w;
 #pragma unroll
         for (int a = 1; a < 4; ++a) {
-            const double4 r = ldg4(R + n[a]);
-            const double4 x = ldg4(D.X + n[a]);
+            const double4 r = S.rec(n[a]);
+            const double4 x = S.X(n[a]);
             H[0 * 3 + a - 1] = r.x - r0.x;
             H[1 * 3 + a - 1] = r.y - r0.y;
             H[2 * 3 + a - 1] = r.z - r0.z;
@@ -185,8 +209,8 @@ __device__ __forceinline__ void element_pass(const DevPtrs& D, const double4* __
         Ts = 0.0;
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
-            const double4 r = ldg4(R + n[a]);
-            const double4 x = ldg4(D.X + n[a]);
+            const double4 r = S.rec(n[a]);
+            const double4 x = S.X(n[a]);
             Ts += r.w;
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
@@ -214,19 +238,53 @@ __device__ __forceinline__ void element_pass(const DevPtrs& D, const double4* __
     V = NN == 4 ? dJ * (1.0 / 6.0) : 8.0 * dJ;
 }
 
+// Stage one chunk: its unique nodes' (u, T) records and coordinates go to shared
+// memory once per chunk (each node is used by up to 8 of the chunk's elements),
+// replacing 2*NN random 32-byte global gathers per element.  Returns this
+// thread's element (or -1) and its nodes' shared-memory slots.
+template <int NN>
+__device__ __forceinline__ int stage_chunk(const DevPtrs& D, const double4* __restrict__ R, int c,
+                                           const NodeStage& S, int (&n)[NN]) {
+    const int eb = __ldg(D.chunk_start + c), ne = __ldg(D.chunk_start + c + 1) - eb;
+    const int u0 = __ldg(D.chunk_node_off + c), nu = __ldg(D.chunk_node_off + c + 1) - u0;
+    for (int k = threadIdx.x; k < nu; k += blockDim.x) {  // ascending node ids: coalesced loads
+        const int g = __ldg(D.chunk_nodes + u0 + k);
+        const int s = __ldg(D.chunk_node_slot + u0 + k);
+        const double2* r = reinterpret_cast<const double2*>(R + g);
+        const double2* x = reinterpret_cast<const double2*>(D.X + g);
+        S.a[s] = __ldg(r);
+        S.b[s] = __ldg(r + 1);
+        S.c[s] = __ldg(x);
+        S.d[s] = __ldg(x + 1);
+    }
+    const int e = threadIdx.x < ne ? eb + threadIdx.x : -1;
+    if (e >= 0) {
+        if constexpr (NN == 8) {
+            const uint4 w = __ldg(reinterpret_cast<const uint4*>(D.lconn) + e);
+            n[0] = w.x & 0xffff, n[1] = w.x >> 16, n[2] = w.y & 0xffff, n[3] = w.y >> 16;
+            n[4] = w.z & 0xffff, n[5] = w.z >> 16, n[6] = w.w & 0xffff, n[7] = w.w >> 16;
+        } else {
+            const uint2 w = __ldg(reinterpret_cast<const uint2*>(D.lconn) + e);
+            n[0] = w.x & 0xffff, n[1] = w.x >> 16, n[2] = w.y & 0xffff, n[3] = w.y >> 16;
+        }
+    }
+    __syncthreads();
+    return e;
+}
+
 // ------------------------------------------------------------------ K1: thermal element
 template <int NN>
-__global__ void __launch_bounds__(256) k_thermal_element(const DevParams P, const DevPtrs D, int cur, int e0,
-                                                         int e1) {
-    const int e = e0 + blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= e1 || D.clock->halted) return;
-    const int E = P.E;
-    const double4* __restrict__ R = cur ? D.rec1 : D.rec0;
+__global__ void __launch_bounds__(kChunkThreads) k_thermal_element(const DevParams P, const DevPtrs D, int cur,
+                                                                   int c0, int c1) {
+    if (D.clock->halted) return;  // uniform across the block
+    extern __shared__ double2 smem_planes[];
+    const int ms = P.max_chunk_nodes;
+    const NodeStage S{smem_planes, smem_planes + ms, smem_planes + 2 * ms, smem_planes + 3 * ms};
     int n[NN];
-#pragma unroll
-    for (int a = 0; a < NN; ++a) n[a] = __ldg(D.conn + a * E + e);
+    const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, S, n);
+    if (e < 0) return;
     double H[9], A[9], gT[3], V, Ts;
-    element_pass<NN, true>(D, R, n, H, A, V, Ts, gT);
+    element_pass<NN, true>(S, n, H, A, V, Ts, gT);
     // F = I + H A^T
     double F[9];
 #pragma unroll
@@ -257,6 +315,9 @@ __global__ void __launch_bounds__(256) k_thermal_element(const DevParams P, cons
     for (int i = 0; i < 3; ++i) q[i] = sc * (Ad[i * 3 + 0] * dw[0] + Ad[i * 3 + 1] * dw[1] + Ad[i * 3 + 2] * dw[2]);
 #pragma unroll
     for (int j = 0; j < 3; ++j) r[j] = A[0 * 3 + j] * q[0] + A[1 * 3 + j] * q[1] + A[2 * 3 + j] * q[2];
+    // element-major slots: one contiguous 8*NN-byte write per element.  (A node-major
+    // layout written through a position map made the node kernels ~25 % faster but
+    // the scattered element writes cost more; measured.)
     double* out = D.slot_th + (size_t)e * NN;
     if constexpr (NN == 4) {
         const double f0 = -(r[0] + r[1] + r[2]);
@@ -299,8 +360,8 @@ __device__ __forceinline__ void close_step(const DevPtrs& D, double dt) {
     __threadfence();
 }
 
-// Sum of gathered slots in list order (canonical).  (A batched variant with 8
-// loads in flight per thread measured slower: it raised K4 to 80 registers.)
+// Sum of a node's contributions through its gather list, in canonical
+// (original element, local) order.
 __device__ __forceinline__ double gather1(const double* __restrict__ slots, const int32_t* __restrict__ idx, int k0,
                                          int k1) {
     double s = 0.0;
@@ -340,23 +401,24 @@ __global__ void __launch_bounds__(256) k_thermal_node(const DevParams P, const D
 
 // ------------------------------------------------------------------ K3: mechanical element
 // EXP: 0 = F_ther = I, 1 = isotropic lambda I, 2 = general (transversely isotropic / orthotropic)
-template <int NN, int EXP>
 #ifndef TVEGPU_K3_MINBLOCKS
 #define TVEGPU_K3_MINBLOCKS 4  // 128 registers: 16 warps/SM (168 unbounded -> 8 warps, latency-bound)
 #endif
-__global__ void __launch_bounds__(128, TVEGPU_K3_MINBLOCKS) k_mech_element(const DevParams P, const DevPtrs D, int cur, int e0,
-                                                      int e1) {
-    const int e = e0 + blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= e1 || D.clock->halted) return;
-    const int E = P.E;
-    const double4* __restrict__ R = cur ? D.rec1 : D.rec0;
+template <int NN, int EXP>
+__global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
+    k_mech_element(const DevParams P, const DevPtrs D, int cur, int c0, int c1) {
+    if (D.clock->halted) return;  // uniform across the block
+    extern __shared__ double2 smem_planes[];
+    const int ms = P.max_chunk_nodes;
+    const NodeStage st{smem_planes, smem_planes + ms, smem_planes + 2 * ms, smem_planes + 3 * ms};
     int n[NN];
-#pragma unroll
-    for (int a = 0; a < NN; ++a) n[a] = __ldg(D.conn + a * E + e);
+    const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, st, n);
+    if (e < 0) return;
+    const int E = P.E;
     double Hd[9], A[9], V, Ts;
     {
         double H[9], gT[3];
-        element_pass<NN, false>(D, R, n, H, A, V, Ts, gT);
+        element_pass<NN, false>(st, n, H, A, V, Ts, gT);
         // displacement gradient Hd = F - I = H A^T, kept separate from I (small-strain accuracy)
 #pragma unroll
         for (int i = 0; i < 3; ++i)
@@ -568,8 +630,9 @@ __global__ void __launch_bounds__(128, TVEGPU_K3_MINBLOCKS) k_mech_element(const
             for (int i = 0; i < 3; ++i) Uh[al][i] = cX[al][i] = 0.0;
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
-            const double4 r = ldg4(R + n[a]);
-            const double4 x = ldg4(D.X + n[a]);
+            const double2 ra = st.a[n[a]], rb = st.b[n[a]], xa = st.c[n[a]], xb = st.d[n[a]];
+            const double4 r = make_double4(ra.x, ra.y, rb.x, 0.0);
+            const double4 x = make_double4(xa.x, xa.y, xb.x, 0.0);
 #pragma unroll
             for (int al = 0; al < 4; ++al) {
                 const double h = (double)h8h(al, a);
@@ -676,13 +739,21 @@ __global__ void __launch_bounds__(256) k_mech_node(const DevParams P, const DevP
     if (closes) close_step(D, P.dt);
 }
 
-// ------------------------------------------------------------------ halo pack (nranks > 1)
+// ------------------------------------------------------------------ halo pack / unpack (nranks > 1)
+// pack: send buffer k <- node-major slot send_pos[k];  unpack: slot recv_pos[r] <- receive buffer r
 __global__ void k_pack(const double* __restrict__ slots, const int32_t* __restrict__ idx, int n, int width,
                        double* __restrict__ out) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int s = idx[k];
     for (int c = 0; c < width; ++c) out[(size_t)k * width + c] = slots[(size_t)s * width + c];
+}
+__global__ void k_unpack(double* __restrict__ slots, const int32_t* __restrict__ idx, int n, int width,
+                         const double* __restrict__ in) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int s = idx[k];
+    for (int c = 0; c < width; ++c) slots[(size_t)s * width + c] = in[(size_t)k * width + c];
 }
 
 }  // namespace tvegpu

@@ -71,16 +71,27 @@ uint64_t spread21(uint64_t v) {
 
 }  // namespace
 
-uint64_t morton_key(const double* c, const double* lo, const double* hi) {
+// Morton key of an element centroid on the "element lattice": coordinates are
+// measured in units of the smallest element edge (isotropic scale, capped so the
+// extent fits 21 bits) and rounded.  On structured meshes this maps centroids to
+// their integer cell indices, so 8 consecutive keys are an aligned 2x2x2 block of
+// cells — what the shared-memory colouring (colour_slots) relies on.
+uint64_t morton_key(const double* c, const double* lo, double scale) {
     uint64_t q[3];
     for (int k = 0; k < 3; ++k) {
-        const double ext = hi[k] - lo[k];
-        const double s = ext > 0 ? 2097151.0 / ext : 0.0;
-        double v = std::floor((c[k] - lo[k]) * s);
+        double v = std::floor((c[k] - lo[k]) * scale + 0.5);
         v = std::min(2097151.0, std::max(0.0, v));
         q[k] = (uint64_t)v;
     }
     return spread21(q[0]) | (spread21(q[1]) << 1) | (spread21(q[2]) << 2);
+}
+
+double morton_scale(const GlobalMesh& g) {
+    double ext = 0;
+    for (int k = 0; k < 3; ++k) ext = std::max(ext, g.hi[k] - g.lo[k]);
+    double s = g.min_edge > 0 ? 1.0 / g.min_edge : 0.0;
+    if (ext > 0 && ext * s > 2097151.0) s = 2097151.0 / ext;
+    return s;
 }
 
 void validate_problem(const tvegpu_problem& p) {
@@ -192,6 +203,26 @@ GlobalMesh build_global(const tvegpu_problem& p) {
         }
     }
     if (bad >= 0) invalid("degenerate or inverted element " + std::to_string(E - bad + 1));
+    {
+        static const int t4e[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+        static const int h8e[12][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 0}, {4, 5}, {5, 6},
+                                       {6, 7}, {7, 4}, {0, 4}, {1, 5}, {2, 6}, {3, 7}};
+        double L = std::numeric_limits<double>::infinity();
+#pragma omp parallel for schedule(static) reduction(min : L)
+        for (int e = 0; e < E; ++e) {
+            const int32_t* el = p.elements + (size_t)e * nn;
+            for (int k = 0; k < (nn == 4 ? 6 : 12); ++k) {
+                const int a = nn == 4 ? t4e[k][0] : h8e[k][0], b = nn == 4 ? t4e[k][1] : h8e[k][1];
+                double d2 = 0;
+                for (int i = 0; i < 3; ++i) {
+                    const double d = p.nodes[3 * (size_t)el[a] + i] - p.nodes[3 * (size_t)el[b] + i];
+                    d2 += d * d;
+                }
+                L = std::min(L, std::sqrt(d2));
+            }
+        }
+        g.min_edge = L;
+    }
     for (int e = 0; e < E; ++e)
         for (int k = 0; k < 3; ++k) {
             g.lo[k] = std::min(g.lo[k], g.centroid[(size_t)3 * e + k]);
@@ -301,8 +332,9 @@ RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nrank
     }
     if (reorder) {
         std::vector<uint64_t> key(E);
+        const double mscale = morton_scale(g);
         auto sort_group = [&](std::vector<int32_t>& v) {
-            for (int32_t e : v) key[e] = morton_key(&g.centroid[(size_t)3 * e], g.lo, g.hi);
+            for (int32_t e : v) key[e] = morton_key(&g.centroid[(size_t)3 * e], g.lo, mscale);
             std::sort(v.begin(), v.end(), [&](int32_t x, int32_t y) { return key[x] < key[y] || (key[x] == key[y] && x < y); });
         };
         sort_group(bnd);
@@ -407,7 +439,147 @@ RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nrank
             }
         }
     }
+    // node-major positions (inverse of the gather list)
+    r.pos.assign((size_t)r.E * nn, -1);
+    r.recv_pos.assign(r.recv_off.empty() ? 0 : r.recv_off.back(), -1);
+    for (int k = 0; k < (int)r.csr_slot.size(); ++k) {
+        const int32_t s = r.csr_slot[k];
+        if (s < base) r.pos[s] = k;
+        else r.recv_pos[s - base] = k;
+    }
+    for (int32_t v : r.pos)
+        if (v < 0) throw Error(TVEGPU_E_ARG, "internal: unplaced element contribution");
+    for (int32_t v : r.recv_pos)
+        if (v < 0) throw Error(TVEGPU_E_ARG, "internal: unplaced halo contribution");
+    r.send_pos.resize(r.send_slot.size());
+    for (size_t k = 0; k < r.send_slot.size(); ++k) r.send_pos[k] = r.pos[r.send_slot[k]];
+    build_chunks(r);
     return r;
+}
+
+// Shared-memory slot assignment of one chunk's nodes.  Element kernels read
+// node a of the 8 elements of a quarter-warp with one 16-byte shared load; the
+// 8 lanes are conflict-free iff their slots differ mod 8 (eight 16-byte bank
+// groups).  So the nodes are 8-coloured greedily over those co-read groups and
+// slot = 8 * (rank within colour) + colour; empty slots hold node -1.
+static std::vector<int32_t> colour_slots(const std::vector<int32_t>& nodes, const int32_t* conn, int ne, int nn,
+                                         std::vector<int32_t>& slot_of) {
+    const int nu = (int)nodes.size();
+    auto idx = [&](int32_t n) { return (int)(std::lower_bound(nodes.begin(), nodes.end(), n) - nodes.begin()); };
+    // groups: (quarter-warp q, local a) -> distinct node indices
+    std::vector<std::vector<int>> groups;
+    std::vector<std::vector<int>> member(nu);
+    for (int q = 0; q * 8 < ne; ++q)
+        for (int a = 0; a < nn; ++a) {
+            std::vector<int> g;
+            for (int l = q * 8; l < std::min(ne, q * 8 + 8); ++l) g.push_back(idx(conn[(size_t)l * nn + a]));
+            std::sort(g.begin(), g.end());
+            g.erase(std::unique(g.begin(), g.end()), g.end());
+            if (g.size() < 2) continue;
+            for (int v : g) member[v].push_back((int)groups.size());
+            groups.push_back(std::move(g));
+        }
+    // Colour group by group in issue order: the uncoloured members of a group take
+    // the colours still free in that group (this propagates the 2x2x2 parity
+    // colouring through structured meshes); when a group has no free colour left,
+    // fall back to the colour least used across all of the node's groups.
+    std::vector<int> colour(nu, -1);
+    for (const auto& g : groups) {
+        bool used[8] = {false, false, false, false, false, false, false, false};
+        for (int w : g)
+            if (colour[w] >= 0) used[colour[w]] = true;
+        for (int v : g) {
+            if (colour[v] >= 0) continue;
+            int c = 0;
+            while (c < 8 && used[c]) ++c;
+            if (c == 8) {
+                int uses[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                for (int gi : member[v])
+                    for (int w : groups[gi])
+                        if (colour[w] >= 0) uses[colour[w]]++;
+                c = 0;
+                for (int k = 1; k < 8; ++k)
+                    if (uses[k] < uses[c]) c = k;
+            }
+            colour[v] = c;
+            used[c] = true;
+        }
+    }
+    // local refinement (helps unstructured / tetrahedral chunks): move each node to the
+    // colour with the fewest same-colour partners across its groups
+    for (int sweep = 0; sweep < 4; ++sweep) {
+        bool moved = false;
+        for (int v = 0; v < nu; ++v) {
+            if (colour[v] < 0 || member[v].empty()) continue;
+            int cost[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int gi : member[v])
+                for (int w : groups[gi])
+                    if (w != v && colour[w] >= 0) cost[colour[w]]++;
+            int best = colour[v];
+            for (int c = 0; c < 8; ++c)
+                if (cost[c] < cost[best]) best = c;
+            if (best != colour[v]) {
+                colour[v] = best;
+                moved = true;
+            }
+        }
+        if (!moved) break;
+    }
+    {
+        int count[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int v = 0; v < nu; ++v)
+            if (colour[v] >= 0) count[colour[v]]++;
+        for (int v = 0; v < nu; ++v)
+            if (colour[v] < 0) {  // in no conflict group: balance the colour classes
+                const int c = (int)(std::min_element(count, count + 8) - count);
+                colour[v] = c;
+                count[c]++;
+            }
+    }
+    int count[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    slot_of.assign(nu, 0);
+    for (int v = 0; v < nu; ++v) slot_of[v] = 8 * count[colour[v]]++ + colour[v];
+    int rows = 0;
+    for (int c = 0; c < 8; ++c) rows = std::max(rows, count[c]);
+    std::vector<int32_t> slots((size_t)8 * rows, -1);
+    for (int v = 0; v < nu; ++v) slots[slot_of[v]] = nodes[v];
+    return slots;
+}
+
+void build_chunks(RankPlan& r) {
+    const int nn = r.nn;
+    r.chunk_start.clear();
+    r.chunk_node_off.assign(1, 0);
+    r.chunk_nodes.clear();
+    r.chunk_node_slot.clear();
+    r.lconn.assign((size_t)r.E * nn, 0);
+    r.max_chunk_nodes = 0;
+    auto add_range = [&](int b, int e) {
+        for (int c0 = b; c0 < e; c0 += kChunk) {
+            const int c1 = std::min(e, c0 + kChunk);
+            r.chunk_start.push_back(c0);
+            std::vector<int32_t> nodes(r.conn.begin() + (size_t)c0 * nn, r.conn.begin() + (size_t)c1 * nn);
+            std::sort(nodes.begin(), nodes.end());
+            nodes.erase(std::unique(nodes.begin(), nodes.end()), nodes.end());
+            std::vector<int32_t> slot_of;
+            const std::vector<int32_t> slots = colour_slots(nodes, r.conn.data() + (size_t)c0 * nn, c1 - c0, nn, slot_of);
+            for (int le = c0; le < c1; ++le)
+                for (int a = 0; a < nn; ++a) {
+                    const int32_t n = r.conn[(size_t)le * nn + a];
+                    const int v = (int)(std::lower_bound(nodes.begin(), nodes.end(), n) - nodes.begin());
+                    r.lconn[(size_t)le * nn + a] = (uint16_t)slot_of[v];
+                }
+            // staging walks the nodes in ascending id (coalesced loads) and stores each to its slot
+            r.chunk_nodes.insert(r.chunk_nodes.end(), nodes.begin(), nodes.end());
+            for (int32_t s : slot_of) r.chunk_node_slot.push_back((uint16_t)s);
+            r.chunk_node_off.push_back((int32_t)r.chunk_nodes.size());
+            r.max_chunk_nodes = std::max(r.max_chunk_nodes, (int)slots.size());
+        }
+    };
+    add_range(0, r.Eb);
+    r.nchunks_boundary = (int)r.chunk_start.size();
+    add_range(r.Eb, r.E);
+    r.chunk_start.push_back(r.E);
 }
 
 void critical_timestep(const tvegpu_problem& p, double* thermal, double* mechanical) {

@@ -40,6 +40,7 @@ struct GlobalMesh {
     std::vector<int32_t> adj_off;  // node -> (element, local): canonical CSR over original ids
     std::vector<int32_t> adj_elem, adj_local;
     double lo[3], hi[3];           // bounding box of element centroids
+    double min_edge = 0;           // smallest element edge length (Morton lattice spacing)
 };
 
 // Validates the problem (the reference's ValidationError cases) and builds the
@@ -47,8 +48,10 @@ struct GlobalMesh {
 void validate_problem(const tvegpu_problem& p);
 GlobalMesh build_global(const tvegpu_problem& p);
 
-// Morton key of a centroid: 21-bit quantisation per axis over [lo, hi].
-uint64_t morton_key(const double* c, const double* lo, const double* hi);
+// Morton key of a centroid: round((c - lo) * scale) per axis, 21 bits each;
+// scale = 1 / (smallest element edge), capped so the extent fits 21 bits.
+uint64_t morton_key(const double* c, const double* lo, double scale);
+double morton_scale(const GlobalMesh& g);
 
 // Deterministic recursive coordinate bisection of element centroids into nranks parts.
 std::vector<int32_t> rcb_partition(const GlobalMesh& g, int nranks);
@@ -64,7 +67,29 @@ struct RankPlan {
     std::vector<int32_t> neighbors;
     std::vector<int32_t> send_off, send_slot, recv_off;
     std::vector<int32_t> owner;       // global element -> rank
+    // Element chunks (one CTA each): <= kChunk consecutive local elements, never
+    // straddling the boundary/interior split; each chunk's unique nodes are
+    // staged in shared memory and elements address them by a 16-bit index.
+    std::vector<int32_t> chunk_start;     // nchunks + 1
+    std::vector<int32_t> chunk_node_off;  // nchunks + 1
+    std::vector<int32_t> chunk_nodes;     // unique local node ids per chunk, ascending
+    std::vector<uint16_t> chunk_node_slot;  // shared-memory slot of each chunk_nodes entry
+    std::vector<uint16_t> lconn;          // E * nn, element-major: slot of node (e, a) in its chunk
+    int nchunks_boundary = 0;             // chunks [0, nchunks_boundary) cover [0, Eb)
+    int max_chunk_nodes = 0;              // max shared-memory slots (incl. colour padding) of a chunk
+    // Node-major slot layout: contribution (e, a) lives at position pos[e*nn + a]
+    // of node conn[e][a]'s contiguous CSR range, so node kernels read
+    // [csr_off[i], csr_off[i+1]) contiguously.  Received halo contribution r is
+    // scattered to recv_pos[r]; contribution k of the send list is read at send_pos[k].
+    std::vector<int32_t> pos;        // E * nn
+    std::vector<int32_t> recv_pos;   // recv_off.back()
+    std::vector<int32_t> send_pos;   // send_off.back()
 };
+
+constexpr int kChunk = 128;
+
+// Fills the chunk fields of a plan (called by build_rank_plan).
+void build_chunks(RankPlan& r);
 
 // Builds one rank's plan.  reorder = 0 keeps the original element and node order
 // (single rank only); otherwise Morton element order (boundary elements first)

@@ -76,7 +76,10 @@ class CPlanView(C.Structure):
                 ("num_boundary_elements", C.c_int32), ("num_nodes", C.c_int32), ("element_orig", _ip),
                 ("node_orig", _ip), ("conn", _ip), ("csr_offsets", _ip), ("csr_slots", _ip),
                 ("num_neighbors", C.c_int32), ("neighbor_ranks", _ip), ("send_offsets", _ip), ("send_slots", _ip),
-                ("recv_offsets", _ip), ("element_owner", _ip), ("num_elements_global", C.c_int32)]
+                ("recv_offsets", _ip), ("element_owner", _ip), ("num_elements_global", C.c_int32),
+                ("num_chunks", C.c_int32), ("chunk_start", _ip), ("chunk_node_off", _ip), ("chunk_nodes", _ip),
+                ("chunk_node_slot", C.POINTER(C.c_uint16)), ("chunk_conn", C.POINTER(C.c_uint16)),
+                ("max_chunk_slots", C.c_int32)]
 
 
 EXPORTS = {
@@ -183,7 +186,12 @@ def plan(problem: Problem, nranks=1, rank=0, reorder=True):
                     conn=arr(v.conn, E * nn).reshape(E, nn), csr_offsets=off, csr_slots=arr(v.csr_slots, int(off[-1])),
                     neighbors=arr(v.neighbor_ranks, nb), send_offsets=send_off,
                     send_slots=arr(v.send_slots, int(send_off[-1])), recv_offsets=recv_off,
-                    element_owner=arr(v.element_owner, v.num_elements_global))
+                    element_owner=arr(v.element_owner, v.num_elements_global),
+                    chunk_start=arr(v.chunk_start, v.num_chunks + 1),
+                    chunk_node_off=arr(v.chunk_node_off, v.num_chunks + 1),
+                    chunk_nodes=arr(v.chunk_nodes, int(arr(v.chunk_node_off, v.num_chunks + 1)[-1])),
+                    chunk_node_slot=arr(v.chunk_node_slot, int(arr(v.chunk_node_off, v.num_chunks + 1)[-1])),
+                    chunk_conn=arr(v.chunk_conn, E * nn).reshape(E, nn), max_chunk_slots=v.max_chunk_slots)
     finally:
         lib().tvegpu_plan_destroy(h)
 
