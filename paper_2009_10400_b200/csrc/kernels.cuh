@@ -142,10 +142,23 @@ __device__ __forceinline__ unsigned long long pack_elem(long long step, int elem
     return ((unsigned long long)step << 32) | (unsigned)elem;
 }
 
+// One 256-bit read-only load (sm_100 LDG.E.256): a 32-byte node record in one
+// request/sector instead of two 128-bit requests.
 __device__ __forceinline__ double4 ldg4(const double4* p) {
-    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
-    return make_double4(a.x, a.y, b.x, b.y);
+    double4 v;
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+    return v;
+}
+// 256-bit coherent load (data written earlier in the same step by another kernel is fine
+// with .nc too, but records this kernel itself writes must not use the read-only path)
+__device__ __forceinline__ double4 ld4(const double4* p) {
+    double4 v;
+    asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st4(double4* p, const double4& v) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w)
+                 : "memory");
 }
 
 // H8 corner signs (standard brick order) and hourglass vectors.
@@ -250,12 +263,12 @@ __device__ __forceinline__ int stage_chunk(const DevPtrs& D, const double4* __re
     for (int k = threadIdx.x; k < nu; k += blockDim.x) {  // ascending node ids: coalesced loads
         const int g = __ldg(D.chunk_nodes + u0 + k);
         const int s = __ldg(D.chunk_node_slot + u0 + k);
-        const double2* r = reinterpret_cast<const double2*>(R + g);
-        const double2* x = reinterpret_cast<const double2*>(D.X + g);
-        S.a[s] = __ldg(r);
-        S.b[s] = __ldg(r + 1);
-        S.c[s] = __ldg(x);
-        S.d[s] = __ldg(x + 1);
+        const double4 r = ldg4(R + g);
+        const double4 x = ldg4(D.X + g);
+        S.a[s] = make_double2(r.x, r.y);
+        S.b[s] = make_double2(r.z, r.w);
+        S.c[s] = make_double2(x.x, x.y);
+        S.d[s] = make_double2(x.z, x.w);
     }
     const int e = threadIdx.x < ne ? eb + threadIdx.x : -1;
     if (e >= 0) {
@@ -696,8 +709,8 @@ __global__ void __launch_bounds__(256) k_mech_node(const DevParams P, const DevP
         double4* Rn = cur ? D.rec0 : D.rec1;  // holds u^{n-1}; receives u^{n+1}
         double f0, f1, f2;
         gather3(D.slot_m, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1), f0, f1, f2);
-        const double4 u = Rc[i];
-        const double4 up = Rn[i];
+        const double4 u = ldg4(Rc + i);  // read-only in this kernel
+        const double4 up = ld4(Rn + i);  // this thread overwrites it below
         const double m = __ldg(D.mass + i);
         const double Dm = P.gamma * m;
         const double a = Dm * P.inv_2dt, b = m * P.inv_dt2;
@@ -729,7 +742,7 @@ __global__ void __launch_bounds__(256) k_mech_node(const DevParams P, const DevP
         }
         if (!(isfinite(x) && isfinite(y) && isfinite(z)))
             atomicMin(D.err_inst, pack_inst(D.clock->step, 1, D.node_orig[i]));
-        Rn[i] = make_double4(x, y, z, u.w);
+        st4(Rn + i, make_double4(x, y, z, u.w));
         if (P.diag) {
             D.diag_f[3 * (size_t)i] = f0;
             D.diag_f[3 * (size_t)i + 1] = f1;
