@@ -1,0 +1,339 @@
+// tve_gpu.hpp — header-only C++ facade over the C ABI (tvegpu.h) with the class
+// shape of the reference's tve::Engine (/root/reference/proj/include/tve/engine.hpp:83-143).
+//
+// The reference types (mesh.hpp, materials.hpp, mechanics.hpp, bioheat.hpp,
+// engine.hpp) are mirrored field for field with std::array<double,3> in place of
+// Eigen::Vector3d (the reference vendors Eigen, which is absent).
+// Errors are the reference exception taxonomy (errors.hpp:8-33).  Porting a
+// caller means: include this header, use tve::gpu:: instead of tve::, and link
+// libtvegpu.so.  See INTEGRATION.md.
+#pragma once
+
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <limits>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "tvegpu.h"
+
+namespace tve::gpu {
+
+using Vec3 = std::array<double, 3>;
+
+// ---------------------------------------------------------------- errors.hpp:8-33
+struct ParseError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ValidationError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct InstabilityError : std::runtime_error {
+    InstabilityError(const std::string& m, long s, int n) : std::runtime_error(m), step(s), node(n) {}
+    long step = -1;
+    int node = -1;
+};
+struct IoError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct DeviceError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+// ---------------------------------------------------------------- mesh.hpp:15-37
+enum class ElementKind { T4, H8 };
+inline int nodes_per_element(ElementKind k) { return k == ElementKind::T4 ? 4 : 8; }
+struct Mesh {
+    std::vector<Vec3> nodes;
+    ElementKind kind = ElementKind::T4;
+    std::vector<std::array<int, 8>> elements;      // first nodes_per_element() entries used
+    std::vector<Vec3> fiber_dirs;                   // empty or one per element
+    std::vector<std::array<Vec3, 2>> expansion_axes;
+    int node_count() const { return (int)nodes.size(); }
+    int element_count() const { return (int)elements.size(); }
+};
+
+// ---------------------------------------------------------------- materials.hpp:13-97
+struct HyperelasticParams { double mu = 0, kappa = 0, eta_a = 0; };
+struct PronyTerm { double phi = 0, tau = 0; };
+struct PronySeries { std::vector<PronyTerm> terms; };
+struct ScalarTable { std::vector<std::pair<double, double>> entries; };
+struct ConductivityTable {
+    struct Entry { double temperature = 0; std::array<double, 9> tensor{}; };  // row-major
+    std::vector<Entry> entries;
+    static ConductivityTable isotropic(double T, double k) {
+        ConductivityTable t;
+        t.entries.push_back({T, {k, 0, 0, 0, k, 0, 0, 0, k}});
+        return t;
+    }
+};
+struct ThermalProps {
+    double density = 0;
+    ScalarTable specific_heat;
+    ConductivityTable conductivity;
+    double perfusion_rate = 0, blood_specific_heat = 0, arterial_temperature = 37.0, metabolic_rate = 0;
+};
+enum class ExpansionKind { Isotropic, TransverselyIsotropic, Orthotropic };
+struct ExpansionSpec {
+    ExpansionKind kind = ExpansionKind::Isotropic;
+    double alpha_i = 0, alpha_m = 0, alpha_n = 0, reference_temperature = 37.0;
+};
+struct MaterialModel {
+    HyperelasticParams hyperelastic;
+    PronySeries prony;
+    ThermalProps thermal;
+    std::optional<ExpansionSpec> expansion;
+    std::optional<Vec3> fiber;
+    Vec3 axis_m{1, 0, 0};
+    Vec3 axis_n{0, 1, 0};
+};
+
+// ---------------------------------------------------------------- bioheat.hpp / mechanics.hpp
+struct SourceRegion {
+    std::vector<int> elements;
+    double q_r = 0, t_start = 0, t_end = std::numeric_limits<double>::infinity();
+};
+struct HeatSourceSet { std::vector<SourceRegion> regional; };
+struct ThermalBCs { std::vector<std::pair<int, double>> fixed; double initial_temperature = 37.0; };
+struct PrescribedDisplacement {
+    std::vector<int> nodes;
+    int component = 0;
+    double target = 0, ramp_time = 0;
+};
+struct MechBCs {
+    std::vector<int> fixed_nodes;
+    std::vector<PrescribedDisplacement> prescribed;
+    std::vector<double> external_force;  // 3 per node or empty
+    Vec3 body_force{0, 0, 0};
+};
+
+// ---------------------------------------------------------------- engine.hpp:16-45
+enum class CouplingMode { Coupled, ThermalOnly, MechanicalOnly };
+struct SimulationConfig {
+    double dt = 0, duration = 0;
+    CouplingMode mode = CouplingMode::Coupled;
+    bool expansion_enabled = false, temperature_dependent = false;
+    double damping_gamma = 0, hourglass_stiffness = 0.1;
+    bool allow_unstable_dt = false;
+    int workers = 0;
+};
+struct SimulationState {
+    std::vector<double> temperatures;  // ThermalState::temperatures
+    double time = 0;                   // ThermalState::time
+    std::vector<double> disp, disp_prev;
+    std::vector<std::array<double, 9>> viscous;  // num_elements * prony_terms (row-major)
+    long step = 0;
+};
+
+struct DeviceOptions {
+    int device = -1;
+    int steps_per_graph = 64;
+    bool diagnostics = false;
+};
+
+// tve::Engine (engine.hpp:83-143) on a B200.
+class Engine {
+public:
+    Engine(const Mesh& mesh, const MaterialModel& material, const MechBCs& mech_bcs, const ThermalBCs& thermal_bcs,
+           const HeatSourceSet& sources, const SimulationConfig& config, const DeviceOptions& opt = {})
+        : N_(mesh.node_count()), E_(mesh.element_count()), P_((int)material.prony.terms.size()) {
+        build(mesh, material, mech_bcs, thermal_bcs, sources, config);
+        tvegpu_options o;
+        tvegpu_default_options(&o);
+        o.device = opt.device;
+        o.steps_per_graph = opt.steps_per_graph;
+        o.diagnostics = opt.diagnostics ? 1 : 0;
+        const tvegpu_status st = tvegpu_create(&p_, &o, &h_);
+        if (st != TVEGPU_OK) rethrow(st, tvegpu_create_error(), -1, -1);
+    }
+    ~Engine() { tvegpu_destroy(h_); }
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    // engine.hpp:89-90
+    void step() { steps(1); }
+    void steps(int64_t n) {
+        push_if_dirty();
+        check(tvegpu_step(h_, n));
+        mirror_valid_ = false;
+    }
+    // engine.hpp:95-97: state() returns a host mirror synced on access; writes made
+    // through mutable_state() are pushed to the device before the next step.
+    const SimulationState& state() {
+        pull_if_stale();
+        return mirror_;
+    }
+    SimulationState& mutable_state() {
+        pull_if_stale();
+        dirty_ = true;
+        return mirror_;
+    }
+    double time() const { return tvegpu_time(h_); }
+    long step_count() const { return (long)tvegpu_step_count(h_); }
+
+    // engine.hpp:99 (fields only)
+    void make_snapshot(std::vector<double>& T, std::vector<double>& u) {
+        T.resize(N_);
+        u.resize(3 * (size_t)N_);
+        check(tvegpu_make_snapshot(h_, T.data(), u.data()));
+    }
+    // engine.hpp:101-105 (needs DeviceOptions::diagnostics)
+    std::vector<double> last_internal_forces() {
+        std::vector<double> f(3 * (size_t)N_);
+        check(tvegpu_get_diagnostics(h_, f.data(), nullptr, nullptr));
+        return f;
+    }
+    // bioheat.hpp:57 nodal source override (power per node [W]); empty restores regions
+    void set_nodal_sources(const std::vector<double>& power) {
+        check(tvegpu_set_nodal_sources(h_, power.empty() ? nullptr : power.data()));
+    }
+    tvegpu_engine* handle() { return h_; }
+
+private:
+    void build(const Mesh& m, const MaterialModel& mat, const MechBCs& mb, const ThermalBCs& tb,
+               const HeatSourceSet& src, const SimulationConfig& c) {
+        const int nn = nodes_per_element(m.kind);
+        for (const auto& x : m.nodes) nodes_.insert(nodes_.end(), x.begin(), x.end());
+        for (const auto& e : m.elements) elems_.insert(elems_.end(), e.begin(), e.begin() + nn);
+        for (const auto& f : m.fiber_dirs) fibers_.insert(fibers_.end(), f.begin(), f.end());
+        for (const auto& ax : m.expansion_axes)
+            for (const auto& v : ax) axes_.insert(axes_.end(), v.begin(), v.end());
+        for (const auto& t : mat.prony.terms) {
+            phi_.push_back(t.phi);
+            tau_.push_back(t.tau);
+        }
+        for (const auto& [T, v] : mat.thermal.specific_heat.entries) {
+            cT_.push_back(T);
+            cV_.push_back(v);
+        }
+        for (const auto& e : mat.thermal.conductivity.entries) {
+            kT_.push_back(e.temperature);
+            kK_.insert(kK_.end(), e.tensor.begin(), e.tensor.end());
+        }
+        fixed_ = mb.fixed_nodes;
+        for (const auto& q : mb.prescribed)
+            presc_.push_back({(int32_t)q.nodes.size(), q.nodes.data(), q.component, q.target, q.ramp_time});
+        for (const auto& [n, v] : tb.fixed) {
+            tfixN_.push_back(n);
+            tfixV_.push_back(v);
+        }
+        for (const auto& r : src.regional)
+            srcs_.push_back({(int32_t)r.elements.size(), r.elements.data(), r.q_r, r.t_start, r.t_end});
+        ext_ = mb.external_force;
+        tvegpu_problem& p = p_;
+        p = tvegpu_problem{};
+        p.kind = m.kind == ElementKind::T4 ? TVEGPU_T4 : TVEGPU_H8;
+        p.num_nodes = m.node_count();
+        p.num_elements = m.element_count();
+        p.nodes = nodes_.data();
+        p.elements = elems_.data();
+        p.fiber_dirs = fibers_.empty() ? nullptr : fibers_.data();
+        p.expansion_axes = axes_.empty() ? nullptr : axes_.data();
+        p.ref_specific_heat = cV_.empty() ? 0.0 : interp(37.0);
+        p.mu = mat.hyperelastic.mu;
+        p.kappa = mat.hyperelastic.kappa;
+        p.eta_a = mat.hyperelastic.eta_a;
+        p.prony_count = (int32_t)phi_.size();
+        p.prony_phi = phi_.data();
+        p.prony_tau = tau_.data();
+        p.density = mat.thermal.density;
+        p.c_table_len = (int32_t)cT_.size();
+        p.c_table_T = cT_.data();
+        p.c_table_value = cV_.data();
+        p.k_table_len = (int32_t)kT_.size();
+        p.k_table_T = kT_.data();
+        p.k_table_tensor = kK_.data();
+        p.perfusion_rate = mat.thermal.perfusion_rate;
+        p.blood_specific_heat = mat.thermal.blood_specific_heat;
+        p.arterial_temperature = mat.thermal.arterial_temperature;
+        p.metabolic_rate = mat.thermal.metabolic_rate;
+        if (mat.expansion) {
+            p.has_expansion = 1;
+            p.expansion_kind = (int32_t)mat.expansion->kind;
+            p.alpha_i = mat.expansion->alpha_i;
+            p.alpha_m = mat.expansion->alpha_m;
+            p.alpha_n = mat.expansion->alpha_n;
+            p.reference_temperature = mat.expansion->reference_temperature;
+        }
+        if (mat.fiber) {
+            p.has_fiber = 1;
+            for (int k = 0; k < 3; ++k) p.fiber[k] = (*mat.fiber)[k];
+        }
+        for (int k = 0; k < 3; ++k) {
+            p.axis_m[k] = mat.axis_m[k];
+            p.axis_n[k] = mat.axis_n[k];
+            p.body_force[k] = mb.body_force[k];
+        }
+        p.num_fixed_nodes = (int32_t)fixed_.size();
+        p.fixed_nodes = fixed_.data();
+        p.num_prescribed = (int32_t)presc_.size();
+        p.prescribed = presc_.data();
+        p.external_force = ext_.empty() ? nullptr : ext_.data();
+        p.num_fixed_temperatures = (int32_t)tfixN_.size();
+        p.fixed_temperature_nodes = tfixN_.data();
+        p.fixed_temperature_values = tfixV_.data();
+        p.initial_temperature = tb.initial_temperature;
+        p.num_sources = (int32_t)srcs_.size();
+        p.sources = srcs_.data();
+        p.dt = c.dt;
+        p.duration = c.duration;
+        p.mode = (int32_t)c.mode;
+        p.expansion_enabled = c.expansion_enabled;
+        p.temperature_dependent = c.temperature_dependent;
+        p.damping_gamma = c.damping_gamma;
+        p.hourglass_stiffness = c.hourglass_stiffness;
+        p.allow_unstable_dt = c.allow_unstable_dt;
+        p.workers = c.workers;
+    }
+    double interp(double T) const {  // ScalarTable::at (materials.hpp:46)
+        if (cT_.size() == 1 || T <= cT_.front()) return cV_.front();
+        if (T >= cT_.back()) return cV_.back();
+        size_t j = 0;
+        while (j + 2 < cT_.size() && T >= cT_[j + 1]) ++j;
+        return cV_[j] + (cV_[j + 1] - cV_[j]) * ((T - cT_[j]) / (cT_[j + 1] - cT_[j]));
+    }
+    void check(tvegpu_status st) {
+        if (st == TVEGPU_OK) return;
+        char msg[512];
+        int64_t s = -1;
+        int32_t n = -1;
+        tvegpu_last_error(h_, msg, sizeof msg, &s, &n);
+        rethrow(st, msg, s, n);
+    }
+    [[noreturn]] static void rethrow(tvegpu_status st, const std::string& msg, int64_t s, int32_t n) {
+        switch (st) {
+            case TVEGPU_E_PARSE: throw ParseError(msg);
+            case TVEGPU_E_VALIDATION: throw ValidationError(msg);
+            case TVEGPU_E_INSTABILITY: throw InstabilityError(msg, (long)s, (int)n);
+            case TVEGPU_E_IO: throw IoError(msg);
+            default: throw DeviceError(std::string(tvegpu_status_string(st)) + ": " + msg);
+        }
+    }
+    void pull_if_stale() {
+        if (mirror_valid_) return;
+        mirror_.temperatures.resize(N_);
+        mirror_.disp.resize(3 * (size_t)N_);
+        mirror_.disp_prev.resize(3 * (size_t)N_);
+        check(tvegpu_get_temperatures(h_, mirror_.temperatures.data()));
+        check(tvegpu_get_displacements(h_, mirror_.disp.data(), mirror_.disp_prev.data()));
+        mirror_.viscous.resize((size_t)E_ * P_);
+        if (P_) check(tvegpu_get_viscous(h_, mirror_.viscous.data()->data()));
+        mirror_.time = tvegpu_time(h_);
+        mirror_.step = (long)tvegpu_step_count(h_);
+        mirror_valid_ = true;
+    }
+    void push_if_dirty() {
+        if (!dirty_) return;
+        check(tvegpu_set_state(h_, mirror_.temperatures.data(), mirror_.disp.data(), mirror_.disp_prev.data(),
+                               P_ ? mirror_.viscous.data()->data() : nullptr, mirror_.time, mirror_.step));
+        dirty_ = false;
+    }
+
+    int N_, E_, P_;
+    tvegpu_engine* h_ = nullptr;
+    tvegpu_problem p_{};
+    std::vector<double> nodes_, fibers_, axes_, phi_, tau_, cT_, cV_, kT_, kK_, tfixV_, ext_;
+    std::vector<int32_t> elems_, fixed_, tfixN_;
+    std::vector<tvegpu_prescribed> presc_;
+    std::vector<tvegpu_source> srcs_;
+    SimulationState mirror_;
+    bool mirror_valid_ = false, dirty_ = false;
+};
+
+}  // namespace tve::gpu

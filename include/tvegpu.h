@@ -270,6 +270,21 @@ void tvegpu_plan_destroy(tvegpu_plan* plan);
 tvegpu_status tvegpu_nccl_unique_id(void* out128);
 
 /* ---------------------------------------------------------------------------
+ * Virtual multi-partition group: nparts RCB partitions of one problem driven in
+ * lockstep on ONE device, the halo exchanged by device copies instead of NCCL.
+ * Runs the multi-GPU data path (partition maps, boundary-first elements, halo
+ * pack, receive-area gathers) where only one GPU exists; results are
+ * bit-identical to a single partition.  get_fields writes every partition's
+ * nodes (shared nodes hold identical values) in original numbering.
+ * ------------------------------------------------------------------------- */
+typedef struct tvegpu_group tvegpu_group;
+tvegpu_status tvegpu_group_create(const tvegpu_problem* problem, int32_t nparts, const tvegpu_options* options,
+                                  tvegpu_group** out);
+tvegpu_status tvegpu_group_step(tvegpu_group* g, int64_t nsteps);
+tvegpu_status tvegpu_group_get_fields(tvegpu_group* g, double* T, double* disp, double* viscous);
+void tvegpu_group_destroy(tvegpu_group* g);
+
+/* ---------------------------------------------------------------------------
  * Measurement hooks (no reference counterpart; used by bench.py).
  * ------------------------------------------------------------------------- */
 /* cudaStream_t (as void*) every step kernel is launched on. */

@@ -348,7 +348,7 @@ tvegpu_status sync_and_check(tvegpu_engine* h, long long step_at_start, int cur_
     Clock c;
     std::memcpy(&c, h->h_words, sizeof(Clock));
     unsigned long long wi = h->h_words[3], we = h->h_words[4];
-    if (h->plan.nranks > 1) {
+    if (h->plan.nranks > 1 && h->comm) {  // NCCL ranks (loopback group partitions report separately)
         // agree on the first failure across ranks
         unsigned long long* dw = reinterpret_cast<unsigned long long*>(h->ptr.err_inst);
         auto& api = nccl();
@@ -388,7 +388,9 @@ tvegpu_status sync_and_check(tvegpu_engine* h, long long step_at_start, int cur_
     return TVEGPU_E_INSTABILITY;
 }
 
-void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_options& o) {
+// loopback: a partition driven by a tvegpu_group on one device (halo copied by the
+// group driver instead of NCCL) — single-GPU validation of the multi-GPU data path.
+void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_options& o, bool loopback = false) {
     if (o.device >= 0) CU(cudaSetDevice(o.device));
     CU(cudaGetDevice(&h->device));
     const int nranks = o.nranks > 0 ? o.nranks : 1;
@@ -651,10 +653,12 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     h->active.assign(h->regions.size(), 0);
     // ---- multi-GPU halo
     if (nranks > 1) {
-        if (!o.nccl_unique_id) throw Error(TVEGPU_E_ARG, "nranks > 1 needs options.nccl_unique_id");
-        ncclUniqueId id;
-        std::memcpy(&id, o.nccl_unique_id, sizeof id);
-        NC(nccl().CommInitRank(&h->comm, nranks, id, o.rank));
+        if (!loopback) {
+            if (!o.nccl_unique_id) throw Error(TVEGPU_E_ARG, "nranks > 1 needs options.nccl_unique_id");
+            ncclUniqueId id;
+            std::memcpy(&id, o.nccl_unique_id, sizeof id);
+            NC(nccl().CommInitRank(&h->comm, nranks, id, o.rank));
+        }
         const size_t ns = pl.send_off.back();
         const size_t nr = pl.recv_off.back();
         (void)nr;
@@ -1121,6 +1125,170 @@ tvegpu_status tvegpu_profile_kernels(tvegpu_engine* h, int32_t nsteps, double* m
         }
         return st;
     });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- virtual multi-partition group
+// P RCB partitions of one problem, each a full partition engine, driven in
+// lockstep on ONE device and stream; the halo is a device-to-device copy of each
+// neighbour's packed send segment into the receive area, in place of
+// ncclSend/ncclRecv.  Everything else — partition maps, boundary-first chunks,
+// pack kernel, receive-area gather lists, per-partition node updates — is the
+// multi-GPU code path, so results must be bit-identical to one partition.
+struct tvegpu_group {
+    std::vector<tvegpu_engine*> parts;
+    cudaStream_t s = nullptr;
+    std::string err;
+};
+
+namespace {
+void loopback_copy(tvegpu_group* G, bool mech) {
+    const int width = mech ? 3 : 1;
+    for (tvegpu_engine* r : G->parts) {
+        const RankPlan& pr = r->plan;
+        double* slots = mech ? r->ptr.slot_m : r->ptr.slot_th;
+        for (size_t j = 0; j < pr.neighbors.size(); ++j) {
+            const tvegpu_engine* q = G->parts[pr.neighbors[j]];
+            const RankPlan& ps = q->plan;
+            const size_t jj = std::find(ps.neighbors.begin(), ps.neighbors.end(), pr.rank) - ps.neighbors.begin();
+            if (jj == ps.neighbors.size()) throw Error(TVEGPU_E_ARG, "internal: asymmetric halo");
+            const size_t n = (size_t)(ps.send_off[jj + 1] - ps.send_off[jj]);
+            if (n != (size_t)(pr.recv_off[j + 1] - pr.recv_off[j])) throw Error(TVEGPU_E_ARG, "internal: halo size");
+            if (!n) continue;
+            const double* src = (mech ? q->send_m : q->send_th) + (size_t)ps.send_off[jj] * width;
+            double* dst = slots + ((size_t)pr.E * pr.nn + pr.recv_off[j]) * width;
+            CU(cudaMemcpyAsync(dst, src, n * width * sizeof(double), cudaMemcpyDeviceToDevice, G->s));
+        }
+    }
+}
+
+void pack(tvegpu_engine* h, bool mech) {
+    const int ns = h->plan.send_off.back();
+    if (ns > 0)
+        k_pack<<<blocks(ns, 256), 256, 0, h->s>>>(mech ? h->ptr.slot_m : h->ptr.slot_th, h->d_send_pos, ns, mech ? 3 : 1,
+                                                  mech ? h->send_m : h->send_th);
+}
+
+void group_step_once(tvegpu_group* G) {
+    tvegpu_engine* h0 = G->parts[0];
+    for (tvegpu_engine* h : G->parts) refresh_sources_if_needed(h, h->host_time);
+    if (h0->mode != TVEGPU_MECHANICAL_ONLY) {
+        for (tvegpu_engine* h : G->parts) {
+            const int nc = (int)h->plan.chunk_start.size() - 1;
+            h->nn == 4 ? launch_thermal_element<4>(h, 0, nc) : launch_thermal_element<8>(h, 0, nc);
+            pack(h, false);
+        }
+        loopback_copy(G, false);
+        for (tvegpu_engine* h : G->parts)
+            k_thermal_node<<<blocks(h->plan.N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur,
+                                                                    h->mode == TVEGPU_THERMAL_ONLY);
+    }
+    if (h0->mode != TVEGPU_THERMAL_ONLY) {
+        for (tvegpu_engine* h : G->parts) {
+            const int nc = (int)h->plan.chunk_start.size() - 1;
+            h->nn == 4 ? launch_mech_element<4>(h, 0, nc) : launch_mech_element<8>(h, 0, nc);
+            pack(h, true);
+        }
+        loopback_copy(G, true);
+        for (tvegpu_engine* h : G->parts) {
+            k_mech_node<<<blocks(h->plan.N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur, 1);
+            h->cur ^= 1;
+        }
+    }
+    CU(cudaGetLastError());
+    for (tvegpu_engine* h : G->parts) {
+        h->host_time += h->dt;
+        h->host_step += 1;
+    }
+}
+}  // namespace
+
+extern "C" {
+
+tvegpu_status tvegpu_group_create(const tvegpu_problem* p, int32_t nparts, const tvegpu_options* o,
+                                  tvegpu_group** out) {
+    if (!p || !out || nparts < 2) return TVEGPU_E_ARG;
+    *out = nullptr;
+    tvegpu_options def;
+    tvegpu_default_options(&def);
+    if (!o) o = &def;
+    auto* G = new tvegpu_group();
+    try {
+        for (int r = 0; r < nparts; ++r) {
+            tvegpu_options oo = *o;
+            oo.nranks = nparts;
+            oo.rank = r;
+            oo.reorder = 1;
+            auto* h = new tvegpu_engine();
+            G->parts.push_back(h);
+            build_engine(h, *p, oo, /*loopback=*/true);
+        }
+        G->s = G->parts[0]->s;
+        for (tvegpu_engine* h : G->parts)
+            if (h->s != G->s) {
+                CU(cudaStreamSynchronize(h->s));
+                CU(cudaStreamDestroy(h->s));
+                h->s = G->s;  // one stream orders the lockstep phases
+            }
+    } catch (const std::exception& e) {
+        g_create_error = e.what();
+        tvegpu_group_destroy(G);
+        return dynamic_cast<const Error*>(&e) ? static_cast<const Error&>(e).status : TVEGPU_E_ARG;
+    }
+    *out = G;
+    return TVEGPU_OK;
+}
+
+void tvegpu_group_destroy(tvegpu_group* G) {
+    if (!G) return;
+    if (G->s) cudaStreamSynchronize(G->s);
+    for (size_t k = 0; k < G->parts.size(); ++k) {
+        if (k > 0 && G->parts[k]->s == G->s) G->parts[k]->s = nullptr;  // shared stream: destroyed once
+        tvegpu_destroy(G->parts[k]);
+    }
+    delete G;
+}
+
+tvegpu_status tvegpu_group_step(tvegpu_group* G, int64_t n) {
+    if (!G || n < 0) return TVEGPU_E_ARG;
+    try {
+        std::vector<long long> s0;
+        std::vector<int> c0;
+        for (tvegpu_engine* h : G->parts) {
+            if (h->halted) return h->last_status;
+            s0.push_back(h->host_step);
+            c0.push_back(h->cur);
+        }
+        for (int64_t k = 0; k < n; ++k) group_step_once(G);
+        tvegpu_status worst = TVEGPU_OK;
+        for (size_t r = 0; r < G->parts.size(); ++r) {
+            tvegpu_engine* h = G->parts[r];
+            h->last_status = sync_and_check(h, s0[r], c0[r]);
+            if (h->last_status != TVEGPU_OK && worst == TVEGPU_OK) {
+                worst = h->last_status;
+                G->err = h->err;
+            }
+        }
+        return worst;
+    } catch (const Error& e) {
+        G->err = e.what();
+        return e.status;
+    }
+}
+
+tvegpu_status tvegpu_group_get_fields(tvegpu_group* G, double* T, double* disp, double* viscous) {
+    if (!G) return TVEGPU_E_ARG;
+    for (tvegpu_engine* h : G->parts) {
+        tvegpu_status st = TVEGPU_OK;
+        if (T || disp) st = tvegpu_make_snapshot(h, T, disp);
+        if (st == TVEGPU_OK && viscous && h->P) st = tvegpu_get_viscous(h, viscous);
+        if (st != TVEGPU_OK) {
+            G->err = h->err;
+            return st;
+        }
+    }
+    return TVEGPU_OK;
 }
 
 }  // extern "C"

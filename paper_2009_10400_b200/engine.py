@@ -112,6 +112,10 @@ EXPORTS = {
     "tvegpu_sync": (C.c_int, [C.c_void_p]),
     "tvegpu_profile_kernels": (C.c_int, [C.c_void_p, C.c_int32, _dp, C.POINTER(C.c_int32), C.c_char_p,
                                          C.c_size_t]),
+    "tvegpu_group_create": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "tvegpu_group_step": (C.c_int, [C.c_void_p, C.c_int64]),
+    "tvegpu_group_get_fields": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
+    "tvegpu_group_destroy": (None, [C.c_void_p]),
 }
 
 
@@ -194,6 +198,50 @@ def plan(problem: Problem, nranks=1, rank=0, reorder=True):
                     chunk_conn=arr(v.chunk_conn, E * nn).reshape(E, nn), max_chunk_slots=v.max_chunk_slots)
     finally:
         lib().tvegpu_plan_destroy(h)
+
+
+class PartitionGroup:
+    """nparts RCB partitions of one problem stepped in lockstep on one GPU, halo by
+    device copies: the multi-GPU data path, validated without a second GPU."""
+
+    def __init__(self, problem: Problem, nparts: int, *, device: int = -1):
+        L = lib()
+        self.problem = problem
+        self._c, self._keep = problem.to_c()
+        o = COptions()
+        L.tvegpu_default_options(C.byref(o))
+        o.device = device
+        h = C.c_void_p()
+        rc = L.tvegpu_group_create(C.byref(self._c), nparts, C.byref(o), C.byref(h))
+        if rc:
+            raise _BY_STATUS.get(rc, TveError)(L.tvegpu_create_error().decode())
+        self._h = h
+        self.N, self.E, self.P = problem.num_nodes, problem.num_elements, problem.prony_count
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tvegpu_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, n: int = 1):
+        rc = lib().tvegpu_group_step(self._h, n)
+        if rc:
+            raise _BY_STATUS.get(rc, TveError)(f"partition group step failed (status {rc})")
+
+    def fields(self):
+        T = np.full(self.N, np.nan)
+        u = np.full(3 * self.N, np.nan)
+        th = np.full(9 * self.E * self.P, np.nan)
+        rc = lib().tvegpu_group_get_fields(self._h, _P(T), _P(u), _P(th) if th.size else None)
+        if rc:
+            raise _BY_STATUS.get(rc, TveError)(f"partition group readback failed (status {rc})")
+        return dict(T=T, u=u, viscous=th)
 
 
 class Engine:
