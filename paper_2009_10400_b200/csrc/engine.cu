@@ -135,6 +135,7 @@ struct tvegpu_engine {
     // graphs keyed by (parity, nsteps)
     std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
     int steps_per_graph = 64;
+    bool warmed = false;  // a plain (un-captured) step has run
     // errors
     std::string err;
     long long err_step = -1;
@@ -268,7 +269,7 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr) {
     if (h->mode != TVEGPU_THERMAL_ONLY) {
         if (multi) {
             h->nn == 4 ? launch_mech_element<4>(h, 0, ncb) : launch_mech_element<8>(h, 0, ncb);
-            exchange(h, h->ptr.slot_m, h->send_m, h->recv_m, 3);
+            exchange(h, h->ptr.slot_m, h->send_m, h->recv_m, kMW);
             h->nn == 4 ? launch_mech_element<4>(h, ncb, nc) : launch_mech_element<8>(h, ncb, nc);
             CU(cudaStreamWaitEvent(h->s, h->ev_comm, 0));
         } else {
@@ -328,11 +329,14 @@ void enqueue_steps(tvegpu_engine* h, long long nsteps) {
             t += h->dt;
             ++k;
         }
-        if (k == h->steps_per_graph) {
+        // Graph replays once the engine has run one plain step (NCCL sets up its
+        // peer connections lazily on first use, which must not happen in capture).
+        if (k == h->steps_per_graph && h->warmed) {
             CU(cudaGraphLaunch(get_graph(h, (int)k), h->s));
             if (flips(h) && (k & 1)) h->cur ^= 1;
         } else {
             for (long long j = 0; j < k; ++j) enqueue_one_step(h);
+            h->warmed = true;
         }
         h->host_time = t;
         h->host_step += k;
@@ -615,9 +619,9 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     const size_t nslots = (size_t)nn * E + nrecv;
     m.nslots = (int)nslots;
     h->ptr.slot_th = dalloc<double>(own, nslots);
-    h->ptr.slot_m = dalloc<double>(own, 3 * nslots);
+    h->ptr.slot_m = dalloc<double>(own, kMW * nslots);
     CU(cudaMemsetAsync(h->ptr.slot_th, 0, nslots * 8, s));
-    CU(cudaMemsetAsync(h->ptr.slot_m, 0, 3 * nslots * 8, s));
+    CU(cudaMemsetAsync(h->ptr.slot_m, 0, kMW * nslots * 8, s));
     // ---- clock and error words
     h->ptr.clock = dalloc<Clock>(own, 1);
     h->ptr.err_inst = dalloc<unsigned long long>(own, 1);
@@ -664,7 +668,7 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
         (void)nr;
         h->d_send_pos = dupload(own, pl.send_slot, s);  // element-major slot ids
         h->send_th = dalloc<double>(own, ns);
-        h->send_m = dalloc<double>(own, 3 * ns);
+        h->send_m = dalloc<double>(own, kMW * ns);
         CU(cudaStreamSynchronize(s));
     }
     CU(cudaStreamSynchronize(s));
@@ -1144,7 +1148,7 @@ struct tvegpu_group {
 
 namespace {
 void loopback_copy(tvegpu_group* G, bool mech) {
-    const int width = mech ? 3 : 1;
+    const int width = mech ? kMW : 1;
     for (tvegpu_engine* r : G->parts) {
         const RankPlan& pr = r->plan;
         double* slots = mech ? r->ptr.slot_m : r->ptr.slot_th;
@@ -1166,7 +1170,7 @@ void loopback_copy(tvegpu_group* G, bool mech) {
 void pack(tvegpu_engine* h, bool mech) {
     const int ns = h->plan.send_off.back();
     if (ns > 0)
-        k_pack<<<blocks(ns, 256), 256, 0, h->s>>>(mech ? h->ptr.slot_m : h->ptr.slot_th, h->d_send_pos, ns, mech ? 3 : 1,
+        k_pack<<<blocks(ns, 256), 256, 0, h->s>>>(mech ? h->ptr.slot_m : h->ptr.slot_th, h->d_send_pos, ns, mech ? kMW : 1,
                                                   mech ? h->send_m : h->send_th);
 }
 

@@ -31,6 +31,10 @@ namespace tvegpu {
 constexpr int kMaxTable = 16;
 constexpr int kMaxProny = 4;
 constexpr int kChunkThreads = 128;  // element kernels: one thread per element of a 128-element chunk
+// Mechanical slot record: (fx, fy, fz, pad), 32 bytes, so an element writes each
+// contribution with one full-sector 256-bit store and a node reads it with one
+// 256-bit load (24-byte records needed three 8-byte requests per contribution).
+constexpr int kMW = 4;
 
 struct Clock {
     double time;
@@ -81,7 +85,7 @@ struct DevPtrs {
     const int32_t* csr_slot;   // gather list: element-major slot ids (e*nn + a, or receive area)
     const int32_t* node_orig;  // [N]
     double* slot_th;           // [nslots]
-    double* slot_m;            // [nslots][3]
+    double* slot_m;            // [nslots][kMW] (fx, fy, fz, pad)
     Clock* clock;
     unsigned long long* err_inst;  // (step << 33) | (field << 32) | orig node
     unsigned long long* err_elem;  // (step << 32) | orig element
@@ -386,10 +390,10 @@ __device__ __forceinline__ void gather3(const double* __restrict__ slots, const 
                                         int k1, double& f0, double& f1, double& f2) {
     f0 = f1 = f2 = 0.0;
     for (int k = k0; k < k1; ++k) {
-        const double* s = slots + (size_t)__ldg(idx + k) * 3;
-        f0 += __ldg(s);
-        f1 += __ldg(s + 1);
-        f2 += __ldg(s + 2);
+        const double4 s = ldg4(reinterpret_cast<const double4*>(slots) + __ldg(idx + k));
+        f0 += s.x;
+        f1 += s.y;
+        f2 += s.z;
     }
 }
 
@@ -619,18 +623,12 @@ __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
             for (int j = 0; j < 3; ++j)
                 Q[i * 3 + j] = Pm[i * 3 + 0] * A[0 * 3 + j] + Pm[i * 3 + 1] * A[1 * 3 + j] + Pm[i * 3 + 2] * A[2 * 3 + j];
     }
-    double* out = D.slot_m + (size_t)e * NN * 3;
+    double4* out = reinterpret_cast<double4*>(D.slot_m) + (size_t)e * NN;
     if constexpr (NN == 4) {
-        double f[12];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            f[0 * 3 + i] = -(Q[i * 3 + 0] + Q[i * 3 + 1] + Q[i * 3 + 2]);
-            f[1 * 3 + i] = Q[i * 3 + 0];
-            f[2 * 3 + i] = Q[i * 3 + 1];
-            f[3 * 3 + i] = Q[i * 3 + 2];
-        }
-#pragma unroll
-        for (int k = 0; k < 12; k += 2) reinterpret_cast<double2*>(out)[k / 2] = make_double2(f[k], f[k + 1]);
+        st4(out + 0, make_double4(-(Q[0] + Q[1] + Q[2]), -(Q[3] + Q[4] + Q[5]), -(Q[6] + Q[7] + Q[8]), 0.0));
+        st4(out + 1, make_double4(Q[0], Q[3], Q[6], 0.0));
+        st4(out + 2, make_double4(Q[1], Q[4], Q[7], 0.0));
+        st4(out + 3, make_double4(Q[2], Q[5], Q[8], 0.0));
     } else {
         // ---- closed-form hourglass, second pass over the element's nodes (L1-hot):
         //   U gamma_hat_al = U h_al - Hd c_al,  |gamma_hat_al|^2 = 8 + 8 |A^T c_al|^2,  c_al = X h_al
@@ -675,22 +673,16 @@ __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
                 for (int j = 0; j < 3; ++j) Q[i * 3 + j] -= k * Uh[al][i] * atc[j];
         }
 #pragma unroll
-        for (int a = 0; a < 8; a += 2) {
-            double f[6];
+        for (int a = 0; a < 8; ++a) {
+            double f[3];
 #pragma unroll
-            for (int b = 0; b < 2; ++b)
-#pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    const int aa = a + b;
-                    const double v = h8s(aa, 0) * Q[i * 3 + 0] + h8s(aa, 1) * Q[i * 3 + 1] + h8s(aa, 2) * Q[i * 3 + 2];
-                    const double hg = h8h(0, aa) * Uh[0][i] + h8h(1, aa) * Uh[1][i] + h8h(2, aa) * Uh[2][i] +
-                                      h8h(3, aa) * Uh[3][i];
-                    f[b * 3 + i] = v + k * hg;
-                }
-            double2* o = reinterpret_cast<double2*>(out + a * 3);
-            o[0] = make_double2(f[0], f[1]);
-            o[1] = make_double2(f[2], f[3]);
-            o[2] = make_double2(f[4], f[5]);
+            for (int i = 0; i < 3; ++i) {
+                const double v = h8s(a, 0) * Q[i * 3 + 0] + h8s(a, 1) * Q[i * 3 + 1] + h8s(a, 2) * Q[i * 3 + 2];
+                const double hg =
+                    h8h(0, a) * Uh[0][i] + h8h(1, a) * Uh[1][i] + h8h(2, a) * Uh[2][i] + h8h(3, a) * Uh[3][i];
+                f[i] = v + k * hg;
+            }
+            st4(out + a, make_double4(f[0], f[1], f[2], 0.0));
         }
     }
     if (P.diag) {
