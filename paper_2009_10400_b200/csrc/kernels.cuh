@@ -259,35 +259,58 @@ __device__ __forceinline__ void element_pass(const NodeStage& S, const int (&n)[
 // memory once per chunk (each node is used by up to 8 of the chunk's elements),
 // replacing 2*NN random 32-byte global gathers per element.  Returns this
 // thread's element (or -1) and its nodes' shared-memory slots.
+// The staging is latency-bound (a dependent index load, then the record loads),
+// so every load is issued before any is consumed: the element's own slot indices,
+// then up to kStageBatch node indices per thread, then all their records.
+constexpr int kStageBatch = 3;
 template <int NN>
 __device__ __forceinline__ int stage_chunk(const DevPtrs& D, const double4* __restrict__ R, int c,
                                            const NodeStage& S, int (&n)[NN]) {
     const int eb = __ldg(D.chunk_start + c), ne = __ldg(D.chunk_start + c + 1) - eb;
     const int u0 = __ldg(D.chunk_node_off + c), nu = __ldg(D.chunk_node_off + c + 1) - u0;
-    for (int k = threadIdx.x; k < nu; k += blockDim.x) {  // ascending node ids: coalesced loads
-        const int g = __ldg(D.chunk_nodes + u0 + k);
-        const int s = __ldg(D.chunk_node_slot + u0 + k);
-        const double4 r = ldg4(R + g);
-        const double4 x = ldg4(D.X + g);
-        S.a[s] = make_double2(r.x, r.y);
-        S.b[s] = make_double2(r.z, r.w);
-        S.c[s] = make_double2(x.x, x.y);
-        S.d[s] = make_double2(x.z, x.w);
-    }
     const int e = threadIdx.x < ne ? eb + threadIdx.x : -1;
+    uint4 w8 = make_uint4(0, 0, 0, 0);
+    uint2 w4 = make_uint2(0, 0);
     if (e >= 0) {
-        if constexpr (NN == 8) {
-            const uint4 w = __ldg(reinterpret_cast<const uint4*>(D.lconn) + e);
-            n[0] = w.x & 0xffff, n[1] = w.x >> 16, n[2] = w.y & 0xffff, n[3] = w.y >> 16;
-            n[4] = w.z & 0xffff, n[5] = w.z >> 16, n[6] = w.w & 0xffff, n[7] = w.w >> 16;
-        } else {
-            const uint2 w = __ldg(reinterpret_cast<const uint2*>(D.lconn) + e);
-            n[0] = w.x & 0xffff, n[1] = w.x >> 16, n[2] = w.y & 0xffff, n[3] = w.y >> 16;
+        if constexpr (NN == 8) w8 = __ldg(reinterpret_cast<const uint4*>(D.lconn) + e);
+        else w4 = __ldg(reinterpret_cast<const uint2*>(D.lconn) + e);
+    }
+    for (int k0 = 0; k0 < nu; k0 += kStageBatch * kChunkThreads) {  // ascending node ids: coalesced loads
+        int g[kStageBatch], s[kStageBatch];
+#pragma unroll
+        for (int j = 0; j < kStageBatch; ++j) {
+            const int k = k0 + j * kChunkThreads + threadIdx.x;
+            g[j] = k < nu ? __ldg(D.chunk_nodes + u0 + k) : -1;
+            s[j] = k < nu ? __ldg(D.chunk_node_slot + u0 + k) : 0;
         }
+        double4 r[kStageBatch], x[kStageBatch];
+#pragma unroll
+        for (int j = 0; j < kStageBatch; ++j)
+            if (g[j] >= 0) {
+                r[j] = ldg4(R + g[j]);
+                x[j] = ldg4(D.X + g[j]);
+            }
+#pragma unroll
+        for (int j = 0; j < kStageBatch; ++j)
+            if (g[j] >= 0) {
+                S.a[s[j]] = make_double2(r[j].x, r[j].y);
+                S.b[s[j]] = make_double2(r[j].z, r[j].w);
+                S.c[s[j]] = make_double2(x[j].x, x[j].y);
+                S.d[s[j]] = make_double2(x[j].z, x[j].w);
+            }
+    }
+    if constexpr (NN == 8) {
+        n[0] = w8.x & 0xffff, n[1] = w8.x >> 16, n[2] = w8.y & 0xffff, n[3] = w8.y >> 16;
+        n[4] = w8.z & 0xffff, n[5] = w8.z >> 16, n[6] = w8.w & 0xffff, n[7] = w8.w >> 16;
+    } else {
+        n[0] = w4.x & 0xffff, n[1] = w4.x >> 16, n[2] = w4.y & 0xffff, n[3] = w4.y >> 16;
     }
     __syncthreads();
     return e;
 }
+
+// Warm L1 with a coalesced SoA stream this thread will read later in the kernel.
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 // ------------------------------------------------------------------ K1: thermal element
 template <int NN>
@@ -429,6 +452,13 @@ __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
     const int ms = P.max_chunk_nodes;
     const NodeStage st{smem_planes, smem_planes + ms, smem_planes + 2 * ms, smem_planes + 3 * ms};
     int n[NN];
+    {  // the Prony history is read late in the kernel: start pulling it into L1 now
+        const int e0 = __ldg(D.chunk_start + c0 + blockIdx.x) + threadIdx.x;
+        if (e0 < P.E)
+            for (int p = 0; p < P.P; ++p)
+#pragma unroll
+                for (int q = 0; q < 6; ++q) prefetch_l1(D.theta + ((size_t)p * 6 + q) * P.E + e0);
+    }
     const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, st, n);
     if (e < 0) return;
     const int E = P.E;
