@@ -51,8 +51,8 @@ def weak_block(nranks, steps):
     p = configs._base(H8, nodes, el, 1e-4, steps)
     top = nodes[:, 2].max()
     p.fixed_nodes = np.nonzero(nodes[:, 2] <= 1e-12)[0].astype(np.int32)
-    p.prescribed = [Prescribed(np.nonzero(np.abs(nodes[:, 2] - top) <= 1e-9)[0].astype(np.int32), 2, 1e-2,
-                               1e-4 * steps)]
+    p.prescribed = [Prescribed(np.nonzero(np.abs(nodes[:, 2] - top) <= 1e-9)[0].astype(np.int32), 2,
+                               1e-2 * nz / 100, configs.ramp_time(top, 1e-4, steps))]
     c = 0.5 * np.array([nx, ny, nz]) * 1e-3
     p.sources = [SourceRegion(meshgen.elements_in_sphere(nodes, el, c, 0.01), configs.Q_R_TABLE5)]
     return p, f"cfg4 physics, H8 {nx}x{ny}x{nz} ({nx*ny*nz:,} el), RCB into {nranks} x 1M partitions"
@@ -70,6 +70,22 @@ def canonical_bytes(p):
         "mech_element": E * (28 * nn + 80 + 96 * P + fib + axes) + N * (32 + (24 if p.kind == H8 else 0)),
         "mech_node": E * 28 * nn + N * (85 + (24 if hasR else 0)),
     }
+
+
+def lumped_source_power(p):
+    """accumulate_nodal_sources (bioheat.hpp:65-69) in numpy: q_r V_e / nn to each node."""
+    X = p.nodes[p.elements]
+    if p.kind == H8:
+        s = np.array([[-1, -1, -1], [1, -1, -1], [1, 1, -1], [-1, 1, -1],
+                      [-1, -1, 1], [1, -1, 1], [1, 1, 1], [-1, 1, 1]], float)
+        V = 8.0 * np.linalg.det(np.einsum("eai,aj->eij", X, s) / 8.0)
+    else:
+        V = np.linalg.det(np.stack([X[:, 1] - X[:, 0], X[:, 2] - X[:, 0], X[:, 3] - X[:, 0]], axis=2)) / 6.0
+    q = np.zeros(p.num_nodes)
+    for r in p.sources:
+        for a in range(p.nn):
+            np.add.at(q, p.elements[r.elements, a], r.q_r * V[r.elements] / p.nn)
+    return q
 
 
 def load_peaks():
@@ -267,13 +283,14 @@ def run_ours(args):
     # end to end through the public API with host buffers: per step upload this step's
     # nodal source powers (pinned H2D, bioheat.hpp:57), step (finite check D2H), read T and u (D2H)
     e2e_steps = max(3, min(args.steps, args.e2e_steps))
-    power = np.zeros(p.num_nodes)
-    Th = np.empty(p.num_nodes)
-    uh = np.empty(3 * p.num_nodes)
+    # pinned host buffers (the contract's "from pinned host memory"); the power vector is
+    # the lumped regional source, re-sent every step as a generator control loop would
+    power = torch.from_numpy(lumped_source_power(p)).pin_memory().numpy()
+    Th = torch.empty(p.num_nodes, dtype=torch.float64, pin_memory=True).numpy()
+    uh = torch.empty(3 * p.num_nodes, dtype=torch.float64, pin_memory=True).numpy()
     barrier()
     t0 = time.perf_counter()
     for k in range(e2e_steps):
-        power[:] = 0.0
         eng.set_nodal_sources(power)
         eng.step(1)
         eng.make_snapshot(Th, uh)

@@ -45,7 +45,9 @@ int main(int argc, char** argv) {
     PrescribedDisplacement top;
     top.component = 2;
     top.target = 0.1;
-    top.ramp_time = 0.01 * steps;
+    // ramp over the run, never faster than ten dilatational wave transits (configs.ramp_time)
+    const double cd = std::sqrt((mat.hyperelastic.kappa + 4.0 * mat.hyperelastic.mu / 3.0) / mat.thermal.density);
+    top.ramp_time = std::max(0.01 * steps, 10.0 * L / cd);
     for (int i = 0; i < mesh.node_count(); ++i) {
         if (std::fabs(mesh.nodes[i][2]) < 1e-12) mb.fixed_nodes.push_back(i);
         if (std::fabs(mesh.nodes[i][2] - L) < 1e-12) top.nodes.push_back(i);

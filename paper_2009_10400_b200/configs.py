@@ -26,6 +26,14 @@ T5 = dict(
 Q_R_TABLE5 = 9_705_360.0
 
 
+def ramp_time(length, dt, steps):
+    """Prescribed-displacement ramp: over the run, but never faster than
+    ten dilatational wave transits of the block — a shorter run must not turn the
+    quasi-static pull into an impact that inverts elements."""
+    cd = math.sqrt((T5["kappa"] + 4 * T5["mu"] / 3) / T5["density"])
+    return max(dt * steps, 10.0 * length / cd)
+
+
 def _faces(nodes, axis, value, tol=1e-12):
     return np.nonzero(np.abs(nodes[:, axis] - value) <= tol)[0].astype(np.int32)
 
@@ -51,7 +59,7 @@ def cube_problem(kind, n, length, dt, steps, top_uz, source_diameter, prony_term
     elif prony_terms == 0:
         p.prony_phi, p.prony_tau = [], []
     p.fixed_nodes = _faces(nodes, 2, 0.0)
-    p.prescribed = [Prescribed(_faces(nodes, 2, length, tol=1e-9 * length), 2, top_uz, dt * steps)]
+    p.prescribed = [Prescribed(_faces(nodes, 2, length, tol=1e-9 * length), 2, top_uz, ramp_time(length, dt, steps))]
     src = meshgen.elements_in_sphere(nodes, el, [0.5 * length] * 3, source_diameter)
     p.sources = [SourceRegion(src, Q_R_TABLE5)]
     return p

@@ -146,6 +146,7 @@ struct tvegpu_engine {
     int pend_cur = 0;
     unsigned long long* h_words = nullptr;  // pinned: clock (3 words) + err_inst + err_elem
     double4* stage = nullptr;               // pinned readback staging (N records)
+    double* d_io = nullptr;                 // device I/O buffer in original numbering (4N doubles)
 };
 
 namespace {
@@ -703,8 +704,53 @@ void to_local_rec(tvegpu_engine* h, std::vector<double4>& r0, std::vector<double
 
 // One D2H copy of the current node record (u, T) into pinned staging, scattered to
 // original numbering; the previous record is copied only when u_prev is wanted.
+// Device-side renumbering for host I/O: the local (Morton/first-touch) order is
+// scattered to the caller's original numbering on the GPU, so the host transfer is
+// one contiguous copy straight into the caller's buffer (pinned buffers give the
+// full link bandwidth) and no host loop touches the data.
+__global__ void k_fields_to_orig(const double4* __restrict__ rec, const int32_t* __restrict__ node_orig, int N,
+                                 double* __restrict__ T, double* __restrict__ u) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const double4 r = rec[i];
+    const size_t o = (size_t)node_orig[i];
+    if (T) T[o] = r.w;
+    if (u) {
+        u[3 * o] = r.x;
+        u[3 * o + 1] = r.y;
+        u[3 * o + 2] = r.z;
+    }
+}
+__global__ void k_orig_to_local(const double* __restrict__ v, const int32_t* __restrict__ node_orig, int N,
+                                double* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < N) out[i] = v[node_orig[i]];
+}
+
+double* io_buffer(tvegpu_engine* h) {
+    if (!h->d_io) h->d_io = dalloc<double>(h->owned, 4 * (size_t)h->plan.N);
+    return h->d_io;
+}
+
 void read_fields(tvegpu_engine* h, double* T, double* u, double* up) {
     const int N = h->plan.N;
+    if (h->plan.nranks == 1 && N == h->N_global) {  // one partition covers every node
+        double* dT = io_buffer(h);
+        double* du = dT + N;
+        const double4* rc = h->cur ? h->ptr.rec1 : h->ptr.rec0;
+        const double4* rp = h->cur ? h->ptr.rec0 : h->ptr.rec1;
+        k_fields_to_orig<<<blocks(N, 256), 256, 0, h->s>>>(rc, h->ptr.node_orig, N, T ? dT : nullptr,
+                                                           u ? du : nullptr);
+        if (T) CU(cudaMemcpyAsync(T, dT, (size_t)N * 8, cudaMemcpyDeviceToHost, h->s));
+        if (u) CU(cudaMemcpyAsync(u, du, (size_t)3 * N * 8, cudaMemcpyDeviceToHost, h->s));
+        if (up) {
+            CU(cudaStreamSynchronize(h->s));  // du is reused
+            k_fields_to_orig<<<blocks(N, 256), 256, 0, h->s>>>(rp, h->ptr.node_orig, N, nullptr, du);
+            CU(cudaMemcpyAsync(up, du, (size_t)3 * N * 8, cudaMemcpyDeviceToHost, h->s));
+        }
+        CU(cudaStreamSynchronize(h->s));
+        return;
+    }
     if (!h->stage) CU(cudaMallocHost(&h->stage, (size_t)N * sizeof(double4)));
     const double4* rc = h->cur ? h->ptr.rec1 : h->ptr.rec0;
     const double4* rp = h->cur ? h->ptr.rec0 : h->ptr.rec1;
@@ -941,6 +987,15 @@ tvegpu_status tvegpu_set_nodal_sources(tvegpu_engine* h, const double* power) {
             return TVEGPU_OK;
         }
         h->source_override = true;
+        if (h->plan.nranks == 1 && h->plan.N == h->N_global) {  // upload as given, renumber on the device
+            double* d = io_buffer(h);
+            CU(cudaMemcpyAsync(d, power, (size_t)h->N_global * 8, cudaMemcpyHostToDevice, h->s));
+            k_orig_to_local<<<blocks(h->plan.N, 256), 256, 0, h->s>>>(d, h->ptr.node_orig, h->plan.N,
+                                                                     const_cast<double*>(h->ptr.qr));
+            CU(cudaGetLastError());
+            CU(cudaStreamSynchronize(h->s));  // the caller may reuse `power` on return
+            return TVEGPU_OK;
+        }
         for (int li = 0; li < h->plan.N; ++li) h->qr_host[li] = power[h->plan.node_orig[li]];
         CU(cudaMemcpyAsync(const_cast<double*>(h->ptr.qr), h->qr_host, (size_t)h->plan.N * 8,
                            cudaMemcpyHostToDevice, h->s));
