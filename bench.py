@@ -288,6 +288,10 @@ def run_ours(args):
     power = torch.from_numpy(lumped_source_power(p)).pin_memory().numpy()
     Th = torch.empty(p.num_nodes, dtype=torch.float64, pin_memory=True).numpy()
     uh = torch.empty(3 * p.num_nodes, dtype=torch.float64, pin_memory=True).numpy()
+    for k in range(2):  # untimed: first-call allocations (device I/O buffer) and page-ins
+        eng.set_nodal_sources(power)
+        eng.step(1)
+        eng.make_snapshot(Th, uh)
     barrier()
     t0 = time.perf_counter()
     for k in range(e2e_steps):
