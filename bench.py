@@ -288,16 +288,12 @@ def run_ours(args):
     power = torch.from_numpy(lumped_source_power(p)).pin_memory().numpy()
     Th = torch.empty(p.num_nodes, dtype=torch.float64, pin_memory=True).numpy()
     uh = torch.empty(3 * p.num_nodes, dtype=torch.float64, pin_memory=True).numpy()
-    for k in range(2):  # untimed: first-call allocations (device I/O buffer) and page-ins
-        eng.set_nodal_sources(power)
-        eng.step(1)
-        eng.make_snapshot(Th, uh)
+    for k in range(2):  # untimed: first-call allocations (device I/O buffers) and page-ins
+        eng.step_io(power, 1, Th, uh)
     barrier()
     t0 = time.perf_counter()
     for k in range(e2e_steps):
-        eng.set_nodal_sources(power)
-        eng.step(1)
-        eng.make_snapshot(Th, uh)
+        eng.step_io(power, 1, Th, uh)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if dist is not None:
@@ -307,7 +303,8 @@ def run_ours(args):
     e2e = {"value": E_total * e2e_steps / e2e_s, "unit": METRIC, "ms_per_step": 1e3 * e2e_s / e2e_steps,
            "h2d_bytes_per_step": 8 * p.num_nodes, "d2h_bytes_per_step": 32 * p.num_nodes + 40,
            "steps": e2e_steps,
-           "calls": "tvegpu_set_nodal_sources + tvegpu_step(1) + tvegpu_make_snapshot (C ABI, host buffers)"}
+           "calls": "tvegpu_step_io(power, 1, T, u): source upload + 1 step + T/u read-back (C ABI, pinned host "
+                    "buffers, copies overlapped with the step on a side stream)"}
 
     line = {"metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",

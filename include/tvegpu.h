@@ -204,6 +204,15 @@ tvegpu_status tvegpu_set_state(tvegpu_engine* h, const double* T, const double* 
  * NULL restores the regional HeatSourceSet schedule. */
 tvegpu_status tvegpu_set_nodal_sources(tvegpu_engine* h, const double* power);
 
+/* One closed-loop iteration with host buffers: the effect of
+ *   tvegpu_set_nodal_sources(h, power) (skipped when power is NULL);
+ *   tvegpu_step(h, n);  tvegpu_make_snapshot(h, T, disp)  (skipped when both are NULL)
+ * with the copies overlapped with the step on a second stream: the source upload
+ * runs while the thermal element kernel computes (only the thermal node update
+ * reads the sources) and the temperature read-back while the mechanical half of
+ * the last step computes.  n >= 1.  On an error return T and disp are undefined. */
+tvegpu_status tvegpu_step_io(tvegpu_engine* h, const double* power, int64_t n, double* T, double* disp);
+
 /* Diagnostics of the last mechanics phase (engine.hpp:101-105); requires
  * options.diagnostics = 1.  f_int: assembled internal force 3N; F, S: 9 per
  * element (row-major) deformation gradients and S_tilde.  Any may be NULL. */

@@ -116,6 +116,8 @@ struct tvegpu_engine {
     std::vector<void*> owned;
     cudaStream_t s = nullptr, sc = nullptr;
     cudaEvent_t ev_pack = nullptr, ev_comm = nullptr;
+    cudaEvent_t ev_src = nullptr, ev_T = nullptr;  // tvegpu_step_io: sources landed / T final
+    double* d_pw = nullptr;                        // tvegpu_step_io: uploaded source powers
     int cur = 0;
     double host_time = 0;
     long long host_step = 0;
@@ -245,7 +247,10 @@ void set_smem_limits(tvegpu_engine* h) {
 
 // One Engine::step() (engine.hpp:70-82): K1 K2 [K3 K4], with the halo exchange of
 // boundary-element slots overlapped with the interior elements.
-void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr) {
+// wait_src: event K2 waits on (sources uploaded on another stream); t_final:
+// event recorded once this step's temperatures are final (after K2).
+void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr, cudaEvent_t wait_src = nullptr,
+                      cudaEvent_t t_final = nullptr) {
     const int N = h->plan.N;
     const int nc = (int)h->plan.chunk_start.size() - 1, ncb = h->plan.nchunks_boundary;
     const bool multi = h->plan.nranks > 1;
@@ -264,9 +269,13 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr) {
             h->nn == 4 ? launch_thermal_element<4>(h, 0, nc) : launch_thermal_element<8>(h, 0, nc);
         }
         mark();
+        if (wait_src) CU(cudaStreamWaitEvent(h->s, wait_src, 0));
         k_thermal_node<<<blocks(N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur, h->mode == TVEGPU_THERMAL_ONLY);
         mark();
+    } else if (wait_src) {
+        CU(cudaStreamWaitEvent(h->s, wait_src, 0));
     }
+    if (t_final) CU(cudaEventRecord(t_final, h->s));
     if (h->mode != TVEGPU_THERMAL_ONLY) {
         if (multi) {
             h->nn == 4 ? launch_mech_element<4>(h, 0, ncb) : launch_mech_element<8>(h, 0, ncb);
@@ -491,6 +500,8 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     CU(cudaStreamCreateWithFlags(&h->sc, cudaStreamNonBlocking));
     CU(cudaEventCreateWithFlags(&h->ev_pack, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&h->ev_comm, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&h->ev_src, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&h->ev_T, cudaEventDisableTiming));
     CU(cudaMallocHost(&h->h_words, 8 * sizeof(unsigned long long)));
     cudaStream_t s = h->s;
     auto& own = h->owned;
@@ -848,6 +859,8 @@ void tvegpu_destroy(tvegpu_engine* h) {
     if (h->stage) cudaFreeHost(h->stage);
     if (h->qr_host) cudaFreeHost(h->qr_host);
     if (h->ev_pack) cudaEventDestroy(h->ev_pack);
+    if (h->ev_src) cudaEventDestroy(h->ev_src);
+    if (h->ev_T) cudaEventDestroy(h->ev_T);
     if (h->ev_comm) cudaEventDestroy(h->ev_comm);
     if (h->s) cudaStreamDestroy(h->s);
     if (h->sc) cudaStreamDestroy(h->sc);
@@ -1001,6 +1014,72 @@ tvegpu_status tvegpu_set_nodal_sources(tvegpu_engine* h, const double* power) {
                            cudaMemcpyHostToDevice, h->s));
         CU(cudaStreamSynchronize(h->s));
         return TVEGPU_OK;
+    });
+}
+
+// Closed-loop iteration with the host copies overlapped with the step (single
+// partition): the source upload runs on the side stream while K1 computes (only K2
+// reads the sources), and the temperature read-back runs there while K3/K4 compute
+// (T is final after K2).  Only the displacement read-back follows the step.
+tvegpu_status tvegpu_step_io(tvegpu_engine* h, const double* power, int64_t n, double* T, double* u) {
+    if (!h || n < 1) return TVEGPU_E_ARG;
+    if (h->plan.nranks != 1 || h->plan.N != h->N_global) {  // no overlap across partitions
+        tvegpu_status st = power ? tvegpu_set_nodal_sources(h, power) : TVEGPU_OK;
+        if (st == TVEGPU_OK) st = tvegpu_step(h, n);
+        if (st == TVEGPU_OK && (T || u)) st = tvegpu_make_snapshot(h, T, u);
+        return st;
+    }
+    return guard(h, [&] {
+        if (h->halted) {
+            h->err = "engine halted by an earlier failure; reset the state with tvegpu_set_state";
+            return h->last_status;
+        }
+        const int N = h->plan.N;
+        if (power) {
+            if (!h->d_pw) h->d_pw = dalloc<double>(h->owned, (size_t)N);
+            h->source_override = true;
+            CU(cudaMemcpyAsync(h->d_pw, power, (size_t)N * 8, cudaMemcpyHostToDevice, h->sc));
+            k_orig_to_local<<<blocks(N, 256), 256, 0, h->sc>>>(h->d_pw, h->ptr.node_orig, N,
+                                                                const_cast<double*>(h->ptr.qr));
+            CU(cudaEventRecord(h->ev_src, h->sc));
+        }
+        if (!h->pending) {
+            h->pending = true;
+            h->pend_step = h->host_step;
+            h->pend_cur = h->cur;
+        }
+        auto one = [&](bool first, bool last) {
+            refresh_sources_if_needed(h, h->host_time);
+            enqueue_one_step(h, nullptr, first && power ? h->ev_src : nullptr, last && T ? h->ev_T : nullptr);
+            h->host_time += h->dt;
+            h->host_step += 1;
+        };
+        one(true, n == 1);
+        if (n > 2) enqueue_steps(h, n - 2);
+        if (n > 1) {
+            // T lives in the record K2 of the last step updates: capture it before the flip
+            one(false, true);
+        }
+        double* dT = io_buffer(h);
+        double* du = dT + N;
+        if (T) {
+            // the record K2 of the last step updated: rec_cur as it was before that step's flip
+            const bool mech = h->mode != TVEGPU_THERMAL_ONLY;
+            const double4* rT = (h->cur ^ (mech ? 1 : 0)) ? h->ptr.rec1 : h->ptr.rec0;
+            CU(cudaStreamWaitEvent(h->sc, h->ev_T, 0));
+            k_fields_to_orig<<<blocks(N, 256), 256, 0, h->sc>>>(rT, h->ptr.node_orig, N, dT, nullptr);
+            CU(cudaMemcpyAsync(T, dT, (size_t)N * 8, cudaMemcpyDeviceToHost, h->sc));
+        }
+        if (u) {
+            const double4* rc = h->cur ? h->ptr.rec1 : h->ptr.rec0;
+            k_fields_to_orig<<<blocks(N, 256), 256, 0, h->s>>>(rc, h->ptr.node_orig, N, nullptr, du);
+            CU(cudaMemcpyAsync(u, du, (size_t)3 * N * 8, cudaMemcpyDeviceToHost, h->s));
+        }
+        CU(cudaGetLastError());
+        CU(cudaStreamSynchronize(h->sc));
+        h->pending = false;
+        h->last_status = sync_and_check(h, h->pend_step, h->pend_cur);
+        return h->last_status;
     });
 }
 

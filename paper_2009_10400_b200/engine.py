@@ -98,6 +98,7 @@ EXPORTS = {
     "tvegpu_step_count": (C.c_int64, [C.c_void_p]),
     "tvegpu_set_state": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp, C.c_double, C.c_int64]),
     "tvegpu_set_nodal_sources": (C.c_int, [C.c_void_p, _dp]),
+    "tvegpu_step_io": (C.c_int, [C.c_void_p, _dp, C.c_int64, _dp, _dp]),
     "tvegpu_get_diagnostics": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
     "tvegpu_last_error": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_int64),
                                     C.POINTER(C.c_int32)]),
@@ -324,6 +325,17 @@ class Engine:
         if rc:
             self._raise(rc)
         return u
+
+    def step_io(self, power=None, n=1, T=None, u=None):
+        """set_nodal_sources(power) + step(n) + make_snapshot(T, u) in one call, the
+        host copies overlapped with the step (tvegpu_step_io).  T/u are filled in place."""
+        src = None if power is None else _f64(power)
+        rc = lib().tvegpu_step_io(self._h, _P(src), int(n), _P(T), _P(u))
+        if power is not None:
+            self._src = src
+        if rc:
+            self._raise(rc)
+        return T, u
 
     def make_snapshot(self, T=None, u=None):
         """Engine::make_snapshot (engine.hpp:99): T and u in one device read."""

@@ -254,3 +254,31 @@ def test_partitioned_path_bit_identical(kind, n, nparts):
     a, b = one.state(), grp.fields()
     for k in ("T", "u", "viscous"):
         np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+
+
+@pytest.mark.parametrize("kind", [T4, H8])
+@pytest.mark.parametrize("mode", [COUPLED, THERMAL_ONLY, MECHANICAL_ONLY])
+@pytest.mark.parametrize("n", [1, 2, 70])
+def test_step_io_matches_separate_calls(kind, mode, n):
+    """tvegpu_step_io (copies overlapped on a side stream) == set_nodal_sources +
+    step + make_snapshot, bit for bit, for every source vector of a changing schedule."""
+    p = configs.small_problem(kind=kind, n=4, steps=6 * n)
+    p.mode = mode
+    a, b = tg.Engine(p), tg.Engine(p)
+    rng = np.random.default_rng(n)
+    Ta, ua = np.empty(p.num_nodes), np.empty(3 * p.num_nodes)
+    for it in range(3):
+        q = rng.uniform(0, 2e-3, p.num_nodes)
+        a.set_nodal_sources(q)
+        a.step(n)
+        Tb_, ub_ = a.make_snapshot()
+        b.step_io(q, n, Ta, ua)
+        np.testing.assert_array_equal(Ta, Tb_)
+        np.testing.assert_array_equal(ua, ub_)
+    b.step_io(None, 1, Ta, None)  # keep the last sources, temperatures only
+    a.step(1)
+    np.testing.assert_array_equal(Ta, a.temperatures())
+    assert a.step_count() == b.step_count() and a.time() == b.time()
+    sa, sb = a.state(), b.state()
+    for k in ("T", "u", "u_prev", "viscous"):
+        np.testing.assert_array_equal(sa[k], sb[k], err_msg=k)
