@@ -42,3 +42,40 @@ for k in range(23):
         ts += [t1 - t0, t2 - t1, t3 - t2]
 ts /= 20
 print("set_nodal_sources %.3f ms  step(1) %.3f ms  make_snapshot %.3f ms  total %.3f" % (*(ts * 1e3), ts.sum() * 1e3))
+
+# set_nodal_sources alone, back to back (no step in between)
+torch.cuda.synchronize()
+t = time.perf_counter()
+for _ in range(20):
+    eng.set_nodal_sources(power)
+print("set_nodal_sources alone %.3f ms" % ((time.perf_counter() - t) / 20 * 1e3))
+t = time.perf_counter()
+for _ in range(20):
+    eng.make_snapshot(Th, uh)
+print("make_snapshot alone %.3f ms" % ((time.perf_counter() - t) / 20 * 1e3))
+t = time.perf_counter()
+for _ in range(20):
+    eng.step(1)
+print("step(1) alone %.3f ms" % ((time.perf_counter() - t) / 20 * 1e3))
+pw = torch.from_numpy(power)
+dd = torch.empty_like(pw, device="cuda")
+torch.cuda.synchronize()
+t = time.perf_counter()
+for _ in range(20):
+    dd.copy_(pw, non_blocking=True)
+    torch.cuda.synchronize()
+print("torch H2D 8MB + sync %.3f ms  (pinned=%s)" % ((time.perf_counter() - t) / 20 * 1e3, pw.is_pinned()))
+pg = np.array(power)  # pageable copy
+t = time.perf_counter()
+for _ in range(20):
+    eng.set_nodal_sources(pg)
+print("set_nodal_sources pageable %.3f ms" % ((time.perf_counter() - t) / 20 * 1e3))
+import ctypes
+from paper_2009_10400_b200 import engine as _e
+L = _e.lib()
+src = _e._f64(power)
+ptr = src.ctypes.data_as(_e._dp)
+t = time.perf_counter()
+for _ in range(20):
+    L.tvegpu_set_nodal_sources(eng._h, ptr)
+print("raw C call (pinned) %.3f ms" % ((time.perf_counter() - t) / 20 * 1e3))
