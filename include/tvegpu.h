@@ -213,6 +213,32 @@ tvegpu_status tvegpu_set_nodal_sources(tvegpu_engine* h, const double* power);
  * the last step computes.  n >= 1.  On an error return T and disp are undefined. */
 tvegpu_status tvegpu_step_io(tvegpu_engine* h, const double* power, int64_t n, double* T, double* disp);
 
+/* ---- run-level outputs on the device ----
+ * RunSummary node extrema (engine.hpp:57-66) by deterministic device reductions
+ * (a 56-byte read-back instead of the full fields); multi-GPU: all-reduced. */
+typedef struct tvegpu_summary {
+    int64_t steps;
+    double time;
+    double max_temperature; /* over nodes, current state */
+    double min_disp[3];     /* per component */
+    double max_disp[3];
+} tvegpu_summary;
+tvegpu_status tvegpu_get_summary(tvegpu_engine* h, tvegpu_summary* out);
+
+/* ablation_volume: exact volume [m^3] of {T >= threshold} for the
+ * piecewise-linear temperature by analytic clipping of each tetrahedron (an H8 is
+ * split into 6 around its 0-6 diagonal), measured at X + u when deformed != 0
+ * (SPEC.md:460).  elements_above (may be NULL): elements with a non-zero clipped
+ * volume.  Multi-GPU: summed over ranks. */
+tvegpu_status tvegpu_ablation_volume(tvegpu_engine* h, double threshold, int32_t deformed, double* volume,
+                                     int64_t* elements_above);
+
+/* Snapshot element fields (engine.hpp:47-55, OutputSpec write_det_f / write_stress):
+ * det F and the largest principal value of S_tilde (PK2) per element, original
+ * order, from the last mechanics phase.  Requires options.diagnostics = 1 and a
+ * single-partition engine.  Either pointer may be NULL. */
+tvegpu_status tvegpu_element_fields(tvegpu_engine* h, double* det_f, double* max_principal_stress);
+
 /* Diagnostics of the last mechanics phase (engine.hpp:101-105); requires
  * options.diagnostics = 1.  f_int: assembled internal force 3N; F, S: 9 per
  * element (row-major) deformation gradients and S_tilde.  Any may be NULL. */

@@ -47,6 +47,8 @@ def lib():
         L.oracle_total_energy.argtypes = [C.c_void_p]
         L.oracle_precompute.argtypes = [C.c_void_p] + [_dp] * 7 + [_ip] * 3
         L.oracle_critical_timestep.argtypes = [C.c_void_p, _dp]
+        L.oracle_ablation_volume.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _ip, _dp, _dp, C.c_double, _dp,
+                                             C.POINTER(C.c_long)]
         L.oracle_strain_energy.argtypes = [_dp, C.c_double, C.c_double, C.c_double, _dp, _dp]
         L.oracle_pk2_stress.argtypes = [_dp, C.c_double, C.c_double, C.c_double, _dp, _dp]
         L.oracle_total_pk2_stress.argtypes = [_dp, _dp, C.c_double, C.c_double, C.c_double, _dp, _dp]
@@ -177,6 +179,20 @@ def critical_timestep(problem):
     if rc:
         raise OracleError(rc, lib().oracle_error().decode())
     return float(out[0]), float(out[1])
+
+
+def ablation_volume(kind, nodes, elements, T, threshold, disp=None):
+    """ablation_volume (SPEC.md:435-443) -> (volume [m^3], elements_above); kind 'T4'/'H8' or 0/1."""
+    k = 1 if kind in (1, "H8") else 0
+    nodes = f64(np.asarray(nodes).reshape(-1))
+    elements = np.ascontiguousarray(np.asarray(elements).reshape(-1), dtype=np.int32)
+    T = f64(T)
+    disp = None if disp is None else f64(np.asarray(disp).reshape(-1))
+    vol, cnt = np.empty(1), C.c_long()
+    nn = 8 if k else 4
+    _chk(lib().oracle_ablation_volume(k, len(T), len(elements) // nn, P(nodes), IP(elements), P(T), P(disp),
+                                      float(threshold), P(vol), C.byref(cnt)))
+    return float(vol[0]), int(cnt.value)
 
 
 def _chk(rc):

@@ -380,4 +380,25 @@ int oracle_step_temperature(int N, double* T, const double* loads, const double*
     });
 }
 
+
+// ablation_volume over raw arrays: kind 0 = T4, 1 = H8.
+int oracle_ablation_volume(int kind, int num_nodes, int num_elements, const double* nodes, const int* elements,
+                           const double* T, const double* disp, double threshold, double* volume, long* count) {
+    return guarded([&] {
+        Mesh m;
+        m.kind = kind == 1 ? ElementKind::H8 : ElementKind::T4;
+        const int nn = kind == 1 ? 8 : 4;
+        m.nodes.resize(num_nodes);
+        for (int i = 0; i < num_nodes; ++i)
+            for (int c = 0; c < 3; ++c) m.nodes[i][c] = nodes[3 * (size_t)i + c];
+        m.elements.resize(num_elements);
+        for (int e = 0; e < num_elements; ++e)
+            for (int a = 0; a < nn; ++a) m.elements[e][a] = elements[(size_t)nn * e + a];
+        std::vector<double> u;
+        if (disp) u.assign(disp, disp + 3 * (size_t)num_nodes);
+        const AblationReport r = ablation_volume(m, std::span<const double>(T, num_nodes), threshold, disp ? &u : nullptr);
+        *volume = r.volume;
+        *count = r.elements_above;
+    });
+}
 }  // extern "C"

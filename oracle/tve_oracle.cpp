@@ -891,4 +891,74 @@ double Engine::total_energy() const {
     return Ek + Es;
 }
 
+// ---- ablation_volume ----
+// k = #nodes at or above the threshold.  With t_ij = (T_i - thr) / (T_i - T_j) the
+// fraction of edge i -> j above the threshold (i above, j below):
+//   k = 1 (node a):      t_ab t_ac t_ad                      (corner tetrahedron)
+//   k = 3 (node d below): 1 - s_da s_db s_dc,  s_dj = (thr - T_d) / (T_j - T_d)
+//   k = 2 (a, b above):  the wedge a p_ac p_ad | b p_bc p_bd split into the tetrahedra
+//                        (a p_ac p_ad p_bd), (a p_ac p_bc p_bd), (a b p_bc p_bd), whose
+//                        barycentric determinants give
+//                        t_ac t_ad (1 - t_bd) + t_ac t_bd (1 - t_bc) + t_bc t_bd.
+double tet_fraction_above(const double T[4], double thr) {
+    int up[4], dn[4], nu = 0, nd = 0;
+    for (int i = 0; i < 4; ++i) {
+        if (T[i] >= thr) up[nu++] = i;
+        else dn[nd++] = i;
+    }
+    auto t = [&](int i, int j) { return (T[i] - thr) / (T[i] - T[j]); };
+    switch (nu) {
+        case 0: return 0.0;
+        case 4: return 1.0;
+        case 1: return t(up[0], dn[0]) * t(up[0], dn[1]) * t(up[0], dn[2]);
+        case 3: {
+            const int d = dn[0];
+            auto s = [&](int j) { return (thr - T[d]) / (T[j] - T[d]); };
+            return 1.0 - s(up[0]) * s(up[1]) * s(up[2]);
+        }
+        default: {
+            const int a = up[0], b = up[1], c = dn[0], d = dn[1];
+            const double tac = t(a, c), tad = t(a, d), tbc = t(b, c), tbd = t(b, d);
+            return tac * tad * (1.0 - tbd) + tac * tbd * (1.0 - tbc) + tbc * tbd;
+        }
+    }
+}
+
+namespace {
+const int kHexTets[6][4] = {{0, 1, 2, 6}, {0, 2, 3, 6}, {0, 3, 7, 6}, {0, 7, 4, 6}, {0, 4, 5, 6}, {0, 5, 1, 6}};
+}
+
+AblationReport ablation_volume(const Mesh& mesh, std::span<const double> T, double threshold,
+                               const std::vector<double>* disp) {
+    AblationReport r;
+    const int nn = mesh.nodes_per_elem();
+    const int ntet = nn == 4 ? 1 : 6;
+    for (int e = 0; e < mesh.element_count(); ++e) {
+        double ve = 0;
+        for (int k = 0; k < ntet; ++k) {
+            int id[4];
+            for (int q = 0; q < 4; ++q) id[q] = mesh.elements[e][nn == 4 ? q : kHexTets[k][q]];
+            Vec3 x[4];
+            double Tv[4];
+            for (int q = 0; q < 4; ++q) {
+                x[q] = mesh.nodes[id[q]];
+                if (disp)
+                    for (int c = 0; c < 3; ++c) x[q][c] += (*disp)[3 * (size_t)id[q] + c];
+                Tv[q] = T[id[q]];
+            }
+            const double f = tet_fraction_above(Tv, threshold);
+            if (f == 0.0) continue;
+            Mat3 M;
+            for (int c = 0; c < 3; ++c)
+                for (int q = 0; q < 3; ++q) M[c][q] = x[q + 1][c] - x[0][c];
+            ve += f * std::fabs(det(M)) / 6.0;
+        }
+        if (ve > 0) {
+            r.volume += ve;
+            ++r.elements_above;
+        }
+    }
+    return r;
+}
+
 }  // namespace tve_oracle

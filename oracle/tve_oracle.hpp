@@ -280,4 +280,19 @@ private:
     int workers_ = 1;
 };
 
+// ---- run-level outputs ----
+// ablation_volume: exact volume of {x : T_h(x) >= threshold} for
+// the piecewise-linear field, by analytic clipping of each tetrahedron; an H8 is
+// split into 6 tetrahedra around its 0-6 diagonal first.  Measured at X + u when
+// disp is given (deformed is the default when displacements exist).
+// *elements_above counts the elements with a non-zero clipped volume.
+struct AblationReport {
+    double volume = 0;
+    long elements_above = 0;
+};
+AblationReport ablation_volume(const Mesh& mesh, std::span<const double> T, double threshold,
+                               const std::vector<double>* disp);
+// Volume fraction of a tetrahedron above `threshold` given its nodal values.
+double tet_fraction_above(const double T[4], double threshold);
+
 }  // namespace tve_oracle

@@ -149,6 +149,10 @@ struct tvegpu_engine {
     unsigned long long* h_words = nullptr;  // pinned: clock (3 words) + err_inst + err_elem
     double4* stage = nullptr;               // pinned readback staging (N records)
     double* d_io = nullptr;                 // device I/O buffer in original numbering (4N doubles)
+    int32_t* d_conn = nullptr;              // local connectivity (run-level outputs only, lazily)
+    double* d_part = nullptr;               // per-block partials of the run-level reductions
+    double* h_part = nullptr;               // pinned: reduced run-level outputs
+    double* d_ef = nullptr;                 // element fields in original order (2E, lazily)
 };
 
 namespace {
@@ -790,6 +794,196 @@ void read_fields(tvegpu_engine* h, double* T, double* u, double* up) {
     }
 }
 
+// ------------------------------------------------------------------ run-level outputs
+// Deterministic two-pass reductions: fixed per-block trees, then one block over the
+// block partials in index order, so repeated calls return identical bits.
+constexpr int kRedThreads = 256, kRedMaxBlocks = 2048;
+
+// Block tree of NV doubles per thread under op (0 sum, 1 max, 2 min), written by thread 0.
+template <int NV>
+__device__ void block_reduce(double (&v)[NV], const int (&op)[NV], double* out) {
+    __shared__ double sh[NV][kRedThreads];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) sh[q][threadIdx.x] = v[q];
+    __syncthreads();
+    for (int s = kRedThreads / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s)
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                const double a = sh[q][threadIdx.x], b = sh[q][threadIdx.x + s];
+                sh[q][threadIdx.x] = op[q] == 0 ? a + b : op[q] == 1 ? fmax(a, b) : fmin(a, b);
+            }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int q = 0; q < NV; ++q) out[q] = sh[q][0];
+}
+
+// Second pass: one block folds the nb partial rows (stride NV) in index order.
+template <int NV>
+__global__ void k_reduce_rows(const double* __restrict__ part, int nb, int o0, int o1, int o2, int o3, int o4,
+                              int o5, int o6, double* __restrict__ out) {
+    const int opsv[7] = {o0, o1, o2, o3, o4, o5, o6};
+    int op[NV];
+    double v[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        op[q] = opsv[q];
+        v[q] = op[q] == 0 ? 0.0 : op[q] == 1 ? -INFINITY : INFINITY;
+    }
+    for (int b = threadIdx.x; b < nb; b += kRedThreads)
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            const double x = part[(size_t)b * NV + q];
+            v[q] = op[q] == 0 ? v[q] + x : op[q] == 1 ? fmax(v[q], x) : fmin(v[q], x);
+        }
+    block_reduce<NV>(v, op, out);
+}
+
+// RunSummary node extrema (engine.hpp:57-66): max T, per-component min and max of u.
+__global__ void __launch_bounds__(kRedThreads) k_summary(const double4* __restrict__ rec, int N, double* part) {
+    const int op[7] = {1, 2, 2, 2, 1, 1, 1};
+    double v[7] = {-INFINITY, INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    for (int i = blockIdx.x * kRedThreads + threadIdx.x; i < N; i += gridDim.x * kRedThreads) {
+        const double4 r = rec[i];
+        v[0] = fmax(v[0], r.w);
+        v[1] = fmin(v[1], r.x), v[2] = fmin(v[2], r.y), v[3] = fmin(v[3], r.z);
+        v[4] = fmax(v[4], r.x), v[5] = fmax(v[5], r.y), v[6] = fmax(v[6], r.z);
+    }
+    block_reduce<7>(v, op, part + (size_t)blockIdx.x * 7);
+}
+
+// Volume fraction of a tetrahedron above thr (oracle tet_fraction_above).
+__device__ double tet_fraction_above(const double (&T)[4], double thr) {
+    int up[4], dn[4], nu = 0, nd = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if (T[i] >= thr) up[nu++] = i;
+        else dn[nd++] = i;
+    }
+    auto t = [&](int i, int j) { return (T[i] - thr) / (T[i] - T[j]); };
+    if (nu == 0) return 0.0;
+    if (nu == 4) return 1.0;
+    if (nu == 1) return t(up[0], dn[0]) * t(up[0], dn[1]) * t(up[0], dn[2]);
+    if (nu == 3) {
+        const int d = dn[0];
+        auto sd = [&](int j) { return (thr - T[d]) / (T[j] - T[d]); };
+        return 1.0 - sd(up[0]) * sd(up[1]) * sd(up[2]);
+    }
+    const int a = up[0], b = up[1], c = dn[0], d = dn[1];
+    const double tac = t(a, c), tad = t(a, d), tbc = t(b, c), tbd = t(b, d);
+    return tac * tad * (1.0 - tbd) + tac * tbd * (1.0 - tbc) + tbc * tbd;
+}
+
+__constant__ int c_hex_tets[6][4] = {{0, 1, 2, 6}, {0, 2, 3, 6}, {0, 3, 7, 6}, {0, 7, 4, 6}, {0, 4, 5, 6}, {0, 5, 1, 6}};
+
+// ablation_volume: per element the clipped volume of its
+// tetrahedra (H8: 6 around the 0-6 diagonal) at X (+ u when deformed); partial rows
+// {volume, #elements with a non-zero clipped volume}.
+template <int NN>
+__global__ void __launch_bounds__(kRedThreads) k_ablation(const int32_t* __restrict__ conn, const double4* __restrict__ X,
+                                                     const double4* __restrict__ rec, int E, double thr, int deformed,
+                                                     double* part) {
+    double v[2] = {0.0, 0.0};
+    const int op[2] = {0, 0};
+    for (int e = blockIdx.x * kRedThreads + threadIdx.x; e < E; e += gridDim.x * kRedThreads) {
+        double px[NN][3], Tn[NN];
+#pragma unroll
+        for (int a = 0; a < NN; ++a) {
+            const int i = conn[(size_t)e * NN + a];
+            const double4 x = X[i], r = rec[i];
+            px[a][0] = x.x + (deformed ? r.x : 0.0);
+            px[a][1] = x.y + (deformed ? r.y : 0.0);
+            px[a][2] = x.z + (deformed ? r.z : 0.0);
+            Tn[a] = r.w;
+        }
+        double ve = 0.0;
+        for (int k = 0; k < (NN == 4 ? 1 : 6); ++k) {
+            int id[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) id[q] = NN == 4 ? q : c_hex_tets[k][q];
+            const double Tq[4] = {Tn[id[0]], Tn[id[1]], Tn[id[2]], Tn[id[3]]};
+            const double f = tet_fraction_above(Tq, thr);
+            if (f == 0.0) continue;
+            double M[3][3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int q = 0; q < 3; ++q) M[c][q] = px[id[q + 1]][c] - px[id[0]][c];
+            const double dt = M[0][0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1]) -
+                              M[0][1] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
+                              M[0][2] * (M[1][0] * M[2][1] - M[1][1] * M[2][0]);
+            ve += f * fabs(dt) / 6.0;
+        }
+        if (ve > 0.0) {
+            v[0] += ve;
+            v[1] += 1.0;
+        }
+    }
+    block_reduce<2>(v, op, part + (size_t)blockIdx.x * 2);
+}
+
+// det F and the largest eigenvalue of S_tilde (PK2) per element, original order,
+// from the diagnostics of the last mechanics phase (Snapshot det_f /
+// max_principal_stress, engine.hpp:47-55).
+__global__ void k_element_fields(const double* __restrict__ F, const double* __restrict__ S,
+                                 const int32_t* __restrict__ elem_orig, int E, double* detf, double* smax) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    const double* f = F + (size_t)e * 9;
+    const double* m = S + (size_t)e * 9;
+    const int o = elem_orig[e];
+    if (detf)
+        detf[o] = f[0] * (f[4] * f[8] - f[5] * f[7]) - f[1] * (f[3] * f[8] - f[5] * f[6]) +
+                  f[2] * (f[3] * f[7] - f[4] * f[6]);
+    if (smax) {
+        // symmetric 3x3 eigenvalues, trigonometric form
+        const double a = m[0], b = m[4], c = m[8], d = m[1], ee = m[5], ff = m[2];
+        const double p1 = d * d + ee * ee + ff * ff;
+        const double q = (a + b + c) / 3.0;
+        double lmax;
+        if (p1 == 0.0) {
+            lmax = fmax(a, fmax(b, c));
+        } else {
+            const double p2 = (a - q) * (a - q) + (b - q) * (b - q) + (c - q) * (c - q) + 2.0 * p1;
+            const double p = sqrt(p2 / 6.0);
+            const double ip = 1.0 / p;
+            const double B0 = (a - q) * ip, B1 = (b - q) * ip, B2 = (c - q) * ip, B3 = d * ip, B4 = ee * ip,
+                         B5 = ff * ip;
+            const double r = 0.5 * (B0 * (B1 * B2 - B4 * B4) - B3 * (B3 * B2 - B4 * B5) + B5 * (B3 * B4 - B1 * B5));
+            const double phi = r <= -1.0 ? M_PI / 3.0 : r >= 1.0 ? 0.0 : acos(r) / 3.0;
+            lmax = q + 2.0 * p * cos(phi);
+        }
+        smax[o] = lmax;
+    }
+}
+
+// Runs one two-pass reduction (kernel writes nb rows of NV) and returns the NV
+// values in h->h_part; for nranks > 1 the values are all-reduced across ranks.
+template <int NV, class Launch>
+void reduce_to_host(tvegpu_engine* h, int nb, const int (&op)[NV], Launch&& launch) {
+    if (!h->d_part) h->d_part = dalloc<double>(h->owned, (size_t)kRedMaxBlocks * 8 + 8);
+    if (!h->h_part) CU(cudaMallocHost(&h->h_part, 8 * sizeof(double)));
+    double* fin = h->d_part + (size_t)kRedMaxBlocks * 8;
+    launch(h->d_part);
+    int o[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int q = 0; q < NV; ++q) o[q] = op[q];
+    k_reduce_rows<NV><<<1, kRedThreads, 0, h->s>>>(h->d_part, nb, o[0], o[1], o[2], o[3], o[4], o[5], o[6], fin);
+    CU(cudaGetLastError());
+    if (h->comm) {
+        NcclApi& api = nccl();
+        // group the ops by kind: sums, maxima, minima (one all-reduce per value, tiny)
+        for (int q = 0; q < NV; ++q)
+            NC(api.AllReduce(fin + q, fin + q, 1, ncclFloat64, op[q] == 0 ? ncclSum : op[q] == 1 ? ncclMax : ncclMin,
+                             h->comm, h->s));
+    }
+    CU(cudaMemcpyAsync(h->h_part, fin, NV * sizeof(double), cudaMemcpyDeviceToHost, h->s));
+    CU(cudaStreamSynchronize(h->s));
+}
+
+int red_blocks(int n) { return std::max(1, std::min(kRedMaxBlocks, (n + kRedThreads - 1) / kRedThreads)); }
+
 }  // namespace
 
 // =====================================================================================
@@ -860,6 +1054,7 @@ void tvegpu_destroy(tvegpu_engine* h) {
     if (h->qr_host) cudaFreeHost(h->qr_host);
     if (h->ev_pack) cudaEventDestroy(h->ev_pack);
     if (h->ev_src) cudaEventDestroy(h->ev_src);
+    if (h->h_part) cudaFreeHost(h->h_part);
     if (h->ev_T) cudaEventDestroy(h->ev_T);
     if (h->ev_comm) cudaEventDestroy(h->ev_comm);
     if (h->s) cudaStreamDestroy(h->s);
@@ -1080,6 +1275,74 @@ tvegpu_status tvegpu_step_io(tvegpu_engine* h, const double* power, int64_t n, d
         h->pending = false;
         h->last_status = sync_and_check(h, h->pend_step, h->pend_cur);
         return h->last_status;
+    });
+}
+
+tvegpu_status tvegpu_get_summary(tvegpu_engine* h, tvegpu_summary* out) {
+    if (!h || !out) return TVEGPU_E_ARG;
+    return guard(h, [&] {
+        const int nb = red_blocks(h->plan.N);
+        const int op[7] = {1, 2, 2, 2, 1, 1, 1};
+        const double4* rc = h->cur ? h->ptr.rec1 : h->ptr.rec0;
+        reduce_to_host<7>(h, nb, op, [&](double* part) {
+            k_summary<<<nb, kRedThreads, 0, h->s>>>(rc, h->plan.N, part);
+        });
+        out->steps = h->host_step;
+        out->time = h->host_time;
+        out->max_temperature = h->h_part[0];
+        for (int c = 0; c < 3; ++c) {
+            out->min_disp[c] = h->h_part[1 + c];
+            out->max_disp[c] = h->h_part[4 + c];
+        }
+        return TVEGPU_OK;
+    });
+}
+
+tvegpu_status tvegpu_ablation_volume(tvegpu_engine* h, double threshold, int32_t deformed, double* volume,
+                                     int64_t* elements_above) {
+    if (!h || !volume || !std::isfinite(threshold)) return TVEGPU_E_ARG;
+    return guard(h, [&] {
+        if (!h->d_conn) {
+            h->d_conn = dalloc<int32_t>(h->owned, h->plan.conn.size());
+            CU(cudaMemcpyAsync(h->d_conn, h->plan.conn.data(), h->plan.conn.size() * 4, cudaMemcpyHostToDevice, h->s));
+        }
+        const int E = h->plan.E, nb = red_blocks(E);
+        const int op[2] = {0, 0};
+        const double4* rc = h->cur ? h->ptr.rec1 : h->ptr.rec0;
+        reduce_to_host<2>(h, nb, op, [&](double* part) {
+            if (h->nn == 8)
+                k_ablation<8><<<nb, kRedThreads, 0, h->s>>>(h->d_conn, h->ptr.X, rc, E, threshold, deformed ? 1 : 0, part);
+            else
+                k_ablation<4><<<nb, kRedThreads, 0, h->s>>>(h->d_conn, h->ptr.X, rc, E, threshold, deformed ? 1 : 0, part);
+        });
+        *volume = h->h_part[0];
+        if (elements_above) *elements_above = (int64_t)llround(h->h_part[1]);
+        return TVEGPU_OK;
+    });
+}
+
+tvegpu_status tvegpu_element_fields(tvegpu_engine* h, double* det_f, double* max_principal_stress) {
+    if (!h || (!det_f && !max_principal_stress)) return TVEGPU_E_ARG;
+    if (!h->prm.diag) {
+        h->err = "element fields need options.diagnostics = 1 (F and S of the last mechanics phase)";
+        return TVEGPU_E_ARG;
+    }
+    if (h->plan.nranks != 1 || h->plan.E != h->E_global) {
+        h->err = "element fields are read on single-partition engines";
+        return TVEGPU_E_ARG;
+    }
+    return guard(h, [&] {
+        const int E = h->plan.E;
+        if (!h->d_ef) h->d_ef = dalloc<double>(h->owned, (size_t)2 * E);
+        double* d = h->d_ef;
+        k_element_fields<<<blocks(E, 256), 256, 0, h->s>>>(h->ptr.diag_F, h->ptr.diag_S, h->ptr.elem_orig, E,
+                                                             det_f ? d : nullptr, max_principal_stress ? d + E : nullptr);
+        CU(cudaGetLastError());
+        if (det_f) CU(cudaMemcpyAsync(det_f, d, (size_t)E * 8, cudaMemcpyDeviceToHost, h->s));
+        if (max_principal_stress)
+            CU(cudaMemcpyAsync(max_principal_stress, d + E, (size_t)E * 8, cudaMemcpyDeviceToHost, h->s));
+        CU(cudaStreamSynchronize(h->s));
+        return TVEGPU_OK;
     });
 }
 

@@ -99,6 +99,9 @@ EXPORTS = {
     "tvegpu_set_state": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp, C.c_double, C.c_int64]),
     "tvegpu_set_nodal_sources": (C.c_int, [C.c_void_p, _dp]),
     "tvegpu_step_io": (C.c_int, [C.c_void_p, _dp, C.c_int64, _dp, _dp]),
+    "tvegpu_get_summary": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "tvegpu_ablation_volume": (C.c_int, [C.c_void_p, C.c_double, C.c_int32, _dp, C.POINTER(C.c_int64)]),
+    "tvegpu_element_fields": (C.c_int, [C.c_void_p, _dp, _dp]),
     "tvegpu_get_diagnostics": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
     "tvegpu_last_error": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_int64),
                                     C.POINTER(C.c_int32)]),
@@ -140,6 +143,11 @@ def lib():
             f.argtypes = args
         _LIB = L
     return _LIB
+
+
+class _Summary(C.Structure):
+    _fields_ = [("steps", C.c_int64), ("time", C.c_double), ("max_temperature", C.c_double),
+                ("min_disp", C.c_double * 3), ("max_disp", C.c_double * 3)]
 
 
 def _f64(a):
@@ -325,6 +333,32 @@ class Engine:
         if rc:
             self._raise(rc)
         return u
+
+    # ---- run-level outputs on the device (engine.hpp:57-66)
+    def summary(self):
+        """RunSummary extrema: dict(steps, time, max_temperature, min_disp, max_disp)."""
+        out = _Summary()
+        rc = lib().tvegpu_get_summary(self._h, C.byref(out))
+        if rc:
+            self._raise(rc)
+        return dict(steps=out.steps, time=out.time, max_temperature=out.max_temperature,
+                    min_disp=np.array(out.min_disp[:]), max_disp=np.array(out.max_disp[:]))
+
+    def ablation_volume(self, threshold=60.0, deformed=True):
+        """(volume [m^3], elements_above) of {T >= threshold} by exact tet clipping."""
+        v, n = np.empty(1), C.c_int64()
+        rc = lib().tvegpu_ablation_volume(self._h, float(threshold), 1 if deformed else 0, _P(v), C.byref(n))
+        if rc:
+            self._raise(rc)
+        return float(v[0]), int(n.value)
+
+    def element_fields(self):
+        """(det F, max principal S_tilde) per element of the last mechanics phase (diagnostics=True)."""
+        d, s = np.empty(self.E), np.empty(self.E)
+        rc = lib().tvegpu_element_fields(self._h, _P(d), _P(s))
+        if rc:
+            self._raise(rc)
+        return d, s
 
     def step_io(self, power=None, n=1, T=None, u=None):
         """set_nodal_sources(power) + step(n) + make_snapshot(T, u) in one call, the
