@@ -518,6 +518,21 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     h->ptr.chunk_node_slot = dupload(own, pl.chunk_node_slot, s);
     h->ptr.lconn = dupload(own, pl.lconn, s);
     m.max_chunk_nodes = std::max(1, pl.max_chunk_nodes);
+    {
+        const int nc = (int)pl.chunk_start.size() - 1;
+        int st = 1;
+        for (int c = 0; c < nc; ++c) st = std::max(st, pl.chunk_node_off[c + 1] - pl.chunk_node_off[c]);
+        std::vector<int32_t> ent((size_t)2 * nc * st, 0);
+        for (int c = 0; c < nc; ++c)
+            for (int k = 0; k < st; ++k) {
+                const int u = pl.chunk_node_off[c] + k;
+                const bool in = u < pl.chunk_node_off[c + 1];
+                ent[2 * ((size_t)c * st + k)] = in ? pl.chunk_nodes[u] : -1;
+                ent[2 * ((size_t)c * st + k) + 1] = in ? pl.chunk_node_slot[u] : 0;
+            }
+        h->ptr.stage_ent = reinterpret_cast<const int2*>(dupload(own, ent, s));
+        m.stage_stride = st;
+    }
     CU(cudaStreamSynchronize(s));
     set_smem_limits(h);
     h->ptr.elem_orig = dupload(own, pl.elem_orig, s);

@@ -46,6 +46,7 @@ struct Clock {
 struct DevParams {
     int nn, E, N, P, mode, td, exp_kind, fiber_mode, axes_per_elem, has_R, diag, nslots;
     int max_chunk_nodes;  // shared-memory stride of the staged node records
+    int stage_stride;     // entries per chunk in stage_ent (max unique nodes of a chunk)
     double dt, mu, kappa, eta_a, kh, rho, wbcb, Ta, Qm, gamma;
     double inv_2dt, inv_dt2;  // 1/(2 dt), 1/dt^2 (Eq. 22 coefficients)
     double fiber[3];
@@ -64,6 +65,7 @@ struct DevPtrs {
     const int32_t* chunk_nodes;     // unique local nodes of each chunk (ascending)
     const uint16_t* chunk_node_slot;  // their shared-memory slots
     const uint16_t* lconn;          // [E][nn] index of node (e, a) in its chunk's node list
+    const int2* stage_ent;          // [nchunks][stage_stride] {local node, shared slot}, {-1, 0} padded
     double* theta;             // [P][6][E]   (xx, yy, zz, xy, yz, xz)
     const double* fiber;       // [3][E] or null
     const double* axes;        // [6][E] or null
@@ -264,10 +266,18 @@ __device__ __forceinline__ void element_pass(const NodeStage& S, const int (&n)[
 // then up to kStageBatch node indices per thread, then all their records.
 constexpr int kStageBatch = 3;
 template <int NN>
-__device__ __forceinline__ int stage_chunk(const DevPtrs& D, const double4* __restrict__ R, int c,
+__device__ __forceinline__ int stage_chunk(const DevPtrs& D, const double4* __restrict__ R, int c, const int st,
                                            const NodeStage& S, int (&n)[NN]) {
+    // fixed-stride entry list: its address needs no load, so the record gathers
+    // are only one dependent load away from the kernel start
+    const int2* ent = D.stage_ent + (size_t)c * st;
+    int2 en[kStageBatch];
+#pragma unroll
+    for (int j = 0; j < kStageBatch; ++j) {
+        const int k = j * kChunkThreads + threadIdx.x;
+        en[j] = k < st ? __ldg(ent + k) : make_int2(-1, 0);
+    }
     const int eb = __ldg(D.chunk_start + c), ne = __ldg(D.chunk_start + c + 1) - eb;
-    const int u0 = __ldg(D.chunk_node_off + c), nu = __ldg(D.chunk_node_off + c + 1) - u0;
     const int e = threadIdx.x < ne ? eb + threadIdx.x : -1;
     uint4 w8 = make_uint4(0, 0, 0, 0);
     uint2 w4 = make_uint2(0, 0);
@@ -275,13 +285,16 @@ __device__ __forceinline__ int stage_chunk(const DevPtrs& D, const double4* __re
         if constexpr (NN == 8) w8 = __ldg(reinterpret_cast<const uint4*>(D.lconn) + e);
         else w4 = __ldg(reinterpret_cast<const uint2*>(D.lconn) + e);
     }
-    for (int k0 = 0; k0 < nu; k0 += kStageBatch * kChunkThreads) {  // ascending node ids: coalesced loads
+    for (int k0 = 0; k0 < st; k0 += kStageBatch * kChunkThreads) {  // ascending node ids: coalesced loads
         int g[kStageBatch], s[kStageBatch];
 #pragma unroll
         for (int j = 0; j < kStageBatch; ++j) {
-            const int k = k0 + j * kChunkThreads + threadIdx.x;
-            g[j] = k < nu ? __ldg(D.chunk_nodes + u0 + k) : -1;
-            s[j] = k < nu ? __ldg(D.chunk_node_slot + u0 + k) : 0;
+            if (k0 > 0) {
+                const int k = k0 + j * kChunkThreads + threadIdx.x;
+                en[j] = k < st ? __ldg(ent + k) : make_int2(-1, 0);
+            }
+            g[j] = en[j].x;
+            s[j] = en[j].y;
         }
         double4 r[kStageBatch], x[kStageBatch];
 #pragma unroll
@@ -321,7 +334,7 @@ __global__ void __launch_bounds__(kChunkThreads) k_thermal_element(const DevPara
     const int ms = P.max_chunk_nodes;
     const NodeStage S{smem_planes, smem_planes + ms, smem_planes + 2 * ms, smem_planes + 3 * ms};
     int n[NN];
-    const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, S, n);
+    const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, P.stage_stride, S, n);
     if (e < 0) return;
     double H[9], A[9], gT[3], V, Ts;
     element_pass<NN, true>(S, n, H, A, V, Ts, gT);
@@ -459,7 +472,7 @@ __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
 #pragma unroll
                 for (int q = 0; q < 6; ++q) prefetch_l1(D.theta + ((size_t)p * 6 + q) * P.E + e0);
     }
-    const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, st, n);
+    const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, P.stage_stride, st, n);
     if (e < 0) return;
     const int E = P.E;
     double Hd[9], A[9], V, Ts;
