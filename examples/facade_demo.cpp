@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <sstream>
 
 #include "tve_gpu.hpp"
 
@@ -83,6 +84,20 @@ int main(int argc, char** argv) {
             }
         std::printf("steps %ld time %.17g  T_max %.17g  u_z [%.17g, %.17g]\n", s.step, s.time, Tmax, umin[2],
                     umax[2]);
+        // run-level outputs on the device: RunSummary extrema and the 40 degC isotherm volume
+        const tvegpu_summary sm = eng.summary();
+        const auto abl = eng.ablation_volume(40.0);
+        std::printf("device summary: T_max %.17g  u_z max %.17g  ablation(40C) %.17g m^3 in %ld elements\n",
+                    sm.max_temperature, sm.max_disp[2], abl.first, abl.second);
+        // checkpoint / restart (engine.hpp:110-111): resume a copy and compare after 10 more steps
+        std::stringstream ck;
+        eng.save_checkpoint(ck);
+        Engine twin(mesh, mat, mb, ThermalBCs{}, src, cfg);
+        twin.load_checkpoint(ck);
+        eng.steps(10);
+        twin.steps(10);
+        const bool same = eng.state().temperatures == twin.state().temperatures && eng.state().disp == twin.state().disp;
+        std::printf("checkpoint resume bit-identical: %s\n", same ? "yes" : "NO");
         // reference-style state() write: cool the whole block back to 37 degC, keep stepping
         SimulationState& w = eng.mutable_state();
         std::fill(w.temperatures.begin(), w.temperatures.end(), 37.0);

@@ -12,7 +12,10 @@
 #include <array>
 #include <cmath>
 #include <cstdint>
+#include <istream>
+#include <iterator>
 #include <limits>
+#include <ostream>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -183,6 +186,48 @@ public:
     void set_nodal_sources(const std::vector<double>& power) {
         check(tvegpu_set_nodal_sources(h_, power.empty() ? nullptr : power.data()));
     }
+    // Closed-loop iteration: sources + n steps + T/u read-back, copies overlapped with
+    // the step (tvegpu_step_io); empty power keeps the current sources.
+    void step_io(const std::vector<double>& power, int64_t n, std::vector<double>& T, std::vector<double>& u) {
+        push_if_dirty();
+        T.resize(N_);
+        u.resize(3 * (size_t)N_);
+        check(tvegpu_step_io(h_, power.empty() ? nullptr : power.data(), n, T.data(), u.data()));
+        mirror_valid_ = false;
+    }
+
+    // engine.hpp:57-66 RunSummary extrema and SPEC.md:435-443 ablation volume, on the device
+    tvegpu_summary summary() {
+        push_if_dirty();
+        tvegpu_summary s;
+        check(tvegpu_get_summary(h_, &s));
+        return s;
+    }
+    std::pair<double, long> ablation_volume(double threshold, bool deformed = true) {
+        push_if_dirty();
+        double v = 0;
+        int64_t n = 0;
+        check(tvegpu_ablation_volume(h_, threshold, deformed ? 1 : 0, &v, &n));
+        return {v, (long)n};
+    }
+
+    // engine.hpp:110-111
+    void save_checkpoint(std::ostream& out) {
+        push_if_dirty();
+        uint64_t n = 0;
+        check(tvegpu_checkpoint_size(h_, &n));
+        std::vector<char> buf(n);
+        check(tvegpu_save_checkpoint(h_, buf.data(), n));
+        out.write(buf.data(), (std::streamsize)n);
+        if (!out) throw IoError("save_checkpoint: write failed");
+    }
+    void load_checkpoint(std::istream& in) {
+        std::vector<char> buf((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+        check(tvegpu_load_checkpoint(h_, buf.data(), buf.size()));
+        dirty_ = false;
+        mirror_valid_ = false;
+    }
+
     tvegpu_engine* handle() { return h_; }
 
 private:

@@ -213,6 +213,16 @@ tvegpu_status tvegpu_set_nodal_sources(tvegpu_engine* h, const double* power);
  * the last step computes.  n >= 1.  On an error return T and disp are undefined. */
 tvegpu_status tvegpu_step_io(tvegpu_engine* h, const double* power, int64_t n, double* T, double* disp);
 
+/* ---- checkpoint / restart (engine.hpp:110-111) ----
+ * A versioned binary image of the state in original numbering (layout in
+ * DESIGN.md): T, u, u_prev, viscous history, time, step and an active nodal-source
+ * override.  Restores bit-exactly, into an engine with any partitioning; saving
+ * needs a single-partition engine.  Errors: E_ARG (buffer too small), E_IO
+ * (bad magic / version / problem mismatch / truncated). */
+tvegpu_status tvegpu_checkpoint_size(tvegpu_engine* h, uint64_t* bytes);
+tvegpu_status tvegpu_save_checkpoint(tvegpu_engine* h, void* buf, uint64_t bytes);
+tvegpu_status tvegpu_load_checkpoint(tvegpu_engine* h, const void* buf, uint64_t bytes);
+
 /* ---- run-level outputs on the device ----
  * RunSummary node extrema (engine.hpp:57-66) by deterministic device reductions
  * (a 56-byte read-back instead of the full fields); multi-GPU: all-reduced. */

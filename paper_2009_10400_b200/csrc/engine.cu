@@ -1293,6 +1293,101 @@ tvegpu_status tvegpu_step_io(tvegpu_engine* h, const double* power, int64_t n, d
     });
 }
 
+// ---- checkpoint / restart (engine.hpp:110-111) ----
+// Layout (little-endian, documented in DESIGN.md): header, then T[N], u[3N],
+// u_prev[3N], viscous[E][P][9] (row-major 3x3), and power[N] when a nodal-source
+// override is active — all in original numbering, so a checkpoint written by one
+// partitioning loads into any other.
+namespace {
+struct CkptHeader {
+    char magic[8];  // "TVEGPUCK"
+    int32_t version, kind, N, E, P, has_sources;
+    int64_t step;
+    double time;
+};
+uint64_t ckpt_bytes(const tvegpu_engine* h) {
+    const uint64_t N = h->N_global, E = h->E_global, P = h->P;
+    return sizeof(CkptHeader) + 8 * (N + 3 * N + 3 * N + 9 * P * E + (h->source_override ? N : 0));
+}
+}  // namespace
+
+tvegpu_status tvegpu_checkpoint_size(tvegpu_engine* h, uint64_t* bytes) {
+    if (!h || !bytes) return TVEGPU_E_ARG;
+    *bytes = ckpt_bytes(h);
+    return TVEGPU_OK;
+}
+
+tvegpu_status tvegpu_save_checkpoint(tvegpu_engine* h, void* buf, uint64_t bytes) {
+    if (!h || !buf) return TVEGPU_E_ARG;
+    if (h->plan.nranks != 1 || h->plan.N != h->N_global || h->plan.E != h->E_global) {
+        h->err = "save_checkpoint needs a single-partition engine (gather the rank states first)";
+        return TVEGPU_E_ARG;
+    }
+    if (bytes < ckpt_bytes(h)) {
+        h->err = "checkpoint buffer too small (tvegpu_checkpoint_size)";
+        return TVEGPU_E_ARG;
+    }
+    return guard(h, [&] {
+        const int N = h->N_global, E = h->E_global, P = h->P;
+        CkptHeader hd{};
+        std::memcpy(hd.magic, "TVEGPUCK", 8);
+        hd.version = 1, hd.kind = h->kind, hd.N = N, hd.E = E, hd.P = P;
+        hd.has_sources = h->source_override ? 1 : 0;
+        hd.step = h->host_step;
+        hd.time = h->host_time;
+        char* o = static_cast<char*>(buf);
+        std::memcpy(o, &hd, sizeof hd);
+        double* T = reinterpret_cast<double*>(o + sizeof hd);
+        double* u = T + N;
+        double* up = u + 3 * (size_t)N;
+        double* vis = up + 3 * (size_t)N;
+        read_fields(h, T, u, up);
+        if (P) {
+            const tvegpu_status st = tvegpu_get_viscous(h, vis);
+            if (st != TVEGPU_OK) return st;
+        }
+        if (h->source_override) {
+            double* pw = vis + 9 * (size_t)P * E;
+            std::vector<double> q(N);
+            CU(cudaMemcpyAsync(q.data(), h->ptr.qr, (size_t)N * 8, cudaMemcpyDeviceToHost, h->s));
+            CU(cudaStreamSynchronize(h->s));
+            for (int i = 0; i < N; ++i) pw[h->plan.node_orig[i]] = q[i];
+        }
+        return TVEGPU_OK;
+    });
+}
+
+tvegpu_status tvegpu_load_checkpoint(tvegpu_engine* h, const void* buf, uint64_t bytes) {
+    if (!h || !buf) return TVEGPU_E_ARG;
+    CkptHeader hd;
+    if (bytes < sizeof hd) {
+        h->err = "checkpoint truncated";
+        return TVEGPU_E_IO;
+    }
+    std::memcpy(&hd, buf, sizeof hd);
+    if (std::memcmp(hd.magic, "TVEGPUCK", 8) != 0 || hd.version != 1) {
+        h->err = "not a version-1 tvegpu checkpoint";
+        return TVEGPU_E_IO;
+    }
+    if (hd.kind != h->kind || hd.N != h->N_global || hd.E != h->E_global || hd.P != h->P) {
+        h->err = "checkpoint does not match this problem (element kind, node/element/Prony counts)";
+        return TVEGPU_E_IO;
+    }
+    const uint64_t N = hd.N, E = hd.E, P = hd.P;
+    const uint64_t need = sizeof hd + 8 * (7 * N + 9 * P * E + (hd.has_sources ? N : 0));
+    if (bytes < need) {
+        h->err = "checkpoint truncated";
+        return TVEGPU_E_IO;
+    }
+    const double* T = reinterpret_cast<const double*>(static_cast<const char*>(buf) + sizeof hd);
+    const double* u = T + N;
+    const double* up = u + 3 * N;
+    const double* vis = up + 3 * N;
+    tvegpu_status st = tvegpu_set_state(h, T, u, up, P ? vis : nullptr, hd.time, hd.step);
+    if (st == TVEGPU_OK) st = tvegpu_set_nodal_sources(h, hd.has_sources ? vis + 9 * P * E : nullptr);
+    return st;
+}
+
 tvegpu_status tvegpu_get_summary(tvegpu_engine* h, tvegpu_summary* out) {
     if (!h || !out) return TVEGPU_E_ARG;
     return guard(h, [&] {

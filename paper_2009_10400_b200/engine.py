@@ -100,6 +100,9 @@ EXPORTS = {
     "tvegpu_set_nodal_sources": (C.c_int, [C.c_void_p, _dp]),
     "tvegpu_step_io": (C.c_int, [C.c_void_p, _dp, C.c_int64, _dp, _dp]),
     "tvegpu_get_summary": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "tvegpu_checkpoint_size": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+    "tvegpu_save_checkpoint": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
+    "tvegpu_load_checkpoint": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "tvegpu_ablation_volume": (C.c_int, [C.c_void_p, C.c_double, C.c_int32, _dp, C.POINTER(C.c_int64)]),
     "tvegpu_element_fields": (C.c_int, [C.c_void_p, _dp, _dp]),
     "tvegpu_get_diagnostics": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
@@ -333,6 +336,30 @@ class Engine:
         if rc:
             self._raise(rc)
         return u
+
+    # ---- checkpoint / restart (engine.hpp:110-111)
+    def save_checkpoint(self, path=None) -> bytes:
+        """Versioned binary state image (original numbering); written to `path` if given."""
+        n = C.c_uint64()
+        rc = lib().tvegpu_checkpoint_size(self._h, C.byref(n))
+        if rc:
+            self._raise(rc)
+        buf = C.create_string_buffer(n.value)
+        rc = lib().tvegpu_save_checkpoint(self._h, buf, n.value)
+        if rc:
+            self._raise(rc)
+        data = buf.raw
+        if path is not None:
+            with open(path, "wb") as f:
+                f.write(data)
+        return data
+
+    def load_checkpoint(self, src):
+        """Restore from bytes or a file path written by save_checkpoint (any partitioning)."""
+        data = src if isinstance(src, (bytes, bytearray)) else open(src, "rb").read()
+        rc = lib().tvegpu_load_checkpoint(self._h, bytes(data), len(data))
+        if rc:
+            self._raise(rc)
 
     # ---- run-level outputs on the device (engine.hpp:57-66, SPEC.md:435-443)
     def summary(self):

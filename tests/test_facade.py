@@ -56,3 +56,10 @@ def test_facade_demo_matches_oracle():
     assert abs(Tmax - s["T"].max()) <= 1e-10 * (s["T"].max() - 37.0)
     assert abs(uzmax - s["u"][2::3].max()) <= 1e-10 * abs(s["u"]).max()
     assert "after reset + 1 step" in out
+    assert "checkpoint resume bit-identical: yes" in out
+    m = re.search(r"device summary: T_max ([0-9.eE+-]+)\s+u_z max ([0-9.eE+-]+)\s+ablation\(40C\) ([0-9.eE+-]+) m\^3 "
+                  r"in (\d+) elements", out)
+    assert m, out
+    assert float(m.group(1)) == Tmax  # device reduction == host max of the same field
+    vo, no = O.ablation_volume("H8", p.nodes, p.elements, s["T"], 40.0, disp=s["u"])
+    assert int(m.group(4)) == no and abs(float(m.group(3)) - vo) <= 1e-9 * max(vo, 1e-30)
