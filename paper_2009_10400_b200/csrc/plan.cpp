@@ -2,12 +2,29 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <numeric>
 
 namespace tvegpu {
+
+// Setup-stage timing to stderr when TVEGPU_TIMING is set.
+struct StageTimer {
+    const char* name;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    explicit StageTimer(const char* n) : name(n) {}
+    ~StageTimer() {
+        static const bool on = std::getenv("TVEGPU_TIMING") != nullptr;
+        if (on)
+            std::fprintf(stderr, "[tvegpu setup] %-28s %8.1f ms\n", name,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
+
 
 const int kH8Sign[8][3] = {{-1, -1, -1}, {1, -1, -1}, {1, 1, -1}, {-1, 1, -1},
                            {-1, -1, 1},  {1, -1, 1},  {1, 1, 1},  {-1, 1, 1}};
@@ -155,6 +172,7 @@ void validate_problem(const tvegpu_problem& p) {
 }
 
 GlobalMesh build_global(const tvegpu_problem& p) {
+    StageTimer tm("build_global");
     validate_problem(p);
     GlobalMesh g;
     g.kind = p.kind;
@@ -308,6 +326,7 @@ std::vector<int32_t> rcb_partition(const GlobalMesh& g, int nranks) {
 
 // ---------------------------------------------------------------- rank plan
 RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nranks, int rank, int reorder) {
+    StageTimer tm("build_rank_plan (total)");
     if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(TVEGPU_E_ARG, "bad rank / nranks");
     if (nranks > 1 && !reorder) throw Error(TVEGPU_E_ARG, "reorder = 0 needs nranks = 1");
     RankPlan r;
@@ -466,37 +485,54 @@ static std::vector<int32_t> colour_slots(const std::vector<int32_t>& nodes, cons
                                          std::vector<int32_t>& slot_of) {
     const int nu = (int)nodes.size();
     auto idx = [&](int32_t n) { return (int)(std::lower_bound(nodes.begin(), nodes.end(), n) - nodes.begin()); };
-    // groups: (quarter-warp q, local a) -> distinct node indices
-    std::vector<std::vector<int>> groups;
-    std::vector<std::vector<int>> member(nu);
+    // groups: (quarter-warp q, local a) -> distinct node indices, flat (<= 8 per group);
+    // member: per node the groups it belongs to, ascending (CSR)
+    const int ngmax = ((ne + 7) / 8) * nn;
+    std::vector<int> gdata((size_t)ngmax * 8), gsize(ngmax), moff(nu + 1, 0);
+    int ng = 0;
     for (int q = 0; q * 8 < ne; ++q)
         for (int a = 0; a < nn; ++a) {
-            std::vector<int> g;
-            for (int l = q * 8; l < std::min(ne, q * 8 + 8); ++l) g.push_back(idx(conn[(size_t)l * nn + a]));
-            std::sort(g.begin(), g.end());
-            g.erase(std::unique(g.begin(), g.end()), g.end());
-            if (g.size() < 2) continue;
-            for (int v : g) member[v].push_back((int)groups.size());
-            groups.push_back(std::move(g));
+            int g[8], k = 0;
+            for (int l = q * 8; l < std::min(ne, q * 8 + 8); ++l) g[k++] = idx(conn[(size_t)l * nn + a]);
+            std::sort(g, g + k);
+            k = (int)(std::unique(g, g + k) - g);
+            if (k < 2) continue;
+            for (int j = 0; j < k; ++j) {
+                gdata[(size_t)ng * 8 + j] = g[j];
+                moff[g[j] + 1]++;
+            }
+            gsize[ng++] = k;
         }
+    for (int v = 0; v < nu; ++v) moff[v + 1] += moff[v];
+    std::vector<int> mlist(moff[nu]);
+    {
+        std::vector<int> fill(moff.begin(), moff.end() - 1);
+        for (int gi = 0; gi < ng; ++gi)
+            for (int j = 0; j < gsize[gi]; ++j) mlist[fill[gdata[(size_t)gi * 8 + j]]++] = gi;
+    }
+    auto group = [&](int gi) { return std::make_pair(&gdata[(size_t)gi * 8], &gdata[(size_t)gi * 8] + gsize[gi]); };
     // Colour group by group in issue order: the uncoloured members of a group take
     // the colours still free in that group (this propagates the 2x2x2 parity
     // colouring through structured meshes); when a group has no free colour left,
     // fall back to the colour least used across all of the node's groups.
     std::vector<int> colour(nu, -1);
-    for (const auto& g : groups) {
+    for (int gi = 0; gi < ng; ++gi) {
+        const auto [g0, g1] = group(gi);
         bool used[8] = {false, false, false, false, false, false, false, false};
-        for (int w : g)
-            if (colour[w] >= 0) used[colour[w]] = true;
-        for (int v : g) {
+        for (const int* w = g0; w < g1; ++w)
+            if (colour[*w] >= 0) used[colour[*w]] = true;
+        for (const int* pv = g0; pv < g1; ++pv) {
+            const int v = *pv;
             if (colour[v] >= 0) continue;
             int c = 0;
             while (c < 8 && used[c]) ++c;
             if (c == 8) {
                 int uses[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                for (int gi : member[v])
-                    for (int w : groups[gi])
-                        if (colour[w] >= 0) uses[colour[w]]++;
+                for (int m = moff[v]; m < moff[v + 1]; ++m) {
+                    const auto [h0, h1] = group(mlist[m]);
+                    for (const int* w = h0; w < h1; ++w)
+                        if (colour[*w] >= 0) uses[colour[*w]]++;
+                }
                 c = 0;
                 for (int k = 1; k < 8; ++k)
                     if (uses[k] < uses[c]) c = k;
@@ -510,11 +546,13 @@ static std::vector<int32_t> colour_slots(const std::vector<int32_t>& nodes, cons
     for (int sweep = 0; sweep < 4; ++sweep) {
         bool moved = false;
         for (int v = 0; v < nu; ++v) {
-            if (colour[v] < 0 || member[v].empty()) continue;
+            if (colour[v] < 0 || moff[v] == moff[v + 1]) continue;
             int cost[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int gi : member[v])
-                for (int w : groups[gi])
-                    if (w != v && colour[w] >= 0) cost[colour[w]]++;
+            for (int m = moff[v]; m < moff[v + 1]; ++m) {
+                const auto [h0, h1] = group(mlist[m]);
+                for (const int* w = h0; w < h1; ++w)
+                    if (*w != v && colour[*w] >= 0) cost[colour[*w]]++;
+            }
             int best = colour[v];
             for (int c = 0; c < 8; ++c)
                 if (cost[c] < cost[best]) best = c;
@@ -547,6 +585,7 @@ static std::vector<int32_t> colour_slots(const std::vector<int32_t>& nodes, cons
 }
 
 void build_chunks(RankPlan& r) {
+    StageTimer tm("build_chunks");
     const int nn = r.nn;
     r.chunk_start.clear();
     r.chunk_node_off.assign(1, 0);
@@ -554,31 +593,42 @@ void build_chunks(RankPlan& r) {
     r.chunk_node_slot.clear();
     r.lconn.assign((size_t)r.E * nn, 0);
     r.max_chunk_nodes = 0;
-    auto add_range = [&](int b, int e) {
-        for (int c0 = b; c0 < e; c0 += kChunk) {
-            const int c1 = std::min(e, c0 + kChunk);
-            r.chunk_start.push_back(c0);
-            std::vector<int32_t> nodes(r.conn.begin() + (size_t)c0 * nn, r.conn.begin() + (size_t)c1 * nn);
-            std::sort(nodes.begin(), nodes.end());
-            nodes.erase(std::unique(nodes.begin(), nodes.end()), nodes.end());
-            std::vector<int32_t> slot_of;
-            const std::vector<int32_t> slots = colour_slots(nodes, r.conn.data() + (size_t)c0 * nn, c1 - c0, nn, slot_of);
-            for (int le = c0; le < c1; ++le)
-                for (int a = 0; a < nn; ++a) {
-                    const int32_t n = r.conn[(size_t)le * nn + a];
-                    const int v = (int)(std::lower_bound(nodes.begin(), nodes.end(), n) - nodes.begin());
-                    r.lconn[(size_t)le * nn + a] = (uint16_t)slot_of[v];
-                }
-            // staging walks the nodes in ascending id (coalesced loads) and stores each to its slot
-            r.chunk_nodes.insert(r.chunk_nodes.end(), nodes.begin(), nodes.end());
-            for (int32_t s : slot_of) r.chunk_node_slot.push_back((uint16_t)s);
-            r.chunk_node_off.push_back((int32_t)r.chunk_nodes.size());
-            r.max_chunk_nodes = std::max(r.max_chunk_nodes, (int)slots.size());
-        }
-    };
-    add_range(0, r.Eb);
-    r.nchunks_boundary = (int)r.chunk_start.size();
-    add_range(r.Eb, r.E);
+    // chunk ranges: boundary elements [0, Eb) then interior [Eb, E), kChunk at a time
+    std::vector<int32_t> starts;
+    for (int c0 = 0; c0 < r.Eb; c0 += kChunk) starts.push_back(c0);
+    r.nchunks_boundary = (int)starts.size();
+    for (int c0 = r.Eb; c0 < r.E; c0 += kChunk) starts.push_back(c0);
+    const int nc = (int)starts.size();
+    auto chunk_end = [&](int c) { return c + 1 < nc ? starts[c + 1] : r.E; };
+    // chunks are independent: unique nodes, colouring and 16-bit connectivity in parallel
+    std::vector<std::vector<int32_t>> cnodes(nc), cslot(nc);
+    std::vector<int32_t> nslots(nc, 0);
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int c = 0; c < nc; ++c) {
+        const int c0 = starts[c], c1 = chunk_end(c);
+        std::vector<int32_t> nodes(r.conn.begin() + (size_t)c0 * nn, r.conn.begin() + (size_t)c1 * nn);
+        std::sort(nodes.begin(), nodes.end());
+        nodes.erase(std::unique(nodes.begin(), nodes.end()), nodes.end());
+        std::vector<int32_t> slot_of;
+        const std::vector<int32_t> slots = colour_slots(nodes, r.conn.data() + (size_t)c0 * nn, c1 - c0, nn, slot_of);
+        for (int le = c0; le < c1; ++le)
+            for (int a = 0; a < nn; ++a) {
+                const int32_t n = r.conn[(size_t)le * nn + a];
+                const int v = (int)(std::lower_bound(nodes.begin(), nodes.end(), n) - nodes.begin());
+                r.lconn[(size_t)le * nn + a] = (uint16_t)slot_of[v];
+            }
+        nslots[c] = (int)slots.size();
+        cnodes[c] = std::move(nodes);
+        cslot[c] = std::move(slot_of);
+    }
+    // staging walks each chunk's nodes in ascending id (coalesced loads), storing each to its slot
+    for (int c = 0; c < nc; ++c) {
+        r.chunk_start.push_back(starts[c]);
+        r.chunk_nodes.insert(r.chunk_nodes.end(), cnodes[c].begin(), cnodes[c].end());
+        for (int32_t s : cslot[c]) r.chunk_node_slot.push_back((uint16_t)s);
+        r.chunk_node_off.push_back((int32_t)r.chunk_nodes.size());
+        r.max_chunk_nodes = std::max(r.max_chunk_nodes, nslots[c]);
+    }
     r.chunk_start.push_back(r.E);
 }
 
