@@ -649,10 +649,23 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     const size_t nrecv = pl.recv_off.empty() ? 0 : pl.recv_off.back();
     const size_t nslots = (size_t)nn * E + nrecv;
     m.nslots = (int)nslots;
-    h->ptr.slot_th = dalloc<double>(own, nslots);
-    h->ptr.slot_m = dalloc<double>(own, kMW * nslots);
-    CU(cudaMemsetAsync(h->ptr.slot_th, 0, nslots * 8, s));
-    CU(cudaMemsetAsync(h->ptr.slot_m, 0, kMW * nslots * 8, s));
+    // + one sentinel slot (index nslots) that nothing writes: the ELL padding target
+    h->ptr.slot_th = dalloc<double>(own, nslots + 1);
+    h->ptr.slot_m = dalloc<double>(own, kMW * (nslots + 1));
+    CU(cudaMemsetAsync(h->ptr.slot_th, 0, (nslots + 1) * 8, s));
+    CU(cudaMemsetAsync(h->ptr.slot_m, 0, kMW * (nslots + 1) * 8, s));
+    {
+        int maxc = 0;
+        for (int i = 0; i < pl.N; ++i) maxc = std::max(maxc, pl.csr_off[i + 1] - pl.csr_off[i]);
+        m.ell = (maxc <= 8 && !std::getenv("TVEGPU_NO_ELL")) ? 1 : 0;
+        if (m.ell) {
+            std::vector<int32_t> ell((size_t)8 * pl.N, (int32_t)nslots);
+            for (int i = 0; i < pl.N; ++i)
+                for (int k = pl.csr_off[i]; k < pl.csr_off[i + 1]; ++k)
+                    ell[(size_t)8 * i + (k - pl.csr_off[i])] = pl.csr_slot[k];
+            h->ptr.ell = reinterpret_cast<const int4*>(dupload(own, ell, s));
+        }
+    }
     // ---- clock and error words
     h->ptr.clock = dalloc<Clock>(own, 1);
     h->ptr.err_inst = dalloc<unsigned long long>(own, 1);

@@ -47,6 +47,7 @@ struct DevParams {
     int nn, E, N, P, mode, td, exp_kind, fiber_mode, axes_per_elem, has_R, diag, nslots;
     int max_chunk_nodes;  // shared-memory stride of the staged node records
     int stage_stride;     // entries per chunk in stage_ent (max unique nodes of a chunk)
+    int ell;              // 1: every node has <= 8 contributions, gathers use the ELL-8 index
     double dt, mu, kappa, eta_a, kh, rho, wbcb, Ta, Qm, gamma;
     double inv_2dt, inv_dt2;  // 1/(2 dt), 1/dt^2 (Eq. 22 coefficients)
     double fiber[3];
@@ -85,6 +86,7 @@ struct DevPtrs {
     const double* R;           // [N][3] external + body force, or null
     const int32_t* csr_off;    // [N+1]
     const int32_t* csr_slot;   // gather list: element-major slot ids (e*nn + a, or receive area)
+    const int4* ell;           // [N][8] the same lists padded with a zero sentinel slot (ell = 1)
     const int32_t* node_orig;  // [N]
     double* slot_th;           // [nslots]
     double* slot_m;            // [nslots][kMW] (fx, fy, fz, pad)
@@ -433,12 +435,42 @@ __device__ __forceinline__ void gather3(const double* __restrict__ slots, const 
     }
 }
 
+// ELL-8 gathers: the node's 8 slot ids in one 32-byte row (two 16-byte loads, no
+// offset load first), then all 8 contributions in flight at once.  Padding entries
+// name a slot that is always +0.0 and sit after the real ones, so the canonical-
+// order sum is unchanged bit for bit (s + 0.0 == s; s is never -0.0 from a +0.0 start).
+__device__ __forceinline__ double gather1_ell(const double* __restrict__ slots, const int4* __restrict__ ell, int i) {
+    const int4 a = __ldg(ell + 2 * (size_t)i), b = __ldg(ell + 2 * (size_t)i + 1);
+    const double v0 = __ldg(slots + a.x), v1 = __ldg(slots + a.y), v2 = __ldg(slots + a.z), v3 = __ldg(slots + a.w);
+    const double v4 = __ldg(slots + b.x), v5 = __ldg(slots + b.y), v6 = __ldg(slots + b.z), v7 = __ldg(slots + b.w);
+    double s = 0.0;
+    s += v0, s += v1, s += v2, s += v3, s += v4, s += v5, s += v6, s += v7;
+    return s;
+}
+__device__ __forceinline__ void gather3_ell(const double* __restrict__ slots, const int4* __restrict__ ell, int i,
+                                            double& f0, double& f1, double& f2) {
+    const int4 a = __ldg(ell + 2 * (size_t)i), b = __ldg(ell + 2 * (size_t)i + 1);
+    const double4* S = reinterpret_cast<const double4*>(slots);
+    const int id[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    double4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = ldg4(S + id[k]);
+    f0 = f1 = f2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        f0 += v[k].x;
+        f1 += v[k].y;
+        f2 += v[k].z;
+    }
+}
+
 // ------------------------------------------------------------------ K2: thermal node
 __global__ void __launch_bounds__(256) k_thermal_node(const DevParams P, const DevPtrs D, int cur, int closes) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < P.N && !D.clock->halted) {
         double4* R = cur ? D.rec1 : D.rec0;
-        const double s = gather1(D.slot_th, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1));
+        const double s = P.ell ? gather1_ell(D.slot_th, D.ell, i)
+                               : gather1(D.slot_th, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1));
         const double T = R[i].w;
         const double V = __ldg(D.vnode + i);
         const double c = P.td ? interp1(P.cT, P.cV, P.c_len, T) : P.c_fixed;
@@ -743,7 +775,8 @@ __global__ void __launch_bounds__(256) k_mech_node(const DevParams P, const DevP
         const double4* Rc = cur ? D.rec1 : D.rec0;
         double4* Rn = cur ? D.rec0 : D.rec1;  // holds u^{n-1}; receives u^{n+1}
         double f0, f1, f2;
-        gather3(D.slot_m, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1), f0, f1, f2);
+        if (P.ell) gather3_ell(D.slot_m, D.ell, i, f0, f1, f2);
+        else gather3(D.slot_m, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1), f0, f1, f2);
         const double4 u = ldg4(Rc + i);  // read-only in this kernel
         const double4 up = ld4(Rn + i);  // this thread overwrites it below
         const double m = __ldg(D.mass + i);
