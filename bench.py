@@ -288,7 +288,9 @@ def run_ours(args):
     power = torch.from_numpy(lumped_source_power(p)).pin_memory().numpy()
     Th = torch.empty(p.num_nodes, dtype=torch.float64, pin_memory=True).numpy()
     uh = torch.empty(3 * p.num_nodes, dtype=torch.float64, pin_memory=True).numpy()
-    for k in range(2):  # untimed: first-call allocations (device I/O buffers) and page-ins
+    # untimed: first-call allocations (device I/O buffers); the first few dozen DMA
+    # reads of a freshly pinned buffer run ~2x slower (measured, scripts/e2e_breakdown.py)
+    for k in range(50):
         eng.step_io(power, 1, Th, uh)
     barrier()
     t0 = time.perf_counter()
