@@ -253,8 +253,9 @@ void set_smem_limits(tvegpu_engine* h) {
 // boundary-element slots overlapped with the interior elements.
 // wait_src: event K2 waits on (sources uploaded on another stream); t_final:
 // event recorded once this step's temperatures are final (after K2).
+// t_out / u_out: original-numbering copies of the new T / u written by K2 / K4.
 void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr, cudaEvent_t wait_src = nullptr,
-                      cudaEvent_t t_final = nullptr) {
+                      cudaEvent_t t_final = nullptr, double* t_out = nullptr, double* u_out = nullptr) {
     const int N = h->plan.N;
     const int nc = (int)h->plan.chunk_start.size() - 1, ncb = h->plan.nchunks_boundary;
     const bool multi = h->plan.nranks > 1;
@@ -274,7 +275,7 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr, cudaEvent_t 
         }
         mark();
         if (wait_src) CU(cudaStreamWaitEvent(h->s, wait_src, 0));
-        k_thermal_node<<<blocks(N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur, h->mode == TVEGPU_THERMAL_ONLY);
+        k_thermal_node<<<blocks(N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur, h->mode == TVEGPU_THERMAL_ONLY, t_out);
         mark();
     } else if (wait_src) {
         CU(cudaStreamWaitEvent(h->s, wait_src, 0));
@@ -290,7 +291,7 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr, cudaEvent_t 
             h->nn == 4 ? launch_mech_element<4>(h, 0, nc) : launch_mech_element<8>(h, 0, nc);
         }
         mark();
-        k_mech_node<<<blocks(N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur, 1);
+        k_mech_node<<<blocks(N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur, 1, u_out);
         mark();
         h->cur ^= 1;
     }
@@ -358,10 +359,15 @@ void enqueue_steps(tvegpu_engine* h, long long nsteps) {
     }
 }
 
-tvegpu_status sync_and_check(tvegpu_engine* h, long long step_at_start, int cur_at_start) {
-    CU(cudaMemcpyAsync(h->h_words, h->ptr.clock, sizeof(Clock), cudaMemcpyDeviceToHost, h->s));
-    CU(cudaMemcpyAsync(h->h_words + 3, h->ptr.err_inst, 8, cudaMemcpyDeviceToHost, h->s));
-    CU(cudaMemcpyAsync(h->h_words + 4, h->ptr.err_elem, 8, cudaMemcpyDeviceToHost, h->s));
+// Enqueues the 40-byte status read (clock + error words) on the main stream.
+void enqueue_status_read(tvegpu_engine* h) {
+    CU(cudaMemcpyAsync(h->h_words, h->ptr.clock, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->s));
+}
+
+// status_enqueued: the caller already enqueued enqueue_status_read after the last step.
+tvegpu_status sync_and_check(tvegpu_engine* h, long long step_at_start, int cur_at_start,
+                             bool status_enqueued = false) {
+    if (!status_enqueued) enqueue_status_read(h);
     CU(cudaStreamSynchronize(h->s));
     Clock c;
     std::memcpy(&c, h->h_words, sizeof(Clock));
@@ -667,9 +673,14 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
         }
     }
     // ---- clock and error words
-    h->ptr.clock = dalloc<Clock>(own, 1);
-    h->ptr.err_inst = dalloc<unsigned long long>(own, 1);
-    h->ptr.err_elem = dalloc<unsigned long long>(own, 1);
+    // clock + the two error words contiguous: the end-of-call check is one 40-byte read
+    static_assert(sizeof(Clock) == 24, "status block layout");
+    {
+        unsigned long long* st = dalloc<unsigned long long>(own, 5);
+        h->ptr.clock = reinterpret_cast<Clock*>(st);
+        h->ptr.err_inst = st + 3;
+        h->ptr.err_elem = st + 4;
+    }
     {
         Clock c{0.0, 0, 0, 0};
         CU(cudaMemcpyAsync(h->ptr.clock, &c, sizeof c, cudaMemcpyHostToDevice, s));
@@ -1271,37 +1282,43 @@ tvegpu_status tvegpu_step_io(tvegpu_engine* h, const double* power, int64_t n, d
             h->pend_step = h->host_step;
             h->pend_cur = h->cur;
         }
+        // K2 / K4 of the last step write T / u straight into the I/O buffer in original
+        // numbering (no renumbering kernel on the tail); modes without that kernel
+        // renumber the unchanged field from the records instead
+        double* dT = io_buffer(h);
+        double* du = dT + N;
+        const bool thermal = h->mode != TVEGPU_MECHANICAL_ONLY, mech = h->mode != TVEGPU_THERMAL_ONLY;
         auto one = [&](bool first, bool last) {
             refresh_sources_if_needed(h, h->host_time);
-            enqueue_one_step(h, nullptr, first && power ? h->ev_src : nullptr, last && T ? h->ev_T : nullptr);
+            enqueue_one_step(h, nullptr, first && power ? h->ev_src : nullptr, last && T ? h->ev_T : nullptr,
+                             last && T && thermal ? dT : nullptr, last && u && mech ? du : nullptr);
             h->host_time += h->dt;
             h->host_step += 1;
         };
         one(true, n == 1);
         if (n > 2) enqueue_steps(h, n - 2);
-        if (n > 1) {
-            // T lives in the record K2 of the last step updates: capture it before the flip
-            one(false, true);
-        }
-        double* dT = io_buffer(h);
-        double* du = dT + N;
+        if (n > 1) one(false, true);
+        const bool early_status = h->plan.nranks == 1;
+        if (early_status) enqueue_status_read(h);  // before the u read-back: no extra tail
         if (T) {
-            // the record K2 of the last step updated: rec_cur as it was before that step's flip
-            const bool mech = h->mode != TVEGPU_THERMAL_ONLY;
-            const double4* rT = (h->cur ^ (mech ? 1 : 0)) ? h->ptr.rec1 : h->ptr.rec0;
-            CU(cudaStreamWaitEvent(h->sc, h->ev_T, 0));
-            k_fields_to_orig<<<blocks(N, 256), 256, 0, h->sc>>>(rT, h->ptr.node_orig, N, dT, nullptr);
+            CU(cudaStreamWaitEvent(h->sc, h->ev_T, 0));  // recorded after K2 (T final)
+            if (!thermal) {
+                const double4* rc = h->cur ? h->ptr.rec1 : h->ptr.rec0;
+                k_fields_to_orig<<<blocks(N, 256), 256, 0, h->sc>>>(rc, h->ptr.node_orig, N, dT, nullptr);
+            }
             CU(cudaMemcpyAsync(T, dT, (size_t)N * 8, cudaMemcpyDeviceToHost, h->sc));
         }
         if (u) {
-            const double4* rc = h->cur ? h->ptr.rec1 : h->ptr.rec0;
-            k_fields_to_orig<<<blocks(N, 256), 256, 0, h->s>>>(rc, h->ptr.node_orig, N, nullptr, du);
+            if (!mech) {
+                const double4* rc = h->cur ? h->ptr.rec1 : h->ptr.rec0;
+                k_fields_to_orig<<<blocks(N, 256), 256, 0, h->s>>>(rc, h->ptr.node_orig, N, nullptr, du);
+            }
             CU(cudaMemcpyAsync(u, du, (size_t)3 * N * 8, cudaMemcpyDeviceToHost, h->s));
         }
         CU(cudaGetLastError());
         CU(cudaStreamSynchronize(h->sc));
         h->pending = false;
-        h->last_status = sync_and_check(h, h->pend_step, h->pend_cur);
+        h->last_status = sync_and_check(h, h->pend_step, h->pend_cur, early_status);
         return h->last_status;
     });
 }
@@ -1706,7 +1723,7 @@ void group_step_once(tvegpu_group* G) {
         loopback_copy(G, false);
         for (tvegpu_engine* h : G->parts)
             k_thermal_node<<<blocks(h->plan.N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur,
-                                                                    h->mode == TVEGPU_THERMAL_ONLY);
+                                                                    h->mode == TVEGPU_THERMAL_ONLY, nullptr);
     }
     if (h0->mode != TVEGPU_THERMAL_ONLY) {
         for (tvegpu_engine* h : G->parts) {
@@ -1716,7 +1733,7 @@ void group_step_once(tvegpu_group* G) {
         }
         loopback_copy(G, true);
         for (tvegpu_engine* h : G->parts) {
-            k_mech_node<<<blocks(h->plan.N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur, 1);
+            k_mech_node<<<blocks(h->plan.N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur, 1, nullptr);
             h->cur ^= 1;
         }
     }

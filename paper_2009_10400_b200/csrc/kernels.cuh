@@ -465,7 +465,9 @@ __device__ __forceinline__ void gather3_ell(const double* __restrict__ slots, co
 }
 
 // ------------------------------------------------------------------ K2: thermal node
-__global__ void __launch_bounds__(256) k_thermal_node(const DevParams P, const DevPtrs D, int cur, int closes) {
+// t_out (tvegpu_step_io only): also write T^{n+1} in original numbering for the host read-back.
+__global__ void __launch_bounds__(256) k_thermal_node(const DevParams P, const DevPtrs D, int cur, int closes,
+                                                      double* __restrict__ t_out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < P.N && !D.clock->halted) {
         double4* R = cur ? D.rec1 : D.rec0;
@@ -480,6 +482,7 @@ __global__ void __launch_bounds__(256) k_thermal_node(const DevParams P, const D
         if (m & BC_TFIX) Tn = __ldg(D.bc_tfix + __ldg(D.bc_index + i));
         if (!isfinite(Tn)) atomicMin(D.err_inst, pack_inst(D.clock->step, 0, D.node_orig[i]));
         R[i].w = Tn;
+        if (t_out) t_out[__ldg(D.node_orig + i)] = Tn;
     }
     if (closes) close_step(D, P.dt);
 }
@@ -769,7 +772,9 @@ __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
 }
 
 // ------------------------------------------------------------------ K4: mechanical node
-__global__ void __launch_bounds__(256) k_mech_node(const DevParams P, const DevPtrs D, int cur, int closes) {
+// u_out (tvegpu_step_io only): also write u^{n+1} in original numbering for the host read-back.
+__global__ void __launch_bounds__(256) k_mech_node(const DevParams P, const DevPtrs D, int cur, int closes,
+                                                   double* __restrict__ u_out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < P.N && !D.clock->halted) {
         const double4* Rc = cur ? D.rec1 : D.rec0;
@@ -811,6 +816,10 @@ __global__ void __launch_bounds__(256) k_mech_node(const DevParams P, const DevP
         if (!(isfinite(x) && isfinite(y) && isfinite(z)))
             atomicMin(D.err_inst, pack_inst(D.clock->step, 1, D.node_orig[i]));
         st4(Rn + i, make_double4(x, y, z, u.w));
+        if (u_out) {
+            double* o = u_out + 3 * (size_t)__ldg(D.node_orig + i);
+            o[0] = x, o[1] = y, o[2] = z;
+        }
         if (P.diag) {
             D.diag_f[3 * (size_t)i] = f0;
             D.diag_f[3 * (size_t)i + 1] = f1;
