@@ -1,0 +1,88 @@
+"""Size ladder on one B200 — the reference's run_bench / bench_scaling_slope
+(engine.hpp:145-162; SPEC.md:371-378 and criterion 9): per-step time of the three
+coupled modes TherMechTI < TherMechExpanTI < TherMechExpanTD on structured cubes
+(H8 n^3 for n = 100..252, i.e. 1M..16M elements; Kuhn T4 n^3), the log-log slope of
+step time vs element count, and the host setup time.  Device-timed (CUDA events on
+the engine's stream, graph-replayed steps after warm-up).
+
+    python scripts/ladder.py [--kinds H8,T4] [--steps 200] [--out profiles/ladder_r1.json]
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2009_10400_b200 as tg
+from paper_2009_10400_b200 import configs
+from paper_2009_10400_b200.problem import H8, T4
+
+MODES = {"TherMechTI": dict(expansion_enabled=False, temperature_dependent=False),
+         "TherMechExpanTI": dict(expansion_enabled=True, temperature_dependent=False),
+         "TherMechExpanTD": dict(expansion_enabled=True, temperature_dependent=True)}
+LADDER = {H8: [100, 126, 159, 200, 252], T4: [40, 50, 63, 80, 100, 126]}
+
+
+def time_steps(eng, steps, warmup):
+    stream = torch.cuda.ExternalStream(eng.stream)
+    eng.step(warmup)
+    eng.sync()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    eng.step(steps)
+    b.record(stream)
+    b.synchronize()
+    return a.elapsed_time(b) / steps
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--kinds", default="H8,T4")
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--out", default="gpurun_out/ladder.json")
+    args = ap.parse_args()
+    rows = []
+    for kname in args.kinds.split(","):
+        kind = H8 if kname == "H8" else T4
+        for n in LADDER[kind]:
+            t0 = time.perf_counter()
+            p = configs.cfg5_h8(n, steps=args.steps + args.warmup + 64) if kind == H8 else \
+                configs.cfg5_t4(n, steps=args.steps + args.warmup + 64)
+            t_mesh = time.perf_counter() - t0
+            row = dict(kind=kname, n=n, elements=p.num_elements, nodes=p.num_nodes, mesh_gen_s=t_mesh)
+            for mname, flags in MODES.items():
+                for k, v in flags.items():
+                    setattr(p, k, v)
+                t0 = time.perf_counter()
+                eng = tg.Engine(p)
+                eng.sync()
+                setup = time.perf_counter() - t0
+                ms = time_steps(eng, args.steps, args.warmup)
+                row[mname] = ms
+                row[mname + "_setup_s"] = setup
+                del eng
+                torch.cuda.empty_cache()
+            rows.append(row)
+            print(json.dumps(row), flush=True)
+    out = {"rows": rows, "slopes": {}}
+    for kname in args.kinds.split(","):
+        r = [x for x in rows if x["kind"] == kname]
+        for mname in MODES:
+            x = np.log([q["elements"] for q in r])
+            y = np.log([q[mname] for q in r])
+            out["slopes"][f"{kname}/{mname}"] = float(np.polyfit(x, y, 1)[0])
+        out[f"{kname}_mode_order_holds"] = all(q["TherMechTI"] < q["TherMechExpanTI"] < q["TherMechExpanTD"] for q in r)
+    print(json.dumps(out["slopes"]), flush=True)
+    os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
+    with open(args.out, "w") as f:
+        json.dump(out, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
