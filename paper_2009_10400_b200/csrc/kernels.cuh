@@ -329,7 +329,10 @@ __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefe
 
 // ------------------------------------------------------------------ K1: thermal element
 template <int NN>
-__global__ void __launch_bounds__(kChunkThreads) k_thermal_element(const DevParams P, const DevPtrs D, int cur,
+#ifndef TVEGPU_K1_MINBLOCKS
+#define TVEGPU_K1_MINBLOCKS 1
+#endif
+__global__ void __launch_bounds__(kChunkThreads, TVEGPU_K1_MINBLOCKS) k_thermal_element(const DevParams P, const DevPtrs D, int cur,
                                                                    int c0, int c1) {
     if (D.clock->halted) return;  // uniform across the block
     extern __shared__ double2 smem_planes[];
