@@ -30,7 +30,10 @@ namespace tvegpu {
 
 constexpr int kMaxTable = 16;
 constexpr int kMaxProny = 4;
-constexpr int kChunkThreads = 128;  // element kernels: one thread per element of a 128-element chunk
+#ifndef TVEGPU_CHUNK
+#define TVEGPU_CHUNK 128
+#endif
+constexpr int kChunkThreads = TVEGPU_CHUNK;  // element kernels: one thread per element of a chunk (plan.hpp kChunk)
 // Mechanical slot record: (fx, fy, fz, pad), 32 bytes, so an element writes each
 // contribution with one full-sector 256-bit store and a node reads it with one
 // 256-bit load (24-byte records needed three 8-byte requests per contribution).

@@ -86,7 +86,10 @@ struct RankPlan {
     std::vector<int32_t> send_pos;   // send_off.back()
 };
 
-constexpr int kChunk = 128;
+#ifndef TVEGPU_CHUNK
+#define TVEGPU_CHUNK 128  // elements per chunk = threads per element-kernel CTA (kernels.cuh kChunkThreads)
+#endif
+constexpr int kChunk = TVEGPU_CHUNK;
 
 // Fills the chunk fields of a plan (called by build_rank_plan).
 void build_chunks(RankPlan& r);
