@@ -14,11 +14,14 @@
 #include <cstdint>
 #include <istream>
 #include <iterator>
+#include <fstream>
 #include <limits>
+#include <map>
 #include <ostream>
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <utility>
 #include <vector>
 
@@ -48,6 +51,7 @@ struct Mesh {
     std::vector<std::array<int, 8>> elements;      // first nodes_per_element() entries used
     std::vector<Vec3> fiber_dirs;                   // empty or one per element
     std::vector<std::array<Vec3, 2>> expansion_axes;
+    std::map<std::string, std::vector<int>> node_sets, element_sets;  // 0-based
     int node_count() const { return (int)nodes.size(); }
     int element_count() const { return (int)elements.size(); }
 };
@@ -380,5 +384,45 @@ private:
     SimulationState mirror_;
     bool mirror_valid_ = false, dirty_ = false;
 };
+
+// mesh.hpp:73-79 load_mesh / load_mesh_file: the library's parallel parser (SPEC.md:88 format).
+inline Mesh load_mesh(std::string_view text) {
+    tvegpu_mesh* h = nullptr;
+    tvegpu_mesh_view v;
+    const tvegpu_status st = tvegpu_load_mesh(text.data(), text.size(), &h, &v);
+    if (st == TVEGPU_E_PARSE) throw ParseError(tvegpu_create_error());
+    if (st == TVEGPU_E_VALIDATION) throw ValidationError(tvegpu_create_error());
+    if (st != TVEGPU_OK) throw std::runtime_error(tvegpu_create_error());
+    Mesh m;
+    const int nn = v.kind == TVEGPU_H8 ? 8 : 4;
+    m.kind = v.kind == TVEGPU_H8 ? ElementKind::H8 : ElementKind::T4;
+    m.nodes.resize(v.num_nodes);
+    for (int i = 0; i < v.num_nodes; ++i) m.nodes[i] = {v.nodes[3 * i], v.nodes[3 * i + 1], v.nodes[3 * i + 2]};
+    m.elements.assign(v.num_elements, std::array<int, 8>{});
+    for (int e = 0; e < v.num_elements; ++e)
+        for (int a = 0; a < nn; ++a) m.elements[e][a] = v.elements[(size_t)nn * e + a];
+    if (v.fiber_dirs)
+        for (int e = 0; e < v.num_elements; ++e)
+            m.fiber_dirs.push_back({v.fiber_dirs[3 * e], v.fiber_dirs[3 * e + 1], v.fiber_dirs[3 * e + 2]});
+    if (v.expansion_axes)
+        for (int e = 0; e < v.num_elements; ++e) {
+            const double* q = v.expansion_axes + 6 * (size_t)e;
+            m.expansion_axes.push_back({Vec3{q[0], q[1], q[2]}, Vec3{q[3], q[4], q[5]}});
+        }
+    for (int k = 0; k < v.num_node_sets; ++k)
+        m.node_sets[v.node_set_names[k]].assign(v.node_set_items + v.node_set_offsets[k],
+                                                v.node_set_items + v.node_set_offsets[k + 1]);
+    for (int k = 0; k < v.num_element_sets; ++k)
+        m.element_sets[v.element_set_names[k]].assign(v.element_set_items + v.element_set_offsets[k],
+                                                      v.element_set_items + v.element_set_offsets[k + 1]);
+    tvegpu_mesh_destroy(h);
+    return m;
+}
+inline Mesh load_mesh_file(const std::string& path) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw IoError("load_mesh_file: cannot open " + path);
+    const std::string text((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    return load_mesh(text);
+}
 
 }  // namespace tve::gpu

@@ -264,6 +264,34 @@ const char* tvegpu_status_string(tvegpu_status s);
 /* critical_timestep(mesh, material) (mesh.hpp:92-97). */
 tvegpu_status tvegpu_critical_timestep(const tvegpu_problem* problem, double* thermal,
                                        double* mechanical);
+/* load_mesh (mesh.hpp:73-79): parse + validate the text mesh format of SPEC.md:88
+ * (sections $nodes, $elements K t4|h8, $nodeset, $elemset, $fibers, $expansion_axes;
+ * 1-based ids in the file, 0-based in the view), bulk lines parsed in parallel.
+ * Errors: E_PARSE with "line L: ..." / E_VALIDATION (mixed kinds, out-of-range index
+ * or inverted element naming the element, non-unit direction) via tvegpu_create_error.
+ * The view's arrays plug straight into tvegpu_problem (nodes, elements, fiber_dirs,
+ * expansion_axes) and stay valid until tvegpu_mesh_destroy. */
+typedef struct tvegpu_mesh tvegpu_mesh;
+typedef struct tvegpu_mesh_view {
+    int32_t kind;                   /* TVEGPU_T4 / TVEGPU_H8 */
+    int32_t num_nodes, num_elements;
+    const double* nodes;            /* 3 * num_nodes */
+    const int32_t* elements;        /* nn * num_elements, 0-based */
+    const double* fiber_dirs;       /* 3 * num_elements or NULL */
+    const double* expansion_axes;   /* 6 * num_elements (m, n) or NULL */
+    int32_t num_node_sets;
+    const char* const* node_set_names;
+    const int32_t* node_set_offsets;  /* num_node_sets + 1 */
+    const int32_t* node_set_items;    /* 0-based node ids */
+    int32_t num_element_sets;
+    const char* const* element_set_names;
+    const int32_t* element_set_offsets;
+    const int32_t* element_set_items;
+} tvegpu_mesh_view;
+tvegpu_status tvegpu_load_mesh(const char* text, uint64_t length, tvegpu_mesh** out, tvegpu_mesh_view* view);
+void tvegpu_mesh_get_view(const tvegpu_mesh* mesh, tvegpu_mesh_view* view);
+void tvegpu_mesh_destroy(tvegpu_mesh* mesh);
+
 /* Library-owned error text for failures before a handle exists. */
 const char* tvegpu_create_error(void);
 int32_t tvegpu_abi_version(void);

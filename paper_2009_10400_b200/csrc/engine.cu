@@ -107,6 +107,10 @@ struct Region {
 
 }  // namespace
 
+namespace tvegpu {
+void set_create_error(const std::string& m) { g_create_error = m; }
+}  // namespace tvegpu
+
 struct tvegpu_engine {
     int device = 0, nn = 4, kind = 0, mode = 0, N_global = 0, E_global = 0, P = 0;
     double dt = 0;
@@ -729,7 +733,6 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     CU(cudaStreamSynchronize(s));
 }
 
-std::string status_name(tvegpu_status st) { return tvegpu_status_string(st); }
 
 template <class F>
 tvegpu_status guard(tvegpu_engine* h, F&& f) {

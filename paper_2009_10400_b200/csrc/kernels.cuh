@@ -283,7 +283,7 @@ __device__ __forceinline__ int stage_chunk(const DevPtrs& D, const double4* __re
         en[j] = k < st ? __ldg(ent + k) : make_int2(-1, 0);
     }
     const int eb = __ldg(D.chunk_start + c), ne = __ldg(D.chunk_start + c + 1) - eb;
-    const int e = threadIdx.x < ne ? eb + threadIdx.x : -1;
+    const int e = (int)threadIdx.x < ne ? eb + (int)threadIdx.x : -1;
     uint4 w8 = make_uint4(0, 0, 0, 0);
     uint2 w4 = make_uint2(0, 0);
     if (e >= 0) {

@@ -494,7 +494,8 @@ static std::vector<int32_t> colour_slots(const std::vector<int32_t>& nodes, cons
         for (int a = 0; a < nn; ++a) {
             int g[8], k = 0;
             for (int l = q * 8; l < std::min(ne, q * 8 + 8); ++l) g[k++] = idx(conn[(size_t)l * nn + a]);
-            std::sort(g, g + k);
+            for (int x = 1; x < k; ++x)  // insertion sort of <= 8 ids
+                for (int y = x; y > 0 && g[y - 1] > g[y]; --y) std::swap(g[y - 1], g[y]);
             k = (int)(std::unique(g, g + k) - g);
             if (k < 2) continue;
             for (int j = 0; j < k; ++j) {

@@ -16,7 +16,7 @@ import subprocess
 
 import numpy as np
 
-from .problem import Problem
+from .problem import H8, Problem
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # TVEGPU_LIB selects an experimental build variant (csrc/Makefile `variant` target).
@@ -100,6 +100,9 @@ EXPORTS = {
     "tvegpu_set_nodal_sources": (C.c_int, [C.c_void_p, _dp]),
     "tvegpu_step_io": (C.c_int, [C.c_void_p, _dp, C.c_int64, _dp, _dp]),
     "tvegpu_get_summary": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "tvegpu_load_mesh": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(C.c_void_p), C.c_void_p]),
+    "tvegpu_mesh_get_view": (None, [C.c_void_p, C.c_void_p]),
+    "tvegpu_mesh_destroy": (None, [C.c_void_p]),
     "tvegpu_checkpoint_size": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
     "tvegpu_save_checkpoint": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "tvegpu_load_checkpoint": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
@@ -177,6 +180,57 @@ def nccl_unique_id() -> bytes:
     if rc:
         raise NcclError(lib().tvegpu_create_error().decode())
     return buf.raw
+
+
+class _MeshView(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("num_nodes", C.c_int32), ("num_elements", C.c_int32),
+                ("nodes", C.POINTER(C.c_double)), ("elements", C.POINTER(C.c_int32)),
+                ("fiber_dirs", C.POINTER(C.c_double)), ("expansion_axes", C.POINTER(C.c_double)),
+                ("num_node_sets", C.c_int32), ("node_set_names", C.POINTER(C.c_char_p)),
+                ("node_set_offsets", C.POINTER(C.c_int32)), ("node_set_items", C.POINTER(C.c_int32)),
+                ("num_element_sets", C.c_int32), ("element_set_names", C.POINTER(C.c_char_p)),
+                ("element_set_offsets", C.POINTER(C.c_int32)), ("element_set_items", C.POINTER(C.c_int32))]
+
+
+def load_mesh(src):
+    """load_mesh / load_mesh_file (mesh.hpp:73-79): parse the SPEC.md:88 text format (str,
+    bytes or a path) with the library's parallel parser.  Returns dict(kind, nodes (N,3),
+    elements (E,nn) 0-based, fiber_dirs, expansion_axes, node_sets, element_sets)."""
+    if isinstance(src, (bytes, bytearray)):
+        data = bytes(src)
+    elif isinstance(src, str) and ("\n" in src or src.lstrip().startswith("$")):
+        data = src.encode()
+    else:
+        with open(src, "rb") as f:
+            data = f.read()
+    h, v = C.c_void_p(), _MeshView()
+    rc = lib().tvegpu_load_mesh(data, len(data), C.byref(h), C.byref(v))
+    if rc:
+        raise _BY_STATUS.get(rc, TveError)(lib().tvegpu_create_error().decode())
+    try:
+        N, E = v.num_nodes, v.num_elements
+        nn = 8 if v.kind == H8 else 4
+
+        def arr(ptr, n, dt=np.float64):
+            return np.ctypeslib.as_array(ptr, shape=(n,)).astype(dt, copy=True)
+
+        def sets(n, names, off, items):
+            out = {}
+            if n:
+                o = arr(off, n + 1, np.int32)
+                it = arr(items, int(o[-1]), np.int32) if o[-1] else np.zeros(0, np.int32)
+                for k in range(n):
+                    out[names[k].decode()] = it[o[k]:o[k + 1]]
+            return out
+        return dict(kind=v.kind, nodes=arr(v.nodes, 3 * N).reshape(N, 3),
+                    elements=arr(v.elements, nn * E, np.int32).reshape(E, nn),
+                    fiber_dirs=arr(v.fiber_dirs, 3 * E).reshape(E, 3) if v.fiber_dirs else None,
+                    expansion_axes=arr(v.expansion_axes, 6 * E).reshape(E, 6) if v.expansion_axes else None,
+                    node_sets=sets(v.num_node_sets, v.node_set_names, v.node_set_offsets, v.node_set_items),
+                    element_sets=sets(v.num_element_sets, v.element_set_names, v.element_set_offsets,
+                                      v.element_set_items))
+    finally:
+        lib().tvegpu_mesh_destroy(h)
 
 
 def plan(problem: Problem, nranks=1, rank=0, reorder=True):

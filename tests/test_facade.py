@@ -63,3 +63,27 @@ def test_facade_demo_matches_oracle():
     assert float(m.group(1)) == Tmax  # device reduction == host max of the same field
     vo, no = O.ablation_volume("H8", p.nodes, p.elements, s["T"], 40.0, disp=s["u"])
     assert int(m.group(4)) == no and abs(float(m.group(3)) - vo) <= 1e-9 * max(vo, 1e-30)
+
+
+def test_facade_load_mesh_on_cpu():
+    """tve::gpu::load_mesh (mesh.hpp:76) from C++: host-only, runs without a GPU."""
+    src = os.path.join(ROOT, "build", "load_mesh_check.cpp")
+    with open(src, "w") as f:
+        f.write(r'''#include <cstdio>
+#include "tve_gpu.hpp"
+int main() {
+    const char* text = "# unit cube\n$nodes 8\n1 0 0 0\n2 1 0 0\n3 1 1 0\n4 0 1 0\n5 0 0 1\n6 1 0 1\n7 1 1 1\n8 0 1 1\n"
+                       "$elements 1 h8\n1 1 2 3 4 5 6 7 8\n$nodeset bottom 4\n1 2 3 4\n";
+    tve::gpu::Mesh m = tve::gpu::load_mesh(text);
+    std::printf("%d %d %d %zu\n", m.node_count(), m.element_count(), m.elements[0][6], m.node_sets["bottom"].size());
+    try { tve::gpu::load_mesh("$nodes 1\n1 0 0\n"); } catch (const tve::gpu::ParseError& e) { std::printf("parse: %s\n", e.what()); }
+    return 0;
+}
+''')
+    cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+    out = os.path.join(ROOT, "build", "load_mesh_check")
+    subprocess.run([cxx, "-std=c++17", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), src, "-L", LIBDIR,
+                    "-ltvegpu", f"-Wl,-rpath,{LIBDIR}", "-o", out], check=True)
+    res = subprocess.run([out], capture_output=True, text=True, check=True).stdout.splitlines()
+    assert res[0] == "8 1 6 4"
+    assert res[1].startswith("parse: line 2")
