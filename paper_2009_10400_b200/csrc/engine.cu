@@ -142,6 +142,7 @@ struct tvegpu_engine {
     std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
     int steps_per_graph = 64;
     bool warmed = false;  // a plain (un-captured) step has run
+    bool pdl = false;     // programmatic dependent launch of the step kernels (single partition)
     // errors
     std::string err;
     long long err_step = -1;
@@ -221,22 +222,39 @@ void exchange(tvegpu_engine* h, double* slots, double* sendbuf, double* /*recvbu
 
 size_t chunk_smem(const tvegpu_engine* h) { return (size_t)4 * h->prm.max_chunk_nodes * sizeof(double2); }
 
+// Launches a step kernel on the compute stream, with programmatic stream
+// serialization when h->pdl (kernels.cuh pdl_wait / pdl_trigger).
+template <typename... KArgs, typename... Args>
+void launch_step_kernel(tvegpu_engine* h, void (*kern)(KArgs...), int grid, int block, size_t smem, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = h->s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = h->pdl ? 1 : 0;
+    CU(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 // Element kernels run one CTA per 128-element chunk over chunk range [c0, c1).
 template <int NN>
 void launch_mech_element(tvegpu_engine* h, int c0, int c1) {
     if (c1 <= c0) return;
     const size_t sm = chunk_smem(h);
     switch (h->prm.exp_kind < 0 ? 0 : (h->prm.exp_kind == 0 ? 1 : 2)) {
-        case 0: k_mech_element<NN, 0><<<c1 - c0, kChunkThreads, sm, h->s>>>(h->prm, h->ptr, h->cur, c0, c1); break;
-        case 1: k_mech_element<NN, 1><<<c1 - c0, kChunkThreads, sm, h->s>>>(h->prm, h->ptr, h->cur, c0, c1); break;
-        default: k_mech_element<NN, 2><<<c1 - c0, kChunkThreads, sm, h->s>>>(h->prm, h->ptr, h->cur, c0, c1); break;
+        case 0: launch_step_kernel(h, k_mech_element<NN, 0>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
+        case 1: launch_step_kernel(h, k_mech_element<NN, 1>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
+        default: launch_step_kernel(h, k_mech_element<NN, 2>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
     }
 }
 
 template <int NN>
 void launch_thermal_element(tvegpu_engine* h, int c0, int c1) {
     if (c1 <= c0) return;
-    k_thermal_element<NN><<<c1 - c0, kChunkThreads, chunk_smem(h), h->s>>>(h->prm, h->ptr, h->cur, c0, c1);
+    launch_step_kernel(h, k_thermal_element<NN>, c1 - c0, kChunkThreads, chunk_smem(h), h->prm, h->ptr, h->cur, c0, c1);
 }
 
 void set_smem_limits(tvegpu_engine* h) {
@@ -279,7 +297,8 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr, cudaEvent_t 
         }
         mark();
         if (wait_src) CU(cudaStreamWaitEvent(h->s, wait_src, 0));
-        k_thermal_node<<<blocks(N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur, h->mode == TVEGPU_THERMAL_ONLY, t_out);
+        launch_step_kernel(h, k_thermal_node, blocks(N, 256), 256, 0, h->prm, h->ptr, h->cur,
+                           (int)(h->mode == TVEGPU_THERMAL_ONLY), t_out);
         mark();
     } else if (wait_src) {
         CU(cudaStreamWaitEvent(h->s, wait_src, 0));
@@ -295,7 +314,7 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr, cudaEvent_t 
             h->nn == 4 ? launch_mech_element<4>(h, 0, nc) : launch_mech_element<8>(h, 0, nc);
         }
         mark();
-        k_mech_node<<<blocks(N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur, 1, u_out);
+        launch_step_kernel(h, k_mech_node, blocks(N, 256), 256, 0, h->prm, h->ptr, h->cur, 1, u_out);
         mark();
         h->cur ^= 1;
     }
@@ -545,6 +564,8 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     }
     CU(cudaStreamSynchronize(s));
     set_smem_limits(h);
+    // PDL only where the four step kernels follow each other directly on one stream
+    h->pdl = !loopback && pl.nranks == 1 && !std::getenv("TVEGPU_NO_PDL");
     h->ptr.elem_orig = dupload(own, pl.elem_orig, s);
     h->ptr.theta = dalloc<double>(own, (size_t)6 * P * E);
     CU(cudaMemsetAsync(h->ptr.theta, 0, std::max<size_t>(1, (size_t)6 * P * E) * 8, s));

@@ -262,6 +262,14 @@ __device__ __forceinline__ void element_pass(const NodeStage& S, const int (&n)[
     V = NN == 4 ? dJ * (1.0 / 6.0) : 8.0 * dJ;
 }
 
+// Programmatic dependent launch (single-partition graphs): a kernel issues the loads
+// of data its immediate predecessor does not write (staging indices, coordinates,
+// node constants), then waits for the predecessor grid; every kernel signals its
+// dependents only after its own wait, so anything two launches back is complete
+// when a kernel starts.  Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Stage one chunk: its unique nodes' (u, T) records and coordinates go to shared
 // memory once per chunk (each node is used by up to 8 of the chunk's elements),
 // replacing 2*NN random 32-byte global gathers per element.  Returns this
@@ -304,10 +312,11 @@ __device__ __forceinline__ int stage_chunk(const DevPtrs& D, const double4* __re
         double4 r[kStageBatch], x[kStageBatch];
 #pragma unroll
         for (int j = 0; j < kStageBatch; ++j)
-            if (g[j] >= 0) {
-                r[j] = ldg4(R + g[j]);
-                x[j] = ldg4(D.X + g[j]);
-            }
+            if (g[j] >= 0) x[j] = ldg4(D.X + g[j]);
+        pdl_wait();  // the node records are the predecessor's output
+#pragma unroll
+        for (int j = 0; j < kStageBatch; ++j)
+            if (g[j] >= 0) r[j] = ldg4(R + g[j]);
 #pragma unroll
         for (int j = 0; j < kStageBatch; ++j)
             if (g[j] >= 0) {
@@ -337,13 +346,12 @@ template <int NN>
 #endif
 __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K1_MINBLOCKS) k_thermal_element(const DevParams P, const DevPtrs D, int cur,
                                                                    int c0, int c1) {
-    if (D.clock->halted) return;  // uniform across the block
     extern __shared__ double2 smem_planes[];
     const int ms = P.max_chunk_nodes;
     const NodeStage S{smem_planes, smem_planes + ms, smem_planes + 2 * ms, smem_planes + 3 * ms};
     int n[NN];
     const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, P.stage_stride, S, n);
-    if (e < 0) return;
+    if (D.clock->halted || e < 0) return;  // halted: uniform across the grid (read after the wait)
     double H[9], A[9], gT[3], V, Ts;
     element_pass<NN, true>(S, n, H, A, V, Ts, gT);
     // F = I + H A^T
@@ -392,6 +400,7 @@ __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K1_MINBLOCKS) k_thermal_
         for (int a = 0; a < 8; a += 2) reinterpret_cast<double2*>(out)[a / 2] = make_double2(f[a], f[a + 1]);
     }
     if (dF == 0.0) atomicMin(D.err_elem, pack_elem(D.clock->step, D.elem_orig[e]));
+    pdl_trigger();  // after this block's work: the successor fills in behind the last wave
 }
 
 // ------------------------------------------------------------------ end of step (last block)
@@ -445,17 +454,15 @@ __device__ __forceinline__ void gather3(const double* __restrict__ slots, const 
 // offset load first), then all 8 contributions in flight at once.  Padding entries
 // name a slot that is always +0.0 and sit after the real ones, so the canonical-
 // order sum is unchanged bit for bit (s + 0.0 == s; s is never -0.0 from a +0.0 start).
-__device__ __forceinline__ double gather1_ell(const double* __restrict__ slots, const int4* __restrict__ ell, int i) {
-    const int4 a = __ldg(ell + 2 * (size_t)i), b = __ldg(ell + 2 * (size_t)i + 1);
+__device__ __forceinline__ double gather1_ell(const double* __restrict__ slots, const int4 a, const int4 b) {
     const double v0 = __ldg(slots + a.x), v1 = __ldg(slots + a.y), v2 = __ldg(slots + a.z), v3 = __ldg(slots + a.w);
     const double v4 = __ldg(slots + b.x), v5 = __ldg(slots + b.y), v6 = __ldg(slots + b.z), v7 = __ldg(slots + b.w);
     double s = 0.0;
     s += v0, s += v1, s += v2, s += v3, s += v4, s += v5, s += v6, s += v7;
     return s;
 }
-__device__ __forceinline__ void gather3_ell(const double* __restrict__ slots, const int4* __restrict__ ell, int i,
-                                            double& f0, double& f1, double& f2) {
-    const int4 a = __ldg(ell + 2 * (size_t)i), b = __ldg(ell + 2 * (size_t)i + 1);
+__device__ __forceinline__ void gather3_ell(const double* __restrict__ slots, const int4 a, const int4 b, double& f0,
+                                            double& f1, double& f2) {
     const double4* S = reinterpret_cast<const double4*>(slots);
     const int id[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
     double4 v[8];
@@ -475,12 +482,18 @@ __device__ __forceinline__ void gather3_ell(const double* __restrict__ slots, co
 __global__ void __launch_bounds__(256) k_thermal_node(const DevParams P, const DevPtrs D, int cur, int closes,
                                                       double* __restrict__ t_out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int4 ia = make_int4(0, 0, 0, 0), ib = ia;
+    double V = 0.0;
+    if (i < P.N) {  // predecessor-independent loads first (index row, node volume)
+        if (P.ell) ia = __ldg(D.ell + 2 * (size_t)i), ib = __ldg(D.ell + 2 * (size_t)i + 1);
+        V = __ldg(D.vnode + i);
+    }
+    pdl_wait();
     if (i < P.N && !D.clock->halted) {
         double4* R = cur ? D.rec1 : D.rec0;
-        const double s = P.ell ? gather1_ell(D.slot_th, D.ell, i)
+        const double s = P.ell ? gather1_ell(D.slot_th, ia, ib)
                                : gather1(D.slot_th, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1));
         const double T = R[i].w;
-        const double V = __ldg(D.vnode + i);
         const double c = P.td ? interp1(P.cT, P.cV, P.c_len, T) : P.c_fixed;
         const double C = P.rho * c * V;
         double Tn = T + P.dt / C * (-s - P.wbcb * V * (T - P.Ta) + P.Qm * V + __ldg(D.qr + i));
@@ -490,6 +503,7 @@ __global__ void __launch_bounds__(256) k_thermal_node(const DevParams P, const D
         R[i].w = Tn;
         if (t_out) t_out[__ldg(D.node_orig + i)] = Tn;
     }
+    pdl_trigger();
     if (closes) close_step(D, P.dt);
 }
 
@@ -501,7 +515,6 @@ __global__ void __launch_bounds__(256) k_thermal_node(const DevParams P, const D
 template <int NN, int EXP>
 __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
     k_mech_element(const DevParams P, const DevPtrs D, int cur, int c0, int c1) {
-    if (D.clock->halted) return;  // uniform across the block
     extern __shared__ double2 smem_planes[];
     const int ms = P.max_chunk_nodes;
     const NodeStage st{smem_planes, smem_planes + ms, smem_planes + 2 * ms, smem_planes + 3 * ms};
@@ -514,7 +527,7 @@ __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
                 for (int q = 0; q < 6; ++q) prefetch_l1(D.theta + ((size_t)p * 6 + q) * P.E + e0);
     }
     const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, P.stage_stride, st, n);
-    if (e < 0) return;
+    if (D.clock->halted || e < 0) return;
     const int E = P.E;
     double Hd[9], A[9], V, Ts;
     {
@@ -775,6 +788,7 @@ __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
 #pragma unroll
         for (int q = 0; q < 9; ++q) D.diag_S[(size_t)e * 9 + q] = Sm[q];
     }
+    pdl_trigger();
 }
 
 // ------------------------------------------------------------------ K4: mechanical node
@@ -782,11 +796,14 @@ __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
 __global__ void __launch_bounds__(256) k_mech_node(const DevParams P, const DevPtrs D, int cur, int closes,
                                                    double* __restrict__ u_out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int4 ia = make_int4(0, 0, 0, 0), ib = ia;
+    if (i < P.N && P.ell) ia = __ldg(D.ell + 2 * (size_t)i), ib = __ldg(D.ell + 2 * (size_t)i + 1);
+    pdl_wait();
     if (i < P.N && !D.clock->halted) {
         const double4* Rc = cur ? D.rec1 : D.rec0;
         double4* Rn = cur ? D.rec0 : D.rec1;  // holds u^{n-1}; receives u^{n+1}
         double f0, f1, f2;
-        if (P.ell) gather3_ell(D.slot_m, D.ell, i, f0, f1, f2);
+        if (P.ell) gather3_ell(D.slot_m, ia, ib, f0, f1, f2);
         else gather3(D.slot_m, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1), f0, f1, f2);
         const double4 u = ldg4(Rc + i);  // read-only in this kernel
         const double4 up = ld4(Rn + i);  // this thread overwrites it below
@@ -832,6 +849,7 @@ __global__ void __launch_bounds__(256) k_mech_node(const DevParams P, const DevP
             D.diag_f[3 * (size_t)i + 2] = f2;
         }
     }
+    pdl_trigger();
     if (closes) close_step(D, P.dt);
 }
 
