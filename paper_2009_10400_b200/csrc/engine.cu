@@ -220,7 +220,10 @@ void exchange(tvegpu_engine* h, double* slots, double* sendbuf, double* /*recvbu
     CU(cudaEventRecord(h->ev_comm, h->sc));
 }
 
-size_t chunk_smem(const tvegpu_engine* h) { return (size_t)4 * h->prm.max_chunk_nodes * sizeof(double2); }
+// staged planes: (ux,uy), (uz,T) [+ (x,y), (z,-) without precomputed geometry]
+size_t chunk_smem(const tvegpu_engine* h) {
+    return (size_t)(TVEGPU_GEO ? 2 : 4) * h->prm.max_chunk_nodes * sizeof(double2);
+}
 
 // Launches a step kernel on the compute stream, with programmatic stream
 // serialization when h->pdl (kernels.cuh pdl_wait / pdl_trigger).
@@ -601,6 +604,21 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
         h->ptr.vnode = dupload(own, vn, s);
         CU(cudaStreamSynchronize(s));
     }
+#if TVEGPU_GEO
+    {  // per-element reference geometry, once (k_geometry, same arithmetic as the in-kernel path)
+        if (!h->d_conn) {
+            h->d_conn = dalloc<int32_t>(own, pl.conn.size());
+            CU(cudaMemcpyAsync(h->d_conn, pl.conn.data(), pl.conn.size() * 4, cudaMemcpyHostToDevice, s));
+        }
+        double* geo = dalloc<double>(own, (size_t)kGeoRows * std::max(1, pl.E));
+        if (pl.E > 0) {
+            if (nn == 8) k_geometry<8><<<blocks(pl.E, 256), 256, 0, s>>>(h->ptr.X, h->d_conn, pl.E, geo);
+            else k_geometry<4><<<blocks(pl.E, 256), 256, 0, s>>>(h->ptr.X, h->d_conn, pl.E, geo);
+            CU(cudaGetLastError());
+        }
+        h->ptr.geo = geo;
+    }
+#endif
     h->ptr.node_orig = dupload(own, pl.node_orig, s);
     CU(cudaMallocHost(&h->qr_host, std::max(1, N) * sizeof(double)));
     std::memset(h->qr_host, 0, std::max(1, N) * sizeof(double));

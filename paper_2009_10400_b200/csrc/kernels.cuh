@@ -39,6 +39,10 @@ constexpr int kChunkThreads = TVEGPU_CHUNK;  // element kernels: one thread per 
 // 256-bit load (24-byte records needed three 8-byte requests per contribution).
 constexpr int kMW = 4;
 
+#ifndef TVEGPU_GEO
+#define TVEGPU_GEO 1  // per-element reference geometry (A, V, H8 c_al) precomputed in HBM (0: from staged X)
+#endif
+
 struct Clock {
     double time;
     long long step;
@@ -70,6 +74,7 @@ struct DevPtrs {
     const uint16_t* chunk_node_slot;  // their shared-memory slots
     const uint16_t* lconn;          // [E][nn] index of node (e, a) in its chunk's node list
     const int2* stage_ent;          // [nchunks][stage_stride] {local node, shared slot}, {-1, 0} padded
+    const double* geo;              // TVEGPU_GEO: [kGeoRows][E] A (9, row-major), V, H8: c_al = X h_al (12)
     double* theta;             // [P][6][E]   (xx, yy, zz, xy, yz, xz)
     const double* fiber;       // [3][E] or null
     const double* axes;        // [6][E] or null
@@ -205,6 +210,112 @@ struct NodeStage {
     }
 };
 
+// Reference geometry from the element's corner coordinates, in exactly the
+// arithmetic order of element_pass: J (T4: edge matrix; H8: X Xi^T / 8), A = J^-T
+// (H8: / 8), V; and for H8 the hourglass geometry c_al = X h_al in corner order.
+constexpr int kGeoRows = 22;
+template <int NN>
+__global__ void k_geometry(const double4* __restrict__ X, const int32_t* __restrict__ conn, int E, double* geo) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    double J[9];
+    if constexpr (NN == 4) {
+        const double4 x0 = X[conn[(size_t)e * 4]];
+#pragma unroll
+        for (int a = 1; a < 4; ++a) {
+            const double4 x = X[conn[(size_t)e * 4 + a]];
+            J[0 * 3 + a - 1] = x.x - x0.x;
+            J[1 * 3 + a - 1] = x.y - x0.y;
+            J[2 * 3 + a - 1] = x.z - x0.z;
+        }
+    } else {
+        double cX[4][3];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) J[q] = 0.0;
+#pragma unroll
+        for (int al = 0; al < 4; ++al) cX[al][0] = cX[al][1] = cX[al][2] = 0.0;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const double4 x = X[conn[(size_t)e * 8 + a]];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const double s = (double)h8s(a, j);
+                J[0 * 3 + j] += s * x.x;
+                J[1 * 3 + j] += s * x.y;
+                J[2 * 3 + j] += s * x.z;
+            }
+#pragma unroll
+            for (int al = 0; al < 4; ++al) {
+                const double h = (double)h8h(al, a);
+                cX[al][0] += h * x.x;
+                cX[al][1] += h * x.y;
+                cX[al][2] += h * x.z;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 9; ++q) J[q] = J[q] / 8.0;
+#pragma unroll
+        for (int al = 0; al < 4; ++al)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) geo[(size_t)(10 + al * 3 + i) * E + e] = cX[al][i];
+    }
+    double Ad[9];
+    const double dJ = adj3(J, Ad);
+    const double s = (NN == 4 ? 1.0 : 0.125) / dJ;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) geo[(size_t)(i * 3 + j) * E + e] = Ad[j * 3 + i] * s;
+    geo[(size_t)9 * E + e] = NN == 4 ? dJ * (1.0 / 6.0) : 8.0 * dJ;
+}
+
+// Warm L1 with the element's geometry rows (constant: issued before the PDL wait).
+__device__ __forceinline__ void prefetch_geo(const DevPtrs& D, int e, int E, int rows) {
+    for (int q = 0; q < rows; ++q) asm volatile("prefetch.global.L1 [%0];" ::"l"(D.geo + (size_t)q * E + e));
+}
+
+// element_pass with precomputed geometry: only the displacement / temperature sums
+// come from the staged records; A and V are read from the geometry rows.
+template <int NN, bool WANT_GT>
+__device__ __forceinline__ void element_pass_geo(const NodeStage& S, const int (&n)[NN], const DevPtrs& D, int e,
+                                                 int E, double H[9], double A[9], double& V, double& Ts,
+                                                 double gT[3]) {
+    if constexpr (NN == 4) {
+        const double4 r0 = S.rec(n[0]);
+        Ts = r0.w;
+#pragma unroll
+        for (int a = 1; a < 4; ++a) {
+            const double4 r = S.rec(n[a]);
+            H[0 * 3 + a - 1] = r.x - r0.x;
+            H[1 * 3 + a - 1] = r.y - r0.y;
+            H[2 * 3 + a - 1] = r.z - r0.z;
+            if constexpr (WANT_GT) gT[a - 1] = r.w - r0.w;
+            Ts += r.w;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) H[q] = 0.0;
+        if constexpr (WANT_GT) gT[0] = gT[1] = gT[2] = 0.0;
+        Ts = 0.0;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const double4 r = S.rec(n[a]);
+            Ts += r.w;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const double s = (double)h8s(a, j);
+                H[0 * 3 + j] += s * r.x;
+                H[1 * 3 + j] += s * r.y;
+                H[2 * 3 + j] += s * r.z;
+                if constexpr (WANT_GT) gT[j] += s * r.w;
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) A[q] = __ldg(D.geo + (size_t)q * E + e);
+    V = __ldg(D.geo + (size_t)9 * E + e);
+}
+
 template <int NN, bool WANT_GT>
 __device__ __forceinline__ void element_pass(const NodeStage& S, const int (&n)[NN], double H[9], double A[9],
                                              double& V, double& Ts, double gT[3]) {
@@ -310,9 +421,11 @@ __device__ __forceinline__ int stage_chunk(const DevPtrs& D, const double4* __re
             s[j] = en[j].y;
         }
         double4 r[kStageBatch], x[kStageBatch];
+#if !TVEGPU_GEO
 #pragma unroll
         for (int j = 0; j < kStageBatch; ++j)
             if (g[j] >= 0) x[j] = ldg4(D.X + g[j]);
+#endif
         pdl_wait();  // the node records are the predecessor's output
 #pragma unroll
         for (int j = 0; j < kStageBatch; ++j)
@@ -322,8 +435,10 @@ __device__ __forceinline__ int stage_chunk(const DevPtrs& D, const double4* __re
             if (g[j] >= 0) {
                 S.a[s[j]] = make_double2(r[j].x, r[j].y);
                 S.b[s[j]] = make_double2(r[j].z, r[j].w);
+#if !TVEGPU_GEO
                 S.c[s[j]] = make_double2(x[j].x, x[j].y);
                 S.d[s[j]] = make_double2(x[j].z, x[j].w);
+#endif
             }
     }
     if constexpr (NN == 8) {
@@ -350,10 +465,20 @@ __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K1_MINBLOCKS) k_thermal_
     const int ms = P.max_chunk_nodes;
     const NodeStage S{smem_planes, smem_planes + ms, smem_planes + 2 * ms, smem_planes + 3 * ms};
     int n[NN];
+#if TVEGPU_GEO
+    {
+        const int e0 = __ldg(D.chunk_start + c0 + blockIdx.x) + threadIdx.x;
+        if (e0 < P.E) prefetch_geo(D, e0, P.E, 10);
+    }
+#endif
     const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, P.stage_stride, S, n);
     if (D.clock->halted || e < 0) return;  // halted: uniform across the grid (read after the wait)
     double H[9], A[9], gT[3], V, Ts;
+#if TVEGPU_GEO
+    element_pass_geo<NN, true>(S, n, D, e, P.E, H, A, V, Ts, gT);
+#else
     element_pass<NN, true>(S, n, H, A, V, Ts, gT);
+#endif
     // F = I + H A^T
     double F[9];
 #pragma unroll
@@ -525,6 +650,9 @@ __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
             for (int p = 0; p < P.P; ++p)
 #pragma unroll
                 for (int q = 0; q < 6; ++q) prefetch_l1(D.theta + ((size_t)p * 6 + q) * P.E + e0);
+#if TVEGPU_GEO
+        if (e0 < P.E) prefetch_geo(D, e0, P.E, NN == 8 ? kGeoRows : 10);
+#endif
     }
     const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, P.stage_stride, st, n);
     if (D.clock->halted || e < 0) return;
@@ -532,7 +660,11 @@ __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
     double Hd[9], A[9], V, Ts;
     {
         double H[9], gT[3];
+#if TVEGPU_GEO
+        element_pass_geo<NN, false>(st, n, D, e, E, H, A, V, Ts, gT);
+#else
         element_pass<NN, false>(st, n, H, A, V, Ts, gT);
+#endif
         // displacement gradient Hd = F - I = H A^T, kept separate from I (small-strain accuracy)
 #pragma unroll
         for (int i = 0; i < 3; ++i)
@@ -736,6 +868,23 @@ __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
         for (int al = 0; al < 4; ++al)
 #pragma unroll
             for (int i = 0; i < 3; ++i) Uh[al][i] = cX[al][i] = 0.0;
+#if TVEGPU_GEO
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const double2 ra = st.a[n[a]], rb = st.b[n[a]];
+#pragma unroll
+            for (int al = 0; al < 4; ++al) {
+                const double h = (double)h8h(al, a);
+                Uh[al][0] += h * ra.x;
+                Uh[al][1] += h * ra.y;
+                Uh[al][2] += h * rb.x;
+            }
+        }
+#pragma unroll
+        for (int al = 0; al < 4; ++al)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) cX[al][i] = __ldg(D.geo + (size_t)(10 + al * 3 + i) * E + e);
+#else
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
             const double2 ra = st.a[n[a]], rb = st.b[n[a]], xa = st.c[n[a]], xb = st.d[n[a]];
@@ -752,6 +901,7 @@ __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
                 cX[al][2] += h * x.z;
             }
         }
+#endif
         const double k = P.kh * cbrt(V);
 #pragma unroll
         for (int al = 0; al < 4; ++al) {
