@@ -257,6 +257,7 @@ void launch_mech_element(tvegpu_engine* h, int c0, int c1) {
 template <int NN>
 void launch_thermal_element(tvegpu_engine* h, int c0, int c1) {
     if (c1 <= c0) return;
+
     launch_step_kernel(h, k_thermal_element<NN>, c1 - c0, kChunkThreads, chunk_smem(h), h->prm, h->ptr, h->cur, c0, c1);
 }
 
@@ -541,9 +542,9 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     CU(cudaMallocHost(&h->h_words, 8 * sizeof(unsigned long long)));
     cudaStream_t s = h->s;
     auto& own = h->owned;
-    // ---- element arrays.  Geometry (A_e, V_e) is recomputed in-kernel from the node
-    // coordinates, so the element data is the chunked connectivity: per 128-element
-    // chunk its unique node list, per element 16-bit indices into that list.
+    // ---- element arrays: the chunked connectivity (per chunk its unique node list as
+    // fixed-stride {node, slot} entries, per element 16-bit indices into the staged
+    // planes); the reference geometry rows follow once the coordinates are on the device.
     h->ptr.chunk_start = dupload(own, pl.chunk_start, s);
     h->ptr.chunk_node_off = dupload(own, pl.chunk_node_off, s);
     h->ptr.chunk_nodes = dupload(own, pl.chunk_nodes, s);

@@ -455,24 +455,13 @@ __device__ __forceinline__ int stage_chunk(const DevPtrs& D, const double4* __re
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 // ------------------------------------------------------------------ K1: thermal element
-template <int NN>
 #ifndef TVEGPU_K1_MINBLOCKS
 #define TVEGPU_K1_MINBLOCKS 1
 #endif
-__global__ void __launch_bounds__(kChunkThreads, TVEGPU_K1_MINBLOCKS) k_thermal_element(const DevParams P, const DevPtrs D, int cur,
-                                                                   int c0, int c1) {
-    extern __shared__ double2 smem_planes[];
-    const int ms = P.max_chunk_nodes;
-    const NodeStage S{smem_planes, smem_planes + ms, smem_planes + 2 * ms, smem_planes + 3 * ms};
-    int n[NN];
-#if TVEGPU_GEO
-    {
-        const int e0 = __ldg(D.chunk_start + c0 + blockIdx.x) + threadIdx.x;
-        if (e0 < P.E) prefetch_geo(D, e0, P.E, 10);
-    }
-#endif
-    const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, P.stage_stride, S, n);
-    if (D.clock->halted || e < 0) return;  // halted: uniform across the grid (read after the wait)
+// K1 element body: element e of the staged chunk S (n = its node slots)
+template <int NN>
+__device__ __forceinline__ void k1_body(const DevParams& P, const DevPtrs& D, const NodeStage& S, const int e,
+                                        const int (&n)[NN]) {
     double H[9], A[9], gT[3], V, Ts;
 #if TVEGPU_GEO
     element_pass_geo<NN, true>(S, n, D, e, P.E, H, A, V, Ts, gT);
@@ -525,6 +514,24 @@ __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K1_MINBLOCKS) k_thermal_
         for (int a = 0; a < 8; a += 2) reinterpret_cast<double2*>(out)[a / 2] = make_double2(f[a], f[a + 1]);
     }
     if (dF == 0.0) atomicMin(D.err_elem, pack_elem(D.clock->step, D.elem_orig[e]));
+}
+
+template <int NN>
+__global__ void __launch_bounds__(kChunkThreads, TVEGPU_K1_MINBLOCKS) k_thermal_element(const DevParams P, const DevPtrs D, int cur,
+                                                                   int c0, int c1) {
+    extern __shared__ double2 smem_planes[];
+    const int ms = P.max_chunk_nodes;
+    const NodeStage S{smem_planes, smem_planes + ms, smem_planes + 2 * ms, smem_planes + 3 * ms};
+    int n[NN];
+#if TVEGPU_GEO
+    {
+        const int e0 = __ldg(D.chunk_start + c0 + blockIdx.x) + threadIdx.x;
+        if (e0 < P.E) prefetch_geo(D, e0, P.E, 10);
+    }
+#endif
+    const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, P.stage_stride, S, n);
+    if (D.clock->halted || e < 0) return;  // halted: uniform across the grid (read after the wait)
+    k1_body<NN>(P, D, S, e, n);
     pdl_trigger();  // after this block's work: the successor fills in behind the last wave
 }
 
@@ -637,25 +644,10 @@ __global__ void __launch_bounds__(256) k_thermal_node(const DevParams P, const D
 #ifndef TVEGPU_K3_MINBLOCKS
 #define TVEGPU_K3_MINBLOCKS 4  // 128 registers: 16 warps/SM (168 unbounded -> 8 warps, latency-bound)
 #endif
+// K3 element body: element e of the staged chunk st (n = its node slots)
 template <int NN, int EXP>
-__global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
-    k_mech_element(const DevParams P, const DevPtrs D, int cur, int c0, int c1) {
-    extern __shared__ double2 smem_planes[];
-    const int ms = P.max_chunk_nodes;
-    const NodeStage st{smem_planes, smem_planes + ms, smem_planes + 2 * ms, smem_planes + 3 * ms};
-    int n[NN];
-    {  // the Prony history is read late in the kernel: start pulling it into L1 now
-        const int e0 = __ldg(D.chunk_start + c0 + blockIdx.x) + threadIdx.x;
-        if (e0 < P.E)
-            for (int p = 0; p < P.P; ++p)
-#pragma unroll
-                for (int q = 0; q < 6; ++q) prefetch_l1(D.theta + ((size_t)p * 6 + q) * P.E + e0);
-#if TVEGPU_GEO
-        if (e0 < P.E) prefetch_geo(D, e0, P.E, NN == 8 ? kGeoRows : 10);
-#endif
-    }
-    const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, P.stage_stride, st, n);
-    if (D.clock->halted || e < 0) return;
+__device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, const NodeStage& st, const int e,
+                                        const int (&n)[NN]) {
     const int E = P.E;
     double Hd[9], A[9], V, Ts;
     {
@@ -938,6 +930,28 @@ __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
 #pragma unroll
         for (int q = 0; q < 9; ++q) D.diag_S[(size_t)e * 9 + q] = Sm[q];
     }
+}
+
+template <int NN, int EXP>
+__global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
+    k_mech_element(const DevParams P, const DevPtrs D, int cur, int c0, int c1) {
+    extern __shared__ double2 smem_planes[];
+    const int ms = P.max_chunk_nodes;
+    const NodeStage st{smem_planes, smem_planes + ms, smem_planes + 2 * ms, smem_planes + 3 * ms};
+    int n[NN];
+    {  // the Prony history is read late in the kernel: start pulling it into L1 now
+        const int e0 = __ldg(D.chunk_start + c0 + blockIdx.x) + threadIdx.x;
+        if (e0 < P.E)
+            for (int p = 0; p < P.P; ++p)
+#pragma unroll
+                for (int q = 0; q < 6; ++q) prefetch_l1(D.theta + ((size_t)p * 6 + q) * P.E + e0);
+#if TVEGPU_GEO
+        if (e0 < P.E) prefetch_geo(D, e0, P.E, NN == 8 ? kGeoRows : 10);
+#endif
+    }
+    const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, P.stage_stride, st, n);
+    if (D.clock->halted || e < 0) return;
+    k3_body<NN, EXP>(P, D, st, e, n);
     pdl_trigger();
 }
 
