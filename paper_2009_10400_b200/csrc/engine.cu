@@ -301,7 +301,7 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr, cudaEvent_t 
         }
         mark();
         if (wait_src) CU(cudaStreamWaitEvent(h->s, wait_src, 0));
-        launch_step_kernel(h, k_thermal_node, blocks(N, 256), 256, 0, h->prm, h->ptr, h->cur,
+        launch_step_kernel(h, k_thermal_node, blocks(N, kNodeThreads), kNodeThreads, 0, h->prm, h->ptr, h->cur,
                            (int)(h->mode == TVEGPU_THERMAL_ONLY), t_out);
         mark();
     } else if (wait_src) {
@@ -318,7 +318,7 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr, cudaEvent_t 
             h->nn == 4 ? launch_mech_element<4>(h, 0, nc) : launch_mech_element<8>(h, 0, nc);
         }
         mark();
-        launch_step_kernel(h, k_mech_node, blocks(N, 256), 256, 0, h->prm, h->ptr, h->cur, 1, u_out);
+        launch_step_kernel(h, k_mech_node, blocks(N, kNodeThreads), kNodeThreads, 0, h->prm, h->ptr, h->cur, 1, u_out);
         mark();
         h->cur ^= 1;
     }
@@ -1765,7 +1765,7 @@ void group_step_once(tvegpu_group* G) {
         }
         loopback_copy(G, false);
         for (tvegpu_engine* h : G->parts)
-            k_thermal_node<<<blocks(h->plan.N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur,
+            k_thermal_node<<<blocks(h->plan.N, kNodeThreads), kNodeThreads, 0, h->s>>>(h->prm, h->ptr, h->cur,
                                                                     h->mode == TVEGPU_THERMAL_ONLY, nullptr);
     }
     if (h0->mode != TVEGPU_THERMAL_ONLY) {
@@ -1776,7 +1776,7 @@ void group_step_once(tvegpu_group* G) {
         }
         loopback_copy(G, true);
         for (tvegpu_engine* h : G->parts) {
-            k_mech_node<<<blocks(h->plan.N, 256), 256, 0, h->s>>>(h->prm, h->ptr, h->cur, 1, nullptr);
+            k_mech_node<<<blocks(h->plan.N, kNodeThreads), kNodeThreads, 0, h->s>>>(h->prm, h->ptr, h->cur, 1, nullptr);
             h->cur ^= 1;
         }
     }

@@ -611,7 +611,17 @@ __device__ __forceinline__ void gather3_ell(const double* __restrict__ slots, co
 
 // ------------------------------------------------------------------ K2: thermal node
 // t_out (tvegpu_step_io only): also write T^{n+1} in original numbering for the host read-back.
-__global__ void __launch_bounds__(256) k_thermal_node(const DevParams P, const DevPtrs D, int cur, int closes,
+#ifndef TVEGPU_NODE_THREADS
+#define TVEGPU_NODE_THREADS 256
+#endif
+constexpr int kNodeThreads = TVEGPU_NODE_THREADS;
+// (an explicit min-blocks of 1 lets ptxas give K4 114 registers: 96 vs 78 us)
+#ifdef TVEGPU_NODE_MINBLOCKS
+#define NODE_BOUNDS __launch_bounds__(kNodeThreads, TVEGPU_NODE_MINBLOCKS)
+#else
+#define NODE_BOUNDS __launch_bounds__(kNodeThreads)
+#endif
+__global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, int cur, int closes,
                                                       double* __restrict__ t_out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     int4 ia = make_int4(0, 0, 0, 0), ib = ia;
@@ -957,7 +967,7 @@ __global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
 
 // ------------------------------------------------------------------ K4: mechanical node
 // u_out (tvegpu_step_io only): also write u^{n+1} in original numbering for the host read-back.
-__global__ void __launch_bounds__(256) k_mech_node(const DevParams P, const DevPtrs D, int cur, int closes,
+__global__ void NODE_BOUNDS k_mech_node(const DevParams P, const DevPtrs D, int cur, int closes,
                                                    double* __restrict__ u_out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     int4 ia = make_int4(0, 0, 0, 0), ib = ia;
