@@ -455,8 +455,10 @@ __device__ __forceinline__ int stage_chunk(const DevPtrs& D, const double4* __re
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 // ------------------------------------------------------------------ K1: thermal element
-#ifndef TVEGPU_K1_MINBLOCKS
-#define TVEGPU_K1_MINBLOCKS 1
+#ifdef TVEGPU_K1_MINBLOCKS
+#define K1_BOUNDS __launch_bounds__(kChunkThreads, TVEGPU_K1_MINBLOCKS)
+#else
+#define K1_BOUNDS __launch_bounds__(kChunkThreads)
 #endif
 // K1 element body: element e of the staged chunk S (n = its node slots)
 template <int NN>
@@ -517,8 +519,7 @@ __device__ __forceinline__ void k1_body(const DevParams& P, const DevPtrs& D, co
 }
 
 template <int NN>
-__global__ void __launch_bounds__(kChunkThreads, TVEGPU_K1_MINBLOCKS) k_thermal_element(const DevParams P, const DevPtrs D, int cur,
-                                                                   int c0, int c1) {
+__global__ void K1_BOUNDS k_thermal_element(const DevParams P, const DevPtrs D, int cur, int c0, int c1) {
     extern __shared__ double2 smem_planes[];
     const int ms = P.max_chunk_nodes;
     const NodeStage S{smem_planes, smem_planes + ms, smem_planes + 2 * ms, smem_planes + 3 * ms};
