@@ -61,14 +61,18 @@ Line clean(Line l) {
 // Tokenizer over one line: numbers are parsed with strtod / strtol on a NUL-terminated copy.
 struct Tok {
     char buf[512];
+    std::string big;  // lines longer than buf (long set lines)
     char* p;
-    bool ok;
     explicit Tok(Line l) {
-        const size_t n = std::min<size_t>(l.e - l.b, sizeof buf - 1);
-        std::memcpy(buf, l.b, n);
-        buf[n] = 0;
-        p = buf;
-        ok = (size_t)(l.e - l.b) < sizeof buf;
+        const size_t n = (size_t)(l.e - l.b);
+        if (n < sizeof buf) {
+            std::memcpy(buf, l.b, n);
+            buf[n] = 0;
+            p = buf;
+        } else {
+            big.assign(l.b, n);
+            p = &big[0];
+        }
     }
     bool more() {
         while (*p && std::isspace((unsigned char)*p)) ++p;
