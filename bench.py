@@ -290,7 +290,7 @@ def run_ours(args):
     uh = torch.empty(3 * p.num_nodes, dtype=torch.float64, pin_memory=True).numpy()
     # untimed: first-call allocations (device I/O buffers); the first few dozen DMA
     # reads of a freshly pinned buffer run ~2x slower (measured, scripts/e2e_breakdown.py)
-    for k in range(50):
+    for k in range(200):  # ~0.2 s; a fresh box's first pinned transfers run slower for longer
         eng.step_io(power, 1, Th, uh)
     barrier()
     t0 = time.perf_counter()
@@ -360,7 +360,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--graph-steps", type=int, default=64)
     ap.add_argument("--soak", type=float, default=0.5)
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=90.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
