@@ -282,3 +282,21 @@ def test_step_io_matches_separate_calls(kind, mode, n):
     sa, sb = a.state(), b.state()
     for k in ("T", "u", "u_prev", "viscous"):
         np.testing.assert_array_equal(sa[k], sb[k], err_msg=k)
+
+
+@pytest.mark.parametrize("kind", [T4, H8])
+def test_single_element_mesh(kind):
+    """Edge case: one element (one partially filled chunk, every node on the boundary)."""
+    from paper_2009_10400_b200 import meshgen
+    nodes, el = meshgen.structured_h8(1, 0.01) if kind == H8 else meshgen.kuhn_t4(1, 0.01)
+    if kind == T4:
+        el = el[:1]
+        nodes = nodes[np.unique(el)]
+        el = np.searchsorted(np.unique(meshgen.kuhn_t4(1, 0.01)[1][:1]), el).astype(np.int32)
+    p = configs.small_problem(kind=kind, n=1, steps=40)
+    p.nodes, p.elements = nodes, el
+    p.fiber_dirs = None
+    p.fixed_nodes = np.array([0], np.int32)
+    p.prescribed = [tg.Prescribed(np.array([len(nodes) - 1]), 2, 1e-4, 0.002)]
+    p.sources = [tg.SourceRegion(np.array([0], np.int32), 5e6)]
+    compare(p, 40)
