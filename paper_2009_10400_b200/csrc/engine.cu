@@ -182,6 +182,7 @@ void refresh_sources_if_needed(tvegpu_engine* h, double t) {
         for (size_t e = 0; e < g.vol.size(); ++e)
             for (int a = 0; a < h->nn; ++a) q[g.nodes[e * h->nn + a]] += g.q_r * g.vol[e] / h->nn;
     }
+#pragma omp parallel for schedule(static)
     for (int li = 0; li < h->plan.N; ++li) h->qr_host[li] = q[h->plan.node_orig[li]];
     CU(cudaMemcpyAsync(const_cast<double*>(h->ptr.qr), h->qr_host, (size_t)h->plan.N * 8,
                        cudaMemcpyHostToDevice, h->s));
@@ -853,7 +854,9 @@ void read_fields(tvegpu_engine* h, double* T, double* u, double* up) {
     const double4* rp = h->cur ? h->ptr.rec0 : h->ptr.rec1;
     CU(cudaMemcpyAsync(h->stage, rc, N * sizeof(double4), cudaMemcpyDeviceToHost, h->s));
     CU(cudaStreamSynchronize(h->s));
+    // partitions: this rank's nodes scattered into the caller's arrays (host threads)
     const int32_t* no = h->plan.node_orig.data();
+#pragma omp parallel for schedule(static)
     for (int i = 0; i < N; ++i) {
         const double4 r = h->stage[i];
         const size_t o = (size_t)no[i];
@@ -867,6 +870,7 @@ void read_fields(tvegpu_engine* h, double* T, double* u, double* up) {
     if (up) {
         CU(cudaMemcpyAsync(h->stage, rp, N * sizeof(double4), cudaMemcpyDeviceToHost, h->s));
         CU(cudaStreamSynchronize(h->s));
+#pragma omp parallel for schedule(static)
         for (int i = 0; i < N; ++i) {
             const size_t o = 3 * (size_t)no[i];
             up[o] = h->stage[i].x;
@@ -1286,6 +1290,7 @@ tvegpu_status tvegpu_set_nodal_sources(tvegpu_engine* h, const double* power) {
             CU(cudaStreamSynchronize(h->s));  // the caller may reuse `power` on return
             return TVEGPU_OK;
         }
+#pragma omp parallel for schedule(static)
         for (int li = 0; li < h->plan.N; ++li) h->qr_host[li] = power[h->plan.node_orig[li]];
         CU(cudaMemcpyAsync(const_cast<double*>(h->ptr.qr), h->qr_host, (size_t)h->plan.N * 8,
                            cudaMemcpyHostToDevice, h->s));
