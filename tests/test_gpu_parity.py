@@ -300,3 +300,23 @@ def test_single_element_mesh(kind):
     p.prescribed = [tg.Prescribed(np.array([len(nodes) - 1]), 2, 1e-4, 0.002)]
     p.sources = [tg.SourceRegion(np.array([0], np.int32), 5e6)]
     compare(p, 40)
+
+
+@pytest.mark.slow
+def test_table1_length_run_is_stable_and_deterministic():
+    """the Table-1 demo runs 62,500 steps (5 s at dt = 8e-5 s).  The liver-
+    shaped T4 mesh for that many steps through the graph path: finite, physically bounded,
+    the RunSummary equal to the host fields, and bit-identical on a second engine."""
+    p = configs.cfg3(steps=62_500)
+    p.dt = 8e-5
+    a = tg.Engine(p)
+    a.step(62_500)
+    s, st = a.summary(), a.state()
+    assert s["steps"] == 62_500 and abs(s["time"] - 5.0) < 1e-9
+    assert np.isfinite(st["T"]).all() and np.isfinite(st["u"]).all()
+    assert 37.0 < s["max_temperature"] < 100.0
+    assert s["max_temperature"] == st["T"].max()
+    b = tg.Engine(p)
+    b.step(62_500)
+    np.testing.assert_array_equal(b.state()["T"], st["T"])
+    np.testing.assert_array_equal(b.state()["u"], st["u"])
