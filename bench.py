@@ -308,6 +308,26 @@ def run_ours(args):
            "calls": "tvegpu_step_io(power, 1, T, u): source upload + 1 step + T/u read-back (C ABI, pinned host "
                     "buffers, copies overlapped with the step on a side stream)"}
 
+    # informational: the closed control loop a thermal-ablation controller runs — upload the
+    # source powers, step, read back the RunSummary (T_max, displacement extrema; 56 B)
+    for k in range(20):
+        eng.step_io(power, 1)
+        eng.summary()
+    barrier()
+    t0 = time.perf_counter()
+    for k in range(e2e_steps):
+        eng.step_io(power, 1)
+        eng.summary()
+    torch.cuda.synchronize()
+    ctl_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([ctl_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ctl_s = float(t.item())
+    e2e_control = {"value": E_total * e2e_steps / ctl_s, "unit": METRIC, "ms_per_step": 1e3 * ctl_s / e2e_steps,
+                   "h2d_bytes_per_step": 8 * p.num_nodes, "d2h_bytes_per_step": 56 + 40, "steps": e2e_steps,
+                   "calls": "tvegpu_step_io(power, 1, NULL, NULL) + tvegpu_get_summary (device reductions)"}
+
     line = {"metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -317,7 +337,7 @@ def run_ours(args):
                        "graph_steps": args.graph_steps},
             "achieved_hbm_gbs_step": step_gbs, "canonical_bytes_per_element_step": step_bytes / p.num_elements,
             "step_roofline_frac": step_gbs / peak,
-            "kernel_ms": prof, "roofline": roofline, "e2e": e2e,
+            "kernel_ms": prof, "roofline": roofline, "e2e": e2e, "e2e_control": e2e_control,
             "gpu_launches": eng.kernels_per_step() * args.steps, "clocks": clocks}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
