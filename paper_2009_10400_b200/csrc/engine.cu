@@ -137,7 +137,7 @@ struct tvegpu_engine {
     double* send_m = nullptr;
     double* recv_th = nullptr;
     double* recv_m = nullptr;
-    const int32_t* d_send_pos = nullptr;
+    const int32_t* d_send_slot = nullptr;  // element-major slot ids of the send lists
     // graphs keyed by (parity, nsteps)
     std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
     int steps_per_graph = 64;
@@ -205,7 +205,7 @@ void exchange(tvegpu_engine* h, double* slots, double* sendbuf, double* /*recvbu
     const RankPlan& pl = h->plan;
     const int ns = pl.send_off.back();
     double* recvbuf = slots + (size_t)pl.E * pl.nn * width;
-    if (ns > 0) k_pack<<<blocks(ns, 256), 256, 0, h->s>>>(slots, h->d_send_pos, ns, width, sendbuf);
+    if (ns > 0) k_pack<<<blocks(ns, 256), 256, 0, h->s>>>(slots, h->d_send_slot, ns, width, sendbuf);
     CU(cudaEventRecord(h->ev_pack, h->s));
     CU(cudaStreamWaitEvent(h->sc, h->ev_pack, 0));
     auto& api = nccl();
@@ -766,7 +766,7 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
         const size_t ns = pl.send_off.back();
         const size_t nr = pl.recv_off.back();
         (void)nr;
-        h->d_send_pos = dupload(own, pl.send_slot, s);  // element-major slot ids
+        h->d_send_slot = dupload(own, pl.send_slot, s);
         h->send_th = dalloc<double>(own, ns);
         h->send_m = dalloc<double>(own, kMW * ns);
         CU(cudaStreamSynchronize(s));
@@ -1755,7 +1755,7 @@ void loopback_copy(tvegpu_group* G, bool mech) {
 void pack(tvegpu_engine* h, bool mech) {
     const int ns = h->plan.send_off.back();
     if (ns > 0)
-        k_pack<<<blocks(ns, 256), 256, 0, h->s>>>(mech ? h->ptr.slot_m : h->ptr.slot_th, h->d_send_pos, ns, mech ? kMW : 1,
+        k_pack<<<blocks(ns, 256), 256, 0, h->s>>>(mech ? h->ptr.slot_m : h->ptr.slot_th, h->d_send_slot, ns, mech ? kMW : 1,
                                                   mech ? h->send_m : h->send_th);
 }
 

@@ -458,20 +458,16 @@ RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nrank
             }
         }
     }
-    // node-major positions (inverse of the gather list)
-    r.pos.assign((size_t)r.E * nn, -1);
-    r.recv_pos.assign(r.recv_off.empty() ? 0 : r.recv_off.back(), -1);
-    for (int k = 0; k < (int)r.csr_slot.size(); ++k) {
-        const int32_t s = r.csr_slot[k];
-        if (s < base) r.pos[s] = k;
-        else r.recv_pos[s - base] = k;
+    // every element contribution and every received one is gathered exactly once
+    {
+        std::vector<char> placed(base + (r.recv_off.empty() ? 0 : r.recv_off.back()), 0);
+        for (int32_t sl : r.csr_slot) {
+            if (placed[sl]) throw Error(TVEGPU_E_ARG, "internal: contribution gathered twice");
+            placed[sl] = 1;
+        }
+        for (char v : placed)
+            if (!v) throw Error(TVEGPU_E_ARG, "internal: unplaced contribution");
     }
-    for (int32_t v : r.pos)
-        if (v < 0) throw Error(TVEGPU_E_ARG, "internal: unplaced element contribution");
-    for (int32_t v : r.recv_pos)
-        if (v < 0) throw Error(TVEGPU_E_ARG, "internal: unplaced halo contribution");
-    r.send_pos.resize(r.send_slot.size());
-    for (size_t k = 0; k < r.send_slot.size(); ++k) r.send_pos[k] = r.pos[r.send_slot[k]];
     build_chunks(r);
     return r;
 }

@@ -77,13 +77,6 @@ struct RankPlan {
     std::vector<uint16_t> lconn;          // E * nn, element-major: slot of node (e, a) in its chunk
     int nchunks_boundary = 0;             // chunks [0, nchunks_boundary) cover [0, Eb)
     int max_chunk_nodes = 0;              // max shared-memory slots (incl. colour padding) of a chunk
-    // Node-major slot layout: contribution (e, a) lives at position pos[e*nn + a]
-    // of node conn[e][a]'s contiguous CSR range, so node kernels read
-    // [csr_off[i], csr_off[i+1]) contiguously.  Received halo contribution r is
-    // scattered to recv_pos[r]; contribution k of the send list is read at send_pos[k].
-    std::vector<int32_t> pos;        // E * nn
-    std::vector<int32_t> recv_pos;   // recv_off.back()
-    std::vector<int32_t> send_pos;   // send_off.back()
 };
 
 #ifndef TVEGPU_CHUNK
