@@ -302,8 +302,8 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr, cudaEvent_t 
         }
         mark();
         if (wait_src) CU(cudaStreamWaitEvent(h->s, wait_src, 0));
-        launch_step_kernel(h, k_thermal_node, blocks(N, kNodeThreads), kNodeThreads, 0, h->prm, h->ptr, h->cur,
-                           (int)(h->mode == TVEGPU_THERMAL_ONLY), t_out);
+        launch_step_kernel(h, h->prm.ell > 1 ? k_thermal_node<true> : k_thermal_node<false>, blocks(N, kNodeThreads),
+                           kNodeThreads, 0, h->prm, h->ptr, h->cur, (int)(h->mode == TVEGPU_THERMAL_ONLY), t_out);
         mark();
     } else if (wait_src) {
         CU(cudaStreamWaitEvent(h->s, wait_src, 0));
@@ -708,12 +708,15 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     {
         int maxc = 0;
         for (int i = 0; i < pl.N; ++i) maxc = std::max(maxc, pl.csr_off[i + 1] - pl.csr_off[i]);
-        m.ell = (maxc <= 8 && !std::getenv("TVEGPU_NO_ELL")) ? 1 : 0;
+        // ELL rows of 8 G ids (G = ceil(max contributions / 8), up to 64 contributions)
+        const int G = (std::max(1, maxc) + 7) / 8;
+        m.ell = (G <= 8 && !std::getenv("TVEGPU_NO_ELL")) ? G : 0;
         if (m.ell) {
-            std::vector<int32_t> ell((size_t)8 * pl.N, (int32_t)nslots);
+            const size_t W = (size_t)8 * G;
+            std::vector<int32_t> ell(W * pl.N, (int32_t)nslots);
             for (int i = 0; i < pl.N; ++i)
                 for (int k = pl.csr_off[i]; k < pl.csr_off[i + 1]; ++k)
-                    ell[(size_t)8 * i + (k - pl.csr_off[i])] = pl.csr_slot[k];
+                    ell[W * i + (k - pl.csr_off[i])] = pl.csr_slot[k];
             h->ptr.ell = reinterpret_cast<const int4*>(dupload(own, ell, s));
         }
     }
@@ -1770,7 +1773,7 @@ void group_step_once(tvegpu_group* G) {
         }
         loopback_copy(G, false);
         for (tvegpu_engine* h : G->parts)
-            k_thermal_node<<<blocks(h->plan.N, kNodeThreads), kNodeThreads, 0, h->s>>>(h->prm, h->ptr, h->cur,
+            (h->prm.ell > 1 ? k_thermal_node<true> : k_thermal_node<false>)<<<blocks(h->plan.N, kNodeThreads), kNodeThreads, 0, h->s>>>(h->prm, h->ptr, h->cur,
                                                                     h->mode == TVEGPU_THERMAL_ONLY, nullptr);
     }
     if (h0->mode != TVEGPU_THERMAL_ONLY) {

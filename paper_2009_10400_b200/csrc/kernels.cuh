@@ -54,7 +54,7 @@ struct DevParams {
     int nn, E, N, P, mode, td, exp_kind, fiber_mode, axes_per_elem, has_R, diag, nslots;
     int max_chunk_nodes;  // shared-memory stride of the staged node records
     int stage_stride;     // entries per chunk in stage_ent (max unique nodes of a chunk)
-    int ell;              // 1: every node has <= 8 contributions, gathers use the ELL-8 index
+    int ell;              // G > 0: ELL gathers with rows of 8 G slot ids (every node has <= 8 G contributions)
     double dt, mu, kappa, eta_a, kh, rho, wbcb, Ta, Qm, gamma;
     double inv_2dt, inv_dt2;  // 1/(2 dt), 1/dt^2 (Eq. 22 coefficients)
     double fiber[3];
@@ -94,7 +94,7 @@ struct DevPtrs {
     const double* R;           // [N][3] external + body force, or null
     const int32_t* csr_off;    // [N+1]
     const int32_t* csr_slot;   // gather list: element-major slot ids (e*nn + a, or receive area)
-    const int4* ell;           // [N][8] the same lists padded with a zero sentinel slot (ell = 1)
+    const int4* ell;           // [N][8 G] the same lists padded with a zero sentinel slot (ell = G > 0)
     const int32_t* node_orig;  // [N]
     double* slot_th;           // [nslots]
     double* slot_m;            // [nslots][kMW] (fx, fy, fz, pad)
@@ -587,13 +587,30 @@ __device__ __forceinline__ void gather3(const double* __restrict__ slots, const 
 // offset load first), then all 8 contributions in flight at once.  Padding entries
 // name a slot that is always +0.0 and sit after the real ones, so the canonical-
 // order sum is unchanged bit for bit (s + 0.0 == s; s is never -0.0 from a +0.0 start).
-__device__ __forceinline__ double gather1_ell(const double* __restrict__ slots, const int4 a, const int4 b) {
-    const double v0 = __ldg(slots + a.x), v1 = __ldg(slots + a.y), v2 = __ldg(slots + a.z), v3 = __ldg(slots + a.w);
-    const double v4 = __ldg(slots + b.x), v5 = __ldg(slots + b.y), v6 = __ldg(slots + b.z), v7 = __ldg(slots + b.w);
+// Rows wider than 8 (T4 meshes: ~24 contributions per node) go in groups of 8: the
+// next group's ids load while the current group's contributions are in flight.
+template <bool WIDE>
+__device__ __forceinline__ double gather1_ell(const double* __restrict__ slots, const int4* __restrict__ row, int G,
+                                             int4 a, int4 b) {
     double s = 0.0;
-    s += v0, s += v1, s += v2, s += v3, s += v4, s += v5, s += v6, s += v7;
+    if (!WIDE) {  // one group: straight line (H8 meshes)
+        const double v0 = __ldg(slots + a.x), v1 = __ldg(slots + a.y), v2 = __ldg(slots + a.z), v3 = __ldg(slots + a.w);
+        const double v4 = __ldg(slots + b.x), v5 = __ldg(slots + b.y), v6 = __ldg(slots + b.z), v7 = __ldg(slots + b.w);
+        s += v0, s += v1, s += v2, s += v3, s += v4, s += v5, s += v6, s += v7;
+        return s;
+    }
+    for (int g = 0; g < G; ++g) {
+        int4 na = a, nb = b;
+        if (g + 1 < G) na = __ldg(row + 2 * (g + 1)), nb = __ldg(row + 2 * (g + 1) + 1);
+        const double v0 = __ldg(slots + a.x), v1 = __ldg(slots + a.y), v2 = __ldg(slots + a.z), v3 = __ldg(slots + a.w);
+        const double v4 = __ldg(slots + b.x), v5 = __ldg(slots + b.y), v6 = __ldg(slots + b.z), v7 = __ldg(slots + b.w);
+        s += v0, s += v1, s += v2, s += v3, s += v4, s += v5, s += v6, s += v7;
+        a = na, b = nb;
+    }
     return s;
 }
+// (the mechanical gather uses the ELL row only for single-group rows: with 3 groups of
+// eight 32-byte loads the grouped loop measured slower than the CSR loop, T4 K4 +35 %)
 __device__ __forceinline__ void gather3_ell(const double* __restrict__ slots, const int4 a, const int4 b, double& f0,
                                             double& f1, double& f2) {
     const double4* S = reinterpret_cast<const double4*>(slots);
@@ -622,19 +639,21 @@ constexpr int kNodeThreads = TVEGPU_NODE_THREADS;
 #else
 #define NODE_BOUNDS __launch_bounds__(kNodeThreads)
 #endif
+// WIDE: ELL rows of more than one group (T4 meshes)
+template <bool WIDE>
 __global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, int cur, int closes,
-                                                      double* __restrict__ t_out) {
+                                           double* __restrict__ t_out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     int4 ia = make_int4(0, 0, 0, 0), ib = ia;
     double V = 0.0;
     if (i < P.N) {  // predecessor-independent loads first (index row, node volume)
-        if (P.ell) ia = __ldg(D.ell + 2 * (size_t)i), ib = __ldg(D.ell + 2 * (size_t)i + 1);
+        if (P.ell) ia = __ldg(D.ell + 2 * (size_t)P.ell * i), ib = __ldg(D.ell + 2 * (size_t)P.ell * i + 1);
         V = __ldg(D.vnode + i);
     }
     pdl_wait();
     if (i < P.N && !D.clock->halted) {
         double4* R = cur ? D.rec1 : D.rec0;
-        const double s = P.ell ? gather1_ell(D.slot_th, ia, ib)
+        const double s = P.ell ? gather1_ell<WIDE>(D.slot_th, D.ell + 2 * (size_t)P.ell * i, P.ell, ia, ib)
                                : gather1(D.slot_th, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1));
         const double T = R[i].w;
         const double c = P.td ? interp1(P.cT, P.cV, P.c_len, T) : P.c_fixed;
@@ -972,13 +991,13 @@ __global__ void NODE_BOUNDS k_mech_node(const DevParams P, const DevPtrs D, int 
                                                    double* __restrict__ u_out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     int4 ia = make_int4(0, 0, 0, 0), ib = ia;
-    if (i < P.N && P.ell) ia = __ldg(D.ell + 2 * (size_t)i), ib = __ldg(D.ell + 2 * (size_t)i + 1);
+    if (i < P.N && P.ell == 1) ia = __ldg(D.ell + 2 * (size_t)i), ib = __ldg(D.ell + 2 * (size_t)i + 1);
     pdl_wait();
     if (i < P.N && !D.clock->halted) {
         const double4* Rc = cur ? D.rec1 : D.rec0;
         double4* Rn = cur ? D.rec0 : D.rec1;  // holds u^{n-1}; receives u^{n+1}
         double f0, f1, f2;
-        if (P.ell) gather3_ell(D.slot_m, ia, ib, f0, f1, f2);
+        if (P.ell == 1) gather3_ell(D.slot_m, ia, ib, f0, f1, f2);
         else gather3(D.slot_m, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1), f0, f1, f2);
         const double4 u = ldg4(Rc + i);  // read-only in this kernel
         const double4 up = ld4(Rn + i);  // this thread overwrites it below
