@@ -98,6 +98,18 @@ int main(int argc, char** argv) {
         twin.steps(10);
         const bool same = eng.state().temperatures == twin.state().temperatures && eng.state().disp == twin.state().disp;
         std::printf("checkpoint resume bit-identical: %s\n", same ? "yes" : "NO");
+        // engine.hpp:92 run(): a fresh engine over 50 steps, a snapshot sink every 10 steps
+        {
+            SimulationConfig c2 = cfg;
+            c2.duration = 50 * cfg.dt;
+            c2.output.snapshot_interval = 10 * cfg.dt;
+            c2.output.ablation_threshold = 37.5;
+            Engine e2(mesh, mat, mb, ThermalBCs{}, src, c2);
+            int nsnap = 0;
+            const RunSummary rs = e2.run([&](const Snapshot& s) { nsnap += s.step > 0 ? 1 : 0; });
+            std::printf("run(): %ld steps, %d snapshots, T_max %.6f, ablation(37.5C) %.6g m^3\n", rs.steps, nsnap,
+                        rs.max_temperature, rs.ablation_volume);
+        }
         // reference-style state() write: cool the whole block back to 37 degC, keep stepping
         SimulationState& w = eng.mutable_state();
         std::fill(w.temperatures.begin(), w.temperatures.end(), 37.0);

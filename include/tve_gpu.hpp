@@ -14,7 +14,10 @@
 #include <cstdint>
 #include <istream>
 #include <iterator>
+#include <algorithm>
+#include <chrono>
 #include <fstream>
+#include <functional>
 #include <limits>
 #include <map>
 #include <ostream>
@@ -112,6 +115,13 @@ struct MechBCs {
 
 // ---------------------------------------------------------------- engine.hpp:16-45
 enum class CouplingMode { Coupled, ThermalOnly, MechanicalOnly };
+struct OutputSpec {                  // engine.hpp:18-24
+    double snapshot_interval = 0;    // [s]; <= 0 disables periodic snapshots
+    std::vector<int> probe_nodes;    // 0-based (carried for callers; snapshots hold every node)
+    bool write_det_f = false;        // needs DeviceOptions::diagnostics
+    bool write_stress = false;       // needs DeviceOptions::diagnostics
+    double ablation_threshold = 60.0;  // [degC]; <= 0 disables the report
+};
 struct SimulationConfig {
     double dt = 0, duration = 0;
     CouplingMode mode = CouplingMode::Coupled;
@@ -119,7 +129,23 @@ struct SimulationConfig {
     double damping_gamma = 0, hourglass_stiffness = 0.1;
     bool allow_unstable_dt = false;
     int workers = 0;
+    OutputSpec output;
 };
+// engine.hpp:47-55: field snapshot handed to sinks (copies, safe to retain)
+struct Snapshot {
+    double time = 0;
+    long step = 0;
+    std::vector<double> temperatures, displacements, det_f, max_principal_stress;
+};
+// engine.hpp:57-66
+struct RunSummary {
+    long steps = 0;
+    double final_time = 0, max_temperature = 0;
+    Vec3 min_displacement{0, 0, 0}, max_displacement{0, 0, 0};
+    double ablation_volume = 0;  // [m^3] at the final step, deformed configuration (0 if disabled)
+    double median_step_seconds = 0, iqr_step_seconds = 0;
+};
+using SnapshotSink = std::function<void(const Snapshot&)>;
 struct SimulationState {
     std::vector<double> temperatures;  // ThermalState::temperatures
     double time = 0;                   // ThermalState::time
@@ -139,7 +165,8 @@ class Engine {
 public:
     Engine(const Mesh& mesh, const MaterialModel& material, const MechBCs& mech_bcs, const ThermalBCs& thermal_bcs,
            const HeatSourceSet& sources, const SimulationConfig& config, const DeviceOptions& opt = {})
-        : N_(mesh.node_count()), E_(mesh.element_count()), P_((int)material.prony.terms.size()) {
+        : N_(mesh.node_count()), E_(mesh.element_count()), P_((int)material.prony.terms.size()),
+          dt_(config.dt), dur_(config.duration), out_(config.output) {
         build(mesh, material, mech_bcs, thermal_bcs, sources, config);
         tvegpu_options o;
         tvegpu_default_options(&o);
@@ -230,6 +257,53 @@ public:
         check(tvegpu_load_checkpoint(h_, buf.data(), buf.size()));
         dirty_ = false;
         mirror_valid_ = false;
+    }
+
+    // engine.hpp:99: Snapshot with the optional element fields of OutputSpec
+    Snapshot make_snapshot() {
+        Snapshot s;
+        s.time = time();
+        s.step = step_count();
+        make_snapshot(s.temperatures, s.displacements);
+        if (out_.write_det_f || out_.write_stress) {
+            std::vector<double> d(E_), m(E_);
+            check(tvegpu_element_fields(h_, out_.write_det_f ? d.data() : nullptr,
+                                        out_.write_stress ? m.data() : nullptr));
+            if (out_.write_det_f) s.det_f = std::move(d);
+            if (out_.write_stress) s.max_principal_stress = std::move(m);
+        }
+        return s;
+    }
+
+    // engine.hpp:92: run duration/dt steps, calling the sink on the output schedule
+    // (every snapshot_interval, and at the end); per-step wall time from the chunks
+    // between snapshots.  Throws InstabilityError like step().
+    RunSummary run(const SnapshotSink& sink = nullptr) {
+        push_if_dirty();
+        const long total = std::max(1L, (long)std::llround(dur_ / dt_));
+        const long every =
+            out_.snapshot_interval > 0 ? std::max(1L, (long)std::llround(out_.snapshot_interval / dt_)) : total;
+        std::vector<double> per;
+        for (long done = 0; done < total;) {
+            const long k = std::min(every, total - done);
+            const auto t0 = std::chrono::steady_clock::now();
+            steps(k);
+            (void)time();
+            per.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / k);
+            done += k;
+            if (sink && (out_.snapshot_interval > 0 || done == total)) sink(make_snapshot());
+        }
+        RunSummary r;
+        const tvegpu_summary sm = summary();
+        r.steps = (long)sm.steps;
+        r.final_time = sm.time;
+        r.max_temperature = sm.max_temperature;
+        for (int c = 0; c < 3; ++c) r.min_displacement[c] = sm.min_disp[c], r.max_displacement[c] = sm.max_disp[c];
+        if (out_.ablation_threshold > 0) r.ablation_volume = ablation_volume(out_.ablation_threshold).first;
+        std::sort(per.begin(), per.end());
+        r.median_step_seconds = per[per.size() / 2];
+        r.iqr_step_seconds = per[(3 * per.size()) / 4] - per[per.size() / 4];
+        return r;
     }
 
     tvegpu_engine* handle() { return h_; }
@@ -375,6 +449,8 @@ private:
     }
 
     int N_, E_, P_;
+    double dt_, dur_;
+    OutputSpec out_;
     tvegpu_engine* h_ = nullptr;
     tvegpu_problem p_{};
     std::vector<double> nodes_, fibers_, axes_, phi_, tau_, cT_, cV_, kT_, kK_, tfixV_, ext_;

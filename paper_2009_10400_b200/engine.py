@@ -391,6 +391,36 @@ class Engine:
             self._raise(rc)
         return u
 
+    # ---- engine.hpp:92 run(sink) -> RunSummary
+    def run(self, sink=None, snapshot_interval=0.0, ablation_threshold=60.0, element_fields=False):
+        """Advance problem.duration / dt steps; call sink(snapshot dict) every snapshot_interval
+        (and at the end); return the RunSummary (engine.hpp:57-66) with per-step wall-time
+        median / IQR measured over the chunks between snapshots."""
+        import time as _time
+        dt = self.problem.dt
+        total = max(1, int(round(self.problem.duration / dt)))
+        every = max(1, int(round(snapshot_interval / dt))) if snapshot_interval > 0 else total
+        per, done = [], 0
+        while done < total:
+            k = min(every, total - done)
+            t0 = _time.perf_counter()
+            self.step(k)
+            per.append((_time.perf_counter() - t0) / k)
+            done += k
+            if sink is not None and (snapshot_interval > 0 or done == total):
+                T, u = self.make_snapshot()
+                snap = dict(time=self.time(), step=self.step_count(), temperatures=T, displacements=u)
+                if element_fields:
+                    snap["det_f"], snap["max_principal_stress"] = self.element_fields()
+                sink(snap)
+        s = self.summary()
+        per = np.sort(np.array(per))
+        return dict(steps=s["steps"], final_time=s["time"], max_temperature=s["max_temperature"],
+                    min_displacement=s["min_disp"], max_displacement=s["max_disp"],
+                    ablation_volume=self.ablation_volume(ablation_threshold)[0] if ablation_threshold > 0 else 0.0,
+                    median_step_seconds=float(per[len(per) // 2]),
+                    iqr_step_seconds=float(per[(3 * len(per)) // 4] - per[len(per) // 4]))
+
     # ---- checkpoint / restart (engine.hpp:110-111)
     def save_checkpoint(self, path=None) -> bytes:
         """Versioned binary state image (original numbering); written to `path` if given."""

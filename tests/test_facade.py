@@ -57,6 +57,7 @@ def test_facade_demo_matches_oracle():
     assert abs(uzmax - s["u"][2::3].max()) <= 1e-10 * abs(s["u"]).max()
     assert "after reset + 1 step" in out
     assert "checkpoint resume bit-identical: yes" in out
+    assert "run(): 50 steps, 5 snapshots" in out
     m = re.search(r"device summary: T_max ([0-9.eE+-]+)\s+u_z max ([0-9.eE+-]+)\s+ablation\(40C\) ([0-9.eE+-]+) m\^3 "
                   r"in (\d+) elements", out)
     assert m, out

@@ -92,3 +92,19 @@ def test_element_fields(kind):
     assert np.abs(smax - ev).max() <= 1e-10 * scale
     with pytest.raises(tg.engine.TveError):
         tg.Engine(p).element_fields()  # needs diagnostics
+
+
+def test_run_with_sink_matches_stepping():  # engine.hpp:92 run(sink) -> RunSummary
+    p = configs.cfg1(steps=120)
+    a = tg.Engine(p)
+    snaps = []
+    r = a.run(sink=snaps.append, snapshot_interval=40 * p.dt, ablation_threshold=37.2)
+    assert r["steps"] == 120 and [s["step"] for s in snaps] == [40, 80, 120]
+    b = tg.Engine(p)
+    b.step(120)
+    st = b.state()
+    np.testing.assert_array_equal(snaps[-1]["temperatures"], st["T"])
+    np.testing.assert_array_equal(snaps[-1]["displacements"], st["u"])
+    assert r["max_temperature"] == st["T"].max()
+    assert r["ablation_volume"] == b.ablation_volume(37.2)[0]
+    assert r["median_step_seconds"] > 0
