@@ -242,6 +242,14 @@ public:
         return {v, (long)n};
     }
 
+    // engine.hpp:108: kinetic plus hyperelastic strain energy of the current state [J]
+    double total_energy() {
+        push_if_dirty();
+        double k = 0, e = 0;
+        check(tvegpu_total_energy(h_, &k, &e));
+        return k + e;
+    }
+
     // engine.hpp:110-111
     void save_checkpoint(std::ostream& out) {
         push_if_dirty();

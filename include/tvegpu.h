@@ -243,6 +243,11 @@ tvegpu_status tvegpu_get_summary(tvegpu_engine* h, tvegpu_summary* out);
 tvegpu_status tvegpu_ablation_volume(tvegpu_engine* h, double threshold, int32_t deformed, double* volume,
                                      int64_t* elements_above);
 
+/* total_energy (engine.hpp:108), split: kinetic sum 1/2 m |(u - u_prev)/dt|^2 and strain
+ * energy sum V det(F_th) Psi(C_el) of the current state (device reductions; either
+ * pointer may be NULL).  Multi-GPU: replicated nodes are counted by every rank that holds them. */
+tvegpu_status tvegpu_total_energy(tvegpu_engine* h, double* kinetic, double* strain);
+
 /* Snapshot element fields (engine.hpp:47-55, OutputSpec write_det_f / write_stress):
  * det F and the largest principal value of S_tilde (PK2) per element, original
  * order, from the last mechanics phase.  Requires options.diagnostics = 1 and a

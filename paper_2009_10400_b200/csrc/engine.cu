@@ -1013,6 +1013,89 @@ __global__ void __launch_bounds__(kRedThreads) k_ablation(const int32_t* __restr
     block_reduce<2>(v, op, part + (size_t)blockIdx.x * 2);
 }
 
+// total_energy (engine.hpp:108): kinetic 1/2 m |(u - u_prev)/dt|^2 per node plus the
+// hyperelastic energy V det(F_th) Psi(C_el) per element (the oracle's definition, with
+// F_th from the current element-mean temperature, i.e. the last mechanics phase's).
+// Psi = mu/2 (J^-2/3 tr C - 3) + kappa/2 (J - 1)^2 [+ eta/2 (J^-2/3 a.Ca - 1)^2].
+template <int NN>
+__global__ void __launch_bounds__(kRedThreads) k_energy(const DevParams P, const DevPtrs D, const int32_t* __restrict__ conn,
+                                                   const double4* __restrict__ rc, const double4* __restrict__ rp,
+                                                   double* part) {
+    double v[2] = {0.0, 0.0};
+    const int op[2] = {0, 0};
+    const int E = P.E, N = P.N;
+    for (int i = blockIdx.x * kRedThreads + threadIdx.x; i < N; i += gridDim.x * kRedThreads) {
+        const double4 a = rc[i], b = rp[i];
+        const double vx = (a.x - b.x) / P.dt, vy = (a.y - b.y) / P.dt, vz = (a.z - b.z) / P.dt;
+        v[0] += 0.5 * D.mass[i] * (vx * vx + vy * vy + vz * vz);
+    }
+    for (int e = blockIdx.x * kRedThreads + threadIdx.x; e < E; e += gridDim.x * kRedThreads) {
+        double H[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, Ts = 0.0;
+        double u[NN][3];
+        for (int q = 0; q < NN; ++q) {
+            const double4 r = rc[conn[(size_t)e * NN + q]];
+            u[q][0] = r.x, u[q][1] = r.y, u[q][2] = r.z;
+            Ts += r.w;
+        }
+        if (NN == 4) {
+            for (int q = 1; q < 4; ++q)
+                for (int i = 0; i < 3; ++i) H[i * 3 + q - 1] = u[q][i] - u[0][i];
+        } else {
+            for (int q = 0; q < 8; ++q)
+                for (int j = 0; j < 3; ++j)
+                    for (int i = 0; i < 3; ++i) H[i * 3 + j] += h8s(q, j) * u[q][i];
+        }
+        double A[9];
+        for (int q = 0; q < 9; ++q) A[q] = D.geo[(size_t)q * E + e];
+        const double V = D.geo[(size_t)9 * E + e];
+        double F[9];
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j)
+                F[i * 3 + j] = (i == j ? 1.0 : 0.0) + H[i * 3 + 0] * A[j * 3 + 0] + H[i * 3 + 1] * A[j * 3 + 1] +
+                               H[i * 3 + 2] * A[j * 3 + 2];
+        double Fth[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+        if (P.exp_kind >= 0) {
+            const double dT = Ts / NN - P.Tref;
+            double m[3], n[3];
+            for (int k = 0; k < 3; ++k) {
+                m[k] = P.axes_per_elem ? D.axes[k * E + e] : P.axis_m[k];
+                n[k] = P.axes_per_elem ? D.axes[(3 + k) * E + e] : P.axis_n[k];
+            }
+            const double ei = P.alpha_i * dT;
+            const double dm = P.exp_kind >= 1 ? P.alpha_m * dT - ei : 0.0;
+            const double dn = P.exp_kind == 2 ? P.alpha_n * dT - ei : 0.0;
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j)
+                    Fth[i * 3 + j] = (i == j ? 1.0 + ei : 0.0) + dm * m[i] * m[j] + dn * n[i] * n[j];
+        }
+        double Ad[9];
+        const double dth = adj3(Fth, Ad);
+        double Fel[9];
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j)
+                Fel[i * 3 + j] = (F[i * 3 + 0] * Ad[0 * 3 + j] + F[i * 3 + 1] * Ad[1 * 3 + j] + F[i * 3 + 2] * Ad[2 * 3 + j]) / dth;
+        double Cm[9];
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j)
+                Cm[i * 3 + j] = Fel[0 * 3 + i] * Fel[0 * 3 + j] + Fel[1 * 3 + i] * Fel[1 * 3 + j] + Fel[2 * 3 + i] * Fel[2 * 3 + j];
+        double Ac[9];
+        const double J = sqrt(adj3(Cm, Ac));
+        const double Jm23 = pow(J, -2.0 / 3.0);
+        double psi = 0.5 * P.mu * (Jm23 * (Cm[0] + Cm[4] + Cm[8]) - 3.0) + 0.5 * P.kappa * (J - 1.0) * (J - 1.0);
+        if (P.eta_a > 0 && P.fiber_mode) {
+            double fa[3];
+            for (int k = 0; k < 3; ++k) fa[k] = P.fiber_mode == 2 ? D.fiber[k * E + e] : P.fiber[k];
+            double aCa = 0;
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) aCa += fa[i] * Cm[i * 3 + j] * fa[j];
+            const double I4 = Jm23 * aCa;
+            psi += 0.5 * P.eta_a * (I4 - 1.0) * (I4 - 1.0);
+        }
+        v[1] += V * dth * psi;
+    }
+    block_reduce<2>(v, op, part + (size_t)blockIdx.x * 2);
+}
+
 // det F and the largest eigenvalue of S_tilde (PK2) per element, original order,
 // from the diagnostics of the last mechanics phase (Snapshot det_f /
 // max_principal_stress, engine.hpp:47-55).
@@ -1508,6 +1591,27 @@ tvegpu_status tvegpu_ablation_volume(tvegpu_engine* h, double threshold, int32_t
         });
         *volume = h->h_part[0];
         if (elements_above) *elements_above = (int64_t)llround(h->h_part[1]);
+        return TVEGPU_OK;
+    });
+}
+
+tvegpu_status tvegpu_total_energy(tvegpu_engine* h, double* kinetic, double* strain) {
+    if (!h || (!kinetic && !strain)) return TVEGPU_E_ARG;
+    return guard(h, [&] {
+        if (!h->d_conn) {
+            h->d_conn = dalloc<int32_t>(h->owned, h->plan.conn.size());
+            CU(cudaMemcpyAsync(h->d_conn, h->plan.conn.data(), h->plan.conn.size() * 4, cudaMemcpyHostToDevice, h->s));
+        }
+        const int nb = red_blocks(std::max(h->plan.E, h->plan.N));
+        const int op[2] = {0, 0};
+        const double4* rc = h->cur ? h->ptr.rec1 : h->ptr.rec0;
+        const double4* rp = h->cur ? h->ptr.rec0 : h->ptr.rec1;
+        reduce_to_host<2>(h, nb, op, [&](double* part) {
+            if (h->nn == 8) k_energy<8><<<nb, kRedThreads, 0, h->s>>>(h->prm, h->ptr, h->d_conn, rc, rp, part);
+            else k_energy<4><<<nb, kRedThreads, 0, h->s>>>(h->prm, h->ptr, h->d_conn, rc, rp, part);
+        });
+        if (kinetic) *kinetic = h->h_part[0];
+        if (strain) *strain = h->h_part[1];
         return TVEGPU_OK;
     });
 }

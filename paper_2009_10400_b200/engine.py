@@ -100,6 +100,7 @@ EXPORTS = {
     "tvegpu_set_nodal_sources": (C.c_int, [C.c_void_p, _dp]),
     "tvegpu_step_io": (C.c_int, [C.c_void_p, _dp, C.c_int64, _dp, _dp]),
     "tvegpu_get_summary": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "tvegpu_total_energy": (C.c_int, [C.c_void_p, _dp, _dp]),
     "tvegpu_load_mesh": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(C.c_void_p), C.c_void_p]),
     "tvegpu_mesh_get_view": (None, [C.c_void_p, C.c_void_p]),
     "tvegpu_mesh_destroy": (None, [C.c_void_p]),
@@ -454,6 +455,14 @@ class Engine:
             self._raise(rc)
         return dict(steps=out.steps, time=out.time, max_temperature=out.max_temperature,
                     min_disp=np.array(out.min_disp[:]), max_disp=np.array(out.max_disp[:]))
+
+    def total_energy(self, split=False):
+        """total_energy (engine.hpp:108): kinetic + strain energy [J] ((kinetic, strain) if split)."""
+        k, e = np.empty(1), np.empty(1)
+        rc = lib().tvegpu_total_energy(self._h, _P(k), _P(e))
+        if rc:
+            self._raise(rc)
+        return (float(k[0]), float(e[0])) if split else float(k[0] + e[0])
 
     def ablation_volume(self, threshold=60.0, deformed=True):
         """(volume [m^3], elements_above) of {T >= threshold} by exact tet clipping."""

@@ -108,3 +108,21 @@ def test_run_with_sink_matches_stepping():  # engine.hpp:92 run(sink) -> RunSumm
     assert r["max_temperature"] == st["T"].max()
     assert r["ablation_volume"] == b.ablation_volume(37.2)[0]
     assert r["median_step_seconds"] > 0
+
+
+@pytest.mark.parametrize("kind", [T4, H8])
+@pytest.mark.parametrize("variant", ["coupled", "orthotropic"])
+def test_total_energy_matches_oracle(kind, variant):  # engine.hpp:108
+    from paper_2009_10400_b200.problem import EXP_ORTHOTROPIC
+    p = configs.small_problem(kind=kind, n=4, steps=30)
+    if variant == "orthotropic":
+        p.expansion = dict(kind=EXP_ORTHOTROPIC, alpha_i=1e-4, alpha_m=3e-4, alpha_n=2e-4, reference_temperature=37.0)
+        p.initial_temperature = 60.0
+    g = tg.Engine(p)
+    o = O.OracleEngine(p)
+    g.step(30)
+    o.step(30)
+    ek, es = g.total_energy(split=True)
+    eo = o.total_energy()
+    assert ek > 0 and es > 0
+    assert abs((ek + es) - eo) <= 1e-8 * eo, (ek + es, eo)
