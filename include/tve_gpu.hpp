@@ -509,4 +509,117 @@ inline Mesh load_mesh_file(const std::string& path) {
     return load_mesh(text);
 }
 
+// ---------------------------------------------------------------- engine.hpp:145-162
+// Structured cube meshes for run_bench: n^3 bricks of side h (H8), or 6 positively
+// oriented tetrahedra per brick around its 0-6 diagonal (T4).
+inline Mesh structured_cube(int n, double h, ElementKind kind) {
+    Mesh m;
+    m.kind = ElementKind::H8;
+    auto id = [&](int i, int j, int k) { return i + (n + 1) * (j + (n + 1) * k); };
+    for (int k = 0; k <= n; ++k)
+        for (int j = 0; j <= n; ++j)
+            for (int i = 0; i <= n; ++i) m.nodes.push_back({i * h, j * h, k * h});
+    for (int k = 0; k < n; ++k)
+        for (int j = 0; j < n; ++j)
+            for (int i = 0; i < n; ++i)
+                m.elements.push_back({id(i, j, k), id(i + 1, j, k), id(i + 1, j + 1, k), id(i, j + 1, k),
+                                      id(i, j, k + 1), id(i + 1, j, k + 1), id(i + 1, j + 1, k + 1), id(i, j + 1, k + 1)});
+    if (kind == ElementKind::H8) return m;
+    static const int t6[6][4] = {{0, 1, 2, 6}, {0, 2, 3, 6}, {0, 3, 7, 6}, {0, 7, 4, 6}, {0, 4, 5, 6}, {0, 5, 1, 6}};
+    Mesh t;
+    t.kind = ElementKind::T4;
+    t.nodes = m.nodes;
+    for (const auto& e : m.elements)
+        for (const auto& q : t6) {
+            std::array<int, 8> v{e[q[0]], e[q[1]], e[q[2]], e[q[3]], 0, 0, 0, 0};
+            const auto &a = t.nodes[v[0]], &b = t.nodes[v[1]], &c = t.nodes[v[2]], &d = t.nodes[v[3]];
+            double x[3], y[3], z[3];
+            for (int r = 0; r < 3; ++r) x[r] = b[r] - a[r], y[r] = c[r] - a[r], z[r] = d[r] - a[r];
+            if (x[0] * (y[1] * z[2] - y[2] * z[1]) - x[1] * (y[0] * z[2] - y[2] * z[0]) + x[2] * (y[0] * z[1] - y[1] * z[0]) < 0)
+                std::swap(v[1], v[2]);
+            t.elements.push_back(v);
+        }
+    return t;
+}
+
+struct BenchResult {
+    int elements = 0, nodes = 0;
+    ElementKind kind = ElementKind::T4;
+    // median / IQR of per-step wall time [s] per coupled mode
+    double ther_mech_ti = 0, ther_mech_ti_iqr = 0;
+    double ther_mech_expan_ti = 0, ther_mech_expan_ti_iqr = 0;
+    double ther_mech_expan_td = 0, ther_mech_expan_td_iqr = 0;
+};
+
+// run_bench: per-step wall time of the three coupled modes (TI, +expansion, +temperature-
+// dependent properties) on structured cubes with Table-5 tissue, bottom face fixed, dt at
+// 0.4 of the dilatational transit of one cell.  Per-step samples are 10-step chunks (one
+// device sync per chunk).  `workers` is accepted for signature parity (host threads only
+// build the plan).
+inline std::vector<BenchResult> run_bench(const std::vector<int>& cells_ladder, ElementKind kind,
+                                          int steps_per_measurement, int workers = 0) {
+    (void)workers;
+    std::vector<BenchResult> out;
+    for (int n : cells_ladder) {
+        const double h = 0.001;
+        const Mesh m = structured_cube(n, h, kind);
+        BenchResult r;
+        r.elements = m.element_count();
+        r.nodes = m.node_count();
+        r.kind = kind;
+        double* med[3] = {&r.ther_mech_ti, &r.ther_mech_expan_ti, &r.ther_mech_expan_td};
+        double* iqr[3] = {&r.ther_mech_ti_iqr, &r.ther_mech_expan_ti_iqr, &r.ther_mech_expan_td_iqr};
+        for (int mode = 0; mode < 3; ++mode) {
+            MaterialModel mat;
+            mat.hyperelastic = {1190.476, 19444.444, 0};
+            mat.prony.terms = {{0.5, 0.58}};
+            mat.thermal.density = 1060;
+            mat.thermal.specific_heat.entries = {{37, 3600}};
+            mat.thermal.conductivity = ConductivityTable::isotropic(37, 0.53);
+            if (mode == 2) {
+                mat.thermal.specific_heat.entries.push_back({90, 4300});
+                mat.thermal.conductivity.entries.push_back({90, {0.75, 0, 0, 0, 0.75, 0, 0, 0, 0.75}});
+            }
+            mat.expansion = ExpansionSpec{ExpansionKind::Isotropic, 1e-4, 0, 0, 37.0};
+            SimulationConfig c;
+            c.dt = 0.4 * 0.9 * h / std::sqrt((19444.444 + 4 * 1190.476 / 3) / 1060);
+            c.expansion_enabled = mode >= 1;
+            c.temperature_dependent = mode == 2;
+            c.damping_gamma = 1;
+            MechBCs mb;
+            for (int i = 0; i < m.node_count(); ++i)
+                if (m.nodes[i][2] < 1e-12) mb.fixed_nodes.push_back(i);
+            Engine e(m, mat, mb, ThermalBCs{}, HeatSourceSet{}, c);
+            e.steps(20);
+            std::vector<double> t;
+            for (int done = 0; done < steps_per_measurement; done += 10) {
+                const int k = std::min(10, steps_per_measurement - done);
+                const auto t0 = std::chrono::steady_clock::now();
+                e.steps(k);
+                t.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / k);
+            }
+            std::sort(t.begin(), t.end());
+            *med[mode] = t[t.size() / 2];
+            *iqr[mode] = t[(3 * t.size()) / 4] - t[t.size() / 4];
+        }
+        out.push_back(r);
+    }
+    return out;
+}
+
+// bench_scaling_slope: least-squares slope of log(median step time) vs log(elements),
+// on the TherMechExpanTD column.
+inline double bench_scaling_slope(const std::vector<BenchResult>& results) {
+    double mx = 0, my = 0;
+    const double n = (double)results.size();
+    for (const auto& r : results) mx += std::log((double)r.elements) / n, my += std::log(r.ther_mech_expan_td) / n;
+    double sxy = 0, sxx = 0;
+    for (const auto& r : results) {
+        const double dx = std::log((double)r.elements) - mx, dy = std::log(r.ther_mech_expan_td) - my;
+        sxy += dx * dy;
+        sxx += dx * dx;
+    }
+    return sxx > 0 ? sxy / sxx : 0.0;
+}
+
 }  // namespace tve::gpu

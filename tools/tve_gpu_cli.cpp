@@ -472,23 +472,6 @@ Mesh box_h8(int nx, int ny, int nz, double h) {
                                       id(i, j, k + 1), id(i + 1, j, k + 1), id(i + 1, j + 1, k + 1), id(i, j + 1, k + 1)});
     return m;
 }
-Mesh kuhn_t4(const Mesh& hex) {  // 6 tets per brick around the 0-6 diagonal, positively oriented
-    static const int t6[6][4] = {{0, 1, 2, 6}, {0, 2, 3, 6}, {0, 3, 7, 6}, {0, 7, 4, 6}, {0, 4, 5, 6}, {0, 5, 1, 6}};
-    Mesh m;
-    m.kind = ElementKind::T4;
-    m.nodes = hex.nodes;
-    for (const auto& e : hex.elements)
-        for (const auto& t : t6) {
-            std::array<int, 8> q{e[t[0]], e[t[1]], e[t[2]], e[t[3]], 0, 0, 0, 0};
-            const auto &a = m.nodes[q[0]], &b = m.nodes[q[1]], &c = m.nodes[q[2]], &d = m.nodes[q[3]];
-            double u[3], v[3], w[3];
-            for (int i = 0; i < 3; ++i) u[i] = b[i] - a[i], v[i] = c[i] - a[i], w[i] = d[i] - a[i];
-            if (u[0] * (v[1] * w[2] - v[2] * w[1]) - u[1] * (v[0] * w[2] - v[2] * w[0]) + u[2] * (v[0] * w[1] - v[1] * w[0]) < 0)
-                std::swap(q[1], q[2]);
-            m.elements.push_back(q);
-        }
-    return m;
-}
 MaterialModel table5(bool td) {
     MaterialModel m;
     m.hyperelastic = {1190.476, 19444.444, 0};
@@ -639,42 +622,12 @@ int cmd_verify(const std::string& only, bool list) {
 int cmd_bench(const std::string& kind, int steps) {  // engine.hpp:145-162 run_bench / bench_scaling_slope
     const bool h8 = kind == "h8";
     const std::vector<int> ladder = h8 ? std::vector<int>{40, 50, 63, 80, 100} : std::vector<int>{20, 25, 32, 40, 50};
+    const auto res = run_bench(ladder, h8 ? ElementKind::H8 : ElementKind::T4, steps);
     std::printf("elements,nodes,TherMechTI_ms,TherMechExpanTI_ms,TherMechExpanTD_ms\n");
-    std::vector<double> lx, ly;
-    for (int n : ladder) {
-        const double L = 0.001 * n, h = L / n;
-        Mesh hex = box_h8(n, n, n, h);
-        Mesh m = h8 ? hex : kuhn_t4(hex);
-        double ms[3];
-        for (int mode = 0; mode < 3; ++mode) {
-            MaterialModel mat = table5(mode == 2);
-            mat.prony.terms = {{0.5, 0.58}};
-            mat.expansion = ExpansionSpec{ExpansionKind::Isotropic, 1e-4, 0, 0, 37.0};
-            SimulationConfig c;
-            c.dt = 0.4 * 0.9 * h / std::sqrt((19444.444 + 4 * 1190.476 / 3) / 1060);
-            c.expansion_enabled = mode >= 1;
-            c.temperature_dependent = mode == 2;
-            c.damping_gamma = 1;
-            MechBCs mb;
-            for (int i = 0; i < m.node_count(); ++i)
-                if (m.nodes[i][2] < 1e-12) mb.fixed_nodes.push_back(i);
-            Engine e(m, mat, mb, ThermalBCs{}, HeatSourceSet{}, c);
-            e.steps(20);
-            (void)e.step_count();
-            const auto t0 = std::chrono::steady_clock::now();
-            e.steps(steps);
-            (void)e.time();
-            ms[mode] = 1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / steps;
-        }
-        std::printf("%d,%d,%.5f,%.5f,%.5f\n", m.element_count(), m.node_count(), ms[0], ms[1], ms[2]);
-        lx.push_back(std::log((double)m.element_count()));
-        ly.push_back(std::log(ms[2]));
-    }
-    double mx = 0, my = 0;
-    for (size_t i = 0; i < lx.size(); ++i) mx += lx[i] / lx.size(), my += ly[i] / ly.size();
-    double sxy = 0, sxx = 0;
-    for (size_t i = 0; i < lx.size(); ++i) sxy += (lx[i] - mx) * (ly[i] - my), sxx += (lx[i] - mx) * (lx[i] - mx);
-    std::printf("# scaling slope (log step time vs log elements, TherMechExpanTD): %.3f\n", sxy / sxx);
+    for (const auto& r : res)
+        std::printf("%d,%d,%.5f,%.5f,%.5f\n", r.elements, r.nodes, 1e3 * r.ther_mech_ti, 1e3 * r.ther_mech_expan_ti,
+                    1e3 * r.ther_mech_expan_td);
+    std::printf("# scaling slope (log step time vs log elements, TherMechExpanTD): %.3f\n", bench_scaling_slope(res));
     return 0;
 }
 
