@@ -72,6 +72,10 @@ int main(int argc, char** argv) {
     cfg.temperature_dependent = true;
     cfg.damping_gamma = 1.0;
     try {
+        const CriticalTimestep ct = critical_timestep(mesh, mat);  // mesh.hpp:97
+        std::printf("%s mesh, %s: critical dt thermal %.6g s, mechanical %.6g s, min edge %.6g m\n",
+                    to_string(mesh.kind).c_str(), to_string(CouplingMode::Coupled).c_str(), ct.thermal, ct.mechanical,
+                    min_edge_length(mesh, 0));
         Engine eng(mesh, mat, mb, ThermalBCs{}, src, cfg);
         eng.steps(steps);
         const SimulationState& s = eng.state();

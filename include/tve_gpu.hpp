@@ -509,6 +509,69 @@ inline Mesh load_mesh_file(const std::string& path) {
     return load_mesh(text);
 }
 
+// ---------------------------------------------------------------- small reference free functions
+inline std::string to_string(ElementKind k) { return k == ElementKind::T4 ? "T4" : "H8"; }  // mesh.hpp:18
+inline std::string to_string(CouplingMode m) {                                              // engine.hpp:18
+    return m == CouplingMode::Coupled ? "Coupled" : m == CouplingMode::ThermalOnly ? "ThermalOnly" : "MechanicalOnly";
+}
+// mesh.hpp:100: shortest edge of element e
+inline double min_edge_length(const Mesh& m, int e) {
+    static const int t4e[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+    static const int h8e[12][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 0}, {4, 5}, {5, 6},
+                                   {6, 7}, {7, 4}, {0, 4}, {1, 5}, {2, 6}, {3, 7}};
+    const bool t4 = m.kind == ElementKind::T4;
+    double L = std::numeric_limits<double>::infinity();
+    for (int k = 0; k < (t4 ? 6 : 12); ++k) {
+        const auto& a = m.nodes[m.elements[e][t4 ? t4e[k][0] : h8e[k][0]]];
+        const auto& b = m.nodes[m.elements[e][t4 ? t4e[k][1] : h8e[k][1]]];
+        L = std::min(L, std::sqrt((a[0] - b[0]) * (a[0] - b[0]) + (a[1] - b[1]) * (a[1] - b[1]) + (a[2] - b[2]) * (a[2] - b[2])));
+    }
+    return L;
+}
+struct CriticalTimestep { double thermal = 0, mechanical = 0; };
+// mesh.hpp:92-97 (host-only, through the C ABI)
+inline CriticalTimestep critical_timestep(const Mesh& m, const MaterialModel& mat) {
+    const int nn = nodes_per_element(m.kind);
+    std::vector<double> xs, cT, cV, kT, kK;
+    std::vector<int32_t> el;
+    for (const auto& x : m.nodes) xs.insert(xs.end(), x.begin(), x.end());
+    for (const auto& e : m.elements) el.insert(el.end(), e.begin(), e.begin() + nn);
+    for (const auto& [T, v] : mat.thermal.specific_heat.entries) cT.push_back(T), cV.push_back(v);
+    for (const auto& e : mat.thermal.conductivity.entries) {
+        kT.push_back(e.temperature);
+        kK.insert(kK.end(), e.tensor.begin(), e.tensor.end());
+    }
+    tvegpu_problem p{};
+    p.kind = m.kind == ElementKind::T4 ? TVEGPU_T4 : TVEGPU_H8;
+    p.num_nodes = m.node_count();
+    p.num_elements = m.element_count();
+    p.nodes = xs.data();
+    p.elements = el.data();
+    p.density = mat.thermal.density;
+    p.mu = mat.hyperelastic.mu;
+    p.kappa = mat.hyperelastic.kappa;
+    p.eta_a = mat.hyperelastic.eta_a;
+    p.c_table_len = (int32_t)cT.size();
+    p.c_table_T = cT.data();
+    p.c_table_value = cV.data();
+    p.k_table_len = (int32_t)kT.size();
+    p.k_table_T = kT.data();
+    p.k_table_tensor = kK.data();
+    std::vector<double> fib;
+    for (const auto& f : m.fiber_dirs) fib.insert(fib.end(), f.begin(), f.end());
+    p.fiber_dirs = fib.empty() ? nullptr : fib.data();
+    if (mat.fiber) {
+        p.has_fiber = 1;
+        for (int k = 0; k < 3; ++k) p.fiber[k] = (*mat.fiber)[k];
+    }
+    p.dt = 1.0;
+    p.allow_unstable_dt = 1;
+    CriticalTimestep ct;
+    if (tvegpu_critical_timestep(&p, &ct.thermal, &ct.mechanical) != TVEGPU_OK)
+        throw ValidationError(tvegpu_create_error());
+    return ct;
+}
+
 // ---------------------------------------------------------------- engine.hpp:145-162
 // Structured cube meshes for run_bench: n^3 bricks of side h (H8), or 6 positively
 // oriented tetrahedra per brick around its 0-6 diagonal (T4).

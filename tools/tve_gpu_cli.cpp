@@ -359,6 +359,14 @@ tvegpu_problem geometry_problem(const Mesh& m, const MaterialModel& mat, std::ve
     p.k_table_len = (int32_t)kT.size();
     p.k_table_T = kT.data();
     p.k_table_tensor = kK.data();
+    static thread_local std::vector<double> fib;  // per-element fibres (lives as long as p is used)
+    fib.clear();
+    for (const auto& f : m.fiber_dirs) fib.insert(fib.end(), f.begin(), f.end());
+    p.fiber_dirs = fib.empty() ? nullptr : fib.data();
+    if (mat.fiber) {
+        p.has_fiber = 1;
+        for (int k = 0; k < 3; ++k) p.fiber[k] = (*mat.fiber)[k];
+    }
     p.dt = 1.0;  // critical_timestep needs a valid problem; the configured dt is checked by the caller
     p.allow_unstable_dt = 1;
     return p;
