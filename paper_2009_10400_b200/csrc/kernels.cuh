@@ -34,10 +34,16 @@ constexpr int kMaxProny = 4;
 #define TVEGPU_CHUNK 128
 #endif
 constexpr int kChunkThreads = TVEGPU_CHUNK;  // element kernels: one thread per element of a chunk (plan.hpp kChunk)
-// Mechanical slot record: (fx, fy, fz, pad), 32 bytes, so an element writes each
-// contribution with one full-sector 256-bit store and a node reads it with one
-// 256-bit load (24-byte records needed three 8-byte requests per contribution).
-constexpr int kMW = 4;
+// Mechanical slot record: packed (fx, fy, fz), 24 bytes.  An element's NN records are
+// 32-byte aligned as a block (96 / 192 bytes): T4 writes them with three 256-bit
+// stores, H8 with one 256-bit + one 128-bit store per corner pair; a node reads a
+// record as one 16-byte + one 8-byte load.  25 % fewer slot bytes than padded 32-byte
+// records (one 256-bit store / load each): K3 -11 %, K4 -9 % on cfg4.
+// TVEGPU_MW=4 builds the padded layout.
+#ifndef TVEGPU_MW
+#define TVEGPU_MW 3
+#endif
+constexpr int kMW = TVEGPU_MW;
 
 #ifndef TVEGPU_GEO
 #define TVEGPU_GEO 1  // per-element reference geometry (A, V, H8 c_al) precomputed in HBM (0: from staged X)
@@ -97,7 +103,7 @@ struct DevPtrs {
     const int4* ell;           // [N][8 G] the same lists padded with a zero sentinel slot (ell = G > 0)
     const int32_t* node_orig;  // [N]
     double* slot_th;           // [nslots]
-    double* slot_m;            // [nslots][kMW] (fx, fy, fz, pad)
+    double* slot_m;            // [nslots][kMW] (fx, fy, fz[, pad])
     Clock* clock;
     unsigned long long* err_inst;  // (step << 33) | (field << 32) | orig node
     unsigned long long* err_elem;  // (step << 32) | orig element
@@ -572,9 +578,27 @@ __device__ __forceinline__ double gather1(const double* __restrict__ slots, cons
     return s;
 }
 
+// Packed 24-byte slot record: the 16-byte-aligned pair is (x, y) for even ids and
+// (y, z) for odd ids; the remaining component is one 8-byte load.
+__device__ __forceinline__ double3 ld_slot3(const double* __restrict__ slots, int id) {
+    const int lo = id & 1;
+    const double* b = slots + 3 * (size_t)id;
+    const double2 v = __ldg(reinterpret_cast<const double2*>(b + lo));
+    const double w = __ldg(b + (lo ? 0 : 2));
+    return lo ? make_double3(w, v.x, v.y) : make_double3(v.x, v.y, w);
+}
 __device__ __forceinline__ void gather3(const double* __restrict__ slots, const int32_t* __restrict__ idx, int k0,
                                         int k1, double& f0, double& f1, double& f2) {
     f0 = f1 = f2 = 0.0;
+    if constexpr (kMW == 3) {
+        for (int k = k0; k < k1; ++k) {
+            const double3 s = ld_slot3(slots, __ldg(idx + k));
+            f0 += s.x;
+            f1 += s.y;
+            f2 += s.z;
+        }
+        return;
+    }
     for (int k = k0; k < k1; ++k) {
         const double4 s = ldg4(reinterpret_cast<const double4*>(slots) + __ldg(idx + k));
         f0 += s.x;
@@ -615,6 +639,19 @@ __device__ __forceinline__ void gather3_ell(const double* __restrict__ slots, co
                                             double& f1, double& f2) {
     const double4* S = reinterpret_cast<const double4*>(slots);
     const int id[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    if constexpr (kMW == 3) {
+        double3 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = ld_slot3(slots, id[k]);
+        f0 = f1 = f2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            f0 += v[k].x;
+            f1 += v[k].y;
+            f2 += v[k].z;
+        }
+        return;
+    }
     double4 v[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] = ldg4(S + id[k]);
@@ -875,7 +912,13 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
                 Q[i * 3 + j] = Pm[i * 3 + 0] * A[0 * 3 + j] + Pm[i * 3 + 1] * A[1 * 3 + j] + Pm[i * 3 + 2] * A[2 * 3 + j];
     }
     double4* out = reinterpret_cast<double4*>(D.slot_m) + (size_t)e * NN;
-    if constexpr (NN == 4) {
+    double* out3 = D.slot_m + (size_t)e * NN * 3;  // kMW == 3: 32-byte aligned (96 / 192 bytes per element)
+    if constexpr (NN == 4 && kMW == 3) {
+        double4* o = reinterpret_cast<double4*>(out3);
+        st4(o + 0, make_double4(-(Q[0] + Q[1] + Q[2]), -(Q[3] + Q[4] + Q[5]), -(Q[6] + Q[7] + Q[8]), Q[0]));
+        st4(o + 1, make_double4(Q[3], Q[6], Q[1], Q[4]));
+        st4(o + 2, make_double4(Q[7], Q[2], Q[5], Q[8]));
+    } else if constexpr (NN == 4) {
         st4(out + 0, make_double4(-(Q[0] + Q[1] + Q[2]), -(Q[3] + Q[4] + Q[5]), -(Q[6] + Q[7] + Q[8]), 0.0));
         st4(out + 1, make_double4(Q[0], Q[3], Q[6], 0.0));
         st4(out + 2, make_double4(Q[1], Q[4], Q[7], 0.0));
@@ -941,9 +984,7 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
 #pragma unroll
                 for (int j = 0; j < 3; ++j) Q[i * 3 + j] -= k * Uh[al][i] * atc[j];
         }
-#pragma unroll
-        for (int a = 0; a < 8; ++a) {
-            double f[3];
+        auto corner = [&](int a, double f[3]) {
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 const double v = h8s(a, 0) * Q[i * 3 + 0] + h8s(a, 1) * Q[i * 3 + 1] + h8s(a, 2) * Q[i * 3 + 2];
@@ -951,7 +992,30 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
                     h8h(0, a) * Uh[0][i] + h8h(1, a) * Uh[1][i] + h8h(2, a) * Uh[2][i] + h8h(3, a) * Uh[3][i];
                 f[i] = v + k * hg;
             }
-            st4(out + a, make_double4(f[0], f[1], f[2], 0.0));
+        };
+        if constexpr (kMW == 3) {
+            // corner pairs: 48 bytes = one 32-byte and one 16-byte store (pair 2p starts 32-byte aligned)
+#pragma unroll
+            for (int a = 0; a < 8; a += 2) {
+                double f[3], g[3];
+                corner(a, f);
+                corner(a + 1, g);
+                double* o = out3 + 3 * a;
+                if ((a / 2) % 2 == 0) {
+                    st4(reinterpret_cast<double4*>(o), make_double4(f[0], f[1], f[2], g[0]));
+                    *reinterpret_cast<double2*>(o + 4) = make_double2(g[1], g[2]);
+                } else {
+                    *reinterpret_cast<double2*>(o) = make_double2(f[0], f[1]);
+                    st4(reinterpret_cast<double4*>(o + 2), make_double4(f[2], g[0], g[1], g[2]));
+                }
+            }
+        } else {
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {
+                double f[3];
+                corner(a, f);
+                st4(out + a, make_double4(f[0], f[1], f[2], 0.0));
+            }
         }
     }
     if (P.diag) {
