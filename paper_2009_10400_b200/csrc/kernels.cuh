@@ -709,7 +709,10 @@ __global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, i
 // ------------------------------------------------------------------ K3: mechanical element
 // EXP: 0 = F_ther = I, 1 = isotropic lambda I, 2 = general (transversely isotropic / orthotropic)
 #ifndef TVEGPU_K3_MINBLOCKS
-#define TVEGPU_K3_MINBLOCKS 4  // 128 registers: 16 warps/SM (168 unbounded -> 8 warps, latency-bound)
+#define TVEGPU_K3_MINBLOCKS 4  // H8: 128 registers, 16 warps/SM (168 unbounded -> 8 warps, latency-bound)
+#endif
+#ifndef TVEGPU_K3_MINBLOCKS_T4
+#define TVEGPU_K3_MINBLOCKS_T4 5  // T4: 102 registers, 20 warps/SM (cfg5 T4 K3 -12 % vs 4)
 #endif
 // K3 element body: element e of the staged chunk st (n = its node slots)
 template <int NN, int EXP>
@@ -1027,7 +1030,7 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
 }
 
 template <int NN, int EXP>
-__global__ void __launch_bounds__(kChunkThreads, TVEGPU_K3_MINBLOCKS)
+__global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T4 : TVEGPU_K3_MINBLOCKS)
     k_mech_element(const DevParams P, const DevPtrs D, int cur, int c0, int c1) {
     extern __shared__ double2 smem_planes[];
     const int ms = P.max_chunk_nodes;
