@@ -23,6 +23,7 @@
 // atomicMin on the error words and the end-of-step ticket.
 #pragma once
 
+#include <cassert>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -460,6 +461,42 @@ __device__ __forceinline__ int stage_chunk(const DevPtrs& D, const double4* __re
 // Warm L1 with a coalesced SoA stream this thread will read later in the kernel.
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
+// ------------------------------------------------------------------ bounds-checking build
+// TVEGPU_BOUNDS_CHECK=1 (csrc/Makefile `variant`, scripts/gpu_bounds_check.sh) asserts every
+// index the step kernels dereference: chunk staging entries and element slots (K1/K3),
+// gather lists (K2/K4).  compute-sanitizer is not available on the GPU pool; this build
+// plus the parity suite stands in for memcheck.  Off: no code.
+#ifndef TVEGPU_BOUNDS_CHECK
+#define TVEGPU_BOUNDS_CHECK 0
+#endif
+template <int NN>
+__device__ __forceinline__ void check_chunk(const DevParams& P, const DevPtrs& D, int c, int e, const int (&n)[NN]) {
+    if constexpr (TVEGPU_BOUNDS_CHECK) {
+        const int eb = D.chunk_start[c], ee = D.chunk_start[c + 1];
+        assert(0 <= eb && eb <= ee && ee <= P.E && ee - eb <= kChunkThreads);
+        assert(e < 0 || (eb <= e && e < ee));
+        for (int k = threadIdx.x; k < P.stage_stride; k += kChunkThreads) {
+            const int2 en = D.stage_ent[(size_t)c * P.stage_stride + k];
+            assert(en.x >= -1 && en.x < P.N && en.y >= 0 && en.y < P.max_chunk_nodes);
+        }
+        if (e >= 0)
+            for (int a = 0; a < NN; ++a) assert(n[a] >= 0 && n[a] < P.max_chunk_nodes);
+    }
+}
+__device__ __forceinline__ void check_gather(const DevParams& P, const DevPtrs& D, int i) {
+    if constexpr (TVEGPU_BOUNDS_CHECK) {
+        const int k0 = D.csr_off[i], k1 = D.csr_off[i + 1];
+        assert(0 <= k0 && k0 <= k1);
+        for (int k = k0; k < k1; ++k) assert(D.csr_slot[k] >= 0 && D.csr_slot[k] < P.nslots);
+        if (P.ell) {
+            const int32_t* row = reinterpret_cast<const int32_t*>(D.ell) + (size_t)8 * P.ell * i;
+            assert(k1 - k0 <= 8 * P.ell);
+            for (int k = 0; k < 8 * P.ell; ++k)
+                assert(k < k1 - k0 ? row[k] == D.csr_slot[k0 + k] : row[k] == P.nslots);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ K1: thermal element
 #ifdef TVEGPU_K1_MINBLOCKS
 #define K1_BOUNDS __launch_bounds__(kChunkThreads, TVEGPU_K1_MINBLOCKS)
@@ -538,6 +575,7 @@ __global__ void K1_BOUNDS k_thermal_element(const DevParams P, const DevPtrs D, 
 #endif
     const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, P.stage_stride, S, n);
     if (D.clock->halted || e < 0) return;  // halted: uniform across the grid (read after the wait)
+    check_chunk<NN>(P, D, c0 + blockIdx.x, e, n);
     k1_body<NN>(P, D, S, e, n);
     pdl_trigger();  // after this block's work: the successor fills in behind the last wave
 }
@@ -690,6 +728,7 @@ __global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, i
     pdl_wait();
     if (i < P.N && !D.clock->halted) {
         double4* R = cur ? D.rec1 : D.rec0;
+        check_gather(P, D, i);
         const double s = P.ell ? gather1_ell<WIDE>(D.slot_th, D.ell + 2 * (size_t)P.ell * i, P.ell, ia, ib)
                                : gather1(D.slot_th, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1));
         const double T = R[i].w;
@@ -1048,6 +1087,7 @@ __global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T
     }
     const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, P.stage_stride, st, n);
     if (D.clock->halted || e < 0) return;
+    check_chunk<NN>(P, D, c0 + blockIdx.x, e, n);
     k3_body<NN, EXP>(P, D, st, e, n);
     pdl_trigger();
 }
@@ -1064,6 +1104,7 @@ __global__ void NODE_BOUNDS k_mech_node(const DevParams P, const DevPtrs D, int 
         const double4* Rc = cur ? D.rec1 : D.rec0;
         double4* Rn = cur ? D.rec0 : D.rec1;  // holds u^{n-1}; receives u^{n+1}
         double f0, f1, f2;
+        check_gather(P, D, i);
         if (P.ell == 1) gather3_ell(D.slot_m, ia, ib, f0, f1, f2);
         else gather3(D.slot_m, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1), f0, f1, f2);
         const double4 u = ldg4(Rc + i);  // read-only in this kernel
