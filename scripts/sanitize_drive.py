@@ -1,6 +1,6 @@
-"""Exercises every kernel of libtvegpu.so on small problems, for compute-sanitizer
-(scripts/sanitize.sh): memcheck / racecheck / synccheck / initcheck (SURVEY.md §5,
-'Race detection / sanitizers').  Graph replays (steps_per_graph = 4), PDL chains,
+"""Exercises every kernel of libtvegpu.so on small problems — run on the bounds-checking
+build by scripts/gpu_bounds_check.sh (compute-sanitizer is not available on the GPU
+pool; SURVEY.md §5 'Race detection / sanitizers').  Graph replays (steps_per_graph = 4), PDL chains,
 step_io, run-level reductions, diagnostics, checkpoint and the lockstep partition
 group (halo pack/unpack) all run; no oracle, no torch."""
 import os
