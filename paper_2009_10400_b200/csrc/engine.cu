@@ -143,6 +143,7 @@ struct tvegpu_engine {
     int steps_per_graph = 64;
     bool warmed = false;  // a plain (un-captured) step has run
     bool pdl = false;     // programmatic dependent launch of the step kernels (single partition)
+    bool pair = false;    // node kernels with two threads per node (long CSR gather lists: T4)
     // errors
     std::string err;
     long long err_step = -1;
@@ -243,6 +244,11 @@ void launch_step_kernel(tvegpu_engine* h, void (*kern)(KArgs...), int grid, int 
     CU(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
+using NodeKernel = void (*)(const DevParams, const DevPtrs, int, int, double*);
+NodeKernel thermal_node_kernel(const tvegpu_engine* h) {
+    return h->pair ? k_thermal_node<2> : (h->prm.ell > 1 ? k_thermal_node<1> : k_thermal_node<0>);
+}
+
 // Element kernels run one CTA per 128-element chunk over chunk range [c0, c1).
 template <int NN>
 void launch_mech_element(tvegpu_engine* h, int c0, int c1) {
@@ -302,7 +308,7 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr, cudaEvent_t 
         }
         mark();
         if (wait_src) CU(cudaStreamWaitEvent(h->s, wait_src, 0));
-        launch_step_kernel(h, h->prm.ell > 1 ? k_thermal_node<true> : k_thermal_node<false>, blocks(N, kNodeThreads),
+        launch_step_kernel(h, thermal_node_kernel(h), blocks(h->pair ? 2 * N : N, kNodeThreads),
                            kNodeThreads, 0, h->prm, h->ptr, h->cur, (int)(h->mode == TVEGPU_THERMAL_ONLY), t_out);
         mark();
     } else if (wait_src) {
@@ -319,7 +325,12 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr, cudaEvent_t 
             h->nn == 4 ? launch_mech_element<4>(h, 0, nc) : launch_mech_element<8>(h, 0, nc);
         }
         mark();
-        launch_step_kernel(h, k_mech_node, blocks(N, kNodeThreads), kNodeThreads, 0, h->prm, h->ptr, h->cur, 1, u_out);
+        if (h->pair)
+            launch_step_kernel(h, k_mech_node<true>, blocks(2 * N, kNodeThreads), kNodeThreads, 0, h->prm, h->ptr,
+                               h->cur, 1, u_out);
+        else
+            launch_step_kernel(h, k_mech_node<false>, blocks(N, kNodeThreads), kNodeThreads, 0, h->prm, h->ptr,
+                               h->cur, 1, u_out);
         mark();
         h->cur ^= 1;
     }
@@ -706,11 +717,22 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     CU(cudaMemsetAsync(h->ptr.slot_th, 0, (nslots + 1) * 8, s));
     CU(cudaMemsetAsync(h->ptr.slot_m, 0, kMW * (nslots + 1) * 8, s));
     {
+        // Node-kernel summation trees must not depend on the partition (bit-identity at any
+        // rank count): two threads per node (halves of the canonical list, then their sum)
+        // iff some node of the GLOBAL mesh has > 8 contributions (T4); otherwise one thread
+        // sums an ELL row of 8 ids in order (H8).
+        {
+            std::vector<int> val(p.num_nodes, 0);
+            for (size_t k = 0; k < (size_t)p.num_elements * nn; ++k) ++val[p.elements[k]];
+            const int gmax = val.empty() ? 0 : *std::max_element(val.begin(), val.end());
+            h->pair = gmax > 8 && !std::getenv("TVEGPU_NO_PAIR");
+        }
         int maxc = 0;
         for (int i = 0; i < pl.N; ++i) maxc = std::max(maxc, pl.csr_off[i + 1] - pl.csr_off[i]);
-        // ELL rows of 8 G ids (G = ceil(max contributions / 8), up to 64 contributions)
+        // ELL rows of 8 G ids (G = ceil(max contributions / 8), up to 64 contributions);
+        // the pair kernels read the CSR lists instead
         const int G = (std::max(1, maxc) + 7) / 8;
-        m.ell = (G <= 8 && !std::getenv("TVEGPU_NO_ELL")) ? G : 0;
+        m.ell = (!h->pair && G <= 8 && !std::getenv("TVEGPU_NO_ELL")) ? G : 0;
         if (m.ell) {
             const size_t W = (size_t)8 * G;
             std::vector<int32_t> ell(W * pl.N, (int32_t)nslots);
@@ -1877,7 +1899,7 @@ void group_step_once(tvegpu_group* G) {
         }
         loopback_copy(G, false);
         for (tvegpu_engine* h : G->parts)
-            (h->prm.ell > 1 ? k_thermal_node<true> : k_thermal_node<false>)<<<blocks(h->plan.N, kNodeThreads), kNodeThreads, 0, h->s>>>(h->prm, h->ptr, h->cur,
+            thermal_node_kernel(h)<<<blocks(h->pair ? 2 * h->plan.N : h->plan.N, kNodeThreads), kNodeThreads, 0, h->s>>>(h->prm, h->ptr, h->cur,
                                                                     h->mode == TVEGPU_THERMAL_ONLY, nullptr);
     }
     if (h0->mode != TVEGPU_THERMAL_ONLY) {
@@ -1888,7 +1910,12 @@ void group_step_once(tvegpu_group* G) {
         }
         loopback_copy(G, true);
         for (tvegpu_engine* h : G->parts) {
-            k_mech_node<<<blocks(h->plan.N, kNodeThreads), kNodeThreads, 0, h->s>>>(h->prm, h->ptr, h->cur, 1, nullptr);
+            if (h->pair)
+                k_mech_node<true><<<blocks(2 * h->plan.N, kNodeThreads), kNodeThreads, 0, h->s>>>(h->prm, h->ptr, h->cur, 1,
+                                                                                              nullptr);
+            else
+                k_mech_node<false><<<blocks(h->plan.N, kNodeThreads), kNodeThreads, 0, h->s>>>(h->prm, h->ptr, h->cur, 1,
+                                                                                               nullptr);
             h->cur ^= 1;
         }
     }

@@ -15,12 +15,15 @@
 // fp64 throughout (north_star parity <= 1e-10).  One thread per element / node.
 // Node state is a packed 32-byte record (ux, uy, uz, T) and reference
 // coordinates a 32-byte record (x, y, z, -), so an element gathers one sector
-// per node and per field.  The element geometry (A_e with G_e = A_e Xi, and
-// V_e) is recomputed from the gathered coordinates instead of being streamed
-// (80 B/element saved per element kernel).  Assembly is a gather in
-// canonical (original element, local) order: no float atomics, results
-// bit-identical at any partition count.  The only atomics are integer
-// atomicMin on the error words and the end-of-step ticket.
+// per node and per field.  The element geometry (A_e with G_e = A_e Xi, V_e and
+// the H8 hourglass vectors c_al = X h_al) is computed once by k_geometry and
+// streamed SoA (TVEGPU_GEO=0 recomputes it from staged coordinates).
+// Assembly is a gather in canonical (original element, local) order — one
+// thread per node in order (H8), or two threads each summing one half and then
+// their sum (T4, > 8 contributions per node) — with a tree chosen from the
+// global mesh: no float atomics, results bit-identical at any partition count.
+// The only atomics are integer atomicMin on the error words and the end-of-step
+// ticket.
 #pragma once
 
 #include <cassert>
@@ -714,23 +717,39 @@ constexpr int kNodeThreads = TVEGPU_NODE_THREADS;
 #else
 #define NODE_BOUNDS __launch_bounds__(kNodeThreads)
 #endif
-// WIDE: ELL rows of more than one group (T4 meshes)
-template <bool WIDE>
+// G: 0 = ELL rows of one group (H8) or CSR, 1 = ELL rows of several groups, 2 = two
+// threads per node over the CSR list (T4; see k_mech_node<PAIR>)
+template <int G>
 __global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, int cur, int closes,
                                            double* __restrict__ t_out) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    constexpr bool PAIR = G == 2, WIDE = G == 1;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = PAIR ? (t >> 1) : t;
+    const bool lead = !PAIR || !(threadIdx.x & 1);
     int4 ia = make_int4(0, 0, 0, 0), ib = ia;
     double V = 0.0;
     if (i < P.N) {  // predecessor-independent loads first (index row, node volume)
-        if (P.ell) ia = __ldg(D.ell + 2 * (size_t)P.ell * i), ib = __ldg(D.ell + 2 * (size_t)P.ell * i + 1);
+        if (!PAIR && P.ell) ia = __ldg(D.ell + 2 * (size_t)P.ell * i), ib = __ldg(D.ell + 2 * (size_t)P.ell * i + 1);
         V = __ldg(D.vnode + i);
     }
     pdl_wait();
-    if (i < P.N && !D.clock->halted) {
+    const bool active = i < P.N && !D.clock->halted;  // the same for both threads of a pair
+    double s = 0.0;
+    if constexpr (PAIR) {
+        if (active) {
+            check_gather(P, D, i);
+            const int k0 = __ldg(D.csr_off + i), k1 = __ldg(D.csr_off + i + 1), km = k0 + ((k1 - k0 + 1) >> 1);
+            s = gather1(D.slot_th, D.csr_slot, lead ? k0 : km, lead ? km : k1);
+        }
+        s += __shfl_down_sync(0xffffffffu, s, 1);
+    }
+    if (active && lead) {
         double4* R = cur ? D.rec1 : D.rec0;
-        check_gather(P, D, i);
-        const double s = P.ell ? gather1_ell<WIDE>(D.slot_th, D.ell + 2 * (size_t)P.ell * i, P.ell, ia, ib)
-                               : gather1(D.slot_th, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1));
+        if constexpr (!PAIR) {
+            check_gather(P, D, i);
+            s = P.ell ? gather1_ell<WIDE>(D.slot_th, D.ell + 2 * (size_t)P.ell * i, P.ell, ia, ib)
+                      : gather1(D.slot_th, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1));
+        }
         const double T = R[i].w;
         const double c = P.td ? interp1(P.cT, P.cV, P.c_len, T) : P.c_fixed;
         const double C = P.rho * c * V;
@@ -1094,19 +1113,38 @@ __global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T
 
 // ------------------------------------------------------------------ K4: mechanical node
 // u_out (tvegpu_step_io only): also write u^{n+1} in original numbering for the host read-back.
+// PAIR: two threads per node for long CSR lists (T4, ~24 contributions): each sums one
+// half in canonical order, the first half's sum + the second's is the node's force (a
+// fixed two-leaf tree: deterministic, partition-invariant).
+template <bool PAIR>
 __global__ void NODE_BOUNDS k_mech_node(const DevParams P, const DevPtrs D, int cur, int closes,
                                                    double* __restrict__ u_out) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = PAIR ? (t >> 1) : t;
+    const bool lead = !PAIR || !(threadIdx.x & 1);
     int4 ia = make_int4(0, 0, 0, 0), ib = ia;
-    if (i < P.N && P.ell == 1) ia = __ldg(D.ell + 2 * (size_t)i), ib = __ldg(D.ell + 2 * (size_t)i + 1);
+    if (!PAIR && i < P.N && P.ell == 1) ia = __ldg(D.ell + 2 * (size_t)i), ib = __ldg(D.ell + 2 * (size_t)i + 1);
     pdl_wait();
-    if (i < P.N && !D.clock->halted) {
+    const bool active = i < P.N && !D.clock->halted;  // the same for both threads of a pair
+    double f0 = 0.0, f1 = 0.0, f2 = 0.0;
+    if constexpr (PAIR) {
+        if (active) {
+            check_gather(P, D, i);
+            const int k0 = __ldg(D.csr_off + i), k1 = __ldg(D.csr_off + i + 1), km = k0 + ((k1 - k0 + 1) >> 1);
+            gather3(D.slot_m, D.csr_slot, lead ? k0 : km, lead ? km : k1, f0, f1, f2);
+        }
+        f0 += __shfl_down_sync(0xffffffffu, f0, 1);
+        f1 += __shfl_down_sync(0xffffffffu, f1, 1);
+        f2 += __shfl_down_sync(0xffffffffu, f2, 1);
+    }
+    if (active && lead) {
         const double4* Rc = cur ? D.rec1 : D.rec0;
         double4* Rn = cur ? D.rec0 : D.rec1;  // holds u^{n-1}; receives u^{n+1}
-        double f0, f1, f2;
-        check_gather(P, D, i);
-        if (P.ell == 1) gather3_ell(D.slot_m, ia, ib, f0, f1, f2);
-        else gather3(D.slot_m, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1), f0, f1, f2);
+        if constexpr (!PAIR) {
+            check_gather(P, D, i);
+            if (P.ell == 1) gather3_ell(D.slot_m, ia, ib, f0, f1, f2);
+            else gather3(D.slot_m, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1), f0, f1, f2);
+        }
         const double4 u = ldg4(Rc + i);  // read-only in this kernel
         const double4 up = ld4(Rn + i);  // this thread overwrites it below
         const double m = __ldg(D.mass + i);
