@@ -28,10 +28,14 @@ MODES = {"TherMechTI": dict(expansion_enabled=False, temperature_dependent=False
 LADDER = {H8: [100, 126, 159, 200, 252], T4: [40, 50, 63, 80, 100, 126]}
 
 
-def time_steps(eng, steps, warmup):
+def time_steps(eng, steps, warmup, soak=0.3):
     stream = torch.cuda.ExternalStream(eng.stream)
     eng.step(warmup)
     eng.sync()
+    t0 = time.perf_counter()  # keep the GPU busy until clocks settle (the first rung ran cold)
+    while time.perf_counter() - t0 < soak:
+        eng.step(64)
+        eng.sync()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
     eng.step(steps)
