@@ -22,6 +22,7 @@
 #include <vector>
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "kernels.cuh"
 #include "plan.hpp"
@@ -164,6 +165,16 @@ struct tvegpu_engine {
 namespace {
 
 int blocks(int n, int t) { return (n + t - 1) / t; }
+
+// NVTX range per C-ABI call (header-only NVTX 3: free unless a tool attaches), so
+// ncu --nvtx / Nsight timelines show which API call enqueued which kernels.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define TVEGPU_RANGE() NvtxRange nvtx_range_(__func__)
 
 void refresh_sources_if_needed(tvegpu_engine* h, double t) {
     if (h->source_override) return;
@@ -1212,6 +1223,7 @@ void tvegpu_default_options(tvegpu_options* o) {
 }
 
 tvegpu_status tvegpu_create(const tvegpu_problem* p, const tvegpu_options* o, tvegpu_engine** out) {
+    TVEGPU_RANGE();
     if (!p || !out) {
         g_create_error = "NULL argument";
         return TVEGPU_E_ARG;
@@ -1257,6 +1269,7 @@ void tvegpu_destroy(tvegpu_engine* h) {
 }
 
 tvegpu_status tvegpu_enqueue_steps(tvegpu_engine* h, int64_t n) {
+    TVEGPU_RANGE();
     if (!h || n < 0) return TVEGPU_E_ARG;
     return guard(h, [&] {
         enqueue_steps(h, n);
@@ -1265,6 +1278,7 @@ tvegpu_status tvegpu_enqueue_steps(tvegpu_engine* h, int64_t n) {
 }
 
 tvegpu_status tvegpu_sync(tvegpu_engine* h) {
+    TVEGPU_RANGE();
     if (!h) return TVEGPU_E_ARG;
     return guard(h, [&] {
         if (h->halted) return h->last_status;
@@ -1279,6 +1293,7 @@ tvegpu_status tvegpu_sync(tvegpu_engine* h) {
 }
 
 tvegpu_status tvegpu_step(tvegpu_engine* h, int64_t n) {
+    TVEGPU_RANGE();
     if (!h || n < 0) return TVEGPU_E_ARG;
     return guard(h, [&] {
         if (h->halted) {
@@ -1312,6 +1327,7 @@ tvegpu_status tvegpu_get_displacements(tvegpu_engine* h, double* u, double* up) 
 }
 
 tvegpu_status tvegpu_make_snapshot(tvegpu_engine* h, double* T, double* u) {
+    TVEGPU_RANGE();
     if (!h || (!T && !u)) return TVEGPU_E_ARG;
     return guard(h, [&] {
         read_fields(h, T, u, nullptr);
@@ -1340,6 +1356,7 @@ tvegpu_status tvegpu_get_viscous(tvegpu_engine* h, double* v) {
 
 tvegpu_status tvegpu_set_state(tvegpu_engine* h, const double* T, const double* u, const double* up,
                                const double* viscous, double time, int64_t step) {
+    TVEGPU_RANGE();
     if (!h) return TVEGPU_E_ARG;
     return guard(h, [&] {
         std::vector<double4> r0, r1;
@@ -1412,6 +1429,7 @@ tvegpu_status tvegpu_set_nodal_sources(tvegpu_engine* h, const double* power) {
 // reads the sources), and the temperature read-back runs there while K3/K4 compute
 // (T is final after K2).  Only the displacement read-back follows the step.
 tvegpu_status tvegpu_step_io(tvegpu_engine* h, const double* power, int64_t n, double* T, double* u) {
+    TVEGPU_RANGE();
     if (!h || n < 1) return TVEGPU_E_ARG;
     if (h->plan.nranks != 1 || h->plan.N != h->N_global) {  // no overlap across partitions
         tvegpu_status st = power ? tvegpu_set_nodal_sources(h, power) : TVEGPU_OK;
@@ -1504,6 +1522,7 @@ tvegpu_status tvegpu_checkpoint_size(tvegpu_engine* h, uint64_t* bytes) {
 }
 
 tvegpu_status tvegpu_save_checkpoint(tvegpu_engine* h, void* buf, uint64_t bytes) {
+    TVEGPU_RANGE();
     if (!h || !buf) return TVEGPU_E_ARG;
     if (h->plan.nranks != 1 || h->plan.N != h->N_global || h->plan.E != h->E_global) {
         h->err = "save_checkpoint needs a single-partition engine (gather the rank states first)";
@@ -1544,6 +1563,7 @@ tvegpu_status tvegpu_save_checkpoint(tvegpu_engine* h, void* buf, uint64_t bytes
 }
 
 tvegpu_status tvegpu_load_checkpoint(tvegpu_engine* h, const void* buf, uint64_t bytes) {
+    TVEGPU_RANGE();
     if (!h || !buf) return TVEGPU_E_ARG;
     CkptHeader hd;
     if (bytes < sizeof hd) {
@@ -1575,6 +1595,7 @@ tvegpu_status tvegpu_load_checkpoint(tvegpu_engine* h, const void* buf, uint64_t
 }
 
 tvegpu_status tvegpu_get_summary(tvegpu_engine* h, tvegpu_summary* out) {
+    TVEGPU_RANGE();
     if (!h || !out) return TVEGPU_E_ARG;
     return guard(h, [&] {
         const int nb = red_blocks(h->plan.N);
@@ -1596,6 +1617,7 @@ tvegpu_status tvegpu_get_summary(tvegpu_engine* h, tvegpu_summary* out) {
 
 tvegpu_status tvegpu_ablation_volume(tvegpu_engine* h, double threshold, int32_t deformed, double* volume,
                                      int64_t* elements_above) {
+    TVEGPU_RANGE();
     if (!h || !volume || !std::isfinite(threshold)) return TVEGPU_E_ARG;
     return guard(h, [&] {
         if (!h->d_conn) {
@@ -1618,6 +1640,7 @@ tvegpu_status tvegpu_ablation_volume(tvegpu_engine* h, double threshold, int32_t
 }
 
 tvegpu_status tvegpu_total_energy(tvegpu_engine* h, double* kinetic, double* strain) {
+    TVEGPU_RANGE();
     if (!h || (!kinetic && !strain)) return TVEGPU_E_ARG;
     return guard(h, [&] {
         if (!h->d_conn) {
@@ -1639,6 +1662,7 @@ tvegpu_status tvegpu_total_energy(tvegpu_engine* h, double* kinetic, double* str
 }
 
 tvegpu_status tvegpu_element_fields(tvegpu_engine* h, double* det_f, double* max_principal_stress) {
+    TVEGPU_RANGE();
     if (!h || (!det_f && !max_principal_stress)) return TVEGPU_E_ARG;
     if (!h->prm.diag) {
         h->err = "element fields need options.diagnostics = 1 (F and S of the last mechanics phase)";
@@ -1974,6 +1998,7 @@ void tvegpu_group_destroy(tvegpu_group* G) {
 }
 
 tvegpu_status tvegpu_group_step(tvegpu_group* G, int64_t n) {
+    TVEGPU_RANGE();
     if (!G || n < 0) return TVEGPU_E_ARG;
     try {
         std::vector<long long> s0;
