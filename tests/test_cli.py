@@ -4,6 +4,7 @@ Exit codes: 0 success, 1 config / validation, 2 instability, 3 verification fail
 import json
 import os
 import subprocess
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -170,3 +171,47 @@ def test_verify_all_pass_and_bench():
     r = cli("bench", "--mesh-kind", "h8", "--steps", "20")
     assert r.returncode == 0, r.stderr
     assert "scaling slope" in r.stdout and len(r.stdout.strip().splitlines()) == 7
+
+
+TET_CFG = """# single tet at rest: no sources, no metabolism, blood at the initial temperature
+[mesh]
+file = tet.mesh
+[material]
+mu = 1190.476
+kappa = 19444.444
+[thermal]
+density = 1060
+specific_heat = 3600
+conductivity = 0.53
+perfusion_rate = 26.6
+blood_specific_heat = 3617
+metabolic_rate = 0
+[sim]
+dt = 0.0001
+duration = 0.0003
+[output]
+snapshot_interval = 0.0001
+"""
+
+
+@pytest.mark.gpu
+def test_single_tet_snapshot_golden(tmp_path):  # SPEC.md:432-434 write_snapshot examples
+    build()
+    (tmp_path / "tet.mesh").write_text("$nodes 4\n1 0 0 0\n2 0.01 0 0\n3 0 0.01 0\n4 0 0 0.01\n"
+                                       "$elements 1 t4\n1 1 2 3 4\n")
+    (tmp_path / "tet.cfg").write_text(TET_CFG)
+    out = tmp_path / "out"
+    r = cli("run", "--config", str(tmp_path / "tet.cfg"), "--out", str(out), "--json")
+    assert r.returncode == 0, r.stderr
+    # golden-file stable: byte-identical to the committed fixture (9 significant digits)
+    golden = (Path(ROOT) / "tests" / "golden" / "single_tet_snapshot.vtk").read_bytes()
+    assert (out / "snapshot_00000000.vtk").read_bytes() == golden
+    # distinct files named by the zero-padded step index
+    snaps = sorted(p.name for p in out.glob("snapshot_*.vtk"))
+    assert snaps == [f"snapshot_{k:08d}.vtk" for k in range(4)]
+    # round trip: re-parsing reproduces the arrays (the rest state stays at rest, SPEC.md:361)
+    text = (out / "snapshot_00000003.vtk").read_text().splitlines()
+    i = text.index("SCALARS temperature double 1")
+    assert [float(v) for v in text[i + 2:i + 6]] == [37.0] * 4
+    j = text.index("VECTORS displacement double")
+    assert [float(v) for line in text[j + 1:j + 5] for v in line.split()] == [0.0] * 12

@@ -320,3 +320,40 @@ def test_table1_length_run_is_stable_and_deterministic():
     b.step(62_500)
     np.testing.assert_array_equal(b.state()["T"], st["T"])
     np.testing.assert_array_equal(b.state()["u"], st["u"])
+
+
+@pytest.mark.parametrize("kind", [T4, H8])
+@pytest.mark.parametrize("mode", [COUPLED, THERMAL_ONLY, MECHANICAL_ONLY])
+def test_one_step_from_random_state(kind, mode):
+    """Kernel-level parity (test plan item 2): one step from a random
+    state — temperatures, displacements (≈1 % strain), previous displacements and a
+    symmetric viscous history — on GPU and oracle; the step's increments agree to
+    1e-12 (relative to the increment itself)."""
+    p = configs.small_problem(kind=kind, n=4, steps=4)
+    p.mode = mode
+    rng = np.random.default_rng(5)
+    N, E, P = p.num_nodes, p.num_elements, p.prony_count
+    T = 37.0 + rng.uniform(-2.0, 10.0, N)
+    u = 1e-4 * rng.normal(size=3 * N)
+    up = u + 1e-6 * rng.normal(size=3 * N)
+    th = rng.normal(size=(E, P, 3, 3)) * 50.0
+    th = (th + np.swapaxes(th, -1, -2)).reshape(-1)
+    g = tg.Engine(p)
+    o = O.OracleEngine(p)
+    for eng in (g, o):
+        eng.set_state(T=T, u=u, u_prev=up, viscous=th, time=0.0, step=0)
+        eng.step(1)
+    a, b = g.state(), o.state()
+    assert a["step"] == b["step"] == 1
+    errs = {"T": inc_err(a["T"], b["T"], T), "u": inc_err(a["u"], b["u"], u),
+            "u_prev": inc_err(a["u_prev"], b["u_prev"], up)}
+    if P and mode != THERMAL_ONLY:
+        errs["viscous"] = inc_err(a["viscous"], b["viscous"], th)
+    for k, e in errs.items():
+        if mode == THERMAL_ONLY and k != "T" or mode == MECHANICAL_ONLY and k == "T":
+            continue  # untouched fields (compared bit-exactly below)
+        assert e <= 1e-12, f"{k} increment err {e:.3e}"
+    if mode == THERMAL_ONLY:
+        assert np.array_equal(a["u"], u) and np.array_equal(b["u"], u)
+    if mode == MECHANICAL_ONLY:
+        assert np.array_equal(a["T"], T) and np.array_equal(b["T"], T)

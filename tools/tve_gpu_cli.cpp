@@ -133,8 +133,11 @@ std::vector<double> nums(const std::string& s, const std::string& key) {
     while (in >> t) v.push_back(num(t, key));
     return v;
 }
-std::vector<std::pair<double, double>> table(const std::string& s, const std::string& key) {  // "T:v, T:v"
+// "T:v, T:v"; with allow_scalar a bare value is a constant property (a one-point table)
+std::vector<std::pair<double, double>> table(const std::string& s, const std::string& key, bool allow_scalar = false) {
     std::vector<std::pair<double, double>> t;
+    if (allow_scalar && s.find(':') == std::string::npos && s.find(',') == std::string::npos)
+        return {{37.0, num(trim(s), key)}};
     std::string item;
     std::istringstream in(s);
     while (std::getline(in, item, ',')) {
@@ -182,10 +185,10 @@ Setup build_setup(const Config& c, const fs::path& base) {
     }
     m.thermal.density = getd(c, "thermal.density", 0);
     if (m.thermal.density <= 0) throw ConfigError("thermal.density must be > 0");
-    for (auto [T, v] : table(get(c, "thermal.specific_heat", "37:3600"), "thermal.specific_heat"))
+    for (auto [T, v] : table(get(c, "thermal.specific_heat", "37:3600"), "thermal.specific_heat", true))
         m.thermal.specific_heat.entries.push_back({T, v});
     m.thermal.conductivity.entries.clear();
-    for (auto [T, k] : table(get(c, "thermal.conductivity", "37:0.53"), "thermal.conductivity"))
+    for (auto [T, k] : table(get(c, "thermal.conductivity", "37:0.53"), "thermal.conductivity", true))
         m.thermal.conductivity.entries.push_back({T, {k, 0, 0, 0, k, 0, 0, 0, k}});
     m.thermal.perfusion_rate = getd(c, "thermal.perfusion_rate", 0);
     m.thermal.blood_specific_heat = getd(c, "thermal.blood_specific_heat", 0);
