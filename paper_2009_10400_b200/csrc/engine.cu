@@ -469,6 +469,7 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     CU(cudaGetDevice(&h->device));
     const int nranks = o.nranks > 0 ? o.nranks : 1;
     if (!p.allow_unstable_dt) {
+        StageTimer tm("critical_timestep");
         double th, me;
         critical_timestep(p, &th, &me);
         if (p.dt > std::min(th, me)) {
@@ -479,6 +480,7 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     }
     GlobalMesh g = build_global(p);
     h->plan = build_rank_plan(p, g, nranks, o.rank, o.reorder);
+    StageTimer tm_dev("device tables + uploads");
     const RankPlan& pl = h->plan;
     h->nn = g.nn;
     h->kind = p.kind;
@@ -728,6 +730,7 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     CU(cudaMemsetAsync(h->ptr.slot_th, 0, (nslots + 1) * 8, s));
     CU(cudaMemsetAsync(h->ptr.slot_m, 0, kMW * (nslots + 1) * 8, s));
     {
+        StageTimer tm("gather tables (ELL, valence)");
         // Node-kernel summation trees must not depend on the partition (bit-identity at any
         // rank count): two threads per node (halves of the canonical list, then their sum)
         // iff some node of the GLOBAL mesh has > 8 contributions (T4); otherwise one thread

@@ -9,21 +9,10 @@
 #include <cstring>
 #include <limits>
 #include <numeric>
+#include <parallel/algorithm>
 
 namespace tvegpu {
 
-// Setup-stage timing to stderr when TVEGPU_TIMING is set.
-struct StageTimer {
-    const char* name;
-    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
-    explicit StageTimer(const char* n) : name(n) {}
-    ~StageTimer() {
-        static const bool on = std::getenv("TVEGPU_TIMING") != nullptr;
-        if (on)
-            std::fprintf(stderr, "[tvegpu setup] %-28s %8.1f ms\n", name,
-                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
-    }
-};
 
 
 const int kH8Sign[8][3] = {{-1, -1, -1}, {1, -1, -1}, {1, 1, -1}, {-1, 1, -1},
@@ -173,7 +162,9 @@ void validate_problem(const tvegpu_problem& p) {
 
 GlobalMesh build_global(const tvegpu_problem& p) {
     StageTimer tm("build_global");
+    LapTimer lap;
     validate_problem(p);
+    lap("validate");
     GlobalMesh g;
     g.kind = p.kind;
     g.nn = p.kind == TVEGPU_T4 ? 4 : 8;
@@ -246,6 +237,7 @@ GlobalMesh build_global(const tvegpu_problem& p) {
             g.lo[k] = std::min(g.lo[k], g.centroid[(size_t)3 * e + k]);
             g.hi[k] = std::max(g.hi[k], g.centroid[(size_t)3 * e + k]);
         }
+    lap("element geometry + bounds");
     // canonical adjacency over original ids
     g.adj_off.assign(N + 1, 0);
     for (int64_t k = 0; k < (int64_t)E * nn; ++k) g.adj_off[p.elements[k] + 1]++;
@@ -262,6 +254,7 @@ GlobalMesh build_global(const tvegpu_problem& p) {
                 fill[i]++;
             }
     }
+    lap("adjacency");
     g.mass.assign(N, 0.0);
     g.vnode.assign(N, 0.0);
     int orphan = -1;
@@ -334,7 +327,9 @@ RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nrank
     r.rank = rank;
     r.nn = g.nn;
     const int nn = g.nn, N = g.N, E = g.E;
+    LapTimer lap;
     r.owner = rcb_partition(g, nranks);
+    lap("rcb partition");
     // sharers of each node: bitmask of ranks touching it (nranks <= 64)
     if (nranks > 64) throw Error(TVEGPU_E_ARG, "at most 64 ranks");
     std::vector<uint64_t> touch(N, 0);
@@ -353,12 +348,16 @@ RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nrank
         std::vector<uint64_t> key(E);
         const double mscale = morton_scale(g);
         auto sort_group = [&](std::vector<int32_t>& v) {
-            for (int32_t e : v) key[e] = morton_key(&g.centroid[(size_t)3 * e], g.lo, mscale);
-            std::sort(v.begin(), v.end(), [&](int32_t x, int32_t y) { return key[x] < key[y] || (key[x] == key[y] && x < y); });
+#pragma omp parallel for schedule(static)
+            for (size_t q = 0; q < v.size(); ++q) key[v[q]] = morton_key(&g.centroid[(size_t)3 * v[q]], g.lo, mscale);
+            // a total order (ties broken by id): the parallel sort's result is unique
+            __gnu_parallel::sort(v.begin(), v.end(),
+                                 [&](int32_t x, int32_t y) { return key[x] < key[y] || (key[x] == key[y] && x < y); });
         };
         sort_group(bnd);
         sort_group(inr);
     }
+    lap("boundary split + morton sort");
     r.Eb = (int)bnd.size();
     r.elem_orig = bnd;
     r.elem_orig.insert(r.elem_orig.end(), inr.begin(), inr.end());
@@ -382,10 +381,12 @@ RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nrank
     r.N = (int)r.node_orig.size();
     r.conn.resize((size_t)r.E * nn);
     std::vector<int32_t> elem_local(E, -1);
+#pragma omp parallel for schedule(static)
     for (int le = 0; le < r.E; ++le) {
         elem_local[r.elem_orig[le]] = le;
         for (int a = 0; a < nn; ++a) r.conn[(size_t)le * nn + a] = local[p.elements[(size_t)r.elem_orig[le] * nn + a]];
     }
+    lap("node numbering + conn");
     // neighbours and halo lists: for each neighbour s, the (orig e, a) contributions of
     // elements owned by the SENDER to nodes shared with the receiver, canonical order.
     std::vector<std::vector<int32_t>> send(nranks), recv_keys(nranks);  // recv: global adjacency index k
@@ -435,6 +436,7 @@ RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nrank
         r.recv_off.push_back(r.recv_off.back() + (int32_t)recv_keys[s].size());
     }
     std::sort(recv_index.begin(), recv_index.end());
+    lap("halo lists");
     // CSR per local node in canonical order: local slots and receive slots interleaved
     r.csr_off.assign(r.N + 1, 0);
     for (int li = 0; li < r.N; ++li) {
@@ -443,6 +445,8 @@ RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nrank
     }
     r.csr_slot.resize(r.csr_off[r.N]);
     const int32_t base = r.E * nn;
+    int halo_miss = 0;
+#pragma omp parallel for schedule(static) reduction(| : halo_miss)
     for (int li = 0; li < r.N; ++li) {
         const int i = r.node_orig[li];
         int32_t pos = r.csr_off[li];
@@ -453,21 +457,34 @@ RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nrank
             } else {
                 const int64_t key = (int64_t)e * nn + a;
                 auto it = std::lower_bound(recv_index.begin(), recv_index.end(), std::make_pair(key, (int32_t)-1));
-                if (it == recv_index.end() || it->first != key) throw Error(TVEGPU_E_ARG, "internal: halo map");
-                r.csr_slot[pos++] = base + it->second;
+                if (it == recv_index.end() || it->first != key) {
+                    halo_miss = 1;
+                    r.csr_slot[pos++] = 0;
+                } else {
+                    r.csr_slot[pos++] = base + it->second;
+                }
             }
         }
     }
+    if (halo_miss) throw Error(TVEGPU_E_ARG, "internal: halo map");
+    lap("gather CSR");
     // every element contribution and every received one is gathered exactly once
     {
-        std::vector<char> placed(base + (r.recv_off.empty() ? 0 : r.recv_off.back()), 0);
-        for (int32_t sl : r.csr_slot) {
-            if (placed[sl]) throw Error(TVEGPU_E_ARG, "internal: contribution gathered twice");
-            placed[sl] = 1;
+        const size_t ns = base + (r.recv_off.empty() ? 0 : r.recv_off.back());
+        std::vector<uint8_t> placed(ns, 0);
+        int twice = 0, unplaced = 0;
+        const size_t nc = r.csr_slot.size();
+#pragma omp parallel for schedule(static) reduction(| : twice)
+        for (size_t k = 0; k < nc; ++k) {
+            const int32_t sl = r.csr_slot[k];
+            if (sl < 0 || (size_t)sl >= ns || __atomic_fetch_add(&placed[sl], 1, __ATOMIC_RELAXED) != 0) twice = 1;
         }
-        for (char v : placed)
-            if (!v) throw Error(TVEGPU_E_ARG, "internal: unplaced contribution");
+#pragma omp parallel for schedule(static) reduction(| : unplaced)
+        for (size_t k = 0; k < ns; ++k) unplaced |= placed[k] == 0;
+        if (twice) throw Error(TVEGPU_E_ARG, "internal: contribution gathered twice");
+        if (unplaced) throw Error(TVEGPU_E_ARG, "internal: unplaced contribution");
     }
+    lap("exactly-once check");
     build_chunks(r);
     return r;
 }
@@ -583,6 +600,7 @@ static std::vector<int32_t> colour_slots(const std::vector<int32_t>& nodes, cons
 
 void build_chunks(RankPlan& r) {
     StageTimer tm("build_chunks");
+    LapTimer lap;
     const int nn = r.nn;
     r.chunk_start.clear();
     r.chunk_node_off.assign(1, 0);
@@ -618,6 +636,7 @@ void build_chunks(RankPlan& r) {
         cnodes[c] = std::move(nodes);
         cslot[c] = std::move(slot_of);
     }
+    lap("unique nodes + colouring");
     // staging walks each chunk's nodes in ascending id (coalesced loads), storing each to its slot
     for (int c = 0; c < nc; ++c) {
         r.chunk_start.push_back(starts[c]);

@@ -11,6 +11,10 @@
 // bit-identical node constants.
 #pragma once
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -19,6 +23,32 @@
 #include "../../include/tvegpu.h"
 
 namespace tvegpu {
+
+// Setup-stage timing to stderr when TVEGPU_TIMING is set.
+struct StageTimer {
+    const char* name;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    explicit StageTimer(const char* n) : name(n) {}
+    ~StageTimer() {
+        static const bool on = std::getenv("TVEGPU_TIMING") != nullptr;
+        if (on)
+            std::fprintf(stderr, "[tvegpu setup] %-28s %8.1f ms\n", name,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
+
+// Lap timer inside one stage: lap("name") reports the time since the previous lap.
+struct LapTimer {
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void operator()(const char* name) {
+        static const bool on = std::getenv("TVEGPU_TIMING") != nullptr;
+        const auto now = std::chrono::steady_clock::now();
+        if (on)
+            std::fprintf(stderr, "[tvegpu setup]   %-26s %8.1f ms\n", name,
+                         std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
 
 struct Error : std::runtime_error {
     Error(tvegpu_status s, const std::string& m) : std::runtime_error(m), status(s) {}

@@ -13,6 +13,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 import subprocess
+import sys
+import time
 
 import numpy as np
 
@@ -20,6 +22,7 @@ from .problem import H8, Problem
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # TVEGPU_LIB selects an experimental build variant (csrc/Makefile `variant` target).
+_TIMING = bool(os.environ.get("TVEGPU_TIMING"))
 _LIBPATH = os.environ.get("TVEGPU_LIB") or os.path.join(_HERE, "lib", "libtvegpu.so")
 _LIB = None
 _dp = C.POINTER(C.c_double)
@@ -319,7 +322,11 @@ class Engine:
                  steps_per_graph: int = 64):
         L = lib()
         self.problem = problem
+        t0 = time.perf_counter()
         self._c, self._keep = problem.to_c()
+        if _TIMING:
+            print(f"[tvegpu setup] {'python problem -> C structs':28s} {1e3 * (time.perf_counter() - t0):8.1f} ms",
+                  file=sys.stderr)
         o = COptions()
         L.tvegpu_default_options(C.byref(o))
         o.device, o.nranks, o.rank = device, nranks, rank
@@ -328,9 +335,13 @@ class Engine:
         o.reorder, o.diagnostics, o.steps_per_graph = int(reorder), int(diagnostics), steps_per_graph
         self._opt = o
         h = C.c_void_p()
+        t0 = time.perf_counter()
         rc = L.tvegpu_create(C.byref(self._c), C.byref(o), C.byref(h))
         if rc:
             raise _BY_STATUS.get(rc, TveError)(L.tvegpu_create_error().decode())
+        if _TIMING:
+            print(f"[tvegpu setup] {'tvegpu_create (total)':28s} {1e3 * (time.perf_counter() - t0):8.1f} ms",
+                  file=sys.stderr)
         self._h = h
         self.N, self.E, self.P = problem.num_nodes, problem.num_elements, problem.prony_count
 
