@@ -630,8 +630,9 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
         h->ptr.vnode = dupload(own, vn, s);
         CU(cudaStreamSynchronize(s));
     }
-#if TVEGPU_GEO
-    {  // per-element reference geometry, once (k_geometry, same arithmetic as the in-kernel path)
+    {  // per-element reference geometry, once (k_geometry, same arithmetic as the in-kernel path);
+       // built in every variant: the step kernels read it with TVEGPU_GEO, the run-level
+       // energy reduction always
         if (!h->d_conn) {
             h->d_conn = dalloc<int32_t>(own, pl.conn.size());
             CU(cudaMemcpyAsync(h->d_conn, pl.conn.data(), pl.conn.size() * 4, cudaMemcpyHostToDevice, s));
@@ -644,7 +645,6 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
         }
         h->ptr.geo = geo;
     }
-#endif
     h->ptr.node_orig = dupload(own, pl.node_orig, s);
     CU(cudaMallocHost(&h->qr_host, std::max(1, N) * sizeof(double)));
     std::memset(h->qr_host, 0, std::max(1, N) * sizeof(double));
