@@ -153,8 +153,9 @@ def test_restart_bit_exact():
     assert a.time() == c.time() and c.step_count() == 40
 
 
-def test_diagnostics_match_oracle():
-    p = configs.small_problem(kind=H8, n=3, steps=10)
+@pytest.mark.parametrize("kind", [T4, H8])  # T4: the two-threads-per-node K4 writes f_int
+def test_diagnostics_match_oracle(kind):
+    p = configs.small_problem(kind=kind, n=3, steps=10)
     g = tg.Engine(p, diagnostics=True)
     o = O.OracleEngine(p)
     g.step(10)
