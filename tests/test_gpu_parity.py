@@ -178,10 +178,11 @@ def test_nodal_source_override():
     assert inc_err(g.temperatures(), o.state()["T"], 37.0) <= TOL
 
 
-def test_instability_matches_oracle():
+@pytest.mark.parametrize("kind", [T4, H8])
+def test_instability_matches_oracle(kind):
     """A non-finite temperature injected at one node: both engines raise InstabilityError
     at the same step naming the same (lowest) node, and leave the same state behind."""
-    p = configs.small_problem(kind=H8, n=4, steps=30)
+    p = configs.small_problem(kind=kind, n=4, steps=30)
     p.expansion_enabled = False  # else the NaN reaches F_ther and both report a non-SPD C element error
     g = tg.Engine(p)
     o = O.OracleEngine(p)
