@@ -215,16 +215,25 @@ public:
     }
     // bioheat.hpp:57 nodal source override (power per node [W]); empty restores regions
     void set_nodal_sources(const std::vector<double>& power) {
+        check_power(power);
         check(tvegpu_set_nodal_sources(h_, power.empty() ? nullptr : power.data()));
     }
     // Closed-loop iteration: sources + n steps + T/u read-back, copies overlapped with
     // the step (tvegpu_step_io); empty power keeps the current sources.
     void step_io(const std::vector<double>& power, int64_t n, std::vector<double>& T, std::vector<double>& u) {
+        check_power(power);
         push_if_dirty();
         T.resize(N_);
         u.resize(3 * (size_t)N_);
         check(tvegpu_step_io(h_, power.empty() ? nullptr : power.data(), n, T.data(), u.data()));
         mirror_valid_ = false;
+    }
+
+    // a power vector is one value per node (the C side reads num_nodes doubles)
+    void check_power(const std::vector<double>& power) const {
+        if (!power.empty() && power.size() != (size_t)N_)
+            throw std::invalid_argument("nodal source power needs one value per node (" + std::to_string(N_) +
+                                        "), got " + std::to_string(power.size()));
     }
 
     // engine.hpp:57-66 RunSummary extrema and SPEC.md:435-443 ablation volume, on the device

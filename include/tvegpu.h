@@ -77,7 +77,8 @@ typedef struct tvegpu_source {
  * (materials.hpp:89-97), MechBCs (mechanics.hpp:37-47, without the host
  * std::function motion_override), ThermalBCs (bioheat.hpp:32-35),
  * HeatSourceSet (bioheat.hpp:28-30) and SimulationConfig (engine.hpp:28-39,
- * without the OutputSpec, which is run-level).
+ * without the OutputSpec, which is run-level).  motion_override is set after
+ * creation with tvegpu_set_motion_override.
  */
 typedef struct tvegpu_problem {
     /* ---- Mesh (mesh.hpp:22-37) ---- */
@@ -204,6 +205,18 @@ tvegpu_status tvegpu_set_state(tvegpu_engine* h, const double* T, const double* 
  * NULL restores the regional HeatSourceSet schedule. */
 tvegpu_status tvegpu_set_nodal_sources(tvegpu_engine* h, const double* power);
 
+/* MechBCs::motion_override (mechanics.hpp:43-46): an optional per-node displacement
+ * trajectory.  fn(user, node, t, disp) returns nonzero and fills disp[3] to pin the
+ * (original) node to disp at time t; it is applied last, after fixed and prescribed
+ * components (mechanics.hpp:89, SPEC.md C9), at t = time + dt of each step.  A host
+ * callback cannot run inside a device step, so this is a slow path: while set, every
+ * step evaluates fn on the host for the candidate nodes (nodes[num_nodes], original
+ * ids; NULL = every node), uploads the pins and launches the step without graph
+ * replay.  fn = NULL removes the override. */
+typedef int32_t (*tvegpu_motion_fn)(void* user, int32_t node, double t, double* disp);
+tvegpu_status tvegpu_set_motion_override(tvegpu_engine* h, tvegpu_motion_fn fn, void* user, int32_t num_nodes,
+                                         const int32_t* nodes);
+
 /* One closed-loop iteration with host buffers: the effect of
  *   tvegpu_set_nodal_sources(h, power) (skipped when power is NULL);
  *   tvegpu_step(h, n);  tvegpu_make_snapshot(h, T, disp)  (skipped when both are NULL)
@@ -216,9 +229,11 @@ tvegpu_status tvegpu_step_io(tvegpu_engine* h, const double* power, int64_t n, d
 /* ---- checkpoint / restart (engine.hpp:110-111) ----
  * A versioned binary image of the state in original numbering (layout in
  * DESIGN.md): T, u, u_prev, viscous history, time, step and an active nodal-source
- * override.  Restores bit-exactly, into an engine with any partitioning; saving
- * needs a single-partition engine.  Errors: E_ARG (buffer too small), E_IO
- * (bad magic / version / problem mismatch / truncated). */
+ * override.  Restores bit-exactly, into an engine with any partitioning.  Saving
+ * from a partitioned engine (nranks > 1) is collective: every rank calls it, the
+ * ranks' nodes and elements are gathered over NCCL and every rank receives the same
+ * image.  Errors: E_ARG (buffer too small), E_IO (bad magic / version / problem
+ * mismatch / truncated). */
 tvegpu_status tvegpu_checkpoint_size(tvegpu_engine* h, uint64_t* bytes);
 tvegpu_status tvegpu_save_checkpoint(tvegpu_engine* h, void* buf, uint64_t bytes);
 tvegpu_status tvegpu_load_checkpoint(tvegpu_engine* h, const void* buf, uint64_t bytes);
@@ -348,18 +363,33 @@ void tvegpu_plan_destroy(tvegpu_plan* plan);
 tvegpu_status tvegpu_nccl_unique_id(void* out128);
 
 /* ---------------------------------------------------------------------------
- * Virtual multi-partition group: nparts RCB partitions of one problem driven in
- * lockstep on ONE device, the halo exchanged by device copies instead of NCCL.
- * Runs the multi-GPU data path (partition maps, boundary-first elements, halo
- * pack, receive-area gathers) where only one GPU exists; results are
- * bit-identical to a single partition.  get_fields writes every partition's
- * nodes (shared nodes hold identical values) in original numbering.
+ * Partition group: nparts RCB partitions of one problem stepped together on ONE
+ * device by the multi-GPU step code (boundary-first elements, halo pack, exchange
+ * on a comm stream ordered by events, interior elements, receive-area gathers,
+ * CUDA-graph replay, agreement on the first failure, device state gather for
+ * checkpoints); the transport is a device copy of each neighbour's packed segment
+ * instead of ncclSend/ncclRecv.  Results are bit-identical to a single partition.
+ * The calls mirror the engine's (tvegpu_step, tvegpu_set_state, ...).  After a
+ * failure every partition reports the same (step, node); the state is then invalid
+ * (the other partitions ran on) until set_state / load_checkpoint — the same rule as
+ * for NCCL ranks (nranks > 1 engines).
  * ------------------------------------------------------------------------- */
 typedef struct tvegpu_group tvegpu_group;
 tvegpu_status tvegpu_group_create(const tvegpu_problem* problem, int32_t nparts, const tvegpu_options* options,
                                   tvegpu_group** out);
 tvegpu_status tvegpu_group_step(tvegpu_group* g, int64_t nsteps);
 tvegpu_status tvegpu_group_get_fields(tvegpu_group* g, double* T, double* disp, double* viscous);
+tvegpu_status tvegpu_group_get_state(tvegpu_group* g, double* T, double* disp, double* disp_prev, double* viscous);
+tvegpu_status tvegpu_group_set_state(tvegpu_group* g, const double* T, const double* disp, const double* disp_prev,
+                                     const double* viscous, double time, int64_t step);
+tvegpu_status tvegpu_group_set_nodal_sources(tvegpu_group* g, const double* power);
+tvegpu_status tvegpu_group_step_io(tvegpu_group* g, const double* power, int64_t n, double* T, double* disp);
+double tvegpu_group_time(const tvegpu_group* g);
+int64_t tvegpu_group_step_count(const tvegpu_group* g);
+tvegpu_status tvegpu_group_last_error(const tvegpu_group* g, char* msg, size_t cap, int64_t* step, int32_t* node);
+tvegpu_status tvegpu_group_checkpoint_size(tvegpu_group* g, uint64_t* bytes);
+tvegpu_status tvegpu_group_save_checkpoint(tvegpu_group* g, void* buf, uint64_t bytes);
+tvegpu_status tvegpu_group_load_checkpoint(tvegpu_group* g, const void* buf, uint64_t bytes);
 void tvegpu_group_destroy(tvegpu_group* g);
 
 /* ---------------------------------------------------------------------------

@@ -33,6 +33,8 @@ def lib():
         L.oracle_error.restype = C.c_char_p
         L.oracle_create.restype = C.c_void_p
         L.oracle_create.argtypes = [C.c_void_p]
+        L.oracle_create_motion.restype = C.c_void_p
+        L.oracle_create_motion.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.oracle_destroy.argtypes = [C.c_void_p]
         L.oracle_step.argtypes = [C.c_void_p, C.c_long, C.POINTER(C.c_long), C.POINTER(C.c_int)]
         L.oracle_get_state.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp]
@@ -97,12 +99,24 @@ class OracleError(RuntimeError):
 class OracleEngine:
     """tve::Engine restated on the CPU (engine.hpp:83-143)."""
 
-    def __init__(self, problem, workers=0):
+    def __init__(self, problem, workers=0, motion_override=None):
+        """motion_override: fn(node, t) -> None or (dx, dy, dz) (MechBCs::motion_override,
+        mechanics.hpp:43-46), evaluated for every node at t + dt of each step."""
         self.problem = problem
         self._c, self._keep = problem.to_c()
         self._c.workers = workers
         L = lib()
-        self._h = L.oracle_create(C.byref(self._c))
+        if motion_override is not None:
+            def cb(_user, node, t, out):
+                v = motion_override(int(node), float(t))
+                if v is None:
+                    return 0
+                out[0], out[1], out[2] = float(v[0]), float(v[1]), float(v[2])
+                return 1
+            self._motion = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_double, _dp)(cb)
+            self._h = L.oracle_create_motion(C.byref(self._c), C.cast(self._motion, C.c_void_p), None)
+        else:
+            self._h = L.oracle_create(C.byref(self._c))
         if not self._h:
             raise OracleError(2, L.oracle_error().decode())
         self.N, self.E, self.P = problem.num_nodes, problem.num_elements, problem.prony_count

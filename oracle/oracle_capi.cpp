@@ -156,6 +156,25 @@ void* oracle_create(const tvegpu_problem* p) {
     if (rc) return nullptr;
     return b.release();
 }
+// The same with MechBCs::motion_override (mechanics.hpp:43-46) bound to a C callback:
+// fn(user, node, t, disp) returns nonzero and fills disp[3] to pin the node at time t.
+typedef int (*oracle_motion_fn)(void* user, int node, double t, double* disp);
+void* oracle_create_motion(const tvegpu_problem* p, oracle_motion_fn fn, void* user) {
+    auto b = std::make_unique<Bundle>();
+    int rc = guarded([&] {
+        build(*p, *b);
+        if (fn)
+            b->mbc.motion_override = [fn, user](int n, double t) -> std::optional<Vec3> {
+                double d[3];
+                if (!fn(user, n, t, d)) return std::nullopt;
+                return Vec3{d[0], d[1], d[2]};
+            };
+        b->pre = precompute(b->mesh, p->density, p->ref_specific_heat);
+        b->eng = std::make_unique<Engine>(b->mesh, b->pre, b->mat, b->mbc, b->tbc, b->src, b->cfg);
+    });
+    if (rc) return nullptr;
+    return b.release();
+}
 void oracle_destroy(void* h) { delete static_cast<Bundle*>(h); }
 
 int oracle_step(void* h, long n, long* err_step, int* err_node) {

@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <string>
@@ -112,6 +113,39 @@ namespace tvegpu {
 void set_create_error(const std::string& m) { g_create_error = m; }
 }  // namespace tvegpu
 
+namespace {
+// Halo transport between the partitions of one step.  The step code
+// (enqueue_partitioned_step) is the same for every transport: boundary elements,
+// pack + ev_pack on the compute stream, exchange() on the comm streams ending in
+// ev_comm, interior elements, node kernel after ev_comm.
+//   NcclTransport      one partition per process and GPU: grouped ncclSend/ncclRecv.
+//   LoopbackTransport  all partitions in this process on one device (tvegpu_group):
+//                      device copies of each neighbour's packed segment, ordered by
+//                      the same events — so only the two NCCL calls differ.
+struct Transport {
+    virtual ~Transport() = default;
+    // Called once every part has packed its send segment of this phase and recorded
+    // ev_pack on its compute stream; fills each part's receive area on its comm stream
+    // and records ev_comm there.
+    virtual void exchange(const std::vector<tvegpu_engine*>& parts, bool mech) = 0;
+    // In-place element-wise all-reduce (max or min) of n unsigned 64-bit words,
+    // buf[k] on parts[k], ordered after each part's compute stream; on return the
+    // result is enqueued on (and complete before later work of) every compute stream.
+    virtual void allreduce_u64(const std::vector<tvegpu_engine*>& parts, const std::vector<unsigned long long*>& buf,
+                               size_t n, bool max) = 0;
+};
+
+// The partitions one process steps together, and their CUDA-graph cache: a single
+// engine is a one-part set; tvegpu_group holds all partitions of a mesh.
+struct Stepper {
+    std::vector<tvegpu_engine*> parts;
+    std::map<std::pair<int, int>, cudaGraphExec_t> graphs;  // (parity, nsteps)
+    int steps_per_graph = 64;
+    bool warmed = false;  // a plain (un-captured) step has run
+    cudaEvent_t ev_fork = nullptr;  // multi-part sets: origin stream -> part streams
+};
+}  // namespace
+
 struct tvegpu_engine {
     int device = 0, nn = 4, kind = 0, mode = 0, N_global = 0, E_global = 0, P = 0;
     double dt = 0;
@@ -134,15 +168,13 @@ struct tvegpu_engine {
     double* qr_host = nullptr;  // pinned staging of the nodal source vector (local order)
     // multi-GPU
     ncclComm_t comm = nullptr;
+    Transport* tx = nullptr;                // halo transport (nranks > 1): own NCCL one or the group's loopback
+    std::unique_ptr<Transport> own_tx;
     double* send_th = nullptr;
     double* send_m = nullptr;
-    double* recv_th = nullptr;
-    double* recv_m = nullptr;
     const int32_t* d_send_slot = nullptr;  // element-major slot ids of the send lists
-    // graphs keyed by (parity, nsteps)
-    std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
-    int steps_per_graph = 64;
-    bool warmed = false;  // a plain (un-captured) step has run
+    cudaEvent_t ev_join = nullptr;          // multi-part sets: part stream -> origin stream
+    Stepper solo;                           // this engine as a one-part step set (graph cache)
     bool pdl = false;     // programmatic dependent launch of the step kernels (single partition)
     bool pair = false;    // node kernels with two threads per node (long CSR gather lists: T4)
     // errors
@@ -150,9 +182,15 @@ struct tvegpu_engine {
     long long err_step = -1;
     int err_node = -1;
     tvegpu_status last_status = TVEGPU_OK;
+    // a failure in a partitioned step leaves the partitions at different steps (the
+    // failing one halts, the others ran on with stale halo values): the state is
+    // unusable until set_state / load_checkpoint (every partition reports the same error)
+    bool state_invalid = false;
     bool pending = false;  // steps enqueued whose finite check has not been read back
     long long pend_step = 0;
     int pend_cur = 0;
+    double pend_time = 0;
+    cudaEvent_t ev_entry = nullptr;  // tvegpu_step_io: work already on s before the side-stream upload
     unsigned long long* h_words = nullptr;  // pinned: clock (3 words) + err_inst + err_elem
     double4* stage = nullptr;               // pinned readback staging (N records)
     double* d_io = nullptr;                 // device I/O buffer in original numbering (4N doubles)
@@ -160,6 +198,14 @@ struct tvegpu_engine {
     double* d_part = nullptr;               // per-block partials of the run-level reductions
     double* h_part = nullptr;               // pinned: reduced run-level outputs
     double* d_ef = nullptr;                 // element fields in original order (2E, lazily)
+    const uint8_t* d_owned = nullptr;       // plan.node_owned on the device (state gathers, lazily)
+    // MechBCs::motion_override (mechanics.hpp:43-46): a host callback, so a slow path —
+    // per step the host evaluates it at t + dt for the candidate nodes into pinned
+    // memory, uploads it and K4 applies the pins last (no graph replay while active)
+    tvegpu_motion_fn motion_fn = nullptr;
+    void* motion_user = nullptr;
+    std::vector<int32_t> motion_orig;       // candidate rows: original node ids
+    double4* motion_host = nullptr;         // pinned [rows]
 };
 
 namespace {
@@ -208,30 +254,101 @@ bool sources_stable(tvegpu_engine* h, double t) {
     return true;
 }
 
-// Halo exchange of interface contributions: pack the boundary
-// elements' contributions on the compute stream, then on the comm stream one
-// grouped ncclSend/ncclRecv per neighbour straight into the receive area that
-// follows the local slots (the gather lists index it).  The node kernel waits on
-// ev_comm; the interior elements run meanwhile.
-void exchange(tvegpu_engine* h, double* slots, double* sendbuf, double* /*recvbuf*/, int width) {
-    const RankPlan& pl = h->plan;
-    const int ns = pl.send_off.back();
-    double* recvbuf = slots + (size_t)pl.E * pl.nn * width;
-    if (ns > 0) k_pack<<<blocks(ns, 256), 256, 0, h->s>>>(slots, h->d_send_slot, ns, width, sendbuf);
+// ---------------------------------------------------------------- halo transports
+// Halo exchange of interface contributions: each part packs its
+// boundary elements' contributions (k_pack) on the compute stream and records
+// ev_pack; the transport delivers every part's receive area (appended to its slot
+// buffer; the gather lists index it) on the comm stream and records ev_comm; the
+// interior elements run meanwhile and the node kernel waits on ev_comm.
+void pack_halo(tvegpu_engine* h, bool mech) {
+    const int ns = h->plan.send_off.back();
+    if (ns > 0)
+        k_pack<<<blocks(ns, 256), 256, 0, h->s>>>(mech ? h->ptr.slot_m : h->ptr.slot_th, h->d_send_slot, ns,
+                                                  mech ? kMW : 1, mech ? h->send_m : h->send_th);
     CU(cudaEventRecord(h->ev_pack, h->s));
-    CU(cudaStreamWaitEvent(h->sc, h->ev_pack, 0));
-    auto& api = nccl();
-    NC(api.GroupStart());
-    for (size_t j = 0; j < pl.neighbors.size(); ++j) {
-        const int peer = pl.neighbors[j];
-        const size_t so = pl.send_off[j], sn = pl.send_off[j + 1] - so;
-        const size_t ro = pl.recv_off[j], rn = pl.recv_off[j + 1] - ro;
-        if (sn) NC(api.Send(sendbuf + so * width, sn * width, ncclFloat64, peer, h->comm, h->sc));
-        if (rn) NC(api.Recv(recvbuf + ro * width, rn * width, ncclFloat64, peer, h->comm, h->sc));
-    }
-    NC(api.GroupEnd());
-    CU(cudaEventRecord(h->ev_comm, h->sc));
 }
+
+double* recv_area(tvegpu_engine* h, bool mech) {
+    const int width = mech ? kMW : 1;
+    return (mech ? h->ptr.slot_m : h->ptr.slot_th) + (size_t)h->plan.E * h->plan.nn * width;
+}
+
+struct NcclTransport final : Transport {
+    ncclComm_t comm = nullptr;
+    void exchange(const std::vector<tvegpu_engine*>& parts, bool mech) override {
+        tvegpu_engine* h = parts[0];  // one partition per process and GPU
+        const RankPlan& pl = h->plan;
+        const int width = mech ? kMW : 1;
+        const double* sendbuf = mech ? h->send_m : h->send_th;
+        double* recvbuf = recv_area(h, mech);
+        CU(cudaStreamWaitEvent(h->sc, h->ev_pack, 0));
+        auto& api = nccl();
+        NC(api.GroupStart());
+        for (size_t j = 0; j < pl.neighbors.size(); ++j) {
+            const int peer = pl.neighbors[j];
+            const size_t so = pl.send_off[j], sn = pl.send_off[j + 1] - so;
+            const size_t ro = pl.recv_off[j], rn = pl.recv_off[j + 1] - ro;
+            if (sn) NC(api.Send(sendbuf + so * width, sn * width, ncclFloat64, peer, comm, h->sc));
+            if (rn) NC(api.Recv(recvbuf + ro * width, rn * width, ncclFloat64, peer, comm, h->sc));
+        }
+        NC(api.GroupEnd());
+        CU(cudaEventRecord(h->ev_comm, h->sc));
+    }
+    void allreduce_u64(const std::vector<tvegpu_engine*>& parts, const std::vector<unsigned long long*>& buf, size_t n,
+                       bool max) override {
+        tvegpu_engine* h = parts[0];
+        NC(nccl().AllReduce(buf[0], buf[0], n, ncclUint64, max ? ncclMax : ncclMin, comm, h->s));
+    }
+};
+
+__global__ void k_combine_u64(unsigned long long* __restrict__ acc, const unsigned long long* __restrict__ v, size_t n,
+                              int max) {
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x)
+        acc[k] = max ? (acc[k] > v[k] ? acc[k] : v[k]) : (acc[k] < v[k] ? acc[k] : v[k]);
+}
+
+struct LoopbackTransport final : Transport {
+    void exchange(const std::vector<tvegpu_engine*>& parts, bool mech) override {
+        const int width = mech ? kMW : 1;
+        for (tvegpu_engine* r : parts) {
+            const RankPlan& pr = r->plan;
+            // the receive area is rewritten only after this part's node kernel of the
+            // previous step read it (ordered before r's own ev_pack)
+            CU(cudaStreamWaitEvent(r->sc, r->ev_pack, 0));
+            double* dst0 = recv_area(r, mech);
+            for (size_t j = 0; j < pr.neighbors.size(); ++j) {
+                const tvegpu_engine* q = parts.at(pr.neighbors[j]);
+                const RankPlan& ps = q->plan;
+                const size_t jj = std::find(ps.neighbors.begin(), ps.neighbors.end(), pr.rank) - ps.neighbors.begin();
+                if (jj == ps.neighbors.size()) throw Error(TVEGPU_E_ARG, "internal: asymmetric halo");
+                const size_t n = (size_t)(ps.send_off[jj + 1] - ps.send_off[jj]);
+                if (n != (size_t)(pr.recv_off[j + 1] - pr.recv_off[j])) throw Error(TVEGPU_E_ARG, "internal: halo size");
+                if (!n) continue;
+                CU(cudaStreamWaitEvent(r->sc, q->ev_pack, 0));  // the neighbour's packed segment (ncclRecv)
+                const double* src = (mech ? q->send_m : q->send_th) + (size_t)ps.send_off[jj] * width;
+                CU(cudaMemcpyAsync(dst0 + (size_t)pr.recv_off[j] * width, src, n * width * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, r->sc));
+            }
+            CU(cudaEventRecord(r->ev_comm, r->sc));
+        }
+    }
+    void allreduce_u64(const std::vector<tvegpu_engine*>& parts, const std::vector<unsigned long long*>& buf, size_t n,
+                       bool max) override {
+        tvegpu_engine* h0 = parts[0];
+        for (size_t k = 1; k < parts.size(); ++k) {
+            CU(cudaEventRecord(parts[k]->ev_join, parts[k]->s));
+            CU(cudaStreamWaitEvent(h0->s, parts[k]->ev_join, 0));
+        }
+        const int nb = (int)std::min<size_t>(1184, (n + 255) / 256);
+        for (size_t k = 1; k < parts.size() && n; ++k)
+            k_combine_u64<<<nb, 256, 0, h0->s>>>(buf[0], buf[k], n, max ? 1 : 0);
+        for (size_t k = 1; k < parts.size() && n; ++k)
+            CU(cudaMemcpyAsync(buf[k], buf[0], n * 8, cudaMemcpyDeviceToDevice, h0->s));
+        CU(cudaGetLastError());
+        CU(cudaEventRecord(h0->ev_join, h0->s));
+        for (size_t k = 1; k < parts.size(); ++k) CU(cudaStreamWaitEvent(parts[k]->s, h0->ev_join, 0));
+    }
+};
 
 // staged planes: (ux,uy), (uz,T) [+ (x,y), (z,-) without precomputed geometry]
 size_t chunk_smem(const tvegpu_engine* h) {
@@ -275,8 +392,27 @@ void launch_mech_element(tvegpu_engine* h, int c0, int c1) {
 template <int NN>
 void launch_thermal_element(tvegpu_engine* h, int c0, int c1) {
     if (c1 <= c0) return;
-
     launch_step_kernel(h, k_thermal_element<NN>, c1 - c0, kChunkThreads, chunk_smem(h), h->prm, h->ptr, h->cur, c0, c1);
+}
+void launch_thermal_elements(tvegpu_engine* h, int c0, int c1) {
+    h->nn == 4 ? launch_thermal_element<4>(h, c0, c1) : launch_thermal_element<8>(h, c0, c1);
+}
+void launch_mech_elements(tvegpu_engine* h, int c0, int c1) {
+    h->nn == 4 ? launch_mech_element<4>(h, c0, c1) : launch_mech_element<8>(h, c0, c1);
+}
+void launch_thermal_node(tvegpu_engine* h, double* t_out) {
+    const int N = h->plan.N;
+    launch_step_kernel(h, thermal_node_kernel(h), blocks(h->pair ? 2 * N : N, kNodeThreads), kNodeThreads, 0, h->prm,
+                       h->ptr, h->cur, (int)(h->mode == TVEGPU_THERMAL_ONLY), t_out);
+}
+void launch_mech_node(tvegpu_engine* h, double* u_out) {
+    const int N = h->plan.N;
+    if (h->pair)
+        launch_step_kernel(h, k_mech_node<true>, blocks(2 * N, kNodeThreads), kNodeThreads, 0, h->prm, h->ptr, h->cur, 1,
+                           u_out);
+    else
+        launch_step_kernel(h, k_mech_node<false>, blocks(N, kNodeThreads), kNodeThreads, 0, h->prm, h->ptr, h->cur, 1,
+                           u_out);
 }
 
 void set_smem_limits(tvegpu_engine* h) {
@@ -293,55 +429,34 @@ void set_smem_limits(tvegpu_engine* h) {
     attr((const void*)k_mech_element<8, 2>);
 }
 
-// One Engine::step() (engine.hpp:70-82): K1 K2 [K3 K4], with the halo exchange of
-// boundary-element slots overlapped with the interior elements.
-// wait_src: event K2 waits on (sources uploaded on another stream); t_final:
-// event recorded once this step's temperatures are final (after K2).
-// t_out / u_out: original-numbering copies of the new T / u written by K2 / K4.
+// One Engine::step() (engine.hpp:70-82) of a single-partition engine: K1 K2 [K3 K4]
+// back to back on one stream (programmatic dependent launch between them).
+// evs: profiling events around each kernel; wait_src: event K2 waits on (sources
+// uploaded on another stream); t_final: event recorded once this step's temperatures
+// are final (after K2); t_out / u_out: original-numbering copies of the new T / u
+// written by K2 / K4.
 void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr, cudaEvent_t wait_src = nullptr,
                       cudaEvent_t t_final = nullptr, double* t_out = nullptr, double* u_out = nullptr) {
-    const int N = h->plan.N;
-    const int nc = (int)h->plan.chunk_start.size() - 1, ncb = h->plan.nchunks_boundary;
-    const bool multi = h->plan.nranks > 1;
+    const int nc = (int)h->plan.chunk_start.size() - 1;
     int ev = 0;
     auto mark = [&]() {
         if (evs) CU(cudaEventRecord(evs[ev++], h->s));
     };
     mark();
     if (h->mode != TVEGPU_MECHANICAL_ONLY) {
-        if (multi) {
-            h->nn == 4 ? launch_thermal_element<4>(h, 0, ncb) : launch_thermal_element<8>(h, 0, ncb);
-            exchange(h, h->ptr.slot_th, h->send_th, h->recv_th, 1);
-            h->nn == 4 ? launch_thermal_element<4>(h, ncb, nc) : launch_thermal_element<8>(h, ncb, nc);
-            CU(cudaStreamWaitEvent(h->s, h->ev_comm, 0));
-        } else {
-            h->nn == 4 ? launch_thermal_element<4>(h, 0, nc) : launch_thermal_element<8>(h, 0, nc);
-        }
+        launch_thermal_elements(h, 0, nc);
         mark();
         if (wait_src) CU(cudaStreamWaitEvent(h->s, wait_src, 0));
-        launch_step_kernel(h, thermal_node_kernel(h), blocks(h->pair ? 2 * N : N, kNodeThreads),
-                           kNodeThreads, 0, h->prm, h->ptr, h->cur, (int)(h->mode == TVEGPU_THERMAL_ONLY), t_out);
+        launch_thermal_node(h, t_out);
         mark();
     } else if (wait_src) {
         CU(cudaStreamWaitEvent(h->s, wait_src, 0));
     }
     if (t_final) CU(cudaEventRecord(t_final, h->s));
     if (h->mode != TVEGPU_THERMAL_ONLY) {
-        if (multi) {
-            h->nn == 4 ? launch_mech_element<4>(h, 0, ncb) : launch_mech_element<8>(h, 0, ncb);
-            exchange(h, h->ptr.slot_m, h->send_m, h->recv_m, kMW);
-            h->nn == 4 ? launch_mech_element<4>(h, ncb, nc) : launch_mech_element<8>(h, ncb, nc);
-            CU(cudaStreamWaitEvent(h->s, h->ev_comm, 0));
-        } else {
-            h->nn == 4 ? launch_mech_element<4>(h, 0, nc) : launch_mech_element<8>(h, 0, nc);
-        }
+        launch_mech_elements(h, 0, nc);
         mark();
-        if (h->pair)
-            launch_step_kernel(h, k_mech_node<true>, blocks(2 * N, kNodeThreads), kNodeThreads, 0, h->prm, h->ptr,
-                               h->cur, 1, u_out);
-        else
-            launch_step_kernel(h, k_mech_node<false>, blocks(N, kNodeThreads), kNodeThreads, 0, h->prm, h->ptr,
-                               h->cur, 1, u_out);
+        launch_mech_node(h, u_out);
         mark();
         h->cur ^= 1;
     }
@@ -349,62 +464,180 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr, cudaEvent_t 
     CU(cudaGetLastError());
 }
 
-cudaGraphExec_t get_graph(tvegpu_engine* h, int nsteps) {
-    auto key = std::make_pair(h->cur, nsteps);
-    auto it = h->graphs.find(key);
-    if (it != h->graphs.end()) return it->second;
-    const int cur0 = h->cur;
+// One step of a partitioned set (every part an RCB partition), phase by
+// phase over the parts so the transport sees every part's packed segment:
+//   boundary elements + pack (ev_pack) | exchange (ev_comm) | interior elements,
+//   wait ev_comm, node kernel.
+// The same code drives one NCCL rank (parts = {h}) and a loopback group.
+// evs (one-part sets only): profiling marks at the phase boundaries.
+void enqueue_partitioned_step(Stepper& S, cudaEvent_t* evs = nullptr) {
+    const std::vector<tvegpu_engine*>& parts = S.parts;
+    tvegpu_engine* h0 = parts[0];
+    int ev = 0;
+    auto mark = [&]() {
+        if (evs) CU(cudaEventRecord(evs[ev++], h0->s));
+    };
+    auto nchunks = [](const tvegpu_engine* h) { return (int)h->plan.chunk_start.size() - 1; };
+    mark();
+    if (h0->mode != TVEGPU_MECHANICAL_ONLY) {
+        for (tvegpu_engine* h : parts) {
+            launch_thermal_elements(h, 0, h->plan.nchunks_boundary);
+            pack_halo(h, false);
+        }
+        h0->tx->exchange(parts, false);
+        for (tvegpu_engine* h : parts) launch_thermal_elements(h, h->plan.nchunks_boundary, nchunks(h));
+        mark();
+        for (tvegpu_engine* h : parts) {
+            CU(cudaStreamWaitEvent(h->s, h->ev_comm, 0));
+            launch_thermal_node(h, nullptr);
+        }
+        mark();
+    }
+    if (h0->mode != TVEGPU_THERMAL_ONLY) {
+        for (tvegpu_engine* h : parts) {
+            launch_mech_elements(h, 0, h->plan.nchunks_boundary);
+            pack_halo(h, true);
+        }
+        h0->tx->exchange(parts, true);
+        for (tvegpu_engine* h : parts) launch_mech_elements(h, h->plan.nchunks_boundary, nchunks(h));
+        mark();
+        for (tvegpu_engine* h : parts) {
+            CU(cudaStreamWaitEvent(h->s, h->ev_comm, 0));
+            launch_mech_node(h, nullptr);
+            h->cur ^= 1;
+        }
+        mark();
+    }
+    CU(cudaGetLastError());
+}
+
+bool partitioned(const Stepper& S) { return S.parts.size() > 1 || S.parts[0]->plan.nranks > 1; }
+
+void enqueue_set_step(Stepper& S) {
+    if (partitioned(S)) enqueue_partitioned_step(S);
+    else enqueue_one_step(S.parts[0]);
+}
+
+// Multi-part sets: the parts' compute streams follow the origin stream (parts[0]->s)
+// after work enqueued on it (fork), and the origin follows every part (join).
+void fork_parts(Stepper& S) {
+    if (S.parts.size() < 2) return;
+    CU(cudaEventRecord(S.ev_fork, S.parts[0]->s));
+    for (size_t k = 1; k < S.parts.size(); ++k) CU(cudaStreamWaitEvent(S.parts[k]->s, S.ev_fork, 0));
+}
+void join_parts(Stepper& S) {
+    for (size_t k = 1; k < S.parts.size(); ++k) {
+        CU(cudaEventRecord(S.parts[k]->ev_join, S.parts[k]->s));
+        CU(cudaStreamWaitEvent(S.parts[0]->s, S.parts[k]->ev_join, 0));
+    }
+}
+
+cudaGraphExec_t get_graph(Stepper& S, int nsteps) {
+    auto key = std::make_pair(S.parts[0]->cur, nsteps);
+    auto it = S.graphs.find(key);
+    if (it != S.graphs.end()) return it->second;
+    std::vector<int> cur0;
+    for (tvegpu_engine* h : S.parts) cur0.push_back(h->cur);
+    auto restore = [&] {
+        for (size_t k = 0; k < S.parts.size(); ++k) S.parts[k]->cur = cur0[k];
+    };
+    cudaStream_t o = S.parts[0]->s;
     cudaGraph_t g;
-    CU(cudaStreamBeginCapture(h->s, cudaStreamCaptureModeThreadLocal));
+    CU(cudaStreamBeginCapture(o, cudaStreamCaptureModeThreadLocal));
     try {
-        for (int k = 0; k < nsteps; ++k) enqueue_one_step(h);
+        fork_parts(S);  // the other parts' streams join the capture
+        for (int k = 0; k < nsteps; ++k) enqueue_set_step(S);
+        join_parts(S);
     } catch (...) {
-        cudaStreamEndCapture(h->s, &g);
-        h->cur = cur0;
+        cudaStreamEndCapture(o, &g);
+        restore();
         throw;
     }
-    CU(cudaStreamEndCapture(h->s, &g));
-    h->cur = cur0;
+    CU(cudaStreamEndCapture(o, &g));
+    restore();
     cudaGraphExec_t ex;
     CU(cudaGraphInstantiate(&ex, g, 0));
     CU(cudaGraphDestroy(g));
-    h->graphs[key] = ex;
+    S.graphs[key] = ex;
     return ex;
 }
 
 bool flips(const tvegpu_engine* h) { return h->mode != TVEGPU_THERMAL_ONLY; }
 
-// Enqueue nsteps: graph chunks, split where the active-source mask changes.
-void enqueue_steps(tvegpu_engine* h, long long nsteps) {
-    if (h->halted) return;
+void begin_pending(tvegpu_engine* h) {
     if (!h->pending) {
         h->pending = true;
         h->pend_step = h->host_step;
         h->pend_cur = h->cur;
+        h->pend_time = h->host_time;
+    }
+}
+
+// motion_override slow path: the pins of the step starting at h->host_time
+// (value at t + dt, like the prescribed ramps, mechanics.hpp:89) for K4 to apply.
+void upload_motion(tvegpu_engine* h) {
+    const size_t rows = h->motion_orig.size();
+    if (!rows) return;
+    CU(cudaStreamSynchronize(h->s));  // the pinned rows of the previous step are uploaded
+    const double t = h->host_time + h->dt;
+    for (size_t r = 0; r < rows; ++r) {
+        double d[3] = {0.0, 0.0, 0.0};
+        const int pin = h->motion_fn(h->motion_user, h->motion_orig[r], t, d);
+        h->motion_host[r] = make_double4(d[0], d[1], d[2], pin ? 1.0 : 0.0);
+    }
+    CU(cudaMemcpyAsync(const_cast<double4*>(h->ptr.motion_val), h->motion_host, rows * sizeof(double4),
+                       cudaMemcpyHostToDevice, h->s));
+}
+
+// Enqueue nsteps: graph chunks, split where the active-source mask changes.
+void enqueue_steps(Stepper& S, long long nsteps) {
+    tvegpu_engine* h0 = S.parts[0];
+    if (h0->halted) return;
+    for (tvegpu_engine* h : S.parts) begin_pending(h);
+    if (h0->prm.motion) {  // host callback every step: plain launches
+        for (long long k = 0; k < nsteps; ++k) {
+            for (tvegpu_engine* h : S.parts) {
+                refresh_sources_if_needed(h, h->host_time);
+                upload_motion(h);
+            }
+            enqueue_set_step(S);
+            S.warmed = true;
+            for (tvegpu_engine* h : S.parts) {
+                h->host_time += h->dt;
+                h->host_step += 1;
+            }
+        }
+        return;
     }
     long long done = 0;
     while (done < nsteps) {
-        refresh_sources_if_needed(h, h->host_time);
-        // how many steps keep the same source mask?
+        for (tvegpu_engine* h : S.parts) refresh_sources_if_needed(h, h->host_time);
+        // how many steps keep the same source mask? (every part holds the same schedule)
         long long k = 0;
-        double t = h->host_time;
-        const long long cap = std::min<long long>(nsteps - done, h->steps_per_graph);
+        double t = h0->host_time;
+        const long long cap = std::min<long long>(nsteps - done, S.steps_per_graph);
         while (k < cap) {
-            if (k > 0 && !sources_stable(h, t)) break;
-            t += h->dt;
+            if (k > 0 && !sources_stable(h0, t)) break;
+            t += h0->dt;
             ++k;
         }
-        // Graph replays once the engine has run one plain step (NCCL sets up its
+        // Graph replays once the set has run one plain step (NCCL sets up its
         // peer connections lazily on first use, which must not happen in capture).
-        if (k == h->steps_per_graph && h->warmed) {
-            CU(cudaGraphLaunch(get_graph(h, (int)k), h->s));
-            if (flips(h) && (k & 1)) h->cur ^= 1;
+        if (k == S.steps_per_graph && S.warmed) {
+            cudaGraphExec_t ex = get_graph(S, (int)k);
+            join_parts(S);
+            CU(cudaGraphLaunch(ex, h0->s));
+            fork_parts(S);
+            if (flips(h0) && (k & 1))
+                for (tvegpu_engine* h : S.parts) h->cur ^= 1;
         } else {
-            for (long long j = 0; j < k; ++j) enqueue_one_step(h);
-            h->warmed = true;
+            for (long long j = 0; j < k; ++j) enqueue_set_step(S);
+            S.warmed = true;
         }
-        h->host_time = t;
-        h->host_step += k;
+        for (tvegpu_engine* h : S.parts) {
+            h->host_time = t;
+            h->host_step += k;
+        }
         done += k;
     }
 }
@@ -414,52 +647,95 @@ void enqueue_status_read(tvegpu_engine* h) {
     CU(cudaMemcpyAsync(h->h_words, h->ptr.clock, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->s));
 }
 
-// status_enqueued: the caller already enqueued enqueue_status_read after the last step.
-tvegpu_status sync_and_check(tvegpu_engine* h, long long step_at_start, int cur_at_start,
-                             bool status_enqueued = false) {
-    if (!status_enqueued) enqueue_status_read(h);
-    CU(cudaStreamSynchronize(h->s));
-    Clock c;
-    std::memcpy(&c, h->h_words, sizeof(Clock));
-    unsigned long long wi = h->h_words[3], we = h->h_words[4];
-    if (h->plan.nranks > 1 && h->comm) {  // NCCL ranks (loopback group partitions report separately)
-        // agree on the first failure across ranks
-        unsigned long long* dw = reinterpret_cast<unsigned long long*>(h->ptr.err_inst);
-        auto& api = nccl();
-        NC(api.AllReduce(dw, dw, 1, ncclUint64, ncclMin, h->comm, h->s));
-        NC(api.AllReduce(h->ptr.err_elem, h->ptr.err_elem, 1, ncclUint64, ncclMin, h->comm, h->s));
-        CU(cudaMemcpyAsync(h->h_words + 3, h->ptr.err_inst, 8, cudaMemcpyDeviceToHost, h->s));
-        CU(cudaMemcpyAsync(h->h_words + 4, h->ptr.err_elem, 8, cudaMemcpyDeviceToHost, h->s));
+// Ends a pending window: waits for every part, agrees on the first failure across
+// the partitions (all-reduce of the packed error words through the transport) and
+// applies one verdict to every part.  status_enqueued: the caller already enqueued
+// enqueue_status_read after the last step (single-partition sets).
+tvegpu_status sync_and_check(Stepper& S, bool status_enqueued = false) {
+    const bool multi = partitioned(S);
+    for (tvegpu_engine* h : S.parts)
+        if (!status_enqueued || multi) enqueue_status_read(h);
+    for (tvegpu_engine* h : S.parts) {
         CU(cudaStreamSynchronize(h->s));
-        wi = h->h_words[3];
-        we = h->h_words[4];
+        h->pending = false;
     }
-    if (!c.halted && wi == ~0ULL && we == ~0ULL) {
-        if (c.step != h->host_step) throw Error(TVEGPU_E_CUDA, "internal: device/host step mismatch");
-        h->host_time = c.time;
+    bool any_halt = false;
+    for (tvegpu_engine* h : S.parts) {
+        Clock c;
+        std::memcpy(&c, h->h_words, sizeof(Clock));
+        any_halt |= c.halted != 0;
+    }
+    unsigned long long wi = S.parts[0]->h_words[3], we = S.parts[0]->h_words[4];
+    if (multi) {
+        // agree on the first failure: min over the partitions of (err_inst, err_elem)
+        std::vector<unsigned long long*> w;
+        for (tvegpu_engine* h : S.parts) w.push_back(reinterpret_cast<unsigned long long*>(h->ptr.err_inst));
+        S.parts[0]->tx->allreduce_u64(S.parts, w, 2, /*max=*/false);
+        for (tvegpu_engine* h : S.parts) {
+            CU(cudaMemcpyAsync(h->h_words + 3, h->ptr.err_inst, 16, cudaMemcpyDeviceToHost, h->s));
+            CU(cudaStreamSynchronize(h->s));
+        }
+        wi = S.parts[0]->h_words[3];
+        we = S.parts[0]->h_words[4];
+    }
+    if (!any_halt && wi == ~0ULL && we == ~0ULL) {
+        for (tvegpu_engine* h : S.parts) {
+            Clock c;
+            std::memcpy(&c, h->h_words, sizeof(Clock));
+            if (c.step != h->host_step) throw Error(TVEGPU_E_CUDA, "internal: device/host step mismatch");
+            h->host_time = c.time;
+        }
         return TVEGPU_OK;
     }
-    // A step failed: the device halted right after it (state = the reference's state
-    // when step() throws: that step applied, time/step not advanced).
-    h->halted = true;
-    h->host_time = c.time;
-    const long long executed = c.step - step_at_start + (c.halted ? 1 : 0);
-    h->host_step = c.step;
-    h->cur = flips(h) ? (cur_at_start ^ (int)(executed & 1)) : cur_at_start;
-    char buf[256];
+    // A step failed.  One partition: the device halted right after it (state = the
+    // reference's state when step() throws: that step applied, time/step not advanced).
+    tvegpu_status status;
+    long long err_step;
+    int err_id;
+    char buf[320];
     if (we != ~0ULL && (wi == ~0ULL || (long long)(we >> 32) <= (long long)(wi >> 33))) {
-        h->err_step = (long long)(we >> 32);
-        h->err_node = (int)(we & 0xffffffffu);
-        std::snprintf(buf, sizeof buf, "non-SPD C or singular F in element %d at step %lld", h->err_node, h->err_step);
-        h->err = buf;
-        return TVEGPU_E_VALIDATION;
+        err_step = (long long)(we >> 32);
+        err_id = (int)(we & 0xffffffffu);
+        std::snprintf(buf, sizeof buf, "non-SPD C or singular F in element %d at step %lld", err_id, err_step);
+        status = TVEGPU_E_VALIDATION;
+    } else {
+        err_step = (long long)(wi >> 33);
+        err_id = (int)(wi & 0xffffffffu);
+        std::snprintf(buf, sizeof buf, "non-finite %s at step %lld, node %d", ((wi >> 32) & 1) ? "displacement" : "temperature",
+                      err_step, err_id);
+        status = TVEGPU_E_INSTABILITY;
     }
-    h->err_step = (long long)(wi >> 33);
-    h->err_node = (int)(wi & 0xffffffffu);
-    std::snprintf(buf, sizeof buf, "non-finite %s at step %lld, node %d", ((wi >> 32) & 1) ? "displacement" : "temperature",
-                  h->err_step, h->err_node);
-    h->err = buf;
-    return TVEGPU_E_INSTABILITY;
+    for (tvegpu_engine* h : S.parts) {
+        Clock c;
+        std::memcpy(&c, h->h_words, sizeof(Clock));
+        h->halted = true;
+        h->err_step = err_step;
+        h->err_node = err_id;
+        h->err = buf;
+        if (!multi) {
+            h->host_time = c.time;
+            const long long executed = c.step - h->pend_step + (c.halted ? 1 : 0);
+            h->host_step = c.step;
+            h->cur = flips(h) ? (h->pend_cur ^ (int)(executed & 1)) : h->pend_cur;
+        } else {
+            // Partitioned: the failing partition halted after err_step; the others ran on
+            // (their halo held stale contributions).  Every partition reports the same
+            // failure at the same step and time; the state must be reset before use.
+            double t = h->pend_time;
+            for (long long k = h->pend_step; k < err_step; ++k) t += h->dt;
+            h->host_time = t;
+            h->host_step = err_step;
+            h->state_invalid = true;
+            h->err += " (partitioned run: the partitions' state is invalid; reset it with set_state or load_checkpoint)";
+        }
+    }
+    return status;
+}
+
+void check_state_valid(const tvegpu_engine* h) {
+    if (h->state_invalid)
+        throw Error(TVEGPU_E_INSTABILITY, "state invalid after a failure in a partitioned step (step " +
+                                              std::to_string(h->err_step) + "); reset it with set_state or load_checkpoint");
 }
 
 // loopback: a partition driven by a tvegpu_group on one device (halo copied by the
@@ -468,17 +744,16 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     if (o.device >= 0) CU(cudaSetDevice(o.device));
     CU(cudaGetDevice(&h->device));
     const int nranks = o.nranks > 0 ? o.nranks : 1;
+    GlobalMesh g = build_global(p);  // validates first: the dt check dereferences element indices
     if (!p.allow_unstable_dt) {
-        StageTimer tm("critical_timestep");
         double th, me;
-        critical_timestep(p, &th, &me);
+        critical_timestep_from_edge(p, g.min_edge, &th, &me);
         if (p.dt > std::min(th, me)) {
             char buf[200];
             std::snprintf(buf, sizeof buf, "dt %.6g above critical timestep (thermal %.6g, mechanical %.6g)", p.dt, th, me);
             throw Error(TVEGPU_E_VALIDATION, buf);
         }
     }
-    GlobalMesh g = build_global(p);
     h->plan = build_rank_plan(p, g, nranks, o.rank, o.reorder);
     StageTimer tm_dev("device tables + uploads");
     const RankPlan& pl = h->plan;
@@ -489,7 +764,7 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     h->N_global = g.N;
     h->E_global = g.E;
     h->P = p.prony_count;
-    if (o.steps_per_graph > 0) h->steps_per_graph = o.steps_per_graph;
+    if (o.steps_per_graph > 0) h->solo.steps_per_graph = o.steps_per_graph;
     const int nn = g.nn, E = pl.E, N = pl.N, P = p.prony_count;
     // ---- params
     DevParams& m = h->prm;
@@ -564,6 +839,9 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     CU(cudaEventCreateWithFlags(&h->ev_comm, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&h->ev_src, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&h->ev_T, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&h->ev_entry, cudaEventDisableTiming));
+    h->solo.parts = {h};
     CU(cudaMallocHost(&h->h_words, 8 * sizeof(unsigned long long)));
     cudaStream_t s = h->s;
     auto& own = h->owned;
@@ -796,15 +1074,17 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     h->active.assign(h->regions.size(), 0);
     // ---- multi-GPU halo
     if (nranks > 1) {
-        if (!loopback) {
+        if (!loopback) {  // one partition per process and GPU: the NCCL transport
             if (!o.nccl_unique_id) throw Error(TVEGPU_E_ARG, "nranks > 1 needs options.nccl_unique_id");
             ncclUniqueId id;
             std::memcpy(&id, o.nccl_unique_id, sizeof id);
             NC(nccl().CommInitRank(&h->comm, nranks, id, o.rank));
-        }
+            auto t = std::make_unique<NcclTransport>();
+            t->comm = h->comm;
+            h->tx = t.get();
+            h->own_tx = std::move(t);
+        }  // loopback: the group installs its transport
         const size_t ns = pl.send_off.back();
-        const size_t nr = pl.recv_off.back();
-        (void)nr;
         h->d_send_slot = dupload(own, pl.send_slot, s);
         h->send_th = dalloc<double>(own, ns);
         h->send_m = dalloc<double>(own, kMW * ns);
@@ -870,6 +1150,7 @@ double* io_buffer(tvegpu_engine* h) {
 }
 
 void read_fields(tvegpu_engine* h, double* T, double* u, double* up) {
+    check_state_valid(h);
     const int N = h->plan.N;
     if (h->plan.nranks == 1 && N == h->N_global) {  // one partition covers every node
         double* dT = io_buffer(h);
@@ -1171,6 +1452,7 @@ __global__ void k_element_fields(const double* __restrict__ F, const double* __r
 // values in h->h_part; for nranks > 1 the values are all-reduced across ranks.
 template <int NV, class Launch>
 void reduce_to_host(tvegpu_engine* h, int nb, const int (&op)[NV], Launch&& launch) {
+    check_state_valid(h);
     if (!h->d_part) h->d_part = dalloc<double>(h->owned, (size_t)kRedMaxBlocks * 8 + 8);
     if (!h->h_part) CU(cudaMallocHost(&h->h_part, 8 * sizeof(double)));
     double* fin = h->d_part + (size_t)kRedMaxBlocks * 8;
@@ -1254,18 +1536,22 @@ tvegpu_status tvegpu_create(const tvegpu_problem* p, const tvegpu_options* o, tv
 
 void tvegpu_destroy(tvegpu_engine* h) {
     if (!h) return;
-    for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : h->solo.graphs) cudaGraphExecDestroy(kv.second);
     if (h->s) cudaStreamSynchronize(h->s);
+    if (h->sc) cudaStreamSynchronize(h->sc);
     if (h->comm) nccl().CommDestroy(h->comm);
     for (void* p : h->owned) cudaFree(p);
     if (h->h_words) cudaFreeHost(h->h_words);
     if (h->stage) cudaFreeHost(h->stage);
     if (h->qr_host) cudaFreeHost(h->qr_host);
+    if (h->motion_host) cudaFreeHost(h->motion_host);
     if (h->ev_pack) cudaEventDestroy(h->ev_pack);
     if (h->ev_src) cudaEventDestroy(h->ev_src);
     if (h->h_part) cudaFreeHost(h->h_part);
     if (h->ev_T) cudaEventDestroy(h->ev_T);
     if (h->ev_comm) cudaEventDestroy(h->ev_comm);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
+    if (h->ev_entry) cudaEventDestroy(h->ev_entry);
     if (h->s) cudaStreamDestroy(h->s);
     if (h->sc) cudaStreamDestroy(h->sc);
     delete h;
@@ -1275,7 +1561,7 @@ tvegpu_status tvegpu_enqueue_steps(tvegpu_engine* h, int64_t n) {
     TVEGPU_RANGE();
     if (!h || n < 0) return TVEGPU_E_ARG;
     return guard(h, [&] {
-        enqueue_steps(h, n);
+        enqueue_steps(h->solo, n);
         return TVEGPU_OK;
     });
 }
@@ -1289,8 +1575,7 @@ tvegpu_status tvegpu_sync(tvegpu_engine* h) {
             CU(cudaStreamSynchronize(h->s));
             return TVEGPU_OK;
         }
-        h->pending = false;
-        h->last_status = sync_and_check(h, h->pend_step, h->pend_cur);
+        h->last_status = sync_and_check(h->solo);
         return h->last_status;
     });
 }
@@ -1303,9 +1588,8 @@ tvegpu_status tvegpu_step(tvegpu_engine* h, int64_t n) {
             h->err = "engine halted by an earlier failure; reset the state with tvegpu_set_state";
             return h->last_status;
         }
-        enqueue_steps(h, n);
-        h->pending = false;
-        h->last_status = sync_and_check(h, h->pend_step, h->pend_cur);
+        enqueue_steps(h->solo, n);
+        h->last_status = sync_and_check(h->solo);
         return h->last_status;
     });
 }
@@ -1341,6 +1625,7 @@ tvegpu_status tvegpu_make_snapshot(tvegpu_engine* h, double* T, double* u) {
 tvegpu_status tvegpu_get_viscous(tvegpu_engine* h, double* v) {
     if (!h || !v) return TVEGPU_E_ARG;
     return guard(h, [&] {
+        check_state_valid(h);
         const int E = h->plan.E, P = h->P;
         std::vector<double> th((size_t)6 * P * E);
         if (!th.empty()) {
@@ -1395,6 +1680,7 @@ tvegpu_status tvegpu_set_state(tvegpu_engine* h, const double* T, const double* 
         h->host_time = time;
         h->host_step = step;
         h->halted = false;
+        h->state_invalid = false;
         h->last_status = TVEGPU_OK;
         return TVEGPU_OK;
     });
@@ -1427,6 +1713,50 @@ tvegpu_status tvegpu_set_nodal_sources(tvegpu_engine* h, const double* power) {
     });
 }
 
+// MechBCs::motion_override (mechanics.hpp:43-46).  nodes (original ids) limits the
+// callback to those candidates; NULL = every node, as the reference evaluates it.
+tvegpu_status tvegpu_set_motion_override(tvegpu_engine* h, tvegpu_motion_fn fn, void* user, int32_t num_nodes,
+                                         const int32_t* nodes) {
+    TVEGPU_RANGE();
+    if (!h || num_nodes < 0 || (num_nodes > 0 && !nodes)) return TVEGPU_E_ARG;
+    return guard(h, [&] {
+        CU(cudaStreamSynchronize(h->s));
+        for (auto& kv : h->solo.graphs) cudaGraphExecDestroy(kv.second);  // captured with the old parameters
+        h->solo.graphs.clear();
+        h->motion_fn = fn;
+        h->motion_user = user;
+        h->motion_orig.clear();
+        h->prm.motion = 0;
+        if (!fn) return TVEGPU_OK;
+        const int N = h->plan.N;
+        std::vector<int32_t> local(h->N_global, -1);
+        for (int i = 0; i < N; ++i) local[h->plan.node_orig[i]] = i;
+        std::vector<int32_t> row(N, -1);
+        auto add = [&](int32_t o) {
+            if (o < 0 || o >= h->N_global) throw Error(TVEGPU_E_ARG, "motion_override node out of range");
+            const int li = local[o];
+            if (li < 0 || row[li] >= 0) return;  // another partition's node, or listed twice
+            row[li] = (int32_t)h->motion_orig.size();
+            h->motion_orig.push_back(o);
+        };
+        if (nodes)
+            for (int k = 0; k < num_nodes; ++k) add(nodes[k]);
+        else
+            for (int o = 0; o < h->N_global; ++o) add(o);
+        const size_t rows = std::max<size_t>(1, h->motion_orig.size());
+        if (h->motion_host) CU(cudaFreeHost(h->motion_host));
+        h->motion_host = nullptr;
+        CU(cudaMallocHost(&h->motion_host, rows * sizeof(double4)));
+        h->ptr.motion_row = dupload(h->owned, row, h->s);
+        double4* val = dalloc<double4>(h->owned, rows);
+        CU(cudaMemsetAsync(val, 0, rows * sizeof(double4), h->s));
+        h->ptr.motion_val = val;
+        CU(cudaStreamSynchronize(h->s));
+        h->prm.motion = 1;
+        return TVEGPU_OK;
+    });
+}
+
 // Closed-loop iteration with the host copies overlapped with the step (single
 // partition): the source upload runs on the side stream while K1 computes (only K2
 // reads the sources), and the temperature read-back runs there while K3/K4 compute
@@ -1434,7 +1764,7 @@ tvegpu_status tvegpu_set_nodal_sources(tvegpu_engine* h, const double* power) {
 tvegpu_status tvegpu_step_io(tvegpu_engine* h, const double* power, int64_t n, double* T, double* u) {
     TVEGPU_RANGE();
     if (!h || n < 1) return TVEGPU_E_ARG;
-    if (h->plan.nranks != 1 || h->plan.N != h->N_global) {  // no overlap across partitions
+    if (h->plan.nranks != 1 || h->plan.N != h->N_global || h->prm.motion) {  // no overlap: partitions, motion pins
         tvegpu_status st = power ? tvegpu_set_nodal_sources(h, power) : TVEGPU_OK;
         if (st == TVEGPU_OK) st = tvegpu_step(h, n);
         if (st == TVEGPU_OK && (T || u)) st = tvegpu_make_snapshot(h, T, u);
@@ -1449,16 +1779,16 @@ tvegpu_status tvegpu_step_io(tvegpu_engine* h, const double* power, int64_t n, d
         if (power) {
             if (!h->d_pw) h->d_pw = dalloc<double>(h->owned, (size_t)N);
             h->source_override = true;
+            // steps still queued from tvegpu_enqueue_steps read the old sources: the
+            // side stream rewrites them only after the work already on the main stream
+            CU(cudaEventRecord(h->ev_entry, h->s));
+            CU(cudaStreamWaitEvent(h->sc, h->ev_entry, 0));
             CU(cudaMemcpyAsync(h->d_pw, power, (size_t)N * 8, cudaMemcpyHostToDevice, h->sc));
             k_orig_to_local<<<blocks(N, 256), 256, 0, h->sc>>>(h->d_pw, h->ptr.node_orig, N,
                                                                 const_cast<double*>(h->ptr.qr));
             CU(cudaEventRecord(h->ev_src, h->sc));
         }
-        if (!h->pending) {
-            h->pending = true;
-            h->pend_step = h->host_step;
-            h->pend_cur = h->cur;
-        }
+        begin_pending(h);
         // K2 / K4 of the last step write T / u straight into the I/O buffer in original
         // numbering (no renumbering kernel on the tail); modes without that kernel
         // renumber the unchanged field from the records instead
@@ -1473,7 +1803,7 @@ tvegpu_status tvegpu_step_io(tvegpu_engine* h, const double* power, int64_t n, d
             h->host_step += 1;
         };
         one(true, n == 1);
-        if (n > 2) enqueue_steps(h, n - 2);
+        if (n > 2) enqueue_steps(h->solo, n - 2);
         if (n > 1) one(false, true);
         const bool early_status = h->plan.nranks == 1;
         if (early_status) enqueue_status_read(h);  // before the u read-back: no extra tail
@@ -1494,8 +1824,7 @@ tvegpu_status tvegpu_step_io(tvegpu_engine* h, const double* power, int64_t n, d
         }
         CU(cudaGetLastError());
         CU(cudaStreamSynchronize(h->sc));
-        h->pending = false;
-        h->last_status = sync_and_check(h, h->pend_step, h->pend_cur, early_status);
+        h->last_status = sync_and_check(h->solo, early_status);
         return h->last_status;
     });
 }
@@ -1524,51 +1853,138 @@ tvegpu_status tvegpu_checkpoint_size(tvegpu_engine* h, uint64_t* bytes) {
     return TVEGPU_OK;
 }
 
+namespace {
+// State image of a partitioned set in original numbering, assembled on the device:
+// every part writes the raw bits of the nodes it owns (the lowest rank touching a
+// node; replicas are bit-identical anyway) and of its elements' viscous history into
+// a zeroed global-size word buffer; an all-reduce(max) over u64 through the set's
+// transport (NCCL, or the loopback group) then leaves the full image on every part
+// (each word has exactly one writer or is 0).  Layout (words):
+//   T[Ng] u[3 Ng] u_prev[3 Ng] power[Ng] theta[Eg][P][6]
+__global__ void k_image_nodes(const double4* __restrict__ rc, const double4* __restrict__ rp,
+                              const double* __restrict__ qr, const int32_t* __restrict__ node_orig,
+                              const uint8_t* __restrict__ owned, int N, size_t Ng, unsigned long long* __restrict__ img) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N || !owned[i]) return;
+    const size_t o = (size_t)node_orig[i];
+    const double4 a = rc[i], b = rp[i];
+    auto w = [](double v) { return (unsigned long long)__double_as_longlong(v); };
+    img[o] = w(a.w);
+    img[Ng + 3 * o] = w(a.x), img[Ng + 3 * o + 1] = w(a.y), img[Ng + 3 * o + 2] = w(a.z);
+    img[4 * Ng + 3 * o] = w(b.x), img[4 * Ng + 3 * o + 1] = w(b.y), img[4 * Ng + 3 * o + 2] = w(b.z);
+    img[7 * Ng + o] = w(qr[i]);
+}
+__global__ void k_image_elems(const double* __restrict__ theta, const int32_t* __restrict__ elem_orig, int E, int P,
+                              unsigned long long* __restrict__ img_th) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    const size_t o = (size_t)elem_orig[e];
+    for (int p = 0; p < P; ++p)
+        for (int c = 0; c < 6; ++c)
+            img_th[(o * P + p) * 6 + c] = (unsigned long long)__double_as_longlong(theta[((size_t)p * 6 + c) * E + e]);
+}
+
+// Fills the host image of a partitioned set (every part's buffer holds it after the
+// all-reduce; parts[0]'s is read back).  Collective over the NCCL ranks.
+void gather_state_image(Stepper& S, std::vector<unsigned long long>& out) {
+    tvegpu_engine* h0 = S.parts[0];
+    const size_t Ng = h0->N_global, Eg = h0->E_global, P = h0->P;
+    // nodes: T, u, u_prev, power (8 words/node) first, then theta (6 P / element)
+    const size_t nwords = 8 * Ng + 6 * P * Eg;
+    std::vector<unsigned long long*> bufs;
+    try {
+        for (tvegpu_engine* h : S.parts) {
+            check_state_valid(h);
+            void* d = nullptr;
+            CU(cudaMalloc(&d, nwords * 8));
+            bufs.push_back(static_cast<unsigned long long*>(d));
+            CU(cudaMemsetAsync(d, 0, nwords * 8, h->s));
+            const double4* rc = h->cur ? h->ptr.rec1 : h->ptr.rec0;
+            const double4* rp = h->cur ? h->ptr.rec0 : h->ptr.rec1;
+            if (!h->d_owned) h->d_owned = dupload(h->owned, h->plan.node_owned, h->s);
+            if (h->plan.N)
+                k_image_nodes<<<blocks(h->plan.N, 256), 256, 0, h->s>>>(rc, rp, h->ptr.qr, h->ptr.node_orig, h->d_owned,
+                                                                        h->plan.N, Ng, bufs.back());
+            if (P && h->plan.E)
+                k_image_elems<<<blocks(h->plan.E, 256), 256, 0, h->s>>>(h->ptr.theta, h->ptr.elem_orig, h->plan.E, (int)P,
+                                                                        bufs.back() + 8 * Ng);
+            CU(cudaGetLastError());
+        }
+        h0->tx->allreduce_u64(S.parts, bufs, nwords, /*max=*/true);
+        out.resize(nwords);
+        CU(cudaMemcpyAsync(out.data(), bufs[0], nwords * 8, cudaMemcpyDeviceToHost, h0->s));
+        for (tvegpu_engine* h : S.parts) CU(cudaStreamSynchronize(h->s));
+    } catch (...) {
+        for (auto* b : bufs) cudaFree(b);
+        throw;
+    }
+    for (auto* b : bufs) cudaFree(b);
+}
+
+// Writes the checkpoint (header + T, u, u_prev, viscous[E][P][9], power) of a set.
+void write_checkpoint(Stepper& S, void* buf) {
+    tvegpu_engine* h = S.parts[0];
+    const size_t N = h->N_global, E = h->E_global, P = h->P;
+    CkptHeader hd{};
+    std::memcpy(hd.magic, "TVEGPUCK", 8);
+    hd.version = 1, hd.kind = h->kind, hd.N = (int32_t)N, hd.E = (int32_t)E, hd.P = (int32_t)P;
+    hd.has_sources = h->source_override ? 1 : 0;
+    hd.step = h->host_step;
+    hd.time = h->host_time;
+    char* o = static_cast<char*>(buf);
+    std::memcpy(o, &hd, sizeof hd);
+    double* T = reinterpret_cast<double*>(o + sizeof hd);
+    double* u = T + N;
+    double* up = u + 3 * N;
+    double* vis = up + 3 * N;
+    double* pw = vis + 9 * P * E;
+    if (!partitioned(S)) {
+        read_fields(h, T, u, up);
+        if (P) {
+            const tvegpu_status st = tvegpu_get_viscous(h, vis);
+            if (st != TVEGPU_OK) throw Error(st, h->err);
+        }
+        if (h->source_override) {
+            std::vector<double> q(N);
+            CU(cudaMemcpyAsync(q.data(), h->ptr.qr, N * 8, cudaMemcpyDeviceToHost, h->s));
+            CU(cudaStreamSynchronize(h->s));
+            for (size_t i = 0; i < N; ++i) pw[h->plan.node_orig[i]] = q[i];
+        }
+        return;
+    }
+    std::vector<unsigned long long> img;
+    gather_state_image(S, img);
+    std::memcpy(T, img.data(), 7 * N * 8);  // T, u, u_prev are contiguous in both layouts
+    static const int map9[9] = {0, 3, 5, 3, 1, 4, 5, 4, 2};
+    const unsigned long long* th = img.data() + 8 * N;
+#pragma omp parallel for schedule(static)
+    for (size_t e = 0; e < E; ++e)
+        for (size_t p = 0; p < P; ++p)
+            for (int q = 0; q < 9; ++q) std::memcpy(vis + (e * P + p) * 9 + q, th + (e * P + p) * 6 + map9[q], 8);
+    if (h->source_override) std::memcpy(pw, img.data() + 7 * N, N * 8);
+}
+}  // namespace
+
+// Single-partition engines read their state directly; a partitioned engine (one NCCL
+// rank) gathers the image over NCCL — collective: every rank calls it and every rank
+// receives the same image.
 tvegpu_status tvegpu_save_checkpoint(tvegpu_engine* h, void* buf, uint64_t bytes) {
     TVEGPU_RANGE();
     if (!h || !buf) return TVEGPU_E_ARG;
-    if (h->plan.nranks != 1 || h->plan.N != h->N_global || h->plan.E != h->E_global) {
-        h->err = "save_checkpoint needs a single-partition engine (gather the rank states first)";
-        return TVEGPU_E_ARG;
-    }
     if (bytes < ckpt_bytes(h)) {
         h->err = "checkpoint buffer too small (tvegpu_checkpoint_size)";
         return TVEGPU_E_ARG;
     }
     return guard(h, [&] {
-        const int N = h->N_global, E = h->E_global, P = h->P;
-        CkptHeader hd{};
-        std::memcpy(hd.magic, "TVEGPUCK", 8);
-        hd.version = 1, hd.kind = h->kind, hd.N = N, hd.E = E, hd.P = P;
-        hd.has_sources = h->source_override ? 1 : 0;
-        hd.step = h->host_step;
-        hd.time = h->host_time;
-        char* o = static_cast<char*>(buf);
-        std::memcpy(o, &hd, sizeof hd);
-        double* T = reinterpret_cast<double*>(o + sizeof hd);
-        double* u = T + N;
-        double* up = u + 3 * (size_t)N;
-        double* vis = up + 3 * (size_t)N;
-        read_fields(h, T, u, up);
-        if (P) {
-            const tvegpu_status st = tvegpu_get_viscous(h, vis);
-            if (st != TVEGPU_OK) return st;
-        }
-        if (h->source_override) {
-            double* pw = vis + 9 * (size_t)P * E;
-            std::vector<double> q(N);
-            CU(cudaMemcpyAsync(q.data(), h->ptr.qr, (size_t)N * 8, cudaMemcpyDeviceToHost, h->s));
-            CU(cudaStreamSynchronize(h->s));
-            for (int i = 0; i < N; ++i) pw[h->plan.node_orig[i]] = q[i];
-        }
+        write_checkpoint(h->solo, buf);
         return TVEGPU_OK;
     });
 }
 
-tvegpu_status tvegpu_load_checkpoint(tvegpu_engine* h, const void* buf, uint64_t bytes) {
-    TVEGPU_RANGE();
-    if (!h || !buf) return TVEGPU_E_ARG;
-    CkptHeader hd;
+namespace {
+// Validates a checkpoint image against an engine's problem; fills the field pointers.
+tvegpu_status parse_checkpoint(tvegpu_engine* h, const void* buf, uint64_t bytes, CkptHeader& hd,
+                               const double*& T, const double*& vis) {
     if (bytes < sizeof hd) {
         h->err = "checkpoint truncated";
         return TVEGPU_E_IO;
@@ -1588,11 +2004,23 @@ tvegpu_status tvegpu_load_checkpoint(tvegpu_engine* h, const void* buf, uint64_t
         h->err = "checkpoint truncated";
         return TVEGPU_E_IO;
     }
-    const double* T = reinterpret_cast<const double*>(static_cast<const char*>(buf) + sizeof hd);
-    const double* u = T + N;
-    const double* up = u + 3 * N;
-    const double* vis = up + 3 * N;
-    tvegpu_status st = tvegpu_set_state(h, T, u, up, P ? vis : nullptr, hd.time, hd.step);
+    T = reinterpret_cast<const double*>(static_cast<const char*>(buf) + sizeof hd);
+    vis = T + 7 * N;
+    return TVEGPU_OK;
+}
+}  // namespace
+
+// Loads into any partitioning: each partition takes its nodes and elements from the
+// original-numbering image (tvegpu_set_state).
+tvegpu_status tvegpu_load_checkpoint(tvegpu_engine* h, const void* buf, uint64_t bytes) {
+    TVEGPU_RANGE();
+    if (!h || !buf) return TVEGPU_E_ARG;
+    CkptHeader hd;
+    const double *T = nullptr, *vis = nullptr;
+    tvegpu_status st = parse_checkpoint(h, buf, bytes, hd, T, vis);
+    if (st != TVEGPU_OK) return st;
+    const uint64_t N = hd.N, E = hd.E, P = hd.P;
+    st = tvegpu_set_state(h, T, T + N, T + 4 * N, P ? vis : nullptr, hd.time, hd.step);
     if (st == TVEGPU_OK) st = tvegpu_set_nodal_sources(h, hd.has_sources ? vis + 9 * P * E : nullptr);
     return st;
 }
@@ -1699,15 +2127,20 @@ tvegpu_status tvegpu_get_diagnostics(tvegpu_engine* h, double* f_int, double* F,
     return guard(h, [&] {
         const int E = h->plan.E, N = h->plan.N;
         std::vector<double> buf((size_t)9 * std::max(E, N));
+        // on the engine stream: steps enqueued by tvegpu_enqueue_steps may still write these
+        auto copy = [&](const double* src, size_t n) {
+            CU(cudaMemcpyAsync(buf.data(), src, n * 8, cudaMemcpyDeviceToHost, h->s));
+            CU(cudaStreamSynchronize(h->s));
+        };
         if (f_int) {
-            CU(cudaMemcpy(buf.data(), h->ptr.diag_f, (size_t)3 * N * 8, cudaMemcpyDeviceToHost));
+            copy(h->ptr.diag_f, (size_t)3 * N);
             for (int i = 0; i < N; ++i)
                 for (int c = 0; c < 3; ++c) f_int[3 * (size_t)h->plan.node_orig[i] + c] = buf[3 * (size_t)i + c];
         }
         for (int k = 0; k < 2; ++k) {
             double* dst = k == 0 ? F : S;
             if (!dst) continue;
-            CU(cudaMemcpy(buf.data(), k == 0 ? h->ptr.diag_F : h->ptr.diag_S, (size_t)9 * E * 8, cudaMemcpyDeviceToHost));
+            copy(k == 0 ? h->ptr.diag_F : h->ptr.diag_S, (size_t)9 * E);
             for (int e = 0; e < E; ++e)
                 for (int q = 0; q < 9; ++q) dst[9 * (size_t)h->plan.elem_orig[e] + q] = buf[9 * (size_t)e + q];
         }
@@ -1824,8 +2257,7 @@ tvegpu_status tvegpu_profile_kernels(tvegpu_engine* h, int32_t nsteps, double* m
     return guard(h, [&] {
         if (h->halted) return h->last_status;
         if (h->pending) {
-            h->pending = false;
-            h->last_status = sync_and_check(h, h->pend_step, h->pend_cur);
+            h->last_status = sync_and_check(h->solo);
             if (h->last_status != TVEGPU_OK) return h->last_status;
         }
         std::vector<std::string> nm;
@@ -1841,15 +2273,18 @@ tvegpu_status tvegpu_profile_kernels(tvegpu_engine* h, int32_t nsteps, double* m
         const int nk = (int)nm.size();
         std::vector<cudaEvent_t> ev((size_t)(nk + 1) * nsteps);
         for (auto& e : ev) CU(cudaEventCreate(&e));
-        const long long s0 = h->host_step;
-        const int c0 = h->cur;
+        // partitioned engines: the marks bracket the phases (element kernels + pack +
+        // exchange enqueue, then the wait for the halo + node kernel)
+        begin_pending(h);
         for (int k = 0; k < nsteps; ++k) {
             refresh_sources_if_needed(h, h->host_time);
-            enqueue_one_step(h, ev.data() + (size_t)k * (nk + 1));
+            if (h->prm.motion) upload_motion(h);
+            if (partitioned(h->solo)) enqueue_partitioned_step(h->solo, ev.data() + (size_t)k * (nk + 1));
+            else enqueue_one_step(h, ev.data() + (size_t)k * (nk + 1));
             h->host_time += h->dt;
             h->host_step += 1;
         }
-        tvegpu_status st = sync_and_check(h, s0, c0);
+        tvegpu_status st = sync_and_check(h->solo);
         std::vector<double> acc(nk, 0.0);
         for (int k = 0; k < nsteps; ++k)
             for (int j = 0; j < nk; ++j) {
@@ -1874,83 +2309,53 @@ tvegpu_status tvegpu_profile_kernels(tvegpu_engine* h, int32_t nsteps, double* m
 
 }  // extern "C"
 
-// ---------------------------------------------------------------- virtual multi-partition group
-// P RCB partitions of one problem, each a full partition engine, driven in
-// lockstep on ONE device and stream; the halo is a device-to-device copy of each
-// neighbour's packed send segment into the receive area, in place of
-// ncclSend/ncclRecv.  Everything else — partition maps, boundary-first chunks,
-// pack kernel, receive-area gather lists, per-partition node updates — is the
-// multi-GPU code path, so results must be bit-identical to one partition.
+// ---------------------------------------------------------------- partition group (loopback transport)
+// P RCB partitions of one problem, each a full partition engine with its own compute
+// and comm streams, stepped by the same code as one NCCL rank per GPU
+// (enqueue_partitioned_step, CUDA-graph capture, verdict agreement, state gather);
+// only the transport differs: device copies of each neighbour's packed send segment
+// into the receive area, ordered by the same ev_pack / ev_comm events, in place of
+// ncclSend / ncclRecv.  Results are bit-identical to a single partition.
 struct tvegpu_group {
     std::vector<tvegpu_engine*> parts;
-    cudaStream_t s = nullptr;
+    Stepper st;
+    LoopbackTransport tx;
     std::string err;
+    tvegpu_status last_status = TVEGPU_OK;
 };
 
 namespace {
-void loopback_copy(tvegpu_group* G, bool mech) {
-    const int width = mech ? kMW : 1;
-    for (tvegpu_engine* r : G->parts) {
-        const RankPlan& pr = r->plan;
-        double* slots = mech ? r->ptr.slot_m : r->ptr.slot_th;
-        for (size_t j = 0; j < pr.neighbors.size(); ++j) {
-            const tvegpu_engine* q = G->parts[pr.neighbors[j]];
-            const RankPlan& ps = q->plan;
-            const size_t jj = std::find(ps.neighbors.begin(), ps.neighbors.end(), pr.rank) - ps.neighbors.begin();
-            if (jj == ps.neighbors.size()) throw Error(TVEGPU_E_ARG, "internal: asymmetric halo");
-            const size_t n = (size_t)(ps.send_off[jj + 1] - ps.send_off[jj]);
-            if (n != (size_t)(pr.recv_off[j + 1] - pr.recv_off[j])) throw Error(TVEGPU_E_ARG, "internal: halo size");
-            if (!n) continue;
-            const double* src = (mech ? q->send_m : q->send_th) + (size_t)ps.send_off[jj] * width;
-            double* dst = slots + ((size_t)pr.E * pr.nn + pr.recv_off[j]) * width;
-            CU(cudaMemcpyAsync(dst, src, n * width * sizeof(double), cudaMemcpyDeviceToDevice, G->s));
+template <class F>
+tvegpu_status group_guard(tvegpu_group* G, F&& f) {
+    try {
+        const tvegpu_status st = f();
+        if (st != TVEGPU_OK) {
+            G->last_status = st;
+            for (tvegpu_engine* h : G->parts)
+                if (!h->err.empty()) {
+                    G->err = h->err;
+                    break;
+                }
         }
+        return st;
+    } catch (const Error& e) {
+        G->err = e.what();
+        G->last_status = e.status;
+        return e.status;
+    } catch (const std::exception& e) {
+        G->err = e.what();
+        return TVEGPU_E_ARG;
     }
 }
-
-void pack(tvegpu_engine* h, bool mech) {
-    const int ns = h->plan.send_off.back();
-    if (ns > 0)
-        k_pack<<<blocks(ns, 256), 256, 0, h->s>>>(mech ? h->ptr.slot_m : h->ptr.slot_th, h->d_send_slot, ns, mech ? kMW : 1,
-                                                  mech ? h->send_m : h->send_th);
-}
-
-void group_step_once(tvegpu_group* G) {
-    tvegpu_engine* h0 = G->parts[0];
-    for (tvegpu_engine* h : G->parts) refresh_sources_if_needed(h, h->host_time);
-    if (h0->mode != TVEGPU_MECHANICAL_ONLY) {
-        for (tvegpu_engine* h : G->parts) {
-            const int nc = (int)h->plan.chunk_start.size() - 1;
-            h->nn == 4 ? launch_thermal_element<4>(h, 0, nc) : launch_thermal_element<8>(h, 0, nc);
-            pack(h, false);
-        }
-        loopback_copy(G, false);
-        for (tvegpu_engine* h : G->parts)
-            thermal_node_kernel(h)<<<blocks(h->pair ? 2 * h->plan.N : h->plan.N, kNodeThreads), kNodeThreads, 0, h->s>>>(h->prm, h->ptr, h->cur,
-                                                                    h->mode == TVEGPU_THERMAL_ONLY, nullptr);
-    }
-    if (h0->mode != TVEGPU_THERMAL_ONLY) {
-        for (tvegpu_engine* h : G->parts) {
-            const int nc = (int)h->plan.chunk_start.size() - 1;
-            h->nn == 4 ? launch_mech_element<4>(h, 0, nc) : launch_mech_element<8>(h, 0, nc);
-            pack(h, true);
-        }
-        loopback_copy(G, true);
-        for (tvegpu_engine* h : G->parts) {
-            if (h->pair)
-                k_mech_node<true><<<blocks(2 * h->plan.N, kNodeThreads), kNodeThreads, 0, h->s>>>(h->prm, h->ptr, h->cur, 1,
-                                                                                              nullptr);
-            else
-                k_mech_node<false><<<blocks(h->plan.N, kNodeThreads), kNodeThreads, 0, h->s>>>(h->prm, h->ptr, h->cur, 1,
-                                                                                               nullptr);
-            h->cur ^= 1;
-        }
-    }
-    CU(cudaGetLastError());
+tvegpu_status each_part(tvegpu_group* G, const std::function<tvegpu_status(tvegpu_engine*)>& f) {
     for (tvegpu_engine* h : G->parts) {
-        h->host_time += h->dt;
-        h->host_step += 1;
+        const tvegpu_status st = f(h);
+        if (st != TVEGPU_OK) {
+            G->err = h->err;
+            return st;
+        }
     }
+    return TVEGPU_OK;
 }
 }  // namespace
 
@@ -1973,14 +2378,11 @@ tvegpu_status tvegpu_group_create(const tvegpu_problem* p, int32_t nparts, const
             auto* h = new tvegpu_engine();
             G->parts.push_back(h);
             build_engine(h, *p, oo, /*loopback=*/true);
+            h->tx = &G->tx;
         }
-        G->s = G->parts[0]->s;
-        for (tvegpu_engine* h : G->parts)
-            if (h->s != G->s) {
-                CU(cudaStreamSynchronize(h->s));
-                CU(cudaStreamDestroy(h->s));
-                h->s = G->s;  // one stream orders the lockstep phases
-            }
+        G->st.parts = G->parts;
+        G->st.steps_per_graph = o->steps_per_graph > 0 ? o->steps_per_graph : 64;
+        CU(cudaEventCreateWithFlags(&G->st.ev_fork, cudaEventDisableTiming));
     } catch (const std::exception& e) {
         g_create_error = e.what();
         tvegpu_group_destroy(G);
@@ -1992,54 +2394,107 @@ tvegpu_status tvegpu_group_create(const tvegpu_problem* p, int32_t nparts, const
 
 void tvegpu_group_destroy(tvegpu_group* G) {
     if (!G) return;
-    if (G->s) cudaStreamSynchronize(G->s);
-    for (size_t k = 0; k < G->parts.size(); ++k) {
-        if (k > 0 && G->parts[k]->s == G->s) G->parts[k]->s = nullptr;  // shared stream: destroyed once
-        tvegpu_destroy(G->parts[k]);
-    }
+    for (tvegpu_engine* h : G->parts)
+        if (h->s) cudaStreamSynchronize(h->s);
+    for (auto& kv : G->st.graphs) cudaGraphExecDestroy(kv.second);
+    if (G->st.ev_fork) cudaEventDestroy(G->st.ev_fork);
+    for (tvegpu_engine* h : G->parts) tvegpu_destroy(h);
     delete G;
 }
 
 tvegpu_status tvegpu_group_step(tvegpu_group* G, int64_t n) {
     TVEGPU_RANGE();
     if (!G || n < 0) return TVEGPU_E_ARG;
-    try {
-        std::vector<long long> s0;
-        std::vector<int> c0;
-        for (tvegpu_engine* h : G->parts) {
-            if (h->halted) return h->last_status;
-            s0.push_back(h->host_step);
-            c0.push_back(h->cur);
-        }
-        for (int64_t k = 0; k < n; ++k) group_step_once(G);
-        tvegpu_status worst = TVEGPU_OK;
-        for (size_t r = 0; r < G->parts.size(); ++r) {
-            tvegpu_engine* h = G->parts[r];
-            h->last_status = sync_and_check(h, s0[r], c0[r]);
-            if (h->last_status != TVEGPU_OK && worst == TVEGPU_OK) {
-                worst = h->last_status;
-                G->err = h->err;
+    return group_guard(G, [&] {
+        if (G->parts[0]->halted) return G->last_status;
+        enqueue_steps(G->st, n);
+        return sync_and_check(G->st);
+    });
+}
+
+tvegpu_status tvegpu_group_get_state(tvegpu_group* G, double* T, double* disp, double* disp_prev, double* viscous) {
+    if (!G) return TVEGPU_E_ARG;
+    return group_guard(G, [&] {
+        return each_part(G, [&](tvegpu_engine* h) {
+            if (T || disp || disp_prev) {
+                check_state_valid(h);
+                read_fields(h, T, disp, disp_prev);
             }
-        }
-        return worst;
-    } catch (const Error& e) {
-        G->err = e.what();
-        return e.status;
-    }
+            return viscous && h->P ? tvegpu_get_viscous(h, viscous) : TVEGPU_OK;
+        });
+    });
 }
 
 tvegpu_status tvegpu_group_get_fields(tvegpu_group* G, double* T, double* disp, double* viscous) {
+    return tvegpu_group_get_state(G, T, disp, nullptr, viscous);
+}
+
+tvegpu_status tvegpu_group_set_state(tvegpu_group* G, const double* T, const double* disp, const double* disp_prev,
+                                     const double* viscous, double time, int64_t step) {
     if (!G) return TVEGPU_E_ARG;
-    for (tvegpu_engine* h : G->parts) {
-        tvegpu_status st = TVEGPU_OK;
-        if (T || disp) st = tvegpu_make_snapshot(h, T, disp);
-        if (st == TVEGPU_OK && viscous && h->P) st = tvegpu_get_viscous(h, viscous);
-        if (st != TVEGPU_OK) {
-            G->err = h->err;
-            return st;
-        }
+    return group_guard(G, [&] {
+        const tvegpu_status st =
+            each_part(G, [&](tvegpu_engine* h) { return tvegpu_set_state(h, T, disp, disp_prev, viscous, time, step); });
+        if (st == TVEGPU_OK) G->last_status = TVEGPU_OK;
+        return st;
+    });
+}
+
+tvegpu_status tvegpu_group_set_nodal_sources(tvegpu_group* G, const double* power) {
+    if (!G) return TVEGPU_E_ARG;
+    return group_guard(G, [&] { return each_part(G, [&](tvegpu_engine* h) { return tvegpu_set_nodal_sources(h, power); }); });
+}
+
+// The partitioned form of tvegpu_step_io (what one NCCL rank runs): sources, n steps,
+// snapshot of T and u in original numbering.
+tvegpu_status tvegpu_group_step_io(tvegpu_group* G, const double* power, int64_t n, double* T, double* disp) {
+    if (!G || n < 1) return TVEGPU_E_ARG;
+    tvegpu_status st = power ? tvegpu_group_set_nodal_sources(G, power) : TVEGPU_OK;
+    if (st == TVEGPU_OK) st = tvegpu_group_step(G, n);
+    if (st == TVEGPU_OK && (T || disp)) st = tvegpu_group_get_state(G, T, disp, nullptr, nullptr);
+    return st;
+}
+
+double tvegpu_group_time(const tvegpu_group* G) { return G ? G->parts[0]->host_time : 0.0; }
+int64_t tvegpu_group_step_count(const tvegpu_group* G) { return G ? G->parts[0]->host_step : 0; }
+
+tvegpu_status tvegpu_group_last_error(const tvegpu_group* G, char* msg, size_t cap, int64_t* step, int32_t* node) {
+    if (!G) return TVEGPU_E_ARG;
+    if (msg && cap) {
+        std::strncpy(msg, G->err.c_str(), cap - 1);
+        msg[cap - 1] = 0;
     }
-    return TVEGPU_OK;
+    if (step) *step = G->parts[0]->err_step;
+    if (node) *node = G->parts[0]->err_node;
+    return G->last_status;
+}
+
+tvegpu_status tvegpu_group_checkpoint_size(tvegpu_group* G, uint64_t* bytes) {
+    return G ? tvegpu_checkpoint_size(G->parts[0], bytes) : TVEGPU_E_ARG;
+}
+
+tvegpu_status tvegpu_group_save_checkpoint(tvegpu_group* G, void* buf, uint64_t bytes) {
+    TVEGPU_RANGE();
+    if (!G || !buf) return TVEGPU_E_ARG;
+    if (bytes < ckpt_bytes(G->parts[0])) {
+        G->err = "checkpoint buffer too small (tvegpu_group_checkpoint_size)";
+        return TVEGPU_E_ARG;
+    }
+    return group_guard(G, [&] {
+        write_checkpoint(G->st, buf);
+        return TVEGPU_OK;
+    });
+}
+
+tvegpu_status tvegpu_group_load_checkpoint(tvegpu_group* G, const void* buf, uint64_t bytes) {
+    TVEGPU_RANGE();
+    if (!G || !buf) return TVEGPU_E_ARG;
+    return group_guard(G, [&] {
+        const tvegpu_status st =
+            each_part(G, [&](tvegpu_engine* h) { return tvegpu_load_checkpoint(h, buf, bytes); });
+        if (st == TVEGPU_OK) G->last_status = TVEGPU_OK;
+        return st;
+    });
 }
 
 }  // extern "C"

@@ -65,6 +65,7 @@ struct DevParams {
     int max_chunk_nodes;  // shared-memory stride of the staged node records
     int stage_stride;     // entries per chunk in stage_ent (max unique nodes of a chunk)
     int ell;              // G > 0: ELL gathers with rows of 8 G slot ids (every node has <= 8 G contributions)
+    int motion;           // MechBCs::motion_override active (host-evaluated pins, K4 reads motion_row/val)
     double dt, mu, kappa, eta_a, kh, rho, wbcb, Ta, Qm, gamma;
     double inv_2dt, inv_dt2;  // 1/(2 dt), 1/dt^2 (Eq. 22 coefficients)
     double fiber[3];
@@ -114,6 +115,8 @@ struct DevPtrs {
     double* diag_F;            // [E][9] or null
     double* diag_S;            // [E][9] or null
     double* diag_f;            // [N][3] or null
+    const int32_t* motion_row;  // [N] row of motion_val for override candidates, else -1 (motion only)
+    const double4* motion_val;  // [rows] (x, y, z, pinned) of this step's motion_override(node, t + dt)
 };
 
 enum : uint8_t { BC_FIXED = 1, BC_PX = 2, BC_PY = 4, BC_PZ = 8, BC_TFIX = 16 };
@@ -1174,6 +1177,13 @@ __global__ void NODE_BOUNDS k_mech_node(const DevParams P, const DevPtrs D, int 
                 if (msk & BC_PX) x = value_at(0);
                 if (msk & BC_PY) y = value_at(1);
                 if (msk & BC_PZ) z = value_at(2);
+            }
+        }
+        if (P.motion) {  // motion_override wins last (mechanics.hpp:43-46, C9)
+            const int r = __ldg(D.motion_row + i);
+            if (r >= 0) {
+                const double4 v = D.motion_val[r];
+                if (v.w != 0.0) x = v.x, y = v.y, z = v.z;
             }
         }
         if (!(isfinite(x) && isfinite(y) && isfinite(z)))

@@ -379,6 +379,13 @@ RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nrank
         std::iota(local.begin(), local.end(), 0);
     }
     r.N = (int)r.node_orig.size();
+    // node ownership for state gathers (checkpoint images): the lowest rank touching it
+    r.node_owned.resize(r.N);
+#pragma omp parallel for schedule(static)
+    for (int li = 0; li < r.N; ++li) {
+        const uint64_t t = touch[r.node_orig[li]];
+        r.node_owned[li] = (uint8_t)((t & (~t + 1)) == me);
+    }
     r.conn.resize((size_t)r.E * nn);
     std::vector<int32_t> elem_local(E, -1);
 #pragma omp parallel for schedule(static)
@@ -648,6 +655,15 @@ void build_chunks(RankPlan& r) {
     r.chunk_start.push_back(r.E);
 }
 
+void critical_timestep_from_edge(const tvegpu_problem& p, double L, double* thermal, double* mechanical) {
+    const double cd = std::sqrt((p.kappa + 4.0 * p.mu / 3.0) / p.density);
+    double cmin = std::numeric_limits<double>::infinity(), kmax = -std::numeric_limits<double>::infinity();
+    for (int i = 0; i < p.c_table_len; ++i) cmin = std::min(cmin, p.c_table_value[i]);
+    for (int i = 0; i < p.k_table_len; ++i) kmax = std::max(kmax, sym_max_eig(p.k_table_tensor + 9 * (size_t)i));
+    *mechanical = 0.9 * L / cd;
+    *thermal = 0.9 * (p.density * cmin * L * L) / (2.0 * kmax * 3.0);
+}
+
 void critical_timestep(const tvegpu_problem& p, double* thermal, double* mechanical) {
     static const int t4e[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
     static const int h8e[12][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 0}, {4, 5}, {5, 6},
@@ -668,12 +684,7 @@ void critical_timestep(const tvegpu_problem& p, double* thermal, double* mechani
             L = std::min(L, std::sqrt(d2));
         }
     }
-    const double cd = std::sqrt((p.kappa + 4.0 * p.mu / 3.0) / p.density);
-    double cmin = std::numeric_limits<double>::infinity(), kmax = -std::numeric_limits<double>::infinity();
-    for (int i = 0; i < p.c_table_len; ++i) cmin = std::min(cmin, p.c_table_value[i]);
-    for (int i = 0; i < p.k_table_len; ++i) kmax = std::max(kmax, sym_max_eig(p.k_table_tensor + 9 * (size_t)i));
-    *mechanical = 0.9 * L / cd;
-    *thermal = 0.9 * (p.density * cmin * L * L) / (2.0 * kmax * 3.0);
+    critical_timestep_from_edge(p, L, thermal, mechanical);
 }
 
 }  // namespace tvegpu

@@ -97,6 +97,7 @@ struct RankPlan {
     std::vector<int32_t> neighbors;
     std::vector<int32_t> send_off, send_slot, recv_off;
     std::vector<int32_t> owner;       // global element -> rank
+    std::vector<uint8_t> node_owned;  // N: 1 if this rank is the lowest one touching the node
     // Element chunks (one CTA each): <= kChunk consecutive local elements, never
     // straddling the boundary/interior split; each chunk's unique nodes are
     // staged in shared memory and elements address them by a 16-bit index.
@@ -122,7 +123,10 @@ void build_chunks(RankPlan& r);
 // and first-touch node order.
 RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nranks, int rank, int reorder);
 
-// Critical timestep (mesh.hpp:92-97).
+// Critical timestep (mesh.hpp:92-97).  The problem must be validated
+// first (element indices are dereferenced unchecked).
 void critical_timestep(const tvegpu_problem& p, double* thermal, double* mechanical);
+// The same from the smallest element edge L (GlobalMesh::min_edge, same arithmetic).
+void critical_timestep_from_edge(const tvegpu_problem& p, double L, double* thermal, double* mechanical);
 
 }  // namespace tvegpu

@@ -102,6 +102,7 @@ EXPORTS = {
     "tvegpu_set_state": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp, C.c_double, C.c_int64]),
     "tvegpu_set_nodal_sources": (C.c_int, [C.c_void_p, _dp]),
     "tvegpu_step_io": (C.c_int, [C.c_void_p, _dp, C.c_int64, _dp, _dp]),
+    "tvegpu_set_motion_override": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, _ip]),
     "tvegpu_get_summary": (C.c_int, [C.c_void_p, C.c_void_p]),
     "tvegpu_total_energy": (C.c_int, [C.c_void_p, _dp, _dp]),
     "tvegpu_load_mesh": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(C.c_void_p), C.c_void_p]),
@@ -129,6 +130,17 @@ EXPORTS = {
     "tvegpu_group_create": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]),
     "tvegpu_group_step": (C.c_int, [C.c_void_p, C.c_int64]),
     "tvegpu_group_get_fields": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
+    "tvegpu_group_get_state": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp]),
+    "tvegpu_group_set_state": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp, C.c_double, C.c_int64]),
+    "tvegpu_group_set_nodal_sources": (C.c_int, [C.c_void_p, _dp]),
+    "tvegpu_group_step_io": (C.c_int, [C.c_void_p, _dp, C.c_int64, _dp, _dp]),
+    "tvegpu_group_time": (C.c_double, [C.c_void_p]),
+    "tvegpu_group_step_count": (C.c_int64, [C.c_void_p]),
+    "tvegpu_group_last_error": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_int64),
+                                          C.POINTER(C.c_int32)]),
+    "tvegpu_group_checkpoint_size": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+    "tvegpu_group_save_checkpoint": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
+    "tvegpu_group_load_checkpoint": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "tvegpu_group_destroy": (None, [C.c_void_p]),
 }
 
@@ -155,17 +167,52 @@ def lib():
     return _LIB
 
 
+# tvegpu_motion_fn: int32 (*)(void* user, int32 node, double t, double* disp)
+MOTION_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int32, C.c_double, _dp)
+
+
+def motion_callback(fn):
+    """Wraps fn(node, t) -> None or (dx, dy, dz) as a tvegpu_motion_fn (keep a reference)."""
+    def cb(_user, node, t, out):
+        v = fn(int(node), float(t))
+        if v is None:
+            return 0
+        out[0], out[1], out[2] = float(v[0]), float(v[1]), float(v[2])
+        return 1
+    return MOTION_FN(cb)
+
+
 class _Summary(C.Structure):
     _fields_ = [("steps", C.c_int64), ("time", C.c_double), ("max_temperature", C.c_double),
                 ("min_disp", C.c_double * 3), ("max_disp", C.c_double * 3)]
 
 
-def _f64(a):
-    return np.ascontiguousarray(a, dtype=np.float64)
-
-
 def _P(a):
     return None if a is None else a.ctypes.data_as(_dp)
+
+
+def _in(a, n, name):
+    """An input array for the C side: float64, C-contiguous, exactly n values (a copy
+    only when the caller's array is not already in that form)."""
+    if a is None:
+        return None
+    v = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+    if v.size != n:
+        raise ValueError(f"{name}: expected {n} values, got {v.size}")
+    return v
+
+
+def _out(a, n, name):
+    """A caller-supplied output buffer the C side writes n doubles into: it must be
+    float64, C-contiguous and hold exactly n values (no silent copy: the caller
+    expects the data in this very array)."""
+    if a is None:
+        return None
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous or not a.flags.writeable:
+        raise ValueError(f"{name}: expected a writeable C-contiguous float64 numpy array")
+    if a.size != n:
+        raise ValueError(f"{name}: expected {n} values, got {a.size}")
+    return a
 
 
 def critical_timestep(problem: Problem):
@@ -271,16 +318,18 @@ def plan(problem: Problem, nranks=1, rank=0, reorder=True):
 
 
 class PartitionGroup:
-    """nparts RCB partitions of one problem stepped in lockstep on one GPU, halo by
-    device copies: the multi-GPU data path, validated without a second GPU."""
+    """nparts RCB partitions of one problem stepped together on one GPU by the
+    multi-GPU step code (tvegpu_group_*; the halo moves by device copies instead of
+    NCCL): the same calls as :class:`Engine`."""
 
-    def __init__(self, problem: Problem, nparts: int, *, device: int = -1):
+    def __init__(self, problem: Problem, nparts: int, *, device: int = -1, steps_per_graph: int = 64):
         L = lib()
         self.problem = problem
         self._c, self._keep = problem.to_c()
         o = COptions()
         L.tvegpu_default_options(C.byref(o))
         o.device = device
+        o.steps_per_graph = steps_per_graph
         h = C.c_void_p()
         rc = L.tvegpu_group_create(C.byref(self._c), nparts, C.byref(o), C.byref(h))
         if rc:
@@ -299,19 +348,78 @@ class PartitionGroup:
         except Exception:
             pass
 
+    def _raise(self, rc):
+        msg = C.create_string_buffer(512)
+        st, nd = C.c_int64(-1), C.c_int32(-1)
+        lib().tvegpu_group_last_error(self._h, msg, 512, C.byref(st), C.byref(nd))
+        text = msg.value.decode()
+        if rc == 3:
+            raise InstabilityError(text, st.value, nd.value)
+        if rc == 2:
+            raise ValidationError(text, st.value, nd.value)
+        raise _BY_STATUS.get(rc, TveError)(text)
+
     def step(self, n: int = 1):
         rc = lib().tvegpu_group_step(self._h, n)
         if rc:
-            raise _BY_STATUS.get(rc, TveError)(f"partition group step failed (status {rc})")
+            self._raise(rc)
 
-    def fields(self):
+    def time(self) -> float:
+        return lib().tvegpu_group_time(self._h)
+
+    def step_count(self) -> int:
+        return lib().tvegpu_group_step_count(self._h)
+
+    def state(self):
         T = np.full(self.N, np.nan)
         u = np.full(3 * self.N, np.nan)
+        up = np.full(3 * self.N, np.nan)
         th = np.full(9 * self.E * self.P, np.nan)
-        rc = lib().tvegpu_group_get_fields(self._h, _P(T), _P(u), _P(th) if th.size else None)
+        rc = lib().tvegpu_group_get_state(self._h, _P(T), _P(u), _P(up), _P(th) if th.size else None)
         if rc:
-            raise _BY_STATUS.get(rc, TveError)(f"partition group readback failed (status {rc})")
-        return dict(T=T, u=u, viscous=th)
+            self._raise(rc)
+        return dict(T=T, u=u, u_prev=up, viscous=th, time=self.time(), step=self.step_count())
+
+    def fields(self):
+        s = self.state()
+        return dict(T=s["T"], u=s["u"], viscous=s["viscous"])
+
+    def set_state(self, T=None, u=None, u_prev=None, viscous=None, time=0.0, step=0):
+        arrs = [_in(T, self.N, "T"), _in(u, 3 * self.N, "u"), _in(u_prev, 3 * self.N, "u_prev"),
+                _in(viscous, 9 * self.E * self.P, "viscous")]
+        rc = lib().tvegpu_group_set_state(self._h, *(_P(a) for a in arrs), time, step)
+        if rc:
+            self._raise(rc)
+
+    def set_nodal_sources(self, power):
+        self._src = _in(power, self.N, "power")
+        rc = lib().tvegpu_group_set_nodal_sources(self._h, _P(self._src))
+        if rc:
+            self._raise(rc)
+
+    def step_io(self, power=None, n=1, T=None, u=None):
+        src = _in(power, self.N, "power")
+        rc = lib().tvegpu_group_step_io(self._h, _P(src), int(n), _P(_out(T, self.N, "T")),
+                                        _P(_out(u, 3 * self.N, "u")))
+        if rc:
+            self._raise(rc)
+        return T, u
+
+    def save_checkpoint(self) -> bytes:
+        n = C.c_uint64()
+        rc = lib().tvegpu_group_checkpoint_size(self._h, C.byref(n))
+        if rc:
+            self._raise(rc)
+        buf = C.create_string_buffer(n.value)
+        rc = lib().tvegpu_group_save_checkpoint(self._h, buf, n.value)
+        if rc:
+            self._raise(rc)
+        return buf.raw
+
+    def load_checkpoint(self, data):
+        rc = lib().tvegpu_group_load_checkpoint(self._h, bytes(data), len(data))
+        if rc:
+            self._raise(rc)
 
 
 class Engine:
@@ -390,15 +498,15 @@ class Engine:
         return lib().tvegpu_step_count(self._h)
 
     def temperatures(self, out=None):
-        T = np.empty(self.N) if out is None else out
+        T = np.empty(self.N) if out is None else _out(out, self.N, "out")
         rc = lib().tvegpu_get_temperatures(self._h, _P(T))
         if rc:
             self._raise(rc)
         return T
 
     def displacements(self, out=None, out_prev=None):
-        u = np.empty(3 * self.N) if out is None else out
-        rc = lib().tvegpu_get_displacements(self._h, _P(u), _P(out_prev))
+        u = np.empty(3 * self.N) if out is None else _out(out, 3 * self.N, "out")
+        rc = lib().tvegpu_get_displacements(self._h, _P(u), _P(_out(out_prev, 3 * self.N, "out_prev")))
         if rc:
             self._raise(rc)
         return u
@@ -494,8 +602,8 @@ class Engine:
     def step_io(self, power=None, n=1, T=None, u=None):
         """set_nodal_sources(power) + step(n) + make_snapshot(T, u) in one call, the
         host copies overlapped with the step (tvegpu_step_io).  T/u are filled in place."""
-        src = None if power is None else _f64(power)
-        rc = lib().tvegpu_step_io(self._h, _P(src), int(n), _P(T), _P(u))
+        src = _in(power, self.N, "power")
+        rc = lib().tvegpu_step_io(self._h, _P(src), int(n), _P(_out(T, self.N, "T")), _P(_out(u, 3 * self.N, "u")))
         if power is not None:
             self._src = src
         if rc:
@@ -504,8 +612,8 @@ class Engine:
 
     def make_snapshot(self, T=None, u=None):
         """Engine::make_snapshot (engine.hpp:99): T and u in one device read."""
-        T = np.empty(self.N) if T is None else T
-        u = np.empty(3 * self.N) if u is None else u
+        T = np.empty(self.N) if T is None else _out(T, self.N, "T")
+        u = np.empty(3 * self.N) if u is None else _out(u, 3 * self.N, "u")
         rc = lib().tvegpu_make_snapshot(self._h, _P(T), _P(u))
         if rc:
             self._raise(rc)
@@ -524,14 +632,30 @@ class Engine:
         return dict(T=T, u=u, u_prev=up, viscous=th, time=self.time(), step=self.step_count())
 
     def set_state(self, T=None, u=None, u_prev=None, viscous=None, time=0.0, step=0):
-        arrs = [None if a is None else _f64(a).reshape(-1) for a in (T, u, u_prev, viscous)]
+        arrs = [_in(T, self.N, "T"), _in(u, 3 * self.N, "u"), _in(u_prev, 3 * self.N, "u_prev"),
+                _in(viscous, 9 * self.E * self.P, "viscous")]
         rc = lib().tvegpu_set_state(self._h, *(_P(a) for a in arrs), time, step)
         if rc:
             self._raise(rc)
 
     def set_nodal_sources(self, power):
-        self._src = None if power is None else _f64(power)
+        self._src = _in(power, self.N, "power")
         rc = lib().tvegpu_set_nodal_sources(self._h, _P(self._src))
+        if rc:
+            self._raise(rc)
+
+    # ---- MechBCs::motion_override (mechanics.hpp:43-46)
+    def set_motion_override(self, fn, nodes=None):
+        """fn(node, t) -> None or (dx, dy, dz): pins original node `node` at time t, applied
+        after the fixed / prescribed components of every step (slow path: one host
+        evaluation per candidate node and step).  nodes limits the candidates (default:
+        every node, as the reference evaluates it).  fn = None removes it."""
+        self._motion = None if fn is None else motion_callback(fn)
+        ids = None if nodes is None else np.ascontiguousarray(nodes, dtype=np.int32).reshape(-1)
+        self._motion_nodes = ids
+        rc = lib().tvegpu_set_motion_override(self._h, C.cast(self._motion, C.c_void_p) if fn is not None else None,
+                                              None, 0 if ids is None else ids.size,
+                                              None if ids is None else ids.ctypes.data_as(_ip))
         if rc:
             self._raise(rc)
 

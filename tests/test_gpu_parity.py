@@ -242,22 +242,6 @@ def test_unstable_dt_refused():
         tg.Engine(p)
 
 
-@pytest.mark.parametrize("kind,n", [(H8, 6), (T4, 5)])
-@pytest.mark.parametrize("nparts", [2, 3, 4, 8])
-def test_partitioned_path_bit_identical(kind, n, nparts):
-    """The multi-GPU data path (RCB partitions, boundary-first elements, halo pack,
-    receive-area gathers in canonical order), run as lockstep partitions on one GPU,
-    reproduces the single-partition state bit for bit."""
-    p = configs.small_problem(kind=kind, n=n, steps=25)
-    one = tg.Engine(p)
-    one.step(25)
-    grp = tg.engine.PartitionGroup(p, nparts)
-    grp.step(25)
-    a, b = one.state(), grp.fields()
-    for k in ("T", "u", "viscous"):
-        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
-
-
 @pytest.mark.parametrize("kind", [T4, H8])
 @pytest.mark.parametrize("mode", [COUPLED, THERMAL_ONLY, MECHANICAL_ONLY])
 @pytest.mark.parametrize("n", [1, 2, 70])

@@ -1,0 +1,170 @@
+"""The multi-GPU step code on one GPU: RCB partitions stepped by
+enqueue_partitioned_step — boundary-first element launches, halo pack + ev_pack on the
+compute stream, the exchange on each partition's comm stream ending in ev_comm,
+interior elements, the node kernels after ev_comm, CUDA-graph capture of all
+partitions' streams, agreement on the first failure and the device state gather of
+checkpoints.  Only the transport differs from one NCCL rank per GPU: a device copy of
+each neighbour's packed segment instead of ncclSend/ncclRecv (engine.cu
+LoopbackTransport vs NcclTransport).
+
+Partition invariance is bit-exact by construction (canonical gather order over
+replicated nodes, node constants built once on the global mesh; engine.hpp:80-82
+determinism claim), so every comparison here is array_equal.
+"""
+import numpy as np
+import pytest
+
+import paper_2009_10400_b200 as tg
+from paper_2009_10400_b200 import configs
+from paper_2009_10400_b200.engine import PartitionGroup
+from paper_2009_10400_b200.problem import COUPLED, H8, MECHANICAL_ONLY, T4, THERMAL_ONLY
+
+pytestmark = pytest.mark.gpu
+FIELDS = ("T", "u", "u_prev", "viscous")
+
+
+def assert_same(a, b, keys=FIELDS):
+    for k in keys:
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+    assert a["time"] == b["time"] and a["step"] == b["step"]
+
+
+@pytest.mark.parametrize("kind,n", [(H8, 6), (T4, 5)])
+@pytest.mark.parametrize("nparts", [2, 3, 4, 8])
+@pytest.mark.parametrize("spg", [7, 64])
+def test_partitioned_step_bit_identical(kind, n, nparts, spg):
+    """P partitions (graph chunks of 7 or 64 steps, so several replays plus direct
+    remainders) reproduce the single-partition state bit for bit."""
+    steps = 150
+    p = configs.small_problem(kind=kind, n=n, steps=steps)
+    one = tg.Engine(p)
+    one.step(steps)
+    grp = PartitionGroup(p, nparts, steps_per_graph=spg)
+    grp.step(3)  # plain steps first, then graph replays
+    grp.step(steps - 3)
+    assert_same(one.state(), grp.state())
+
+
+@pytest.mark.parametrize("mode", [THERMAL_ONLY, MECHANICAL_ONLY])
+def test_partitioned_modes(mode):
+    p = configs.small_problem(kind=H8, n=5, steps=80)
+    p.mode = mode
+    one = tg.Engine(p)
+    one.step(80)
+    grp = PartitionGroup(p, 4, steps_per_graph=16)
+    grp.step(80)
+    assert_same(one.state(), grp.state())
+
+
+def test_partitioned_source_windows():
+    """Source windows switching mid-run split the graph chunks on every partition alike."""
+    p = configs.small_problem(kind=T4, n=5, steps=100)
+    p.sources[0].t_start, p.sources[0].t_end = 9.5 * p.dt, 61.5 * p.dt
+    one = tg.Engine(p)
+    one.step(100)
+    grp = PartitionGroup(p, 3, steps_per_graph=16)
+    grp.step(100)
+    assert_same(one.state(), grp.state())
+
+
+@pytest.mark.parametrize("kind", [T4, H8])
+@pytest.mark.parametrize("mode", [COUPLED, THERMAL_ONLY])
+def test_partitioned_step_io(kind, mode):
+    """tvegpu_group_step_io == the single engine's tvegpu_step_io, bit for bit, for a
+    changing source schedule (the partitioned form a NCCL rank runs)."""
+    p = configs.small_problem(kind=kind, n=4, steps=60)
+    p.mode = mode
+    a = tg.Engine(p)
+    g = PartitionGroup(p, 4, steps_per_graph=8)
+    rng = np.random.default_rng(3)
+    Ta, ua = np.empty(p.num_nodes), np.empty(3 * p.num_nodes)
+    Tg, ug = np.empty(p.num_nodes), np.empty(3 * p.num_nodes)
+    for n in (1, 2, 17):
+        q = rng.uniform(0, 2e-3, p.num_nodes)
+        a.step_io(q, n, Ta, ua)
+        g.step_io(q, n, Tg, ug)
+        np.testing.assert_array_equal(Ta, Tg)
+        np.testing.assert_array_equal(ua, ug)
+    assert_same(a.state(), g.state())
+
+
+def test_partitioned_checkpoint_round_trip():
+    """SPEC.md:386/395 across partition counts: save from 4 partitions (device gather +
+    all-reduce through the transport), load into 2 partitions and into one engine, run
+    on; all bit-identical to the uninterrupted single-partition run.  The image itself
+    equals the one a single-partition engine writes, byte for byte."""
+    p = configs.small_problem(kind=H8, n=6, steps=60)
+    ref = tg.Engine(p)
+    ref.step(25)
+    g4 = PartitionGroup(p, 4, steps_per_graph=8)
+    g4.step(25)
+    q = np.random.default_rng(4).uniform(0, 1e-3, p.num_nodes)  # with a source override in the image
+    ref.set_nodal_sources(q)
+    g4.set_nodal_sources(q)
+    img = g4.save_checkpoint()
+    assert img == ref.save_checkpoint()
+    ref.step(35)
+    g2 = PartitionGroup(p, 2, steps_per_graph=8)
+    g2.load_checkpoint(img)
+    g2.step(35)
+    e1 = tg.Engine(p)
+    e1.load_checkpoint(img)
+    e1.step(35)
+    assert_same(ref.state(), g2.state())
+    assert_same(ref.state(), e1.state())
+    # and back: the single engine's image loads into 4 partitions
+    g4b = PartitionGroup(p, 4)
+    g4b.load_checkpoint(e1.save_checkpoint())
+    assert_same(e1.state(), g4b.state())
+
+
+@pytest.mark.parametrize("kind", [T4, H8])
+def test_partitioned_failure_is_collective(kind):
+    """A NaN injected into one node (held by one or several partitions): every partition
+    reports the same InstabilityError (step, node) as the single engine, the group's
+    state is then refused until set_state, and after a reset the group runs on bit-
+    identically to the single engine (ADVICE: the halt must not leave partitions at
+    different steps silently)."""
+    p = configs.small_problem(kind=kind, n=5, steps=40)
+    p.expansion_enabled = False  # the NaN would reach F_ther and be reported as an element error instead
+    one = tg.Engine(p)
+    grp = PartitionGroup(p, 4, steps_per_graph=4)
+    one.step(5)
+    grp.step(5)
+    s = one.state()
+    T = s["T"].copy()
+    T[p.num_nodes // 2] = np.nan
+    for e in (one, grp):
+        e.set_state(T, s["u"], s["u_prev"], s["viscous"], s["time"], s["step"])
+    with pytest.raises(tg.InstabilityError) as e1:
+        one.step(10)
+    with pytest.raises(tg.InstabilityError) as eg:
+        grp.step(10)
+    assert (eg.value.step, eg.value.node) == (e1.value.step, e1.value.node)
+    assert grp.step_count() == one.step_count() and grp.time() == one.time()
+    with pytest.raises(tg.InstabilityError, match="invalid"):
+        grp.state()
+    with pytest.raises(tg.InstabilityError):  # halted until reset
+        grp.step(1)
+    s = one.state()
+    s["T"][np.isnan(s["T"])] = 37.0
+    for e in (one, grp):
+        e.set_state(s["T"], s["u"], s["u_prev"], s["viscous"], s["time"], s["step"])
+        e.step(7)
+    assert_same(one.state(), grp.state())
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("nparts", [2, 8])
+def test_cfg4_partitions_bit_identical(nparts):
+    """cfg4 (1M-element H8, the benchmark workload) at 200 steps: 2 and 8 partitions
+    (multi-chunk boundary ordering, 128-element chunks on both sides of each cut)
+    bit-identical to one partition."""
+    p = configs.cfg4(steps=200)
+    one = tg.Engine(p)
+    one.step(200)
+    a = one.state()
+    one.close()
+    grp = PartitionGroup(p, nparts)
+    grp.step(200)
+    assert_same(a, grp.state())
