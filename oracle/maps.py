@@ -111,6 +111,8 @@ def rank_plan(nodes, el, nranks=1, rank=0, reorder=True):
         keys = morton_keys(c, lo, morton_scale(c, lo, hi, min_edge(nodes, el)))
         bnd = bnd[np.lexsort((bnd, keys[bnd]))]
         inr = inr[np.lexsort((inr, keys[inr]))]
+        if len(bnd) % 2 == 1 and len(inr):  # even chunk starts (plan.cpp: aligned element rows)
+            bnd, inr = np.append(bnd, inr[0]), inr[1:]
         elem_orig = np.concatenate([bnd, inr]).astype(np.int32)
         seen = np.full(N, -1, np.int64)
         node_orig = []

@@ -350,9 +350,18 @@ struct LoopbackTransport final : Transport {
     }
 };
 
-// staged planes: (ux,uy), (uz,T) [+ (x,y), (z,-) without precomputed geometry]
-size_t chunk_smem(const tvegpu_engine* h) {
-    return (size_t)(TVEGPU_GEO ? 2 : 4) * h->prm.max_chunk_nodes * sizeof(double2);
+// element-kernel dynamic shared memory: mbarrier, the chunk's element rows (TMA),
+// the staged node planes (ux,uy), (uz,T)
+size_t elem_smem(const tvegpu_engine* h, int rows) {
+    return kRowsOffset + (size_t)rows * kChunkThreads * sizeof(double) + 2 * (size_t)h->prm.max_chunk_nodes * sizeof(double2);
+}
+size_t k1_smem(const tvegpu_engine* h) { return elem_smem(h, kTmaK1 ? k1_rows().total() : 0); }
+size_t k3_smem(const tvegpu_engine* h) {
+    const int exp = h->prm.exp_kind < 0 ? 0 : (h->prm.exp_kind == 0 ? 1 : 2);
+    const RowPlan r = h->nn == 8 ? (exp == 2 ? k3_rows<8, 2>(h->prm) : k3_rows<8, 0>(h->prm))
+                                 : (exp == 2 ? k3_rows<4, 2>(h->prm) : k3_rows<4, 0>(h->prm));
+    const bool xst = h->nn == 8 ? k3_xstage<8>() : k3_xstage<4>();
+    return elem_smem(h, kTmaK3 ? r.total() : 0) + (xst ? (size_t)h->prm.xstride * sizeof(double) : 0);
 }
 
 // Launches a step kernel on the compute stream, with programmatic stream
@@ -381,7 +390,7 @@ NodeKernel thermal_node_kernel(const tvegpu_engine* h) {
 template <int NN>
 void launch_mech_element(tvegpu_engine* h, int c0, int c1) {
     if (c1 <= c0) return;
-    const size_t sm = chunk_smem(h);
+    const size_t sm = k3_smem(h);
     switch (h->prm.exp_kind < 0 ? 0 : (h->prm.exp_kind == 0 ? 1 : 2)) {
         case 0: launch_step_kernel(h, k_mech_element<NN, 0>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
         case 1: launch_step_kernel(h, k_mech_element<NN, 1>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
@@ -392,7 +401,7 @@ void launch_mech_element(tvegpu_engine* h, int c0, int c1) {
 template <int NN>
 void launch_thermal_element(tvegpu_engine* h, int c0, int c1) {
     if (c1 <= c0) return;
-    launch_step_kernel(h, k_thermal_element<NN>, c1 - c0, kChunkThreads, chunk_smem(h), h->prm, h->ptr, h->cur, c0, c1);
+    launch_step_kernel(h, k_thermal_element<NN>, c1 - c0, kChunkThreads, k1_smem(h), h->prm, h->ptr, h->cur, c0, c1);
 }
 void launch_thermal_elements(tvegpu_engine* h, int c0, int c1) {
     h->nn == 4 ? launch_thermal_element<4>(h, c0, c1) : launch_thermal_element<8>(h, c0, c1);
@@ -416,7 +425,7 @@ void launch_mech_node(tvegpu_engine* h, double* u_out) {
 }
 
 void set_smem_limits(tvegpu_engine* h) {
-    const int sm = (int)chunk_smem(h);
+    const int sm = (int)std::max(k1_smem(h), k3_smem(h));
     if (sm <= 48 * 1024) return;
     auto attr = [&](const void* f) { CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); };
     attr((const void*)k_thermal_element<4>);
@@ -770,6 +779,7 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     DevParams& m = h->prm;
     m.nn = nn;
     m.E = E;
+    m.es = ((E + 1) + 15) / 16 * 16;  // per-element row stride: 128-byte aligned rows, one pad element
     m.N = N;
     m.P = P;
     m.mode = p.mode;
@@ -868,25 +878,53 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
             }
         h->ptr.stage_ent = reinterpret_cast<const int2*>(dupload(own, ent, s));
         m.stage_stride = st;
+        // K3's coordinate blocks (k3_xstage): per chunk its nodes' reference coordinates in
+        // shared-slot order, x[S] y[S] z[S] with S = slots used (even), one bulk copy each
+        const int ms2 = (m.max_chunk_nodes + 1) & ~1;
+        m.xstride = 3 * ms2;
+        if (pl.nn == 8 ? k3_xstage<8>() : k3_xstage<4>()) {
+            std::vector<double> cx((size_t)nc * m.xstride, 0.0);
+            std::vector<int32_t> cs(std::max(1, nc), 2);
+#pragma omp parallel for schedule(static)
+            for (int c = 0; c < nc; ++c) {
+                int S = 0;
+                for (int u = pl.chunk_node_off[c]; u < pl.chunk_node_off[c + 1]; ++u)
+                    S = std::max(S, (int)pl.chunk_node_slot[u] + 1);
+                S = std::max(2, (S + 1) & ~1);
+                cs[c] = S;
+                double* b = cx.data() + (size_t)c * m.xstride;
+                for (int u = pl.chunk_node_off[c]; u < pl.chunk_node_off[c + 1]; ++u) {
+                    const int sl = pl.chunk_node_slot[u];
+                    const size_t o = 3 * (size_t)pl.node_orig[pl.chunk_nodes[u]];
+                    b[sl] = p.nodes[o];
+                    b[S + sl] = p.nodes[o + 1];
+                    b[2 * S + sl] = p.nodes[o + 2];
+                }
+            }
+            h->ptr.chunk_x = dupload(own, cx, s);
+            h->ptr.chunk_xs = dupload(own, cs, s);
+            CU(cudaStreamSynchronize(s));
+        }
     }
     CU(cudaStreamSynchronize(s));
     set_smem_limits(h);
     // PDL only where the four step kernels follow each other directly on one stream
     h->pdl = !loopback && pl.nranks == 1 && !std::getenv("TVEGPU_NO_PDL");
     h->ptr.elem_orig = dupload(own, pl.elem_orig, s);
-    h->ptr.theta = dalloc<double>(own, (size_t)6 * P * E);
-    CU(cudaMemsetAsync(h->ptr.theta, 0, std::max<size_t>(1, (size_t)6 * P * E) * 8, s));
+    const size_t es = (size_t)m.es;
+    h->ptr.theta = dalloc<double>(own, (size_t)6 * P * es);
+    CU(cudaMemsetAsync(h->ptr.theta, 0, std::max<size_t>(1, (size_t)6 * P * es) * 8, s));
     if (p.fiber_dirs && m.fiber_mode == 2) {
-        std::vector<double> f((size_t)3 * E);
+        std::vector<double> f((size_t)3 * es, 0.0);
         for (int e = 0; e < E; ++e)
-            for (int k = 0; k < 3; ++k) f[(size_t)k * E + e] = p.fiber_dirs[3 * (size_t)pl.elem_orig[e] + k];
+            for (int k = 0; k < 3; ++k) f[(size_t)k * es + e] = p.fiber_dirs[3 * (size_t)pl.elem_orig[e] + k];
         h->ptr.fiber = dupload(own, f, s);
         CU(cudaStreamSynchronize(s));
     }
     if (p.expansion_axes && expansion) {
-        std::vector<double> f((size_t)6 * E);
+        std::vector<double> f((size_t)6 * es, 0.0);
         for (int e = 0; e < E; ++e)
-            for (int k = 0; k < 6; ++k) f[(size_t)k * E + e] = p.expansion_axes[6 * (size_t)pl.elem_orig[e] + k];
+            for (int k = 0; k < 6; ++k) f[(size_t)k * es + e] = p.expansion_axes[6 * (size_t)pl.elem_orig[e] + k];
         h->ptr.axes = dupload(own, f, s);
         CU(cudaStreamSynchronize(s));
     }
@@ -909,16 +947,20 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
         CU(cudaStreamSynchronize(s));
     }
     {  // per-element reference geometry, once (k_geometry, same arithmetic as the in-kernel path);
-       // built in every variant: the step kernels read it with TVEGPU_GEO, the run-level
+       // read by the element kernels (TMA rows) and by the run-level
        // energy reduction always
         if (!h->d_conn) {
             h->d_conn = dalloc<int32_t>(own, pl.conn.size());
             CU(cudaMemcpyAsync(h->d_conn, pl.conn.data(), pl.conn.size() * 4, cudaMemcpyHostToDevice, s));
         }
-        double* geo = dalloc<double>(own, (size_t)kGeoRows * std::max(1, pl.E));
+        // A, V (10 rows) for K1 and the run-level energy; + the H8 hourglass vectors when K3
+        // reads them instead of rebuilding them from the chunk coordinates (k3_xstage)
+        const int grows = (nn == 8 && !k3_xstage<8>()) ? kGeoRows : 10;
+        double* geo = dalloc<double>(own, (size_t)grows * es);
+        CU(cudaMemsetAsync(geo, 0, (size_t)grows * es * 8, s));  // the pad columns feed whole-chunk bulk copies
         if (pl.E > 0) {
-            if (nn == 8) k_geometry<8><<<blocks(pl.E, 256), 256, 0, s>>>(h->ptr.X, h->d_conn, pl.E, geo);
-            else k_geometry<4><<<blocks(pl.E, 256), 256, 0, s>>>(h->ptr.X, h->d_conn, pl.E, geo);
+            if (nn == 8) k_geometry<8><<<blocks(pl.E, 256), 256, 0, s>>>(h->ptr.X, h->d_conn, pl.E, m.es, grows, geo);
+            else k_geometry<4><<<blocks(pl.E, 256), 256, 0, s>>>(h->ptr.X, h->d_conn, pl.E, m.es, grows, geo);
             CU(cudaGetLastError());
         }
         h->ptr.geo = geo;
@@ -1363,8 +1405,8 @@ __global__ void __launch_bounds__(kRedThreads) k_energy(const DevParams P, const
                     for (int i = 0; i < 3; ++i) H[i * 3 + j] += h8s(q, j) * u[q][i];
         }
         double A[9];
-        for (int q = 0; q < 9; ++q) A[q] = D.geo[(size_t)q * E + e];
-        const double V = D.geo[(size_t)9 * E + e];
+        for (int q = 0; q < 9; ++q) A[q] = D.geo[(size_t)q * P.es + e];
+        const double V = D.geo[(size_t)9 * P.es + e];
         double F[9];
         for (int i = 0; i < 3; ++i)
             for (int j = 0; j < 3; ++j)
@@ -1375,8 +1417,8 @@ __global__ void __launch_bounds__(kRedThreads) k_energy(const DevParams P, const
             const double dT = Ts / NN - P.Tref;
             double m[3], n[3];
             for (int k = 0; k < 3; ++k) {
-                m[k] = P.axes_per_elem ? D.axes[k * E + e] : P.axis_m[k];
-                n[k] = P.axes_per_elem ? D.axes[(3 + k) * E + e] : P.axis_n[k];
+                m[k] = P.axes_per_elem ? D.axes[(size_t)k * P.es + e] : P.axis_m[k];
+                n[k] = P.axes_per_elem ? D.axes[(size_t)(3 + k) * P.es + e] : P.axis_n[k];
             }
             const double ei = P.alpha_i * dT;
             const double dm = P.exp_kind >= 1 ? P.alpha_m * dT - ei : 0.0;
@@ -1401,7 +1443,7 @@ __global__ void __launch_bounds__(kRedThreads) k_energy(const DevParams P, const
         double psi = 0.5 * P.mu * (Jm23 * (Cm[0] + Cm[4] + Cm[8]) - 3.0) + 0.5 * P.kappa * (J - 1.0) * (J - 1.0);
         if (P.eta_a > 0 && P.fiber_mode) {
             double fa[3];
-            for (int k = 0; k < 3; ++k) fa[k] = P.fiber_mode == 2 ? D.fiber[k * E + e] : P.fiber[k];
+            for (int k = 0; k < 3; ++k) fa[k] = P.fiber_mode == 2 ? D.fiber[(size_t)k * P.es + e] : P.fiber[k];
             double aCa = 0;
             for (int i = 0; i < 3; ++i)
                 for (int j = 0; j < 3; ++j) aCa += fa[i] * Cm[i * 3 + j] * fa[j];
@@ -1627,7 +1669,8 @@ tvegpu_status tvegpu_get_viscous(tvegpu_engine* h, double* v) {
     return guard(h, [&] {
         check_state_valid(h);
         const int E = h->plan.E, P = h->P;
-        std::vector<double> th((size_t)6 * P * E);
+        const size_t es = (size_t)h->prm.es;
+        std::vector<double> th((size_t)6 * P * es);
         if (!th.empty()) {
             CU(cudaMemcpyAsync(th.data(), h->ptr.theta, th.size() * 8, cudaMemcpyDeviceToHost, h->s));
             CU(cudaStreamSynchronize(h->s));
@@ -1636,7 +1679,7 @@ tvegpu_status tvegpu_get_viscous(tvegpu_engine* h, double* v) {
         for (int e = 0; e < E; ++e)
             for (int p = 0; p < P; ++p) {
                 double* o = v + ((size_t)h->plan.elem_orig[e] * P + p) * 9;
-                for (int q = 0; q < 9; ++q) o[q] = th[((size_t)p * 6 + map9[q]) * E + e];
+                for (int q = 0; q < 9; ++q) o[q] = th[((size_t)p * 6 + map9[q]) * es + e];
             }
         return TVEGPU_OK;
     });
@@ -1662,12 +1705,13 @@ tvegpu_status tvegpu_set_state(tvegpu_engine* h, const double* T, const double* 
         CU(cudaMemcpyAsync(h->ptr.rec1, r1.data(), N * sizeof(double4), cudaMemcpyHostToDevice, h->s));
         if (viscous && h->P) {
             const int E = h->plan.E, P = h->P;
-            std::vector<double> th((size_t)6 * P * E);
+            const size_t es = (size_t)h->prm.es;
+            std::vector<double> th((size_t)6 * P * es, 0.0);
             static const int pick[6] = {0, 4, 8, 1, 5, 2};  // xx yy zz xy yz xz from row-major 3x3
             for (int e = 0; e < E; ++e)
                 for (int p = 0; p < P; ++p) {
                     const double* iv = viscous + ((size_t)h->plan.elem_orig[e] * P + p) * 9;
-                    for (int q = 0; q < 6; ++q) th[((size_t)p * 6 + q) * E + e] = iv[pick[q]];
+                    for (int q = 0; q < 6; ++q) th[((size_t)p * 6 + q) * es + e] = iv[pick[q]];
                 }
             CU(cudaMemcpyAsync(h->ptr.theta, th.data(), th.size() * 8, cudaMemcpyHostToDevice, h->s));
             CU(cudaStreamSynchronize(h->s));
@@ -1874,14 +1918,14 @@ __global__ void k_image_nodes(const double4* __restrict__ rc, const double4* __r
     img[4 * Ng + 3 * o] = w(b.x), img[4 * Ng + 3 * o + 1] = w(b.y), img[4 * Ng + 3 * o + 2] = w(b.z);
     img[7 * Ng + o] = w(qr[i]);
 }
-__global__ void k_image_elems(const double* __restrict__ theta, const int32_t* __restrict__ elem_orig, int E, int P,
-                              unsigned long long* __restrict__ img_th) {
+__global__ void k_image_elems(const double* __restrict__ theta, const int32_t* __restrict__ elem_orig, int E, int es,
+                              int P, unsigned long long* __restrict__ img_th) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E) return;
     const size_t o = (size_t)elem_orig[e];
     for (int p = 0; p < P; ++p)
         for (int c = 0; c < 6; ++c)
-            img_th[(o * P + p) * 6 + c] = (unsigned long long)__double_as_longlong(theta[((size_t)p * 6 + c) * E + e]);
+            img_th[(o * P + p) * 6 + c] = (unsigned long long)__double_as_longlong(theta[((size_t)p * 6 + c) * es + e]);
 }
 
 // Fills the host image of a partitioned set (every part's buffer holds it after the
@@ -1906,7 +1950,8 @@ void gather_state_image(Stepper& S, std::vector<unsigned long long>& out) {
                 k_image_nodes<<<blocks(h->plan.N, 256), 256, 0, h->s>>>(rc, rp, h->ptr.qr, h->ptr.node_orig, h->d_owned,
                                                                         h->plan.N, Ng, bufs.back());
             if (P && h->plan.E)
-                k_image_elems<<<blocks(h->plan.E, 256), 256, 0, h->s>>>(h->ptr.theta, h->ptr.elem_orig, h->plan.E, (int)P,
+                k_image_elems<<<blocks(h->plan.E, 256), 256, 0, h->s>>>(h->ptr.theta, h->ptr.elem_orig, h->plan.E,
+                                                                        h->prm.es, (int)P,
                                                                         bufs.back() + 8 * Ng);
             CU(cudaGetLastError());
         }

@@ -13,11 +13,11 @@
 //   (engine.hpp:89-90, 120), so a step is 4 launches.
 //
 // fp64 throughout (north_star parity <= 1e-10).  One thread per element / node.
-// Node state is a packed 32-byte record (ux, uy, uz, T) and reference
-// coordinates a 32-byte record (x, y, z, -), so an element gathers one sector
-// per node and per field.  The element geometry (A_e with G_e = A_e Xi, V_e and
-// the H8 hourglass vectors c_al = X h_al) is computed once by k_geometry and
-// streamed SoA (TVEGPU_GEO=0 recomputes it from staged coordinates).
+// Node state is a packed 32-byte record (ux, uy, uz, T), so an element gathers one
+// sector per node.  The element geometry (A_e with G_e = A_e Xi, V_e and the H8
+// hourglass vectors c_al = X h_al) is computed once by k_geometry and stored SoA
+// with the other per-element rows (Prony history, fibres, axes); an element kernel
+// pulls its chunk's rows into shared memory with TMA bulk copies.
 // Assembly is a gather in canonical (original element, local) order — one
 // thread per node in order (H8), or two threads each summing one half and then
 // their sum (T4, > 8 contributions per node) — with a tree chosen from the
@@ -49,9 +49,20 @@ constexpr int kChunkThreads = TVEGPU_CHUNK;  // element kernels: one thread per 
 #endif
 constexpr int kMW = TVEGPU_MW;
 
-#ifndef TVEGPU_GEO
-#define TVEGPU_GEO 1  // per-element reference geometry (A, V, H8 c_al) precomputed in HBM (0: from staged X)
+#ifndef TVEGPU_TMA_ROWS
+#define TVEGPU_TMA_ROWS 3  // per-element rows into shared memory by cp.async.bulk: bit 0 K1, bit 1 K3 (else L1 prefetch)
 #endif
+constexpr bool kTmaK1 = (TVEGPU_TMA_ROWS & 1) != 0, kTmaK3 = (TVEGPU_TMA_ROWS & 2) != 0;
+// K3 rebuilds A, V (and the H8 hourglass vectors) from a bulk-copied block of the chunk's
+// node coordinates instead of reading the stored geometry rows: bit 0 T4, bit 1 H8.
+// T4 chunks hold few nodes (~9 B of coordinates per element against 80 B of rows); H8
+// chunks save more bytes but the rebuild's FP64 work and register pressure cost more
+// than they save (K3 cfg4 120.6 vs 109.1 us, measured).
+#ifndef TVEGPU_K3_XSTAGE
+#define TVEGPU_K3_XSTAGE 1
+#endif
+template <int NN>
+__host__ __device__ constexpr bool k3_xstage() { return kTmaK3 && (TVEGPU_K3_XSTAGE & (NN == 4 ? 1 : 2)) != 0; }
 
 struct Clock {
     double time;
@@ -66,6 +77,8 @@ struct DevParams {
     int stage_stride;     // entries per chunk in stage_ent (max unique nodes of a chunk)
     int ell;              // G > 0: ELL gathers with rows of 8 G slot ids (every node has <= 8 G contributions)
     int motion;           // MechBCs::motion_override active (host-evaluated pins, K4 reads motion_row/val)
+    int es;               // row stride of the per-element SoA arrays (geo, theta, fiber, axes): >= E + 1, 16-aligned
+    int xstride;          // doubles per chunk in chunk_x (3 * even max_chunk_nodes)
     double dt, mu, kappa, eta_a, kh, rho, wbcb, Ta, Qm, gamma;
     double inv_2dt, inv_dt2;  // 1/(2 dt), 1/dt^2 (Eq. 22 coefficients)
     double fiber[3];
@@ -85,10 +98,12 @@ struct DevPtrs {
     const uint16_t* chunk_node_slot;  // their shared-memory slots
     const uint16_t* lconn;          // [E][nn] index of node (e, a) in its chunk's node list
     const int2* stage_ent;          // [nchunks][stage_stride] {local node, shared slot}, {-1, 0} padded
-    const double* geo;              // TVEGPU_GEO: [kGeoRows][E] A (9, row-major), V, H8: c_al = X h_al (12)
-    double* theta;             // [P][6][E]   (xx, yy, zz, xy, yz, xz)
-    const double* fiber;       // [3][E] or null
-    const double* axes;        // [6][E] or null
+    const double* chunk_x;          // [nchunks][xstride] per chunk its nodes' coordinates by shared slot: x[S], y[S], z[S]
+    const int32_t* chunk_xs;        // [nchunks] S: slots used (even)
+    const double* geo;              // [kGeoRows][es] A (9, row-major), V, H8: c_al = X h_al (12)
+    double* theta;             // [P][6][es]   (xx, yy, zz, xy, yz, xz)
+    const double* fiber;       // [3][es] or null
+    const double* axes;        // [6][es] or null
     const int32_t* elem_orig;  // [E]
     double4* rec0;             // node record (ux, uy, uz, T), two rotating buffers
     double4* rec1;
@@ -201,34 +216,103 @@ __device__ __forceinline__ constexpr int h8h(int al, int a) {
                    : al == 1 ? h8s(a, 2) * h8s(a, 0) : al == 2 ? h8s(a, 0) * h8s(a, 1) : h8s(a, 0) * h8s(a, 1) * h8s(a, 2);
 }
 
-// Element kinematics from one pass over the element's nodes:
-//   H = U Xi^T (displacement sums), J = X Xi^T (T4: edge matrix; H8: 8 J0), Ts = sum T,
-//   gT = Xi T_e (thermal only).  Then A = J^-T (T4) or J0^-T / 8 (H8) and V (mesh.hpp:44).
-//   R and Xs point to the chunk's node records staged in shared memory.
-// A chunk's nodes staged in shared memory as four 16-byte planes, (ux, uy),
-// (uz, T), (x, y), (z, -), indexed by colour-assigned slot (plan.cpp colour_slots):
-// each quarter-warp's 16-byte reads of node a hit 8 distinct bank groups.
+// A chunk's nodes staged in shared memory as two 16-byte planes, (ux, uy) and
+// (uz, T), indexed by colour-assigned slot (plan.cpp colour_slots): each
+// quarter-warp's 16-byte reads of node a hit 8 distinct bank groups.
 struct NodeStage {
     double2* a;
     double2* b;
-    double2* c;
-    double2* d;
     __device__ __forceinline__ double4 rec(int n) const {
         const double2 p = a[n], q = b[n];
         return make_double4(p.x, p.y, q.x, q.y);
     }
-    __device__ __forceinline__ double4 X(int n) const {
-        const double2 p = c[n], q = d[n];
-        return make_double4(p.x, p.y, q.x, 0.0);
+};
+
+// ------------------------------------------------------------------ per-element rows by TMA
+// A chunk's per-element SoA rows (geometry, Prony history, per-element fibres / axes)
+// are contiguous 128-element segments: row stride P.es (a multiple of 16 elements)
+// and even chunk starts (plan.cpp) make each segment a 16-byte-aligned bulk copy.  At
+// kernel start one warp issues one cp.async.bulk per row into shared memory (none of
+// these rows is written by the predecessor kernel, so before the PDL wait), completing
+// on one mbarrier; the element threads read their column after the node staging.
+// This replaces per-thread L1 prefetches + global loads of every row.
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init_expect(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_row(double* dst, const double* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(unsigned long long* bar) {
+    asm volatile(
+        "{\n .reg .pred p;\n TMA_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+        " @!p bra TMA_WAIT_%=;\n}" ::"r"(smem_addr(bar)) : "memory");
+}
+
+// Rows of one element kernel: [0, ngeo) geometry, then 6 P Prony history, then 3
+// fibre and 6 expansion-axis rows when those are per element.
+struct RowPlan {
+    int ngeo, ntheta, nfib, nax;
+    __host__ __device__ __forceinline__ int total() const { return ngeo + ntheta + nfib + nax; }
+    __host__ __device__ __forceinline__ int theta0() const { return ngeo; }
+    __host__ __device__ __forceinline__ int fib0() const { return ngeo + ntheta; }
+    __host__ __device__ __forceinline__ int ax0() const { return ngeo + ntheta + nfib; }
+};
+
+// The element rows of this thread's chunk: shared memory (TMA) or global (L1 prefetch).
+template <bool TMA>
+struct ElemRows {
+    const double* s;  // [rows][kChunkThreads] (TMA)
+    int t;            // element within the chunk
+    // row r of the shared block, or element e of global row g
+    __device__ __forceinline__ double get(int r, const double* g) const {
+        if constexpr (TMA) return s[r * kChunkThreads + t];
+        else return __ldg(g);
     }
 };
+
+// Warp 0: issue the chunk's row copies (or, without TMA, every thread prefetches its
+// rows into L1).  e0 = first element of the chunk, ne = its element count.
+template <bool TMA>
+__device__ __forceinline__ void load_elem_rows(const DevParams& P, const DevPtrs& D, const RowPlan& rp, int e0, int ne,
+                                               double* rows, unsigned long long* bar, double* blob = nullptr,
+                                               const double* blob_src = nullptr, unsigned blob_bytes = 0) {
+    const int R = rp.total();
+    auto src = [&](int r) -> const double* {
+        if (r < rp.theta0()) return D.geo + (size_t)r * P.es;
+        if (r < rp.fib0()) return D.theta + (size_t)(r - rp.theta0()) * P.es;
+        if (r < rp.ax0()) return D.fiber + (size_t)(r - rp.fib0()) * P.es;
+        return D.axes + (size_t)(r - rp.ax0()) * P.es;
+    };
+    if constexpr (TMA) {
+        if (threadIdx.x >= 32) return;
+        const unsigned bytes = (unsigned)((ne + 1) & ~1) * 8u;  // even: 16-byte multiple (rows are padded)
+        if (threadIdx.x == 0) mbar_init_expect(bar, bytes * (unsigned)R + blob_bytes);
+        __syncwarp();
+        for (int r = threadIdx.x; r < R; r += 32) tma_row(rows + r * kChunkThreads, src(r) + e0, bytes, bar);
+        if (blob_bytes && threadIdx.x == 31) tma_row(blob, blob_src, blob_bytes, bar);
+    } else if ((int)threadIdx.x < ne) {
+        for (int r = 0; r < R; ++r) asm volatile("prefetch.global.L1 [%0];" ::"l"(src(r) + e0 + threadIdx.x));
+    }
+}
+template <bool TMA>
+__device__ __forceinline__ void wait_elem_rows(unsigned long long* bar) {
+    if constexpr (TMA) mbar_wait0(bar);
+}
+
+// Dynamic shared memory of an element kernel: [mbarrier | pad to 128 B][rows][2 staged planes].
+constexpr int kRowsOffset = 128;
 
 // Reference geometry from the element's corner coordinates, in exactly the
 // arithmetic order of element_pass: J (T4: edge matrix; H8: X Xi^T / 8), A = J^-T
 // (H8: / 8), V; and for H8 the hourglass geometry c_al = X h_al in corner order.
 constexpr int kGeoRows = 22;
 template <int NN>
-__global__ void k_geometry(const double4* __restrict__ X, const int32_t* __restrict__ conn, int E, double* geo) {
+__global__ void k_geometry(const double4* __restrict__ X, const int32_t* __restrict__ conn, int E, int es, int rows,
+                           double* geo) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E) return;
     double J[9];
@@ -267,10 +351,11 @@ __global__ void k_geometry(const double4* __restrict__ X, const int32_t* __restr
         }
 #pragma unroll
         for (int q = 0; q < 9; ++q) J[q] = J[q] / 8.0;
+        if (rows > 10)
 #pragma unroll
-        for (int al = 0; al < 4; ++al)
+            for (int al = 0; al < 4; ++al)
 #pragma unroll
-            for (int i = 0; i < 3; ++i) geo[(size_t)(10 + al * 3 + i) * E + e] = cX[al][i];
+                for (int i = 0; i < 3; ++i) geo[(size_t)(10 + al * 3 + i) * es + e] = cX[al][i];
     }
     double Ad[9];
     const double dJ = adj3(J, Ad);
@@ -278,21 +363,17 @@ __global__ void k_geometry(const double4* __restrict__ X, const int32_t* __restr
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
-        for (int j = 0; j < 3; ++j) geo[(size_t)(i * 3 + j) * E + e] = Ad[j * 3 + i] * s;
-    geo[(size_t)9 * E + e] = NN == 4 ? dJ * (1.0 / 6.0) : 8.0 * dJ;
+        for (int j = 0; j < 3; ++j) geo[(size_t)(i * 3 + j) * es + e] = Ad[j * 3 + i] * s;
+    geo[(size_t)9 * es + e] = NN == 4 ? dJ * (1.0 / 6.0) : 8.0 * dJ;
 }
 
-// Warm L1 with the element's geometry rows (constant: issued before the PDL wait).
-__device__ __forceinline__ void prefetch_geo(const DevPtrs& D, int e, int E, int rows) {
-    for (int q = 0; q < rows; ++q) asm volatile("prefetch.global.L1 [%0];" ::"l"(D.geo + (size_t)q * E + e));
-}
-
-// element_pass with precomputed geometry: only the displacement / temperature sums
-// come from the staged records; A and V are read from the geometry rows.
-template <int NN, bool WANT_GT>
-__device__ __forceinline__ void element_pass_geo(const NodeStage& S, const int (&n)[NN], const DevPtrs& D, int e,
-                                                 int E, double H[9], double A[9], double& V, double& Ts,
-                                                 double gT[3]) {
+// Element kinematics from one pass over the element's staged nodes:
+//   H = U Xi^T (displacement sums), Ts = sum T, gT = Xi T_e (thermal only);
+//   A (G_e = A Xi) and V from the geometry rows.
+template <int NN, bool WANT_GT, bool TMA, bool SUMS_ONLY = false>
+__device__ __forceinline__ void element_pass(const NodeStage& S, const int (&n)[NN], const DevParams& P,
+                                             const DevPtrs& D, const ElemRows<TMA>& rows, int e, double H[9],
+                                             double A[9], double& V, double& Ts, double gT[3]) {
     if constexpr (NN == 4) {
         const double4 r0 = S.rec(n[0]);
         Ts = r0.w;
@@ -324,60 +405,53 @@ __device__ __forceinline__ void element_pass_geo(const NodeStage& S, const int (
             }
         }
     }
+    if constexpr (SUMS_ONLY) return;
+    // ptxas would hoist these shared-memory reads up into the record loads above and
+    // spill (584 B at K3's 128 registers); a CTA-scope fence keeps them after the sums
+    if constexpr (TMA) __threadfence_block();
 #pragma unroll
-    for (int q = 0; q < 9; ++q) A[q] = __ldg(D.geo + (size_t)q * E + e);
-    V = __ldg(D.geo + (size_t)9 * E + e);
+    for (int q = 0; q < 9; ++q) A[q] = rows.get(q, D.geo + (size_t)q * P.es + e);
+    V = rows.get(9, D.geo + (size_t)9 * P.es + e);
 }
 
-template <int NN, bool WANT_GT>
-__device__ __forceinline__ void element_pass(const NodeStage& S, const int (&n)[NN], double H[9], double A[9],
-                                             double& V, double& Ts, double gT[3]) {
+// The chunk's node coordinates in shared memory by slot (k3_xstage): x[S], y[S], z[S].
+struct CoordStage {
+    const double* x;
+    const double* y;
+    const double* z;
+};
+// A (G_e = A Xi) and V from the element's corner coordinates, in exactly k_geometry's
+// arithmetic, so the result is bit-identical to the stored geometry rows.
+template <int NN>
+__device__ __forceinline__ void geometry_from_coords(const CoordStage& X, const int (&n)[NN], double A[9], double& V) {
     double J[9];
     if constexpr (NN == 4) {
-        const double4 r0 = S.rec(n[0]);
-        const double4 x0 = S.X(n[0]);
-        Ts = r0.w;
+        const double x0 = X.x[n[0]], y0 = X.y[n[0]], z0 = X.z[n[0]];
 #pragma unroll
         for (int a = 1; a < 4; ++a) {
-            const double4 r = S.rec(n[a]);
-            const double4 x = S.X(n[a]);
-            H[0 * 3 + a - 1] = r.x - r0.x;
-            H[1 * 3 + a - 1] = r.y - r0.y;
-            H[2 * 3 + a - 1] = r.z - r0.z;
-            J[0 * 3 + a - 1] = x.x - x0.x;
-            J[1 * 3 + a - 1] = x.y - x0.y;
-            J[2 * 3 + a - 1] = x.z - x0.z;
-            if constexpr (WANT_GT) gT[a - 1] = r.w - r0.w;
-            Ts += r.w;
+            J[0 * 3 + a - 1] = X.x[n[a]] - x0;
+            J[1 * 3 + a - 1] = X.y[n[a]] - y0;
+            J[2 * 3 + a - 1] = X.z[n[a]] - z0;
         }
     } else {
 #pragma unroll
-        for (int q = 0; q < 9; ++q) H[q] = J[q] = 0.0;
-        if constexpr (WANT_GT) gT[0] = gT[1] = gT[2] = 0.0;
-        Ts = 0.0;
+        for (int q = 0; q < 9; ++q) J[q] = 0.0;
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
-            const double4 r = S.rec(n[a]);
-            const double4 x = S.X(n[a]);
-            Ts += r.w;
+            const double x = X.x[n[a]], y = X.y[n[a]], z = X.z[n[a]];
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
                 const double s = (double)h8s(a, j);
-                H[0 * 3 + j] += s * r.x;
-                H[1 * 3 + j] += s * r.y;
-                H[2 * 3 + j] += s * r.z;
-                J[0 * 3 + j] += s * x.x;
-                J[1 * 3 + j] += s * x.y;
-                J[2 * 3 + j] += s * x.z;
-                if constexpr (WANT_GT) gT[j] += s * r.w;
+                J[0 * 3 + j] += s * x;
+                J[1 * 3 + j] += s * y;
+                J[2 * 3 + j] += s * z;
             }
         }
 #pragma unroll
-        for (int q = 0; q < 9; ++q) J[q] = J[q] / 8.0;  // J0 = X Xi^T / 8
+        for (int q = 0; q < 9; ++q) J[q] = J[q] / 8.0;
     }
     double Ad[9];
     const double dJ = adj3(J, Ad);
-    // A = (J^-1)^T = Ad^T / det   (H8: / 8 more); one reciprocal, fp64 division is ~15 instructions
     const double s = (NN == 4 ? 1.0 : 0.125) / dJ;
 #pragma unroll
     for (int i = 0; i < 3; ++i)
@@ -394,8 +468,7 @@ __device__ __forceinline__ void element_pass(const NodeStage& S, const int (&n)[
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// Stage one chunk: its unique nodes' (u, T) records and coordinates go to shared
-// memory once per chunk (each node is used by up to 8 of the chunk's elements),
+// Stage one chunk: its unique nodes' (u, T) records go to shared memory once per chunk (each node is used by up to 8 of the chunk's elements),
 // replacing 2*NN random 32-byte global gathers per element.  Returns this
 // thread's element (or -1) and its nodes' shared-memory slots.
 // The staging is latency-bound (a dependent index load, then the record loads),
@@ -433,12 +506,7 @@ __device__ __forceinline__ int stage_chunk(const DevPtrs& D, const double4* __re
             g[j] = en[j].x;
             s[j] = en[j].y;
         }
-        double4 r[kStageBatch], x[kStageBatch];
-#if !TVEGPU_GEO
-#pragma unroll
-        for (int j = 0; j < kStageBatch; ++j)
-            if (g[j] >= 0) x[j] = ldg4(D.X + g[j]);
-#endif
+        double4 r[kStageBatch];
         pdl_wait();  // the node records are the predecessor's output
 #pragma unroll
         for (int j = 0; j < kStageBatch; ++j)
@@ -448,10 +516,6 @@ __device__ __forceinline__ int stage_chunk(const DevPtrs& D, const double4* __re
             if (g[j] >= 0) {
                 S.a[s[j]] = make_double2(r[j].x, r[j].y);
                 S.b[s[j]] = make_double2(r[j].z, r[j].w);
-#if !TVEGPU_GEO
-                S.c[s[j]] = make_double2(x[j].x, x[j].y);
-                S.d[s[j]] = make_double2(x[j].z, x[j].w);
-#endif
             }
     }
     if constexpr (NN == 8) {
@@ -463,9 +527,6 @@ __device__ __forceinline__ int stage_chunk(const DevPtrs& D, const double4* __re
     __syncthreads();
     return e;
 }
-
-// Warm L1 with a coalesced SoA stream this thread will read later in the kernel.
-__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 // ------------------------------------------------------------------ bounds-checking build
 // TVEGPU_BOUNDS_CHECK=1 (csrc/Makefile `variant`, scripts/gpu_bounds_check.sh) asserts every
@@ -511,14 +572,10 @@ __device__ __forceinline__ void check_gather(const DevParams& P, const DevPtrs& 
 #endif
 // K1 element body: element e of the staged chunk S (n = its node slots)
 template <int NN>
-__device__ __forceinline__ void k1_body(const DevParams& P, const DevPtrs& D, const NodeStage& S, const int e,
-                                        const int (&n)[NN]) {
+__device__ __forceinline__ void k1_body(const DevParams& P, const DevPtrs& D, const NodeStage& S,
+                                        const ElemRows<kTmaK1>& rows, const int e, const int (&n)[NN]) {
     double H[9], A[9], gT[3], V, Ts;
-#if TVEGPU_GEO
-    element_pass_geo<NN, true>(S, n, D, e, P.E, H, A, V, Ts, gT);
-#else
-    element_pass<NN, true>(S, n, H, A, V, Ts, gT);
-#endif
+    element_pass<NN, true, kTmaK1>(S, n, P, D, rows, e, H, A, V, Ts, gT);
     // F = I + H A^T
     double F[9];
 #pragma unroll
@@ -567,22 +624,29 @@ __device__ __forceinline__ void k1_body(const DevParams& P, const DevPtrs& D, co
     if (dF == 0.0) atomicMin(D.err_elem, pack_elem(D.clock->step, D.elem_orig[e]));
 }
 
+// K1 rows: A (9) and V
+__host__ __device__ __forceinline__ RowPlan k1_rows() { return RowPlan{10, 0, 0, 0}; }
+
 template <int NN>
 __global__ void K1_BOUNDS k_thermal_element(const DevParams P, const DevPtrs D, int cur, int c0, int c1) {
-    extern __shared__ double2 smem_planes[];
+    extern __shared__ __align__(128) unsigned char smem[];
+    const RowPlan rp = k1_rows();
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem);
+    double* rows = reinterpret_cast<double*>(smem + kRowsOffset);
+    double2* planes = reinterpret_cast<double2*>(rows + (kTmaK1 ? rp.total() * kChunkThreads : 0));
     const int ms = P.max_chunk_nodes;
-    const NodeStage S{smem_planes, smem_planes + ms, smem_planes + 2 * ms, smem_planes + 3 * ms};
-    int n[NN];
-#if TVEGPU_GEO
+    const NodeStage S{planes, planes + ms};
+    const int c = c0 + blockIdx.x;
     {
-        const int e0 = __ldg(D.chunk_start + c0 + blockIdx.x) + threadIdx.x;
-        if (e0 < P.E) prefetch_geo(D, e0, P.E, 10);
+        const int e0 = __ldg(D.chunk_start + c), ne = __ldg(D.chunk_start + c + 1) - e0;
+        load_elem_rows<kTmaK1>(P, D, rp, e0, ne, rows, bar);
     }
-#endif
-    const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, P.stage_stride, S, n);
+    int n[NN];
+    const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c, P.stage_stride, S, n);
+    wait_elem_rows<kTmaK1>(bar);  // every thread: the CTA must not retire with bulk copies in flight
     if (D.clock->halted || e < 0) return;  // halted: uniform across the grid (read after the wait)
-    check_chunk<NN>(P, D, c0 + blockIdx.x, e, n);
-    k1_body<NN>(P, D, S, e, n);
+    check_chunk<NN>(P, D, c, e, n);
+    k1_body<NN>(P, D, S, ElemRows<kTmaK1>{rows, (int)threadIdx.x}, e, n);
     pdl_trigger();  // after this block's work: the successor fills in behind the last wave
 }
 
@@ -777,17 +841,20 @@ __global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, i
 #endif
 // K3 element body: element e of the staged chunk st (n = its node slots)
 template <int NN, int EXP>
-__device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, const NodeStage& st, const int e,
-                                        const int (&n)[NN]) {
-    const int E = P.E;
+__device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, const NodeStage& st,
+                                        const ElemRows<kTmaK3>& rows, const RowPlan& rp, const CoordStage& xs,
+                                        const int e, const int (&n)[NN]) {
+    const size_t es = (size_t)P.es;
     double Hd[9], A[9], V, Ts;
     {
         double H[9], gT[3];
-#if TVEGPU_GEO
-        element_pass_geo<NN, false>(st, n, D, e, E, H, A, V, Ts, gT);
-#else
-        element_pass<NN, false>(st, n, H, A, V, Ts, gT);
-#endif
+        if constexpr (k3_xstage<NN>()) {
+            element_pass<NN, false, kTmaK3, true>(st, n, P, D, rows, e, H, A, V, Ts, gT);
+            __threadfence_block();  // keep the coordinate reads after the record sums (register pressure)
+            geometry_from_coords<NN>(xs, n, A, V);
+        } else {
+            element_pass<NN, false, kTmaK3>(st, n, P, D, rows, e, H, A, V, Ts, gT);
+        }
         // displacement gradient Hd = F - I = H A^T, kept separate from I (small-strain accuracy)
 #pragma unroll
         for (int i = 0; i < 3; ++i)
@@ -816,8 +883,8 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
         if (P.axes_per_elem) {
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                m[k] = __ldg(D.axes + k * E + e);
-                nn_[k] = __ldg(D.axes + (3 + k) * E + e);
+                m[k] = rows.get(rp.ax0() + k, D.axes + k * es + e);
+                nn_[k] = rows.get(rp.ax0() + 3 + k, D.axes + (3 + k) * es + e);
             }
         } else {
 #pragma unroll
@@ -893,7 +960,7 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
         double fa[3];
         if (P.fiber_mode == 2) {
 #pragma unroll
-            for (int k = 0; k < 3; ++k) fa[k] = __ldg(D.fiber + k * E + e);
+            for (int k = 0; k < 3; ++k) fa[k] = rows.get(rp.fib0() + k, D.fiber + k * es + e);
         } else {
 #pragma unroll
             for (int k = 0; k < 3; ++k) fa[k] = P.fiber[k];
@@ -947,14 +1014,14 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
     for (int q = 0; q < 6; ++q) St[q] = S[q];
 #pragma unroll 1
     for (int p = 0; p < P.P; ++p) {
-        double* th = D.theta + (size_t)p * 6 * E + e;
+        double* th = D.theta + (size_t)p * 6 * es + e;
         double t[6];
 #pragma unroll
-        for (int q = 0; q < 6; ++q) t[q] = th[(size_t)q * E];
+        for (int q = 0; q < 6; ++q) t[q] = rows.get(rp.theta0() + p * 6 + q, th + q * es);
 #pragma unroll
         for (int q = 0; q < 6; ++q) {
             t[q] = P.pa[p] * S[q] + P.pb[p] * t[q];
-            th[(size_t)q * E] = t[q];
+            th[q * es] = t[q];
             St[q] -= t[q];
         }
     }
@@ -996,8 +1063,7 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
 #pragma unroll
         for (int al = 0; al < 4; ++al)
 #pragma unroll
-            for (int i = 0; i < 3; ++i) Uh[al][i] = cX[al][i] = 0.0;
-#if TVEGPU_GEO
+            for (int i = 0; i < 3; ++i) Uh[al][i] = 0.0;
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
             const double2 ra = st.a[n[a]], rb = st.b[n[a]];
@@ -1009,28 +1075,27 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
                 Uh[al][2] += h * rb.x;
             }
         }
+        if constexpr (k3_xstage<NN>()) {  // c_al = X h_al in corner order (k_geometry's arithmetic)
+            __threadfence_block();  // (keeps ptxas from hoisting these reads into the Uh sums: spills)
 #pragma unroll
-        for (int al = 0; al < 4; ++al)
+            for (int al = 0; al < 4; ++al) cX[al][0] = cX[al][1] = cX[al][2] = 0.0;
 #pragma unroll
-            for (int i = 0; i < 3; ++i) cX[al][i] = __ldg(D.geo + (size_t)(10 + al * 3 + i) * E + e);
-#else
+            for (int a = 0; a < 8; ++a) {
+                const double x = xs.x[n[a]], y = xs.y[n[a]], z = xs.z[n[a]];
 #pragma unroll
-        for (int a = 0; a < 8; ++a) {
-            const double2 ra = st.a[n[a]], rb = st.b[n[a]], xa = st.c[n[a]], xb = st.d[n[a]];
-            const double4 r = make_double4(ra.x, ra.y, rb.x, 0.0);
-            const double4 x = make_double4(xa.x, xa.y, xb.x, 0.0);
-#pragma unroll
-            for (int al = 0; al < 4; ++al) {
-                const double h = (double)h8h(al, a);
-                Uh[al][0] += h * r.x;
-                Uh[al][1] += h * r.y;
-                Uh[al][2] += h * r.z;
-                cX[al][0] += h * x.x;
-                cX[al][1] += h * x.y;
-                cX[al][2] += h * x.z;
+                for (int al = 0; al < 4; ++al) {
+                    const double h = (double)h8h(al, a);
+                    cX[al][0] += h * x;
+                    cX[al][1] += h * y;
+                    cX[al][2] += h * z;
+                }
             }
+        } else {
+#pragma unroll
+            for (int al = 0; al < 4; ++al)
+#pragma unroll
+                for (int i = 0; i < 3; ++i) cX[al][i] = rows.get(10 + al * 3 + i, D.geo + (10 + al * 3 + i) * es + e);
         }
-#endif
         const double k = P.kh * cbrt(V);
 #pragma unroll
         for (int al = 0; al < 4; ++al) {
@@ -1090,27 +1155,43 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
     }
 }
 
+// K3 rows: geometry (T4 10, H8 22 with the hourglass vectors), Prony history, and the
+// per-element fibres / expansion axes when the material has them
+template <int NN, int EXP>
+__host__ __device__ __forceinline__ RowPlan k3_rows(const DevParams& P) {
+    return RowPlan{k3_xstage<NN>() ? 0 : (NN == 8 ? kGeoRows : 10), 6 * P.P, P.fiber_mode == 2 ? 3 : 0,
+                   (EXP == 2 && P.axes_per_elem) ? 6 : 0};
+}
+
 template <int NN, int EXP>
 __global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T4 : TVEGPU_K3_MINBLOCKS)
     k_mech_element(const DevParams P, const DevPtrs D, int cur, int c0, int c1) {
-    extern __shared__ double2 smem_planes[];
+    extern __shared__ __align__(128) unsigned char smem[];
+    const RowPlan rp = k3_rows<NN, EXP>(P);
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem);
+    double* rows = reinterpret_cast<double*>(smem + kRowsOffset);
+    double* xblk = rows + (kTmaK3 ? rp.total() * kChunkThreads : 0);  // k3_xstage: the chunk's coordinates
+    double2* planes = reinterpret_cast<double2*>(xblk + (k3_xstage<NN>() ? P.xstride : 0));
     const int ms = P.max_chunk_nodes;
-    const NodeStage st{smem_planes, smem_planes + ms, smem_planes + 2 * ms, smem_planes + 3 * ms};
-    int n[NN];
-    {  // the Prony history is read late in the kernel: start pulling it into L1 now
-        const int e0 = __ldg(D.chunk_start + c0 + blockIdx.x) + threadIdx.x;
-        if (e0 < P.E)
-            for (int p = 0; p < P.P; ++p)
-#pragma unroll
-                for (int q = 0; q < 6; ++q) prefetch_l1(D.theta + ((size_t)p * 6 + q) * P.E + e0);
-#if TVEGPU_GEO
-        if (e0 < P.E) prefetch_geo(D, e0, P.E, NN == 8 ? kGeoRows : 10);
-#endif
+    const NodeStage st{planes, planes + ms};
+    const int c = c0 + blockIdx.x;
+    CoordStage xs{nullptr, nullptr, nullptr};
+    {
+        const int e0 = __ldg(D.chunk_start + c), ne = __ldg(D.chunk_start + c + 1) - e0;
+        if constexpr (k3_xstage<NN>()) {
+            const int S = __ldg(D.chunk_xs + c);
+            xs = CoordStage{xblk, xblk + S, xblk + 2 * S};
+            load_elem_rows<kTmaK3>(P, D, rp, e0, ne, rows, bar, xblk, D.chunk_x + (size_t)c * P.xstride, 24u * S);
+        } else {
+            load_elem_rows<kTmaK3>(P, D, rp, e0, ne, rows, bar);
+        }
     }
-    const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c0 + blockIdx.x, P.stage_stride, st, n);
+    int n[NN];
+    const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c, P.stage_stride, st, n);
+    wait_elem_rows<kTmaK3>(bar);  // every thread: the CTA must not retire with bulk copies in flight
     if (D.clock->halted || e < 0) return;
-    check_chunk<NN>(P, D, c0 + blockIdx.x, e, n);
-    k3_body<NN, EXP>(P, D, st, e, n);
+    check_chunk<NN>(P, D, c, e, n);
+    k3_body<NN, EXP>(P, D, st, ElemRows<kTmaK3>{rows, (int)threadIdx.x}, rp, xs, e, n);
     pdl_trigger();
 }
 

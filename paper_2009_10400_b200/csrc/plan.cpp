@@ -357,6 +357,12 @@ RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nrank
         sort_group(bnd);
         sort_group(inr);
     }
+    // chunks start at even elements (16-byte aligned per-element rows for the element
+    // kernels' bulk copies): an odd boundary group takes the first interior element
+    if (bnd.size() % 2 == 1 && !inr.empty()) {
+        bnd.push_back(inr.front());
+        inr.erase(inr.begin());
+    }
     lap("boundary split + morton sort");
     r.Eb = (int)bnd.size();
     r.elem_orig = bnd;
