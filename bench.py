@@ -6,8 +6,10 @@ Workload at N=1: cfg4 (BASELINE configs[3]) — H8 block 100^3 = 1,000,000 eleme
 1,030,301 nodes, coupled TherMechExpanTD (temperature-dependent c/k, isotropic
 thermal expansion), hourglass control, one Prony term, central RFA source.  It is
 the configuration the north_star's >= 60 % HBM-roofline target is stated on.
-At N>1 (torchrun, one rank per GPU): weak scaling, a 100a x 100b x 100c block with
-a*b*c = N, split by RCB into one 1M-element partition per GPU with the NCCL halo.
+At N>1 (torchrun, one rank per GPU): strong scaling of the fixed 16M-element H8 mesh
+(BASELINE configs[4], cfg5 H8 252^3) split by RCB into N partitions with the NCCL halo
+exchange overlapped with the interior elements; --workload cfg4 runs
+configs[3] at N GPUs instead.  Each rank reports its halo volume and exchange time.
 
 --impl reference: the reference's algorithm on the host CPU (the fp64 oracle,
 OpenMP over all host threads) on the same workload — the reference ships no
@@ -36,26 +38,30 @@ from paper_2009_10400_b200.problem import H8  # noqa: E402
 METRIC = "element-steps/s"
 
 
-def weak_block(nranks, steps):
-    """cfg4 physics on a (100a, 100b, 100c) block, a*b*c = nranks, h = 1 mm."""
-    f = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}.get(nranks)
-    if f is None:
-        a = nranks
-        f = (a, 1, 1)
-    from paper_2009_10400_b200 import meshgen
-    from paper_2009_10400_b200.problem import Prescribed, SourceRegion
-    nx, ny, nz = 100 * f[0], 100 * f[1], 100 * f[2]
-    if f == (1, 1, 1):
-        return configs.cfg4(steps=steps), "cfg4: H8 100^3 (1,000,000 el) TherMechExpanTD, hourglass, Prony P=1"
-    nodes, el = meshgen.structured_h8(100, 0.1, nx=nx, ny=ny, nz=nz)
-    p = configs._base(H8, nodes, el, 1e-4, steps)
-    top = nodes[:, 2].max()
-    p.fixed_nodes = np.nonzero(nodes[:, 2] <= 1e-12)[0].astype(np.int32)
-    p.prescribed = [Prescribed(np.nonzero(np.abs(nodes[:, 2] - top) <= 1e-9)[0].astype(np.int32), 2,
-                               1e-2 * nz / 100, configs.ramp_time(top, 1e-4, steps))]
-    c = 0.5 * np.array([nx, ny, nz]) * 1e-3
-    p.sources = [SourceRegion(meshgen.elements_in_sphere(nodes, el, c, 0.01), configs.Q_R_TABLE5)]
-    return p, f"cfg4 physics, H8 {nx}x{ny}x{nz} ({nx*ny*nz:,} el), RCB into {nranks} x 1M partitions"
+WORKLOADS = {
+    # BASELINE configs[3]: the N = 1 headline and the 2-GPU cfg4 point
+    "cfg4": ("cfg4: H8 100^3 (1,000,000 el) TherMechExpanTD, hourglass, Prony P=1",
+             lambda steps: configs.cfg4(steps=steps)),
+    # BASELINE configs[4] top rung: the fixed 16M-element mesh strong-scaled over 1/2/4/8 GPUs
+    "cfg5_16m": ("cfg5: H8 252^3 (16,003,008 el) TherMechExpanTD, hourglass, Prony P=1, dt = 1/2 critical",
+                 lambda steps: configs.cfg5_h8(252, steps=steps)),
+}
+
+
+def workload_for(args, world):
+    """N = 1: cfg4 (the metric's configuration).  N > 1: the fixed 16M-element mesh split
+    by RCB over the N GPUs (strong scaling), or --workload cfg4."""
+    name = args.workload or ("cfg4" if world == 1 else "cfg5_16m")
+    label, make = WORKLOADS[name]
+    return name, label, make
+
+
+def bench_config(name, label, p, world, graph_steps):
+    """The config dict both arms print (identical for the same workload and N)."""
+    return {"workload": label, "elements": p.num_elements, "nodes": p.num_nodes,
+            "parallelism": f"rcb{world}" if world > 1 else "single",
+            "l2": "working set > 1 GB per GPU vs 126 MB L2: no flush needed",
+            "graph_steps": graph_steps, "name": name}
 
 
 def canonical_bytes(p):
@@ -189,15 +195,16 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
-    p, workload = weak_block(world, args.steps)
+    name, label, make = workload_for(args, world)
+    p = make(args.steps)
     warm = max(1, min(args.warmup, 10))  # ~0.1 s per CPU step on cfg4: bounded, >= 3 when asked for >= 3
     rate, n, dt, threads = cpu_oracle_rate(p, budget_s=args.ref_budget, max_steps=args.steps, warmup=warm)
     sample = (f"{n} of {args.steps} requested steps of the full {p.num_elements:,}-element workload "
               f"({dt:.1f} s, fp64 oracle, OpenMP {threads} threads on {cpu_model()})")
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": METRIC, "n_gpus": world,
             "steps": n, "warmup": warm, "ms_per_step": 1e3 * dt / n, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload, "elements": p.num_elements, "nodes": p.num_nodes},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": bench_config(name, label, p, world, args.graph_steps),
             "cpu_baseline": {"value": rate, "unit": METRIC, "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": rate, "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -212,11 +219,20 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    if args.gpus != world:
+        raise SystemExit(f"bench.py --gpus {args.gpus} needs {args.gpus} ranks (torchrun --nproc-per-node "
+                         f"{args.gpus}); this process group has {world}")
+    if world > torch.cuda.device_count():
+        raise SystemExit(f"--gpus {world}: only {torch.cuda.device_count()} CUDA device(s) visible")
     dist = None
     if world > 1:
+        # communicator-init lines (rank count) of the halo communicator and torch's
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    p, workload = weak_block(world, args.steps + args.warmup + 64)
+    wname, workload, make = workload_for(args, world)
+    p = make(args.steps + args.warmup + 64)
     nccl_id = None
     if world > 1:
         obj = [tg.nccl_unique_id() if rank == 0 else None]
@@ -255,7 +271,7 @@ def run_ours(args):
         ms = float(t.item())
     clocks = sampler.summary(wall0, wall1)
     sampler.stop()
-    E_total = p.num_elements  # weak scaling: the global mesh holds all ranks' elements
+    E_total = p.num_elements  # the whole mesh (split over the ranks)
     value = E_total * args.steps / (ms / 1e3)
     ms_step = ms / args.steps
 
@@ -275,10 +291,23 @@ def run_ours(args):
     ach = b_dom / (t_dom / 1e3) / 1e9
     step_bytes = sum(local_bytes.values())
     step_gbs = step_bytes * args.steps / (ms / 1e3) / 1e9
-    wkey = f"cfg4_n{world}" if world > 1 else "cfg4"
+    wkey = wname if world == 1 else f"{wname}_n{world}"
     roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": ncu_traffic(wkey, dom), "kernel": dom, "kernel_ms": t_dom,
-                "algorithmic_bytes_per_launch": b_dom, "peak_source": peak_src}
+                "algorithmic_bytes_per_launch": b_dom, "peak_source": peak_src,
+                "traffic_source": "profiles/ncu_dram_bytes.json (dram__bytes_read.sum + dram__bytes_write.sum of "
+                                  "the committed ncu --set full capture of this workload)"}
+    halo = None
+    if world > 1:  # per rank: halo volume and the transfer time on the comm stream
+        nb, sb, rb = eng.halo_info()
+        mine = [float(nb), float(sb), float(rb), 1e3 * prof.get("halo_exchange_thermal", 0.0),
+                1e3 * prof.get("halo_exchange_mech", 0.0), float(eng.problem.num_elements)]
+        t = torch.tensor(mine, device="cuda", dtype=torch.float64)
+        allr = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(allr, t)
+        halo = [{"rank": r, "neighbors": int(v[0]), "send_bytes_per_step": int(v[1]), "recv_bytes_per_step": int(v[2]),
+                 "exchange_us_thermal": v[3], "exchange_us_mech": v[4]} for r, v in
+                enumerate(x.tolist() for x in allr)]
 
     # end to end through the public API with host buffers: per step upload this step's
     # nodal source powers (pinned H2D, bioheat.hpp:57), step (finite check D2H), read T and u (D2H)
@@ -329,16 +358,15 @@ def run_ours(args):
                    "calls": "tvegpu_step_io(power, 1, NULL, NULL) + tvegpu_get_summary (device reductions)"}
 
     line = {"metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload, "elements": p.num_elements, "nodes": p.num_nodes,
-                       "parallelism": f"rcb{world}" if world > 1 else "single",
-                       "l2": "working set > 1 GB per GPU vs 126 MB L2: no flush needed",
-                       "graph_steps": args.graph_steps},
+            "config": bench_config(wname, workload, p, world, args.graph_steps),
             "achieved_hbm_gbs_step": step_gbs, "canonical_bytes_per_element_step": step_bytes / p.num_elements,
             "step_roofline_frac": step_gbs / peak,
             "kernel_ms": prof, "roofline": roofline, "e2e": e2e, "e2e_control": e2e_control,
             "gpu_launches": eng.kernels_per_step() * args.steps, "clocks": clocks}
+    if halo is not None:
+        line["halo"] = halo
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, n, dt, threads = cpu_oracle_rate(p, budget_s=args.cpu_budget, max_steps=1000)
@@ -359,9 +387,18 @@ def run_ours(args):
         b.synchronize()
         e3.sync()
         t3 = a.elapsed_time(b) / n3
+        b3 = sum(canonical_bytes(p3).values())
+        prof3 = e3.profile_kernels(200)
         line["cfg3_liver"] = {"elements": p3.num_elements, "nodes": p3.num_nodes, "ms_per_step": t3,
                               "element_steps_per_s": p3.num_elements / (t3 / 1e3),
-                              "realtime_dt_ms": 1e3 * p3.dt, "steps": n3}
+                              "realtime_dt_ms": 1e3 * p3.dt, "steps": n3,
+                              "canonical_bytes_per_step": b3,
+                              "achieved_gbs": b3 / (t3 / 1e3) / 1e9,
+                              "hbm_frac_l2_regime": b3 / (t3 / 1e3) / 1e9 / peak,
+                              "regime": "L2-resident: the step's canonical traffic (~61 MB) fits the 126 MB L2, so "
+                                        "the HBM fraction can exceed 1; four launches of a few us each",
+                              "kernel_us_direct_launches": {k: 1e3 * v for k, v in prof3.items()},
+                              "launch_overhead_us": 1e3 * (sum(prof3.values()) - t3)}
         e3.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -378,6 +415,8 @@ def main():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: cfg4 at N = 1, the 16M-element cfg5 mesh at N > 1")
     ap.add_argument("--graph-steps", type=int, default=64)
     ap.add_argument("--soak", type=float, default=0.5)
     ap.add_argument("--e2e-steps", type=int, default=50)

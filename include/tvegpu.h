@@ -397,6 +397,9 @@ void tvegpu_group_destroy(tvegpu_group* g);
  * ------------------------------------------------------------------------- */
 /* cudaStream_t (as void*) every step kernel is launched on. */
 void* tvegpu_stream(tvegpu_engine* h);
+/* Halo exchange volume of one partition (nranks > 1): neighbours, and bytes sent /
+ * received per step (every contribution of a shared node, both coupled phases). */
+tvegpu_status tvegpu_halo_info(const tvegpu_engine* h, int32_t* neighbors, int64_t* send_bytes, int64_t* recv_bytes);
 /* Kernel launches per step (K1..K5, plus halo packs when nranks > 1). */
 int32_t tvegpu_kernels_per_step(const tvegpu_engine* h);
 /* Enqueue nsteps on the stream without waiting or reading back the finite
@@ -405,7 +408,10 @@ tvegpu_status tvegpu_enqueue_steps(tvegpu_engine* h, int64_t nsteps);
 tvegpu_status tvegpu_sync(tvegpu_engine* h);
 /* Time each kernel of the step with CUDA events over nsteps direct (un-graphed)
  * steps; ms_per_kernel[k] = mean duration of kernel k per step (up to 8 kinds),
- * names = ';'-separated kernel names.  Returns the number of kinds in *count. */
+ * names = ';'-separated kernel names.  Returns the number of kinds in *count.
+ * Partitioned engines: the element entries span their phase (boundary elements, pack,
+ * exchange enqueue, interior elements), the node entries include the wait for the
+ * halo, and two more entries time the halo transfers on the comm stream. */
 tvegpu_status tvegpu_profile_kernels(tvegpu_engine* h, int32_t nsteps, double* ms_per_kernel, int32_t* count,
                                      char* names, size_t cap);
 

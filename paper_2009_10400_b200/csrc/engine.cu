@@ -127,7 +127,8 @@ struct Transport {
     // Called once every part has packed its send segment of this phase and recorded
     // ev_pack on its compute stream; fills each part's receive area on its comm stream
     // and records ev_comm there.
-    virtual void exchange(const std::vector<tvegpu_engine*>& parts, bool mech) = 0;
+    // t0 (profiling, may be null): recorded on parts[0]'s comm stream once the transfer may start.
+    virtual void exchange(const std::vector<tvegpu_engine*>& parts, bool mech, cudaEvent_t t0 = nullptr) = 0;
     // In-place element-wise all-reduce (max or min) of n unsigned 64-bit words,
     // buf[k] on parts[k], ordered after each part's compute stream; on return the
     // result is enqueued on (and complete before later work of) every compute stream.
@@ -275,13 +276,14 @@ double* recv_area(tvegpu_engine* h, bool mech) {
 
 struct NcclTransport final : Transport {
     ncclComm_t comm = nullptr;
-    void exchange(const std::vector<tvegpu_engine*>& parts, bool mech) override {
+    void exchange(const std::vector<tvegpu_engine*>& parts, bool mech, cudaEvent_t t0) override {
         tvegpu_engine* h = parts[0];  // one partition per process and GPU
         const RankPlan& pl = h->plan;
         const int width = mech ? kMW : 1;
         const double* sendbuf = mech ? h->send_m : h->send_th;
         double* recvbuf = recv_area(h, mech);
         CU(cudaStreamWaitEvent(h->sc, h->ev_pack, 0));
+        if (t0) CU(cudaEventRecord(t0, h->sc));
         auto& api = nccl();
         NC(api.GroupStart());
         for (size_t j = 0; j < pl.neighbors.size(); ++j) {
@@ -308,13 +310,16 @@ __global__ void k_combine_u64(unsigned long long* __restrict__ acc, const unsign
 }
 
 struct LoopbackTransport final : Transport {
-    void exchange(const std::vector<tvegpu_engine*>& parts, bool mech) override {
+    void exchange(const std::vector<tvegpu_engine*>& parts, bool mech, cudaEvent_t t0) override {
         const int width = mech ? kMW : 1;
         for (tvegpu_engine* r : parts) {
             const RankPlan& pr = r->plan;
             // the receive area is rewritten only after this part's node kernel of the
             // previous step read it (ordered before r's own ev_pack)
             CU(cudaStreamWaitEvent(r->sc, r->ev_pack, 0));
+            if (t0 && r == parts[0])
+                for (const tvegpu_engine* q : parts) CU(cudaStreamWaitEvent(r->sc, q->ev_pack, 0));
+            if (t0 && r == parts[0]) CU(cudaEventRecord(t0, r->sc));
             double* dst0 = recv_area(r, mech);
             for (size_t j = 0; j < pr.neighbors.size(); ++j) {
                 const tvegpu_engine* q = parts.at(pr.neighbors[j]);
@@ -355,7 +360,11 @@ struct LoopbackTransport final : Transport {
 size_t elem_smem(const tvegpu_engine* h, int rows) {
     return kRowsOffset + (size_t)rows * kChunkThreads * sizeof(double) + 2 * (size_t)h->prm.max_chunk_nodes * sizeof(double2);
 }
-size_t k1_smem(const tvegpu_engine* h) { return elem_smem(h, kTmaK1 ? k1_rows().total() : 0); }
+size_t k1_smem(const tvegpu_engine* h) {
+    const bool xst = h->nn == 8 ? k1_xstage<8>() : k1_xstage<4>();
+    const int rows = kTmaK1 ? (h->nn == 8 ? k1_rows<8>() : k1_rows<4>()).total() : 0;
+    return elem_smem(h, rows) + (xst ? (size_t)h->prm.xstride * sizeof(double) : 0);
+}
 size_t k3_smem(const tvegpu_engine* h) {
     const int exp = h->prm.exp_kind < 0 ? 0 : (h->prm.exp_kind == 0 ? 1 : 2);
     const RowPlan r = h->nn == 8 ? (exp == 2 ? k3_rows<8, 2>(h->prm) : k3_rows<8, 0>(h->prm))
@@ -479,7 +488,9 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr, cudaEvent_t 
 //   wait ev_comm, node kernel.
 // The same code drives one NCCL rank (parts = {h}) and a loopback group.
 // evs (one-part sets only): profiling marks at the phase boundaries.
-void enqueue_partitioned_step(Stepper& S, cudaEvent_t* evs = nullptr) {
+// xev (profiling, one-part sets): per phase a (start, end) pair on the comm stream
+// around the halo transfer itself.
+void enqueue_partitioned_step(Stepper& S, cudaEvent_t* evs = nullptr, cudaEvent_t* xev = nullptr) {
     const std::vector<tvegpu_engine*>& parts = S.parts;
     tvegpu_engine* h0 = parts[0];
     int ev = 0;
@@ -493,7 +504,8 @@ void enqueue_partitioned_step(Stepper& S, cudaEvent_t* evs = nullptr) {
             launch_thermal_elements(h, 0, h->plan.nchunks_boundary);
             pack_halo(h, false);
         }
-        h0->tx->exchange(parts, false);
+        h0->tx->exchange(parts, false, xev ? xev[0] : nullptr);
+        if (xev) CU(cudaEventRecord(xev[1], h0->sc));
         for (tvegpu_engine* h : parts) launch_thermal_elements(h, h->plan.nchunks_boundary, nchunks(h));
         mark();
         for (tvegpu_engine* h : parts) {
@@ -507,7 +519,8 @@ void enqueue_partitioned_step(Stepper& S, cudaEvent_t* evs = nullptr) {
             launch_mech_elements(h, 0, h->plan.nchunks_boundary);
             pack_halo(h, true);
         }
-        h0->tx->exchange(parts, true);
+        h0->tx->exchange(parts, true, xev ? xev[2] : nullptr);
+        if (xev) CU(cudaEventRecord(xev[3], h0->sc));
         for (tvegpu_engine* h : parts) launch_mech_elements(h, h->plan.nchunks_boundary, nchunks(h));
         mark();
         for (tvegpu_engine* h : parts) {
@@ -878,11 +891,11 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
             }
         h->ptr.stage_ent = reinterpret_cast<const int2*>(dupload(own, ent, s));
         m.stage_stride = st;
-        // K3's coordinate blocks (k3_xstage): per chunk its nodes' reference coordinates in
+        // element-kernel coordinate blocks (k1_xstage / k3_xstage): per chunk its nodes' reference coordinates in
         // shared-slot order, x[S] y[S] z[S] with S = slots used (even), one bulk copy each
         const int ms2 = (m.max_chunk_nodes + 1) & ~1;
         m.xstride = 3 * ms2;
-        if (pl.nn == 8 ? k3_xstage<8>() : k3_xstage<4>()) {
+        if (pl.nn == 8 ? (k3_xstage<8>() || k1_xstage<8>()) : (k3_xstage<4>() || k1_xstage<4>())) {
             std::vector<double> cx((size_t)nc * m.xstride, 0.0);
             std::vector<int32_t> cs(std::max(1, nc), 2);
 #pragma omp parallel for schedule(static)
@@ -2287,6 +2300,19 @@ tvegpu_status tvegpu_nccl_unique_id(void* out128) {
 
 void* tvegpu_stream(tvegpu_engine* h) { return h ? (void*)h->s : nullptr; }
 
+tvegpu_status tvegpu_halo_info(const tvegpu_engine* h, int32_t* neighbors, int64_t* send_bytes, int64_t* recv_bytes) {
+    if (!h) return TVEGPU_E_ARG;
+    const RankPlan& pl = h->plan;
+    const int64_t ns = pl.send_off.empty() ? 0 : pl.send_off.back(), nr = pl.recv_off.empty() ? 0 : pl.recv_off.back();
+    int64_t per = 0;  // doubles per contribution and step: 1 thermal + kMW mechanical, per coupled phase
+    if (h->mode != TVEGPU_MECHANICAL_ONLY) per += 1;
+    if (h->mode != TVEGPU_THERMAL_ONLY) per += kMW;
+    if (neighbors) *neighbors = (int32_t)pl.neighbors.size();
+    if (send_bytes) *send_bytes = 8 * per * ns;
+    if (recv_bytes) *recv_bytes = 8 * per * nr;
+    return TVEGPU_OK;
+}
+
 int32_t tvegpu_kernels_per_step(const tvegpu_engine* h) {
     if (!h) return 0;
     const bool multi = h->plan.nranks > 1;
@@ -2316,15 +2342,18 @@ tvegpu_status tvegpu_profile_kernels(tvegpu_engine* h, int32_t nsteps, double* m
         }
         // (the end-of-step verdict runs inside the last node kernel)
         const int nk = (int)nm.size();
-        std::vector<cudaEvent_t> ev((size_t)(nk + 1) * nsteps);
+        const bool part = partitioned(h->solo);
+        std::vector<cudaEvent_t> ev((size_t)(nk + 1) * nsteps), xev(part ? (size_t)4 * nsteps : 0);
         for (auto& e : ev) CU(cudaEventCreate(&e));
+        for (auto& e : xev) CU(cudaEventCreate(&e));
         // partitioned engines: the marks bracket the phases (element kernels + pack +
         // exchange enqueue, then the wait for the halo + node kernel)
         begin_pending(h);
         for (int k = 0; k < nsteps; ++k) {
             refresh_sources_if_needed(h, h->host_time);
             if (h->prm.motion) upload_motion(h);
-            if (partitioned(h->solo)) enqueue_partitioned_step(h->solo, ev.data() + (size_t)k * (nk + 1));
+            if (part)
+                enqueue_partitioned_step(h->solo, ev.data() + (size_t)k * (nk + 1), xev.data() + (size_t)4 * k);
             else enqueue_one_step(h, ev.data() + (size_t)k * (nk + 1));
             h->host_time += h->dt;
             h->host_step += 1;
@@ -2337,13 +2366,29 @@ tvegpu_status tvegpu_profile_kernels(tvegpu_engine* h, int32_t nsteps, double* m
                 CU(cudaEventElapsedTime(&t, ev[(size_t)k * (nk + 1) + j], ev[(size_t)k * (nk + 1) + j + 1]));
                 acc[j] += t;
             }
+        // partitioned: the halo transfers (thermal, mechanical) on the comm stream
+        double xacc[2] = {0.0, 0.0};
+        const bool th = h->mode != TVEGPU_MECHANICAL_ONLY, me = h->mode != TVEGPU_THERMAL_ONLY;
+        for (int k = 0; k < nsteps && part; ++k)
+            for (int q = 0; q < 2; ++q) {
+                if ((q == 0 && !th) || (q == 1 && !me)) continue;
+                float t = 0;
+                CU(cudaEventElapsedTime(&t, xev[(size_t)4 * k + 2 * q], xev[(size_t)4 * k + 2 * q + 1]));
+                xacc[q] += t;
+            }
         for (auto& e : ev) cudaEventDestroy(e);
-        *count = nk;
+        for (auto& e : xev) cudaEventDestroy(e);
         std::string all;
         for (int j = 0; j < nk; ++j) {
             ms[j] = acc[j] / nsteps;
             all += (j ? ";" : "") + nm[j];
         }
+        int cnt = nk;
+        if (part) {
+            if (th) ms[cnt++] = xacc[0] / nsteps, all += ";halo_exchange_thermal";
+            if (me) ms[cnt++] = xacc[1] / nsteps, all += ";halo_exchange_mech";
+        }
+        *count = cnt;
         if (names && cap) {
             std::strncpy(names, all.c_str(), cap - 1);
             names[cap - 1] = 0;

@@ -63,6 +63,12 @@ constexpr bool kTmaK1 = (TVEGPU_TMA_ROWS & 1) != 0, kTmaK3 = (TVEGPU_TMA_ROWS & 
 #endif
 template <int NN>
 __host__ __device__ constexpr bool k3_xstage() { return kTmaK3 && (TVEGPU_K3_XSTAGE & (NN == 4 ? 1 : 2)) != 0; }
+// The same choice for K1 (A and V only).
+#ifndef TVEGPU_K1_XSTAGE
+#define TVEGPU_K1_XSTAGE 1
+#endif
+template <int NN>
+__host__ __device__ constexpr bool k1_xstage() { return kTmaK1 && (TVEGPU_K1_XSTAGE & (NN == 4 ? 1 : 2)) != 0; }
 
 struct Clock {
     double time;
@@ -573,9 +579,16 @@ __device__ __forceinline__ void check_gather(const DevParams& P, const DevPtrs& 
 // K1 element body: element e of the staged chunk S (n = its node slots)
 template <int NN>
 __device__ __forceinline__ void k1_body(const DevParams& P, const DevPtrs& D, const NodeStage& S,
-                                        const ElemRows<kTmaK1>& rows, const int e, const int (&n)[NN]) {
+                                        const ElemRows<kTmaK1>& rows, const CoordStage& xs, const int e,
+                                        const int (&n)[NN]) {
     double H[9], A[9], gT[3], V, Ts;
-    element_pass<NN, true, kTmaK1>(S, n, P, D, rows, e, H, A, V, Ts, gT);
+    if constexpr (k1_xstage<NN>()) {
+        element_pass<NN, true, kTmaK1, true>(S, n, P, D, rows, e, H, A, V, Ts, gT);
+        __threadfence_block();  // keep the coordinate reads after the record sums (register pressure)
+        geometry_from_coords<NN>(xs, n, A, V);
+    } else {
+        element_pass<NN, true, kTmaK1>(S, n, P, D, rows, e, H, A, V, Ts, gT);
+    }
     // F = I + H A^T
     double F[9];
 #pragma unroll
@@ -624,29 +637,38 @@ __device__ __forceinline__ void k1_body(const DevParams& P, const DevPtrs& D, co
     if (dF == 0.0) atomicMin(D.err_elem, pack_elem(D.clock->step, D.elem_orig[e]));
 }
 
-// K1 rows: A (9) and V
-__host__ __device__ __forceinline__ RowPlan k1_rows() { return RowPlan{10, 0, 0, 0}; }
+// K1 rows: A (9) and V, unless rebuilt from the chunk coordinates
+template <int NN>
+__host__ __device__ __forceinline__ RowPlan k1_rows() { return RowPlan{k1_xstage<NN>() ? 0 : 10, 0, 0, 0}; }
 
 template <int NN>
 __global__ void K1_BOUNDS k_thermal_element(const DevParams P, const DevPtrs D, int cur, int c0, int c1) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const RowPlan rp = k1_rows();
+    const RowPlan rp = k1_rows<NN>();
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem);
     double* rows = reinterpret_cast<double*>(smem + kRowsOffset);
-    double2* planes = reinterpret_cast<double2*>(rows + (kTmaK1 ? rp.total() * kChunkThreads : 0));
+    double* xblk = rows + (kTmaK1 ? rp.total() * kChunkThreads : 0);  // k1_xstage: the chunk's coordinates
+    double2* planes = reinterpret_cast<double2*>(xblk + (k1_xstage<NN>() ? P.xstride : 0));
     const int ms = P.max_chunk_nodes;
     const NodeStage S{planes, planes + ms};
     const int c = c0 + blockIdx.x;
+    CoordStage xs{nullptr, nullptr, nullptr};
     {
         const int e0 = __ldg(D.chunk_start + c), ne = __ldg(D.chunk_start + c + 1) - e0;
-        load_elem_rows<kTmaK1>(P, D, rp, e0, ne, rows, bar);
+        if constexpr (k1_xstage<NN>()) {
+            const int Sx = __ldg(D.chunk_xs + c);
+            xs = CoordStage{xblk, xblk + Sx, xblk + 2 * Sx};
+            load_elem_rows<kTmaK1>(P, D, rp, e0, ne, rows, bar, xblk, D.chunk_x + (size_t)c * P.xstride, 24u * Sx);
+        } else {
+            load_elem_rows<kTmaK1>(P, D, rp, e0, ne, rows, bar);
+        }
     }
     int n[NN];
     const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c, P.stage_stride, S, n);
     wait_elem_rows<kTmaK1>(bar);  // every thread: the CTA must not retire with bulk copies in flight
     if (D.clock->halted || e < 0) return;  // halted: uniform across the grid (read after the wait)
     check_chunk<NN>(P, D, c, e, n);
-    k1_body<NN>(P, D, S, ElemRows<kTmaK1>{rows, (int)threadIdx.x}, e, n);
+    k1_body<NN>(P, D, S, ElemRows<kTmaK1>{rows, (int)threadIdx.x}, xs, e, n);
     pdl_trigger();  // after this block's work: the successor fills in behind the last wave
 }
 

@@ -123,6 +123,7 @@ EXPORTS = {
     "tvegpu_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "tvegpu_stream": (C.c_void_p, [C.c_void_p]),
     "tvegpu_kernels_per_step": (C.c_int32, [C.c_void_p]),
+    "tvegpu_halo_info": (C.c_int, [C.c_void_p, _ip, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "tvegpu_enqueue_steps": (C.c_int, [C.c_void_p, C.c_int64]),
     "tvegpu_sync": (C.c_int, [C.c_void_p]),
     "tvegpu_profile_kernels": (C.c_int, [C.c_void_p, C.c_int32, _dp, C.POINTER(C.c_int32), C.c_char_p,
@@ -676,6 +677,14 @@ class Engine:
 
     def kernels_per_step(self) -> int:
         return lib().tvegpu_kernels_per_step(self._h)
+
+    def halo_info(self):
+        """(neighbours, bytes sent, bytes received) per step of this partition's halo exchange."""
+        nb, sb, rb = C.c_int32(), C.c_int64(), C.c_int64()
+        rc = lib().tvegpu_halo_info(self._h, C.byref(nb), C.byref(sb), C.byref(rb))
+        if rc:
+            self._raise(rc)
+        return nb.value, sb.value, rb.value
 
     def profile_kernels(self, nsteps: int):
         ms = np.zeros(8)
