@@ -19,6 +19,7 @@
 #include <functional>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -93,10 +94,48 @@ T* dalloc(std::vector<void*>& owned, size_t n) {
     owned.push_back(p);
     return static_cast<T*>(p);
 }
-template <class T>
-T* dupload(std::vector<void*>& owned, const std::vector<T>& v, cudaStream_t s) {
+// Host -> device upload of setup arrays.  A pageable cudaMemcpy is staged by the driver
+// through a single-threaded copy (~6 GB/s); large arrays instead go through a
+// process-wide double-buffered pinned ring (2 x 32 MB, allocated once): the host threads
+// fill one buffer (parallel memcpy) while the other is in flight at link speed.
+// Returns after the source may be reused (like a pageable cudaMemcpyAsync).
+void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    constexpr size_t kSmall = (size_t)4 << 20, kBuf = (size_t)32 << 20;
+    if (bytes <= kSmall) {
+        CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        return;
+    }
+    static std::mutex mu;
+    static char* buf[2] = {nullptr, nullptr};
+    static cudaEvent_t done[2] = {nullptr, nullptr};
+    std::lock_guard<std::mutex> lock(mu);
+    if (!buf[0])
+        for (int k = 0; k < 2; ++k) {
+            CU(cudaMallocHost(&buf[k], kBuf));
+            CU(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
+            CU(cudaEventRecord(done[k], s));
+        }
+    const char* in = static_cast<const char*>(src);
+    char* out = static_cast<char*>(dst);
+    int k = 0;
+    for (size_t off = 0; off < bytes; off += kBuf, k ^= 1) {
+        const size_t n = std::min(kBuf, bytes - off);
+        CU(cudaEventSynchronize(done[k]));  // this buffer's previous copy has left
+        const int pieces = (int)((n + ((size_t)1 << 20) - 1) >> 20);
+#pragma omp parallel for schedule(static)
+        for (int q = 0; q < pieces; ++q) {
+            const size_t a = (size_t)q << 20, b = std::min(n, a + ((size_t)1 << 20));
+            std::memcpy(buf[k] + a, in + off + a, b - a);
+        }
+        CU(cudaMemcpyAsync(out + off, buf[k], n, cudaMemcpyHostToDevice, s));
+        CU(cudaEventRecord(done[k], s));
+    }
+}
+
+template <class T, class Al>
+T* dupload(std::vector<void*>& owned, const std::vector<T, Al>& v, cudaStream_t s) {
     T* p = dalloc<T>(owned, v.size());
-    if (!v.empty()) CU(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    if (!v.empty()) h2d(p, v.data(), v.size() * sizeof(T), s);
     return p;
 }
 
@@ -881,7 +920,8 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
         const int nc = (int)pl.chunk_start.size() - 1;
         int st = 1;
         for (int c = 0; c < nc; ++c) st = std::max(st, pl.chunk_node_off[c + 1] - pl.chunk_node_off[c]);
-        std::vector<int32_t> ent((size_t)2 * nc * st, 0);
+        fvec<int32_t> ent((size_t)2 * nc * st);
+#pragma omp parallel for schedule(static)
         for (int c = 0; c < nc; ++c)
             for (int k = 0; k < st; ++k) {
                 const int u = pl.chunk_node_off[c] + k;
@@ -929,6 +969,7 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     CU(cudaMemsetAsync(h->ptr.theta, 0, std::max<size_t>(1, (size_t)6 * P * es) * 8, s));
     if (p.fiber_dirs && m.fiber_mode == 2) {
         std::vector<double> f((size_t)3 * es, 0.0);
+#pragma omp parallel for schedule(static)
         for (int e = 0; e < E; ++e)
             for (int k = 0; k < 3; ++k) f[(size_t)k * es + e] = p.fiber_dirs[3 * (size_t)pl.elem_orig[e] + k];
         h->ptr.fiber = dupload(own, f, s);
@@ -936,6 +977,7 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     }
     if (p.expansion_axes && expansion) {
         std::vector<double> f((size_t)6 * es, 0.0);
+#pragma omp parallel for schedule(static)
         for (int e = 0; e < E; ++e)
             for (int k = 0; k < 6; ++k) f[(size_t)k * es + e] = p.expansion_axes[6 * (size_t)pl.elem_orig[e] + k];
         h->ptr.axes = dupload(own, f, s);
@@ -943,8 +985,9 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     }
     // ---- node arrays
     {
-        std::vector<double4> rec(N), X(N);
-        std::vector<double> mass(N), vn(N);
+        fvec<double4> rec(N), X(N);
+        fvec<double> mass(N), vn(N);
+#pragma omp parallel for schedule(static)
         for (int i = 0; i < N; ++i) {
             const int oi = pl.node_orig[i];
             rec[i] = make_double4(0.0, 0.0, 0.0, p.initial_temperature);
@@ -962,10 +1005,7 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     {  // per-element reference geometry, once (k_geometry, same arithmetic as the in-kernel path);
        // read by the element kernels (TMA rows) and by the run-level
        // energy reduction always
-        if (!h->d_conn) {
-            h->d_conn = dalloc<int32_t>(own, pl.conn.size());
-            CU(cudaMemcpyAsync(h->d_conn, pl.conn.data(), pl.conn.size() * 4, cudaMemcpyHostToDevice, s));
-        }
+        if (!h->d_conn) h->d_conn = dupload(own, pl.conn, s);
         // A, V (10 rows) for K1 and the run-level energy; + the H8 hourglass vectors when K3
         // reads them instead of rebuilding them from the chunk coordinates (k3_xstage)
         const int grows = (nn == 8 && !k3_xstage<8>()) ? kGeoRows : 10;
@@ -985,10 +1025,15 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     CU(cudaMemsetAsync(const_cast<double*>(h->ptr.qr), 0, std::max(1, N) * sizeof(double), s));
     // ---- boundary conditions (mechanics.hpp:37-47, bioheat.hpp:32-35)
     {
-        std::vector<int32_t> local(g.N, -1);
+        fvec<int32_t> local(g.N);
+#pragma omp parallel for schedule(static)
+        for (int i = 0; i < g.N; ++i) local[i] = -1;
+#pragma omp parallel for schedule(static)
         for (int i = 0; i < N; ++i) local[pl.node_orig[i]] = i;
-        std::vector<uint8_t> mask(N, 0);
-        std::vector<int32_t> row(N, -1);
+        fvec<uint8_t> mask(N);
+        fvec<int32_t> row(N);
+#pragma omp parallel for schedule(static)
+        for (int i = 0; i < N; ++i) mask[i] = 0, row[i] = -1;
         std::vector<int32_t> presc;  // [nbc][3]
         std::vector<double> tfix;
         auto get_row = [&](int li) {
@@ -1021,6 +1066,7 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
             mask[li] |= BC_TFIX;
             tfix[get_row(li)] = p.fixed_temperature_values[k];  // last wins
         }
+#pragma omp parallel for schedule(static)
         for (int i = 0; i < N; ++i)
             if (row[i] < 0) row[i] = 0;
         if (tfix.empty()) {
@@ -1069,12 +1115,13 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
         // iff some node of the GLOBAL mesh has > 8 contributions (T4); otherwise one thread
         // sums an ELL row of 8 ids in order (H8).
         {
-            std::vector<int> val(p.num_nodes, 0);
-            for (size_t k = 0; k < (size_t)p.num_elements * nn; ++k) ++val[p.elements[k]];
-            const int gmax = val.empty() ? 0 : *std::max_element(val.begin(), val.end());
+            int gmax = 0;  // the global mesh's largest valence
+#pragma omp parallel for schedule(static) reduction(max : gmax)
+            for (int i = 0; i < g.N; ++i) gmax = std::max(gmax, g.adj_off[i + 1] - g.adj_off[i]);
             h->pair = gmax > 8 && !std::getenv("TVEGPU_NO_PAIR");
         }
         int maxc = 0;
+#pragma omp parallel for schedule(static) reduction(max : maxc)
         for (int i = 0; i < pl.N; ++i) maxc = std::max(maxc, pl.csr_off[i + 1] - pl.csr_off[i]);
         // ELL rows of 8 G ids (G = ceil(max contributions / 8), up to 64 contributions);
         // the pair kernels read the CSR lists instead
@@ -1082,10 +1129,12 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
         m.ell = (!h->pair && G <= 8 && !std::getenv("TVEGPU_NO_ELL")) ? G : 0;
         if (m.ell) {
             const size_t W = (size_t)8 * G;
-            std::vector<int32_t> ell(W * pl.N, (int32_t)nslots);
-            for (int i = 0; i < pl.N; ++i)
-                for (int k = pl.csr_off[i]; k < pl.csr_off[i + 1]; ++k)
-                    ell[W * i + (k - pl.csr_off[i])] = pl.csr_slot[k];
+            fvec<int32_t> ell(W * pl.N);
+#pragma omp parallel for schedule(static)
+            for (int i = 0; i < pl.N; ++i) {
+                const int k0 = pl.csr_off[i], d = pl.csr_off[i + 1] - k0;
+                for (int k = 0; k < (int)W; ++k) ell[W * i + k] = k < d ? pl.csr_slot[k0 + k] : (int32_t)nslots;
+            }
             h->ptr.ell = reinterpret_cast<const int4*>(dupload(own, ell, s));
         }
     }

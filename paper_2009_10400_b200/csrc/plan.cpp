@@ -11,6 +11,8 @@
 #include <numeric>
 #include <parallel/algorithm>
 
+#include <omp.h>
+
 namespace tvegpu {
 
 
@@ -30,19 +32,6 @@ namespace {
 double det3(const double m[3][3]) {
     return m[0][0] * (m[1][1] * m[2][2] - m[1][2] * m[2][1]) - m[0][1] * (m[1][0] * m[2][2] - m[1][2] * m[2][0]) +
            m[0][2] * (m[1][0] * m[2][1] - m[1][1] * m[2][0]);
-}
-
-// inverse-transpose via the adjugate: (J^-1)^T = cof(J) / det J
-void inv_transpose(const double J[3][3], double d, double out[3][3]) {
-    out[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) / d;
-    out[0][1] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) / d;
-    out[0][2] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) / d;
-    out[1][0] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / d;
-    out[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / d;
-    out[1][2] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / d;
-    out[2][0] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / d;
-    out[2][1] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / d;
-    out[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / d;
 }
 
 double sym_max_eig(const double* t) {
@@ -104,10 +93,17 @@ void validate_problem(const tvegpu_problem& p) {
     if (p.kind != TVEGPU_T4 && p.kind != TVEGPU_H8) invalid("unknown element kind");
     if (p.num_nodes <= 0 || p.num_elements <= 0 || !p.nodes || !p.elements) invalid("empty mesh");
     const int nn = p.kind == TVEGPU_T4 ? 4 : 8;
-    for (int64_t k = 0; k < (int64_t)p.num_elements * nn; ++k) {
-        const int v = p.elements[k];
-        if (v < 0 || v >= p.num_nodes)
-            invalid("element " + std::to_string(k / nn + 1) + " references out-of-range node " + std::to_string(v + 1));
+    {
+        const int64_t n = (int64_t)p.num_elements * nn;
+        int64_t first = n;  // lowest offending entry (the message names its element)
+#pragma omp parallel for schedule(static) reduction(min : first)
+        for (int64_t k = 0; k < n; ++k) {
+            const int v = p.elements[k];
+            if ((v < 0 || v >= p.num_nodes) && k < first) first = k;
+        }
+        if (first < n)
+            invalid("element " + std::to_string(first / nn + 1) + " references out-of-range node " +
+                    std::to_string(p.elements[first] + 1));
     }
     if (!(p.mu > 0) || !(p.kappa > 0) || p.eta_a < 0) invalid("hyperelastic parameters need mu > 0, kappa > 0, eta_a >= 0");
     double sphi = 0;
@@ -160,6 +156,39 @@ void validate_problem(const tvegpu_problem& p) {
                 invalid("source element out of range");
 }
 
+// Node -> (element, local) lists in canonical order (ascending element, then local;
+// mesh.hpp:58-61) as keys e * nn + a: a counting sort in which every thread owns a range
+// of node ids and scans the whole connectivity for its own nodes — no atomics, and each
+// node's list fills in ascending key order, i.e. already canonical.
+static void build_adjacency(const int32_t* elements, int E, int N, int nn, fvec<int32_t>& off, fvec<int32_t>& key) {
+    const int64_t n = (int64_t)E * nn;
+    off.resize((size_t)N + 1);
+    key.resize((size_t)n);
+    fvec<int32_t> fill((size_t)N);
+#pragma omp parallel
+    {
+        const int t = omp_get_thread_num(), nt = omp_get_num_threads();
+        const int32_t n0 = (int32_t)((int64_t)N * t / nt), n1 = (int32_t)((int64_t)N * (t + 1) / nt);
+        const uint32_t span = (uint32_t)(n1 - n0);
+        for (int32_t i = n0; i < n1; ++i) fill[i] = 0;
+        for (int64_t k = 0; k < n; ++k) {
+            const uint32_t d = (uint32_t)(elements[k] - n0);
+            if (d < span) fill[n0 + d]++;
+        }
+#pragma omp barrier
+#pragma omp single
+        {
+            off[0] = 0;
+            for (int i = 0; i < N; ++i) off[i + 1] = off[i] + fill[i];
+        }
+        for (int32_t i = n0; i < n1; ++i) fill[i] = off[i];
+        for (int64_t k = 0; k < n; ++k) {
+            const uint32_t d = (uint32_t)(elements[k] - n0);
+            if (d < span) key[fill[n0 + d]++] = (int32_t)k;
+        }
+    }
+}
+
 GlobalMesh build_global(const tvegpu_problem& p) {
     StageTimer tm("build_global");
     LapTimer lap;
@@ -171,92 +200,91 @@ GlobalMesh build_global(const tvegpu_problem& p) {
     g.N = p.num_nodes;
     g.E = p.num_elements;
     const int nn = g.nn, E = g.E, N = g.N;
-    g.A.resize((size_t)9 * E);
     g.vol.resize(E);
     g.centroid.resize((size_t)3 * E);
     for (int k = 0; k < 3; ++k) {
         g.lo[k] = std::numeric_limits<double>::infinity();
         g.hi[k] = -std::numeric_limits<double>::infinity();
     }
+    // one pass over the elements: volume (det J; its sign validates the element),
+    // centroid, smallest edge, centroid bounding box
+    static const int t4e[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+    static const int h8e[12][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 0}, {4, 5}, {5, 6},
+                                   {6, 7}, {7, 4}, {0, 4}, {1, 5}, {2, 6}, {3, 7}};
     int bad = -1;
-#pragma omp parallel for schedule(static) reduction(max : bad)
-    for (int e = 0; e < E; ++e) {
-        const int32_t* el = p.elements + (size_t)e * nn;
-        double J[3][3];
-        if (nn == 4) {
-            for (int i = 0; i < 3; ++i)
-                for (int j = 0; j < 3; ++j) J[i][j] = p.nodes[3 * (size_t)el[j + 1] + i] - p.nodes[3 * (size_t)el[0] + i];
-        } else {
-            for (int i = 0; i < 3; ++i)
-                for (int j = 0; j < 3; ++j) {
-                    double s = 0;
-                    for (int a = 0; a < 8; ++a) s += p.nodes[3 * (size_t)el[a] + i] * kH8Sign[a][j];
-                    J[i][j] = s / 8.0;
-                }
-        }
-        const double d = det3(J);
-        const double V = nn == 4 ? d / 6.0 : 8.0 * d;
-        if (!(V > 0)) {
-            bad = std::max(bad, E - e);  // keep the LOWEST failing element
-            continue;
-        }
-        double Ai[3][3];
-        inv_transpose(J, d, Ai);
-        for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j) g.A[(size_t)9 * e + i * 3 + j] = nn == 4 ? Ai[i][j] : Ai[i][j] / 8.0;
-        g.vol[e] = V;
-        for (int k = 0; k < 3; ++k) {
-            double s = 0;
-            for (int a = 0; a < nn; ++a) s += p.nodes[3 * (size_t)el[a] + k];
-            g.centroid[(size_t)3 * e + k] = s / nn;
-        }
-    }
-    if (bad >= 0) invalid("degenerate or inverted element " + std::to_string(E - bad + 1));
+    double L = std::numeric_limits<double>::infinity();
+#pragma omp parallel reduction(max : bad) reduction(min : L)
     {
-        static const int t4e[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
-        static const int h8e[12][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 0}, {4, 5}, {5, 6},
-                                       {6, 7}, {7, 4}, {0, 4}, {1, 5}, {2, 6}, {3, 7}};
-        double L = std::numeric_limits<double>::infinity();
-#pragma omp parallel for schedule(static) reduction(min : L)
+        double lo[3], hi[3];
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = std::numeric_limits<double>::infinity();
+            hi[k] = -std::numeric_limits<double>::infinity();
+        }
+#pragma omp for schedule(static) nowait
         for (int e = 0; e < E; ++e) {
             const int32_t* el = p.elements + (size_t)e * nn;
+            double X[8][3];
+            for (int a = 0; a < nn; ++a)
+                for (int i = 0; i < 3; ++i) X[a][i] = p.nodes[3 * (size_t)el[a] + i];
+            double J[3][3];
+            if (nn == 4) {
+                for (int i = 0; i < 3; ++i)
+                    for (int j = 0; j < 3; ++j) J[i][j] = X[j + 1][i] - X[0][i];
+            } else {
+                for (int i = 0; i < 3; ++i)
+                    for (int j = 0; j < 3; ++j) {
+                        double s = 0;
+                        for (int a = 0; a < 8; ++a) s += X[a][i] * kH8Sign[a][j];
+                        J[i][j] = s / 8.0;
+                    }
+            }
+            const double d = det3(J);
+            const double V = nn == 4 ? d / 6.0 : 8.0 * d;
+            if (!(V > 0)) {
+                bad = std::max(bad, E - e);  // keep the LOWEST failing element
+                continue;
+            }
+            g.vol[e] = V;
+            for (int k = 0; k < 3; ++k) {
+                double s = 0;
+                for (int a = 0; a < nn; ++a) s += X[a][k];
+                const double c = s / nn;
+                g.centroid[(size_t)3 * e + k] = c;
+                lo[k] = std::min(lo[k], c);
+                hi[k] = std::max(hi[k], c);
+            }
             for (int k = 0; k < (nn == 4 ? 6 : 12); ++k) {
                 const int a = nn == 4 ? t4e[k][0] : h8e[k][0], b = nn == 4 ? t4e[k][1] : h8e[k][1];
                 double d2 = 0;
                 for (int i = 0; i < 3; ++i) {
-                    const double d = p.nodes[3 * (size_t)el[a] + i] - p.nodes[3 * (size_t)el[b] + i];
-                    d2 += d * d;
+                    const double dd = X[a][i] - X[b][i];
+                    d2 += dd * dd;
                 }
                 L = std::min(L, std::sqrt(d2));
             }
         }
-        g.min_edge = L;
-    }
-    for (int e = 0; e < E; ++e)
+#pragma omp critical
         for (int k = 0; k < 3; ++k) {
-            g.lo[k] = std::min(g.lo[k], g.centroid[(size_t)3 * e + k]);
-            g.hi[k] = std::max(g.hi[k], g.centroid[(size_t)3 * e + k]);
+            g.lo[k] = std::min(g.lo[k], lo[k]);
+            g.hi[k] = std::max(g.hi[k], hi[k]);
         }
+    }
+    if (bad >= 0) invalid("degenerate or inverted element " + std::to_string(E - bad + 1));
+    g.min_edge = L;
     lap("element geometry + bounds");
     // canonical adjacency over original ids
-    g.adj_off.assign(N + 1, 0);
-    for (int64_t k = 0; k < (int64_t)E * nn; ++k) g.adj_off[p.elements[k] + 1]++;
-    for (int i = 0; i < N; ++i) g.adj_off[i + 1] += g.adj_off[i];
-    g.adj_elem.resize((size_t)E * nn);
-    g.adj_local.resize((size_t)E * nn);
-    {
-        std::vector<int32_t> fill(g.adj_off.begin(), g.adj_off.end() - 1);
-        for (int e = 0; e < E; ++e)
-            for (int a = 0; a < nn; ++a) {
-                const int i = p.elements[(size_t)e * nn + a];
-                g.adj_elem[fill[i]] = e;
-                g.adj_local[fill[i]] = a;
-                fill[i]++;
-            }
+    fvec<int32_t> key;
+    build_adjacency(p.elements, E, N, nn, g.adj_off, key);
+    g.adj_elem.resize(key.size());
+    g.adj_local.resize(key.size());
+#pragma omp parallel for schedule(static)
+    for (size_t k = 0; k < key.size(); ++k) {
+        g.adj_elem[k] = key[k] / nn;
+        g.adj_local[k] = key[k] % nn;
     }
     lap("adjacency");
-    g.mass.assign(N, 0.0);
-    g.vnode.assign(N, 0.0);
+    g.mass.resize(N);
+    g.vnode.resize(N);
     int orphan = -1;
 #pragma omp parallel for schedule(static) reduction(max : orphan)
     for (int i = 0; i < N; ++i) {
@@ -271,6 +299,7 @@ GlobalMesh build_global(const tvegpu_problem& p) {
         g.vnode[i] = v;
     }
     if (orphan >= 0) invalid("node " + std::to_string(N - orphan) + " is not attached to any element (zero lumped mass)");
+    lap("lumped node constants");
     return g;
 }
 
@@ -317,6 +346,70 @@ std::vector<int32_t> rcb_partition(const GlobalMesh& g, int nranks) {
     return owner;
 }
 
+// ---------------------------------------------------------------- parallel helpers
+// Stable LSD radix sort of ids by key[id] (8-bit digits up to kmax's top bit): with the
+// ids initially ascending, the result is the total order (key, id).
+static void radix_sort_by_key(std::vector<int32_t>& ids, const uint64_t* key, uint64_t kmax) {
+    const size_t n = ids.size();
+    if (n < 2) return;
+    int bits = 0;
+    while (bits < 64 && (kmax >> bits)) ++bits;
+    fvec<int32_t> tmp(n);
+    int32_t* src = ids.data();
+    int32_t* dst = tmp.data();
+    const int T = std::max(1, omp_get_max_threads());
+    std::vector<size_t> hist((size_t)T * 256);
+    int passes = 0;
+    for (int shift = 0; shift < bits; shift += 8, ++passes) {
+#pragma omp parallel num_threads(T)
+        {
+            const int t = omp_get_thread_num(), nt = omp_get_num_threads();
+            const size_t b0 = n * t / nt, b1 = n * (t + 1) / nt;
+            size_t* h = hist.data() + (size_t)t * 256;
+            std::fill(h, h + 256, 0);
+            for (size_t q = b0; q < b1; ++q) h[(key[src[q]] >> shift) & 255]++;
+#pragma omp barrier
+#pragma omp single
+            {
+                size_t run = 0;  // digit-major, thread-minor: stable across the thread blocks
+                for (int d = 0; d < 256; ++d)
+                    for (int u = 0; u < nt; ++u) {
+                        const size_t c = hist[(size_t)u * 256 + d];
+                        hist[(size_t)u * 256 + d] = run;
+                        run += c;
+                    }
+            }
+            for (size_t q = b0; q < b1; ++q) dst[h[(key[src[q]] >> shift) & 255]++] = src[q];
+        }
+        std::swap(src, dst);
+    }
+    if (passes & 1) std::copy(tmp.begin(), tmp.end(), ids.begin());
+}
+
+// The non-negative entries of `at` in index order (parallel compaction).
+static void compact_in_order(const fvec<int32_t>& at, std::vector<int32_t>& out) {
+    const size_t n = at.size();
+    const int T = std::max(1, omp_get_max_threads());
+    std::vector<size_t> cnt((size_t)T + 1, 0);
+#pragma omp parallel num_threads(T)
+    {
+        const int t = omp_get_thread_num(), nt = omp_get_num_threads();
+        const size_t b0 = n * t / nt, b1 = n * (t + 1) / nt;
+        size_t c = 0;
+        for (size_t q = b0; q < b1; ++q) c += at[q] >= 0;
+        cnt[t + 1] = c;
+#pragma omp barrier
+#pragma omp single
+        {
+            for (int u = 0; u < nt; ++u) cnt[u + 1] += cnt[u];
+            out.resize(cnt[nt]);
+        }
+        size_t o = cnt[t];
+        for (size_t q = b0; q < b1; ++q)
+            if (at[q] >= 0) out[o++] = at[q];
+    }
+}
+
 // ---------------------------------------------------------------- rank plan
 RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nranks, int rank, int reorder) {
     StageTimer tm("build_rank_plan (total)");
@@ -330,29 +423,48 @@ RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nrank
     LapTimer lap;
     r.owner = rcb_partition(g, nranks);
     lap("rcb partition");
-    // sharers of each node: bitmask of ranks touching it (nranks <= 64)
+    // sharers of each node: bitmask of ranks touching it (nranks <= 64), from its adjacency
     if (nranks > 64) throw Error(TVEGPU_E_ARG, "at most 64 ranks");
-    std::vector<uint64_t> touch(N, 0);
-    for (int e = 0; e < E; ++e)
-        for (int a = 0; a < nn; ++a) touch[p.elements[(size_t)e * nn + a]] |= 1ULL << r.owner[e];
+    fvec<uint64_t> touch((size_t)N);
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < N; ++i) {
+        uint64_t t = 0;
+        for (int k = g.adj_off[i]; k < g.adj_off[i + 1]; ++k) t |= 1ULL << r.owner[g.adj_elem[k]];
+        touch[i] = t;
+    }
     const uint64_t me = 1ULL << rank;
     // owned elements, split into boundary (touches a shared node) and interior
     std::vector<int32_t> bnd, inr;
-    for (int e = 0; e < E; ++e) {
-        if (r.owner[e] != rank) continue;
-        bool b = false;
-        for (int a = 0; a < nn && !b; ++a) b = (touch[p.elements[(size_t)e * nn + a]] & ~me) != 0;
-        (b ? bnd : inr).push_back(e);
+    if (nranks == 1) {
+        inr.resize(E);
+        std::iota(inr.begin(), inr.end(), 0);
+    } else {
+        fvec<uint8_t> cls((size_t)E);  // 0 other rank, 1 boundary, 2 interior
+#pragma omp parallel for schedule(static)
+        for (int e = 0; e < E; ++e) {
+            if (r.owner[e] != rank) {
+                cls[e] = 0;
+                continue;
+            }
+            bool b = false;
+            for (int a = 0; a < nn && !b; ++a) b = (touch[p.elements[(size_t)e * nn + a]] & ~me) != 0;
+            cls[e] = b ? 1 : 2;
+        }
+        for (int e = 0; e < E; ++e)
+            if (cls[e]) (cls[e] == 1 ? bnd : inr).push_back(e);
     }
     if (reorder) {
-        std::vector<uint64_t> key(E);
+        fvec<uint64_t> key((size_t)E);
         const double mscale = morton_scale(g);
         auto sort_group = [&](std::vector<int32_t>& v) {
-#pragma omp parallel for schedule(static)
-            for (size_t q = 0; q < v.size(); ++q) key[v[q]] = morton_key(&g.centroid[(size_t)3 * v[q]], g.lo, mscale);
-            // a total order (ties broken by id): the parallel sort's result is unique
-            __gnu_parallel::sort(v.begin(), v.end(),
-                                 [&](int32_t x, int32_t y) { return key[x] < key[y] || (key[x] == key[y] && x < y); });
+            uint64_t kmax = 0;
+#pragma omp parallel for schedule(static) reduction(max : kmax)
+            for (size_t q = 0; q < v.size(); ++q) {
+                key[v[q]] = morton_key(&g.centroid[(size_t)3 * v[q]], g.lo, mscale);
+                kmax = std::max(kmax, key[v[q]]);
+            }
+            // total order (key, id): a stable radix sort of the id-ordered list by key
+            radix_sort_by_key(v, key.data(), kmax);
         };
         sort_group(bnd);
         sort_group(inr);
@@ -365,20 +477,38 @@ RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nrank
     }
     lap("boundary split + morton sort");
     r.Eb = (int)bnd.size();
-    r.elem_orig = bnd;
-    r.elem_orig.insert(r.elem_orig.end(), inr.begin(), inr.end());
+    r.elem_orig.resize(bnd.size() + inr.size());
+    std::copy(bnd.begin(), bnd.end(), r.elem_orig.begin());
+    std::copy(inr.begin(), inr.end(), r.elem_orig.begin() + bnd.size());
     r.E = (int)r.elem_orig.size();
-    // first-touch node numbering (identity when reorder = 0, nranks = 1)
-    std::vector<int32_t> local(N, -1);
+    fvec<int32_t> elem_local((size_t)E);
+#pragma omp parallel for schedule(static)
+    for (int e = 0; e < E; ++e) elem_local[e] = -1;
+#pragma omp parallel for schedule(static)
+    for (int le = 0; le < r.E; ++le) elem_local[r.elem_orig[le]] = le;
+    // first-touch node numbering (identity when reorder = 0, nranks = 1): a node's number
+    // is its rank by first local touch (local element, local index) — the minimum of
+    // le * nn + a over its adjacency; those keys are distinct, so scattering the nodes to
+    // their keys and compacting gives the numbering without a serial walk
+    fvec<int32_t> local((size_t)N);
     if (reorder) {
-        for (int le = 0; le < r.E; ++le)
-            for (int a = 0; a < nn; ++a) {
-                const int i = p.elements[(size_t)r.elem_orig[le] * nn + a];
-                if (local[i] < 0) {
-                    local[i] = (int)r.node_orig.size();
-                    r.node_orig.push_back(i);
-                }
+        const int64_t nk = (int64_t)r.E * nn;
+        fvec<int32_t> at((size_t)std::max<int64_t>(1, nk));
+#pragma omp parallel for schedule(static)
+        for (int64_t k = 0; k < nk; ++k) at[k] = -1;
+#pragma omp parallel for schedule(static)
+        for (int i = 0; i < N; ++i) {
+            int64_t first = INT64_MAX;
+            for (int k = g.adj_off[i]; k < g.adj_off[i + 1]; ++k) {
+                const int le = elem_local[g.adj_elem[k]];
+                if (le >= 0) first = std::min(first, (int64_t)le * nn + g.adj_local[k]);
             }
+            if (first != INT64_MAX) at[first] = i;
+            local[i] = -1;
+        }
+        compact_in_order(at, r.node_orig);
+#pragma omp parallel for schedule(static)
+        for (size_t li = 0; li < r.node_orig.size(); ++li) local[r.node_orig[li]] = (int32_t)li;
     } else {
         r.node_orig.resize(N);
         std::iota(r.node_orig.begin(), r.node_orig.end(), 0);
@@ -393,10 +523,8 @@ RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nrank
         r.node_owned[li] = (uint8_t)((t & (~t + 1)) == me);
     }
     r.conn.resize((size_t)r.E * nn);
-    std::vector<int32_t> elem_local(E, -1);
 #pragma omp parallel for schedule(static)
     for (int le = 0; le < r.E; ++le) {
-        elem_local[r.elem_orig[le]] = le;
         for (int a = 0; a < nn; ++a) r.conn[(size_t)le * nn + a] = local[p.elements[(size_t)r.elem_orig[le] * nn + a]];
     }
     lap("node numbering + conn");
@@ -484,7 +612,9 @@ RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nrank
     // every element contribution and every received one is gathered exactly once
     {
         const size_t ns = base + (r.recv_off.empty() ? 0 : r.recv_off.back());
-        std::vector<uint8_t> placed(ns, 0);
+        fvec<uint8_t> placed(ns);
+#pragma omp parallel for schedule(static)
+        for (size_t k = 0; k < ns; ++k) placed[k] = 0;
         int twice = 0, unplaced = 0;
         const size_t nc = r.csr_slot.size();
 #pragma omp parallel for schedule(static) reduction(| : twice)
@@ -507,14 +637,55 @@ RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nrank
 // 8 lanes are conflict-free iff their slots differ mod 8 (eight 16-byte bank
 // groups).  So the nodes are 8-coloured greedily over those co-read groups and
 // slot = 8 * (rank within colour) + colour; empty slots hold node -1.
-static std::vector<int32_t> colour_slots(const std::vector<int32_t>& nodes, const int32_t* conn, int ne, int nn,
-                                         std::vector<int32_t>& slot_of) {
+// Per-thread scratch of the chunk build (capacity kept across chunks: no allocation per
+// chunk), with an open-addressing map node id -> index in the chunk's sorted node list.
+struct ColourScratch {
+    std::vector<int> gdata, gsize, moff, mlist, fill, colour;
+    std::vector<int32_t> hkey, hval;
+    std::vector<unsigned> used;  // occupied slots (cleared after each chunk)
+    unsigned hmask = 0;
+    void map_reserve(size_t n) {
+        size_t cap = 64;
+        while (cap < 2 * n) cap *= 2;
+        if (hkey.size() < cap) {  // (only between chunks: the map is empty)
+            hkey.assign(cap, -1);
+            hval.assign(cap, 0);
+        }
+        hmask = (unsigned)hkey.size() - 1;
+    }
+    unsigned slot(int32_t n) const {
+        unsigned h = (unsigned)n * 2654435761u;
+        while (hkey[h & hmask] != -1 && hkey[h & hmask] != n) ++h;
+        return h & hmask;
+    }
+    bool insert(int32_t n) {  // true if new
+        const unsigned h = slot(n);
+        if (hkey[h] == n) return false;
+        hkey[h] = n;
+        used.push_back(h);
+        return true;
+    }
+    int index(int32_t n) const { return hval[slot(n)]; }
+    void set_index(int32_t n, int v) { hval[slot(n)] = v; }
+    void clear() {
+        for (unsigned h : used) hkey[h] = -1;
+        used.clear();
+    }
+};
+
+static void colour_slots(const std::vector<int32_t>& nodes, const int32_t* conn, int ne, int nn,
+                         std::vector<int32_t>& slot_of, std::vector<int32_t>& slots, ColourScratch& w) {
     const int nu = (int)nodes.size();
-    auto idx = [&](int32_t n) { return (int)(std::lower_bound(nodes.begin(), nodes.end(), n) - nodes.begin()); };
+    auto idx = [&](int32_t n) { return w.index(n); };
     // groups: (quarter-warp q, local a) -> distinct node indices, flat (<= 8 per group);
     // member: per node the groups it belongs to, ascending (CSR)
     const int ngmax = ((ne + 7) / 8) * nn;
-    std::vector<int> gdata((size_t)ngmax * 8), gsize(ngmax), moff(nu + 1, 0);
+    w.gdata.resize((size_t)ngmax * 8);
+    w.gsize.resize(ngmax);
+    w.moff.assign(nu + 1, 0);
+    int* gdata = w.gdata.data();
+    int* gsize = w.gsize.data();
+    int* moff = w.moff.data();
     int ng = 0;
     for (int q = 0; q * 8 < ne; ++q)
         for (int a = 0; a < nn; ++a) {
@@ -531,23 +702,23 @@ static std::vector<int32_t> colour_slots(const std::vector<int32_t>& nodes, cons
             gsize[ng++] = k;
         }
     for (int v = 0; v < nu; ++v) moff[v + 1] += moff[v];
-    std::vector<int> mlist(moff[nu]);
-    {
-        std::vector<int> fill(moff.begin(), moff.end() - 1);
-        for (int gi = 0; gi < ng; ++gi)
-            for (int j = 0; j < gsize[gi]; ++j) mlist[fill[gdata[(size_t)gi * 8 + j]]++] = gi;
-    }
+    w.mlist.resize(moff[nu]);
+    int* mlist = w.mlist.data();
+    w.fill.assign(moff, moff + nu);
+    for (int gi = 0; gi < ng; ++gi)
+        for (int j = 0; j < gsize[gi]; ++j) mlist[w.fill[gdata[(size_t)gi * 8 + j]]++] = gi;
     auto group = [&](int gi) { return std::make_pair(&gdata[(size_t)gi * 8], &gdata[(size_t)gi * 8] + gsize[gi]); };
     // Colour group by group in issue order: the uncoloured members of a group take
     // the colours still free in that group (this propagates the 2x2x2 parity
     // colouring through structured meshes); when a group has no free colour left,
     // fall back to the colour least used across all of the node's groups.
-    std::vector<int> colour(nu, -1);
+    w.colour.assign(nu, -1);
+    int* colour = w.colour.data();
     for (int gi = 0; gi < ng; ++gi) {
         const auto [g0, g1] = group(gi);
         bool used[8] = {false, false, false, false, false, false, false, false};
-        for (const int* w = g0; w < g1; ++w)
-            if (colour[*w] >= 0) used[colour[*w]] = true;
+        for (const int* x = g0; x < g1; ++x)
+            if (colour[*x] >= 0) used[colour[*x]] = true;
         for (const int* pv = g0; pv < g1; ++pv) {
             const int v = *pv;
             if (colour[v] >= 0) continue;
@@ -557,8 +728,8 @@ static std::vector<int32_t> colour_slots(const std::vector<int32_t>& nodes, cons
                 int uses[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                 for (int m = moff[v]; m < moff[v + 1]; ++m) {
                     const auto [h0, h1] = group(mlist[m]);
-                    for (const int* w = h0; w < h1; ++w)
-                        if (colour[*w] >= 0) uses[colour[*w]]++;
+                    for (const int* x = h0; x < h1; ++x)
+                        if (colour[*x] >= 0) uses[colour[*x]]++;
                 }
                 c = 0;
                 for (int k = 1; k < 8; ++k)
@@ -577,8 +748,8 @@ static std::vector<int32_t> colour_slots(const std::vector<int32_t>& nodes, cons
             int cost[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             for (int m = moff[v]; m < moff[v + 1]; ++m) {
                 const auto [h0, h1] = group(mlist[m]);
-                for (const int* w = h0; w < h1; ++w)
-                    if (*w != v && colour[*w] >= 0) cost[colour[*w]]++;
+                for (const int* x = h0; x < h1; ++x)
+                    if (*x != v && colour[*x] >= 0) cost[colour[*x]]++;
             }
             int best = colour[v];
             for (int c = 0; c < 8; ++c)
@@ -602,13 +773,12 @@ static std::vector<int32_t> colour_slots(const std::vector<int32_t>& nodes, cons
             }
     }
     int count[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    slot_of.assign(nu, 0);
+    slot_of.resize(nu);
     for (int v = 0; v < nu; ++v) slot_of[v] = 8 * count[colour[v]]++ + colour[v];
     int rows = 0;
     for (int c = 0; c < 8; ++c) rows = std::max(rows, count[c]);
-    std::vector<int32_t> slots((size_t)8 * rows, -1);
+    slots.assign((size_t)8 * rows, -1);
     for (int v = 0; v < nu; ++v) slots[slot_of[v]] = nodes[v];
-    return slots;
 }
 
 void build_chunks(RankPlan& r) {
@@ -619,7 +789,7 @@ void build_chunks(RankPlan& r) {
     r.chunk_node_off.assign(1, 0);
     r.chunk_nodes.clear();
     r.chunk_node_slot.clear();
-    r.lconn.assign((size_t)r.E * nn, 0);
+    r.lconn.resize((size_t)r.E * nn);  // every entry written below
     r.max_chunk_nodes = 0;
     // chunk ranges: boundary elements [0, Eb) then interior [Eb, E), kChunk at a time
     std::vector<int32_t> starts;
@@ -631,34 +801,48 @@ void build_chunks(RankPlan& r) {
     // chunks are independent: unique nodes, colouring and 16-bit connectivity in parallel
     std::vector<std::vector<int32_t>> cnodes(nc), cslot(nc);
     std::vector<int32_t> nslots(nc, 0);
-#pragma omp parallel for schedule(dynamic, 16)
-    for (int c = 0; c < nc; ++c) {
-        const int c0 = starts[c], c1 = chunk_end(c);
-        std::vector<int32_t> nodes(r.conn.begin() + (size_t)c0 * nn, r.conn.begin() + (size_t)c1 * nn);
-        std::sort(nodes.begin(), nodes.end());
-        nodes.erase(std::unique(nodes.begin(), nodes.end()), nodes.end());
-        std::vector<int32_t> slot_of;
-        const std::vector<int32_t> slots = colour_slots(nodes, r.conn.data() + (size_t)c0 * nn, c1 - c0, nn, slot_of);
-        for (int le = c0; le < c1; ++le)
-            for (int a = 0; a < nn; ++a) {
-                const int32_t n = r.conn[(size_t)le * nn + a];
-                const int v = (int)(std::lower_bound(nodes.begin(), nodes.end(), n) - nodes.begin());
-                r.lconn[(size_t)le * nn + a] = (uint16_t)slot_of[v];
-            }
-        nslots[c] = (int)slots.size();
-        cnodes[c] = std::move(nodes);
-        cslot[c] = std::move(slot_of);
+#pragma omp parallel
+    {
+        ColourScratch w;
+        std::vector<int32_t> slots;
+#pragma omp for schedule(dynamic, 16)
+        for (int c = 0; c < nc; ++c) {
+            const int c0 = starts[c], c1 = chunk_end(c);
+            const int32_t* cc = r.conn.data() + (size_t)c0 * nn;
+            const int m = (c1 - c0) * nn;
+            w.map_reserve(m);
+            std::vector<int32_t> nodes;
+            nodes.reserve(m);
+            for (int k = 0; k < m; ++k)
+                if (w.insert(cc[k])) nodes.push_back(cc[k]);
+            std::sort(nodes.begin(), nodes.end());
+            for (int v = 0; v < (int)nodes.size(); ++v) w.set_index(nodes[v], v);
+            std::vector<int32_t> slot_of;
+            colour_slots(nodes, cc, c1 - c0, nn, slot_of, slots, w);
+            for (int k = 0; k < m; ++k) r.lconn[(size_t)c0 * nn + k] = (uint16_t)slot_of[w.index(cc[k])];
+            w.clear();
+            nslots[c] = (int)slots.size();
+            cnodes[c] = std::move(nodes);
+            cslot[c] = std::move(slot_of);
+        }
     }
     lap("unique nodes + colouring");
     // staging walks each chunk's nodes in ascending id (coalesced loads), storing each to its slot
+    r.chunk_start.assign(starts.begin(), starts.end());
+    r.chunk_start.push_back(r.E);
+    r.chunk_node_off.resize((size_t)nc + 1);
+    r.chunk_node_off[0] = 0;
     for (int c = 0; c < nc; ++c) {
-        r.chunk_start.push_back(starts[c]);
-        r.chunk_nodes.insert(r.chunk_nodes.end(), cnodes[c].begin(), cnodes[c].end());
-        for (int32_t s : cslot[c]) r.chunk_node_slot.push_back((uint16_t)s);
-        r.chunk_node_off.push_back((int32_t)r.chunk_nodes.size());
+        r.chunk_node_off[c + 1] = r.chunk_node_off[c] + (int32_t)cnodes[c].size();
         r.max_chunk_nodes = std::max(r.max_chunk_nodes, nslots[c]);
     }
-    r.chunk_start.push_back(r.E);
+    r.chunk_nodes.resize(r.chunk_node_off[nc]);
+    r.chunk_node_slot.resize(r.chunk_node_off[nc]);
+#pragma omp parallel for schedule(static)
+    for (int c = 0; c < nc; ++c) {
+        std::copy(cnodes[c].begin(), cnodes[c].end(), r.chunk_nodes.begin() + r.chunk_node_off[c]);
+        for (size_t k = 0; k < cslot[c].size(); ++k) r.chunk_node_slot[r.chunk_node_off[c] + k] = (uint16_t)cslot[c][k];
+    }
 }
 
 void critical_timestep_from_edge(const tvegpu_problem& p, double L, double* thermal, double* mechanical) {

@@ -16,8 +16,11 @@
 #include <cstdlib>
 
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "../../include/tvegpu.h"
@@ -50,6 +53,28 @@ struct LapTimer {
     }
 };
 
+// std::vector whose resize leaves trivially constructible elements uninitialised, so
+// large setup arrays are first touched by the parallel loops that fill them (a zeroing
+// resize of a 128M-entry array is a serial memset of half a gigabyte).
+template <class T, class A = std::allocator<T>>
+struct default_init_allocator : A {
+    using A::A;
+    template <class U>
+    struct rebind {
+        using other = default_init_allocator<U, typename std::allocator_traits<A>::template rebind_alloc<U>>;
+    };
+    template <class U>
+    void construct(U* p) noexcept(std::is_nothrow_default_constructible<U>::value) {
+        ::new (static_cast<void*>(p)) U;
+    }
+    template <class U, class... Args>
+    void construct(U* p, Args&&... args) {
+        std::allocator_traits<A>::construct(static_cast<A&>(*this), p, std::forward<Args>(args)...);
+    }
+};
+template <class T>
+using fvec = std::vector<T, default_init_allocator<T>>;
+
 struct Error : std::runtime_error {
     Error(tvegpu_status s, const std::string& m) : std::runtime_error(m), status(s) {}
     tvegpu_status status;
@@ -62,13 +87,12 @@ extern const int kHg[4][8];
 
 struct GlobalMesh {
     int kind = TVEGPU_T4, nn = 4, N = 0, E = 0;
-    std::vector<double> A;         // 9 per element (row-major), G_e = A_e Xi
-    std::vector<double> vol;       // per element (T4: V; H8: 8 det J0)
-    std::vector<double> centroid;  // 3 per element
-    std::vector<double> mass;      // per node: sum rho V_e / nn (canonical order)
-    std::vector<double> vnode;     // per node: sum V_e / nn (canonical order)
-    std::vector<int32_t> adj_off;  // node -> (element, local): canonical CSR over original ids
-    std::vector<int32_t> adj_elem, adj_local;
+    fvec<double> vol;              // per element (T4: V; H8: 8 det J0)
+    fvec<double> centroid;         // 3 per element
+    fvec<double> mass;             // per node: sum rho V_e / nn (canonical order)
+    fvec<double> vnode;            // per node: sum V_e / nn (canonical order)
+    fvec<int32_t> adj_off;         // node -> (element, local): canonical CSR over original ids
+    fvec<int32_t> adj_elem, adj_local;
     double lo[3], hi[3];           // bounding box of element centroids
     double min_edge = 0;           // smallest element edge length (Morton lattice spacing)
 };
@@ -91,9 +115,9 @@ struct RankPlan {
     int E = 0, Eb = 0, N = 0;
     std::vector<int32_t> elem_orig;   // local -> original element
     std::vector<int32_t> node_orig;   // local -> original node
-    std::vector<int32_t> conn;        // nn * E, element-major, local node ids
-    std::vector<int32_t> csr_off;     // N + 1
-    std::vector<int32_t> csr_slot;    // local slot (e*nn + a) or nn*E + receive index
+    fvec<int32_t> conn;               // nn * E, element-major, local node ids
+    fvec<int32_t> csr_off;            // N + 1
+    fvec<int32_t> csr_slot;           // local slot (e*nn + a) or nn*E + receive index
     std::vector<int32_t> neighbors;
     std::vector<int32_t> send_off, send_slot, recv_off;
     std::vector<int32_t> owner;       // global element -> rank
@@ -105,7 +129,7 @@ struct RankPlan {
     std::vector<int32_t> chunk_node_off;  // nchunks + 1
     std::vector<int32_t> chunk_nodes;     // unique local node ids per chunk, ascending
     std::vector<uint16_t> chunk_node_slot;  // shared-memory slot of each chunk_nodes entry
-    std::vector<uint16_t> lconn;          // E * nn, element-major: slot of node (e, a) in its chunk
+    fvec<uint16_t> lconn;                 // E * nn, element-major: slot of node (e, a) in its chunk
     int nchunks_boundary = 0;             // chunks [0, nchunks_boundary) cover [0, Eb)
     int max_chunk_nodes = 0;              // max shared-memory slots (incl. colour padding) of a chunk
 };
