@@ -139,6 +139,60 @@ T* dupload(std::vector<void*>& owned, const std::vector<T, Al>& v, cudaStream_t 
     return p;
 }
 
+// Temporary device buffers of one setup stage, freed on scope exit (the caller
+// synchronises the stream first).
+struct DeviceScratch {
+    std::vector<void*> p;
+    template <class T>
+    T* get(size_t n) {
+        void* q = nullptr;
+        CU(cudaMalloc(&q, std::max<size_t>(1, n) * sizeof(T)));
+        p.push_back(q);
+        return static_cast<T*>(q);
+    }
+    ~DeviceScratch() {
+        for (void* q : p) cudaFree(q);
+    }
+};
+
+// Setup kernels: node records / coordinates / lumped constants in local order from the
+// original-order inputs; the chunks' fixed-stride staging entries; the chunks'
+// coordinate blocks in shared-slot order.
+__global__ void k_init_nodes(const int32_t* __restrict__ node_orig, const double* __restrict__ xyz,
+                             const double* __restrict__ mass_o, const double* __restrict__ vn_o, double T0, int N,
+                             double4* rec0, double4* rec1, double4* X, double* mass, double* vn) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const size_t o = (size_t)node_orig[i];
+    rec0[i] = rec1[i] = make_double4(0.0, 0.0, 0.0, T0);
+    X[i] = make_double4(xyz[3 * o], xyz[3 * o + 1], xyz[3 * o + 2], 0.0);
+    mass[i] = mass_o[o];
+    vn[i] = vn_o[o];
+}
+__global__ void k_stage_entries(const int32_t* __restrict__ off, const int32_t* __restrict__ nodes,
+                                const uint16_t* __restrict__ slot, int st, int2* __restrict__ ent) {
+    const int c = blockIdx.x;
+    const int u0 = off[c], u1 = off[c + 1];
+    for (int k = threadIdx.x; k < st; k += blockDim.x) {
+        const int u = u0 + k;
+        ent[(size_t)c * st + k] = u < u1 ? make_int2(nodes[u], (int)slot[u]) : make_int2(-1, 0);
+    }
+}
+__global__ void k_chunk_coords(const int32_t* __restrict__ off, const int32_t* __restrict__ nodes,
+                               const uint16_t* __restrict__ slot, const int32_t* __restrict__ xs,
+                               const double4* __restrict__ X, int xstride, double* __restrict__ cx) {
+    const int c = blockIdx.x;
+    const int S = xs[c];
+    double* b = cx + (size_t)c * xstride;
+    for (int u = off[c] + threadIdx.x; u < off[c + 1]; u += blockDim.x) {
+        const double4 x = X[nodes[u]];
+        const int sl = slot[u];
+        b[sl] = x.x;
+        b[S + sl] = x.y;
+        b[2 * S + sl] = x.z;
+    }
+}
+
 struct Region {
     double q_r, t_start, t_end;
     std::vector<int32_t> nodes;  // nn per element, original ids
@@ -817,6 +871,7 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     }
     h->plan = build_rank_plan(p, g, nranks, o.rank, o.reorder);
     StageTimer tm_dev("device tables + uploads");
+    LapTimer lap;
     const RankPlan& pl = h->plan;
     h->nn = g.nn;
     h->kind = p.kind;
@@ -907,9 +962,35 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     CU(cudaMallocHost(&h->h_words, 8 * sizeof(unsigned long long)));
     cudaStream_t s = h->s;
     auto& own = h->owned;
+    // ---- node arrays, built on the device from the original-order inputs (no host
+    // loops over N, and only the inputs cross the link)
+    h->ptr.node_orig = dupload(own, pl.node_orig, s);
+    h->ptr.rec0 = dalloc<double4>(own, N);
+    h->ptr.rec1 = dalloc<double4>(own, N);
+    h->ptr.X = dalloc<double4>(own, N);
+    h->ptr.mass = dalloc<double>(own, N);
+    h->ptr.vnode = dalloc<double>(own, N);
+    {
+        const size_t Ng = (size_t)g.N;
+        DeviceScratch tmp;
+        double* xyz = tmp.get<double>(3 * Ng);
+        double* mo = tmp.get<double>(Ng);
+        double* vo = tmp.get<double>(Ng);
+        h2d(xyz, p.nodes, 3 * Ng * 8, s);
+        h2d(mo, g.mass.data(), Ng * 8, s);
+        h2d(vo, g.vnode.data(), Ng * 8, s);
+        if (N > 0)
+            k_init_nodes<<<blocks(N, 256), 256, 0, s>>>(h->ptr.node_orig, xyz, mo, vo, p.initial_temperature, N,
+                                                        h->ptr.rec0, h->ptr.rec1, const_cast<double4*>(h->ptr.X),
+                                                        const_cast<double*>(h->ptr.mass),
+                                                        const_cast<double*>(h->ptr.vnode));
+        CU(cudaGetLastError());
+        CU(cudaStreamSynchronize(s));  // before the scratch is freed
+    }
+    lap("node arrays");
     // ---- element arrays: the chunked connectivity (per chunk its unique node list as
-    // fixed-stride {node, slot} entries, per element 16-bit indices into the staged
-    // planes); the reference geometry rows follow once the coordinates are on the device.
+    // fixed-stride {node, slot} staging entries, per element 16-bit indices into the staged
+    // planes), built on the device from the per-chunk lists
     h->ptr.chunk_start = dupload(own, pl.chunk_start, s);
     h->ptr.chunk_node_off = dupload(own, pl.chunk_node_off, s);
     h->ptr.chunk_nodes = dupload(own, pl.chunk_nodes, s);
@@ -919,47 +1000,39 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     {
         const int nc = (int)pl.chunk_start.size() - 1;
         int st = 1;
+#pragma omp parallel for schedule(static) reduction(max : st)
         for (int c = 0; c < nc; ++c) st = std::max(st, pl.chunk_node_off[c + 1] - pl.chunk_node_off[c]);
-        fvec<int32_t> ent((size_t)2 * nc * st);
-#pragma omp parallel for schedule(static)
-        for (int c = 0; c < nc; ++c)
-            for (int k = 0; k < st; ++k) {
-                const int u = pl.chunk_node_off[c] + k;
-                const bool in = u < pl.chunk_node_off[c + 1];
-                ent[2 * ((size_t)c * st + k)] = in ? pl.chunk_nodes[u] : -1;
-                ent[2 * ((size_t)c * st + k) + 1] = in ? pl.chunk_node_slot[u] : 0;
-            }
-        h->ptr.stage_ent = reinterpret_cast<const int2*>(dupload(own, ent, s));
+        int2* ent = dalloc<int2>(own, (size_t)nc * st);
+        if (nc > 0)
+            k_stage_entries<<<nc, 128, 0, s>>>(h->ptr.chunk_node_off, h->ptr.chunk_nodes, h->ptr.chunk_node_slot, st,
+                                               ent);
+        CU(cudaGetLastError());
+        h->ptr.stage_ent = ent;
         m.stage_stride = st;
-        // element-kernel coordinate blocks (k1_xstage / k3_xstage): per chunk its nodes' reference coordinates in
-        // shared-slot order, x[S] y[S] z[S] with S = slots used (even), one bulk copy each
+        // element-kernel coordinate blocks (k1_xstage / k3_xstage): per chunk its nodes'
+        // reference coordinates in shared-slot order, x[S] y[S] z[S] with S = slots used
+        // (even), one bulk copy each
         const int ms2 = (m.max_chunk_nodes + 1) & ~1;
         m.xstride = 3 * ms2;
         if (pl.nn == 8 ? (k3_xstage<8>() || k1_xstage<8>()) : (k3_xstage<4>() || k1_xstage<4>())) {
-            std::vector<double> cx((size_t)nc * m.xstride, 0.0);
             std::vector<int32_t> cs(std::max(1, nc), 2);
 #pragma omp parallel for schedule(static)
             for (int c = 0; c < nc; ++c) {
                 int S = 0;
                 for (int u = pl.chunk_node_off[c]; u < pl.chunk_node_off[c + 1]; ++u)
                     S = std::max(S, (int)pl.chunk_node_slot[u] + 1);
-                S = std::max(2, (S + 1) & ~1);
-                cs[c] = S;
-                double* b = cx.data() + (size_t)c * m.xstride;
-                for (int u = pl.chunk_node_off[c]; u < pl.chunk_node_off[c + 1]; ++u) {
-                    const int sl = pl.chunk_node_slot[u];
-                    const size_t o = 3 * (size_t)pl.node_orig[pl.chunk_nodes[u]];
-                    b[sl] = p.nodes[o];
-                    b[S + sl] = p.nodes[o + 1];
-                    b[2 * S + sl] = p.nodes[o + 2];
-                }
+                cs[c] = std::max(2, (S + 1) & ~1);
             }
-            h->ptr.chunk_x = dupload(own, cx, s);
             h->ptr.chunk_xs = dupload(own, cs, s);
-            CU(cudaStreamSynchronize(s));
+            double* cx = dalloc<double>(own, (size_t)std::max(1, nc) * m.xstride);
+            CU(cudaMemsetAsync(cx, 0, (size_t)std::max(1, nc) * m.xstride * 8, s));
+            if (nc > 0)
+                k_chunk_coords<<<nc, 128, 0, s>>>(h->ptr.chunk_node_off, h->ptr.chunk_nodes, h->ptr.chunk_node_slot,
+                                                  h->ptr.chunk_xs, h->ptr.X, m.xstride, cx);
+            CU(cudaGetLastError());
+            h->ptr.chunk_x = cx;
         }
     }
-    CU(cudaStreamSynchronize(s));
     set_smem_limits(h);
     // PDL only where the four step kernels follow each other directly on one stream
     h->pdl = !loopback && pl.nranks == 1 && !std::getenv("TVEGPU_NO_PDL");
@@ -968,43 +1041,24 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     h->ptr.theta = dalloc<double>(own, (size_t)6 * P * es);
     CU(cudaMemsetAsync(h->ptr.theta, 0, std::max<size_t>(1, (size_t)6 * P * es) * 8, s));
     if (p.fiber_dirs && m.fiber_mode == 2) {
-        std::vector<double> f((size_t)3 * es, 0.0);
+        fvec<double> f((size_t)3 * es);
 #pragma omp parallel for schedule(static)
-        for (int e = 0; e < E; ++e)
-            for (int k = 0; k < 3; ++k) f[(size_t)k * es + e] = p.fiber_dirs[3 * (size_t)pl.elem_orig[e] + k];
+        for (size_t e = 0; e < es; ++e)
+            for (int k = 0; k < 3; ++k)
+                f[(size_t)k * es + e] = e < (size_t)E ? p.fiber_dirs[3 * (size_t)pl.elem_orig[e] + k] : 0.0;
         h->ptr.fiber = dupload(own, f, s);
-        CU(cudaStreamSynchronize(s));
     }
     if (p.expansion_axes && expansion) {
-        std::vector<double> f((size_t)6 * es, 0.0);
+        fvec<double> f((size_t)6 * es);
 #pragma omp parallel for schedule(static)
-        for (int e = 0; e < E; ++e)
-            for (int k = 0; k < 6; ++k) f[(size_t)k * es + e] = p.expansion_axes[6 * (size_t)pl.elem_orig[e] + k];
+        for (size_t e = 0; e < es; ++e)
+            for (int k = 0; k < 6; ++k)
+                f[(size_t)k * es + e] = e < (size_t)E ? p.expansion_axes[6 * (size_t)pl.elem_orig[e] + k] : 0.0;
         h->ptr.axes = dupload(own, f, s);
-        CU(cudaStreamSynchronize(s));
     }
-    // ---- node arrays
-    {
-        fvec<double4> rec(N), X(N);
-        fvec<double> mass(N), vn(N);
-#pragma omp parallel for schedule(static)
-        for (int i = 0; i < N; ++i) {
-            const int oi = pl.node_orig[i];
-            rec[i] = make_double4(0.0, 0.0, 0.0, p.initial_temperature);
-            X[i] = make_double4(p.nodes[3 * (size_t)oi], p.nodes[3 * (size_t)oi + 1], p.nodes[3 * (size_t)oi + 2], 0.0);
-            mass[i] = g.mass[oi];
-            vn[i] = g.vnode[oi];
-        }
-        h->ptr.rec0 = dupload(own, rec, s);
-        h->ptr.rec1 = dupload(own, rec, s);
-        h->ptr.X = dupload(own, X, s);
-        h->ptr.mass = dupload(own, mass, s);
-        h->ptr.vnode = dupload(own, vn, s);
-        CU(cudaStreamSynchronize(s));
-    }
-    {  // per-element reference geometry, once (k_geometry, same arithmetic as the in-kernel path);
-       // read by the element kernels (TMA rows) and by the run-level
-       // energy reduction always
+    lap("chunks, element rows");
+    {  // per-element reference geometry, once (k_geometry): read by the element kernels
+       // (TMA rows) and the run-level energy reduction
         if (!h->d_conn) h->d_conn = dupload(own, pl.conn, s);
         // A, V (10 rows) for K1 and the run-level energy; + the H8 hourglass vectors when K3
         // reads them instead of rebuilding them from the chunk coordinates (k3_xstage)
@@ -1018,11 +1072,11 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
         }
         h->ptr.geo = geo;
     }
-    h->ptr.node_orig = dupload(own, pl.node_orig, s);
     CU(cudaMallocHost(&h->qr_host, std::max(1, N) * sizeof(double)));
     std::memset(h->qr_host, 0, std::max(1, N) * sizeof(double));
     h->ptr.qr = dalloc<double>(own, N);
     CU(cudaMemsetAsync(const_cast<double*>(h->ptr.qr), 0, std::max(1, N) * sizeof(double), s));
+    lap("geometry kernel");
     // ---- boundary conditions (mechanics.hpp:37-47, bioheat.hpp:32-35)
     {
         fvec<int32_t> local(g.N);
@@ -1097,6 +1151,7 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
             CU(cudaStreamSynchronize(s));
         }
     }
+    lap("boundary conditions");
     // ---- gather CSR and slot buffers
     h->ptr.csr_off = dupload(own, pl.csr_off, s);
     h->ptr.csr_slot = dupload(own, pl.csr_slot, s);
@@ -1138,6 +1193,7 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
             h->ptr.ell = reinterpret_cast<const int4*>(dupload(own, ell, s));
         }
     }
+    lap("gather lists, slot buffers");
     // ---- clock and error words
     // clock + the two error words contiguous: the end-of-call check is one 40-byte read
     static_assert(sizeof(Clock) == 24, "status block layout");

@@ -19,16 +19,19 @@ import numpy as np
 import torch
 
 import paper_2009_10400_b200 as tg
+from bench import ClockSampler, canonical_bytes, load_peaks
 from paper_2009_10400_b200 import configs
 from paper_2009_10400_b200.problem import H8, T4
 
 MODES = {"TherMechTI": dict(expansion_enabled=False, temperature_dependent=False),
          "TherMechExpanTI": dict(expansion_enabled=True, temperature_dependent=False),
          "TherMechExpanTD": dict(expansion_enabled=True, temperature_dependent=True)}
-LADDER = {H8: [100, 126, 159, 200, 252], T4: [40, 50, 63, 80, 100, 126]}
+LADDER = {H8: [100, 126, 159, 200, 252], T4: [55, 69, 87, 110, 126, 139]}  # up to 16.0M / 16.1M elements
 
 
-def time_steps(eng, steps, warmup, soak=0.3):
+def time_steps(eng, steps, warmup, sampler, soak=0.3):
+    """ms per step (CUDA events on the engine stream, graph replays) and the clocks
+    sampled by nvidia-smi during the timed window (the bench's clock record)."""
     stream = torch.cuda.ExternalStream(eng.stream)
     eng.step(warmup)
     eng.sync()
@@ -37,11 +40,14 @@ def time_steps(eng, steps, warmup, soak=0.3):
         eng.step(64)
         eng.sync()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.time()
     a.record(stream)
-    eng.step(steps)
+    eng.enqueue(steps)
     b.record(stream)
     b.synchronize()
-    return a.elapsed_time(b) / steps
+    w1 = time.time()
+    eng.sync()
+    return a.elapsed_time(b) / steps, sampler.summary(w0, w1)
 
 
 def main():
@@ -52,6 +58,8 @@ def main():
     ap.add_argument("--out", default="gpurun_out/ladder.json")
     args = ap.parse_args()
     rows = []
+    sampler = ClockSampler(0)
+    peak, _ = load_peaks()
     for kname in args.kinds.split(","):
         kind = H8 if kname == "H8" else T4
         for n in LADDER[kind]:
@@ -67,9 +75,15 @@ def main():
                 eng = tg.Engine(p)
                 eng.sync()
                 setup = time.perf_counter() - t0
-                ms = time_steps(eng, args.steps, args.warmup)
+                ms, clk = time_steps(eng, args.steps, args.warmup, sampler)
                 row[mname] = ms
                 row[mname + "_setup_s"] = setup
+                row[mname + "_clocks"] = clk
+                if mname == "TherMechExpanTD":  # the bench mode: element-steps/s and canonical HBM fraction
+                    cb = sum(canonical_bytes(p).values())
+                    row["element_steps_per_s"] = p.num_elements / (ms / 1e3)
+                    row["canonical_bytes_per_step"] = cb
+                    row["hbm_frac"] = cb / (ms / 1e3) / 1e9 / peak
                 del eng
                 torch.cuda.empty_cache()
             rows.append(row)
@@ -82,6 +96,7 @@ def main():
             y = np.log([q[mname] for q in r])
             out["slopes"][f"{kname}/{mname}"] = float(np.polyfit(x, y, 1)[0])
         out[f"{kname}_mode_order_holds"] = all(q["TherMechTI"] < q["TherMechExpanTI"] < q["TherMechExpanTD"] for q in r)
+    sampler.stop()
     print(json.dumps(out["slopes"]), flush=True)
     os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
     with open(args.out, "w") as f:

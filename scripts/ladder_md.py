@@ -10,13 +10,16 @@ print(f"# Size ladder {tag} — one B200 (scripts/ladder.py)\n")
 print("Per-step time [ms] (CUDA events, graph-replayed, 200 steps after 20 warm-up) of the three coupled "
       "modes on structured cubes; setup = `tvegpu_create` wall time (plan + upload). Reference API: "
       "`run_bench` / `bench_scaling_slope` (engine.hpp:145-162), SPEC.md criterion 9.\n")
-print("| kind | n | elements | nodes | " + " | ".join(modes) + " | element-steps/s (ExpanTD) | setup [s] |")
-print("|---|---|---|---|---|---|---|---|---|")
+print("| kind | n | elements | nodes | " + " | ".join(modes) +
+      " | element-steps/s (ExpanTD) | canonical HBM frac | setup [s] | SM MHz (median) | throttle reasons |")
+print("|---|---|---|---|---|---|---|---|---|---|---|---|")
 for r in d["rows"]:
     eps = r["elements"] / (r["TherMechExpanTD"] * 1e-3)
+    clk = r.get("TherMechExpanTD_clocks") or {}
     print(f"| {r['kind']} | {r['n']} | {r['elements']:,} | {r['nodes']:,} | "
           + " | ".join(f"{r[m]:.3f}" for m in modes)
-          + f" | {eps:.2e} | {r['TherMechExpanTD_setup_s']:.1f} |")
+          + f" | {eps:.2e} | {r.get('hbm_frac', float('nan')):.3f} | {r['TherMechExpanTD_setup_s']:.1f} | "
+          + f"{clk.get('sm_mhz')} | {', '.join(clk.get('reasons', [])) or '-'} |")
 print("\nlog-log slope of step time vs elements (SPEC criterion 9 asks for [0.9, 1.2]):\n")
 for k, v in d["slopes"].items():
     print(f"- {k}: {v:.3f}")
