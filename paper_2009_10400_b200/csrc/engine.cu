@@ -285,6 +285,11 @@ struct tvegpu_engine {
     int pend_cur = 0;
     double pend_time = 0;
     cudaEvent_t ev_entry = nullptr;  // tvegpu_step_io: work already on s before the side-stream upload
+    // tvegpu_step_io read-back slices: K4 of the last step runs over local nodes
+    // [io_cut[k], io_cut[k+1]); once slice k is done every node of original id < io_done[k]
+    // is final, so u[io_done[k-1], io_done[k]) is copied while the next slices compute
+    std::vector<int> io_cut, io_done;
+    std::vector<cudaEvent_t> ev_u;
     unsigned long long* h_words = nullptr;  // pinned: clock (3 words) + err_inst + err_elem
     double4* stage = nullptr;               // pinned readback staging (N records)
     double* d_io = nullptr;                 // device I/O buffer in original numbering (4N doubles)
@@ -516,14 +521,15 @@ void launch_thermal_node(tvegpu_engine* h, double* t_out) {
     launch_step_kernel(h, thermal_node_kernel(h), blocks(h->pair ? 2 * N : N, kNodeThreads), kNodeThreads, 0, h->prm,
                        h->ptr, h->cur, (int)(h->mode == TVEGPU_THERMAL_ONLY), t_out);
 }
-void launch_mech_node(tvegpu_engine* h, double* u_out) {
-    const int N = h->plan.N;
+void launch_mech_node(tvegpu_engine* h, double* u_out, int n0 = 0, int n1 = -1, int closes = 1) {
+    if (n1 < 0) n1 = h->plan.N;
+    const int n = std::max(0, n1 - n0);
     if (h->pair)
-        launch_step_kernel(h, k_mech_node<true>, blocks(2 * N, kNodeThreads), kNodeThreads, 0, h->prm, h->ptr, h->cur, 1,
-                           u_out);
+        launch_step_kernel(h, k_mech_node<true>, std::max(1, blocks(2 * n, kNodeThreads)), kNodeThreads, 0, h->prm,
+                           h->ptr, h->cur, closes, u_out, n0, n1);
     else
-        launch_step_kernel(h, k_mech_node<false>, blocks(N, kNodeThreads), kNodeThreads, 0, h->prm, h->ptr, h->cur, 1,
-                           u_out);
+        launch_step_kernel(h, k_mech_node<false>, std::max(1, blocks(n, kNodeThreads)), kNodeThreads, 0, h->prm,
+                           h->ptr, h->cur, closes, u_out, n0, n1);
 }
 
 void set_smem_limits(tvegpu_engine* h) {
@@ -567,7 +573,15 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr, cudaEvent_t 
     if (h->mode != TVEGPU_THERMAL_ONLY) {
         launch_mech_elements(h, 0, nc);
         mark();
-        launch_mech_node(h, u_out);
+        const int ns = (int)h->io_cut.size() - 1;
+        if (u_out && ns > 1) {  // tvegpu_step_io: K4 in node slices, each read back once complete
+            for (int k = 0; k < ns; ++k) {
+                launch_mech_node(h, u_out, h->io_cut[k], h->io_cut[k + 1], k == ns - 1 ? 1 : 0);
+                CU(cudaEventRecord(h->ev_u[k], h->s));
+            }
+        } else {
+            launch_mech_node(h, u_out);
+        }
         mark();
         h->cur ^= 1;
     }
@@ -1232,6 +1246,18 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
         h->regions.push_back(std::move(reg));
     }
     h->active.assign(h->regions.size(), 0);
+    // ---- tvegpu_step_io read-back slices (single partition)
+    if (pl.nranks == 1 && N == g.N && N > 0) {
+        const char* env = std::getenv("TVEGPU_IO_SLICES");
+        const int ns = std::max(1, std::min(16, env ? std::atoi(env) : 4));
+        fvec<int32_t> suf((size_t)N + 1);  // min original id over local nodes [i, N)
+        suf[N] = g.N;
+        for (int i = N - 1; i >= 0; --i) suf[i] = std::min(suf[i + 1], pl.node_orig[i]);
+        for (int k = 0; k <= ns; ++k) h->io_cut.push_back((int)((int64_t)N * k / ns));
+        for (int k = 0; k < ns; ++k) h->io_done.push_back(suf[h->io_cut[k + 1]]);
+        h->ev_u.resize(ns);
+        for (auto& ev : h->ev_u) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
     // ---- multi-GPU halo
     if (nranks > 1) {
         if (!loopback) {  // one partition per process and GPU: the NCCL transport
@@ -1712,6 +1738,7 @@ void tvegpu_destroy(tvegpu_engine* h) {
     if (h->ev_comm) cudaEventDestroy(h->ev_comm);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
     if (h->ev_entry) cudaEventDestroy(h->ev_entry);
+    for (cudaEvent_t ev : h->ev_u) cudaEventDestroy(ev);
     if (h->s) cudaStreamDestroy(h->s);
     if (h->sc) cudaStreamDestroy(h->sc);
     delete h;
@@ -1977,7 +2004,19 @@ tvegpu_status tvegpu_step_io(tvegpu_engine* h, const double* power, int64_t n, d
             }
             CU(cudaMemcpyAsync(T, dT, (size_t)N * 8, cudaMemcpyDeviceToHost, h->sc));
         }
-        if (u) {
+        if (u && mech && h->io_cut.size() > 2) {
+            // each K4 slice's completion releases the original-id prefix it finished: the
+            // read-back of u overlaps the remaining slices (same side stream as T, in order)
+            int done = 0;
+            for (size_t k = 0; k + 1 < h->io_cut.size(); ++k) {
+                const int upto = h->io_done[k];
+                if (upto <= done) continue;
+                CU(cudaStreamWaitEvent(h->sc, h->ev_u[k], 0));
+                CU(cudaMemcpyAsync(u + 3 * (size_t)done, du + 3 * (size_t)done, (size_t)3 * (upto - done) * 8,
+                                   cudaMemcpyDeviceToHost, h->sc));
+                done = upto;
+            }
+        } else if (u) {
             if (!mech) {
                 const double4* rc = h->cur ? h->ptr.rec1 : h->ptr.rec0;
                 k_fields_to_orig<<<blocks(N, 256), 256, 0, h->s>>>(rc, h->ptr.node_orig, N, nullptr, du);

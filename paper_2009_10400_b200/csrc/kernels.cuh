@@ -800,6 +800,12 @@ __device__ __forceinline__ void gather3_ell(const double* __restrict__ slots, co
 #define TVEGPU_NODE_THREADS 256
 #endif
 constexpr int kNodeThreads = TVEGPU_NODE_THREADS;
+// Node kernels issue the loads of data their predecessor does not write (node record,
+// sources, masks, masses) before the PDL wait, so only the slot gathers follow it:
+// bit 0 K2, bit 1 K4.
+#ifndef TVEGPU_NODE_HOIST
+#define TVEGPU_NODE_HOIST 1
+#endif
 // (an explicit min-blocks of 1 lets ptxas give K4 114 registers: 96 vs 78 us)
 #ifdef TVEGPU_NODE_MINBLOCKS
 #define NODE_BOUNDS __launch_bounds__(kNodeThreads, TVEGPU_NODE_MINBLOCKS)
@@ -816,10 +822,18 @@ __global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, i
     const int i = PAIR ? (t >> 1) : t;
     const bool lead = !PAIR || !(threadIdx.x & 1);
     int4 ia = make_int4(0, 0, 0, 0), ib = ia;
-    double V = 0.0;
+    double V = 0.0, T = 0.0, qr = 0.0;
+    uint8_t m = 0;
+    double4* R = cur ? D.rec1 : D.rec0;
+    constexpr bool HOIST = (TVEGPU_NODE_HOIST & 1) != 0;
     if (i < P.N) {  // predecessor-independent loads first (index row, node volume)
         if (!PAIR && P.ell) ia = __ldg(D.ell + 2 * (size_t)P.ell * i), ib = __ldg(D.ell + 2 * (size_t)P.ell * i + 1);
         V = __ldg(D.vnode + i);
+        if (HOIST && lead) {  // T^n: K4 of the previous step (two launches back) wrote it
+            T = R[i].w;
+            qr = __ldg(D.qr + i);
+            m = __ldg(D.mask + i);
+        }
     }
     pdl_wait();
     const bool active = i < P.N && !D.clock->halted;  // the same for both threads of a pair
@@ -833,17 +847,19 @@ __global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, i
         s += __shfl_down_sync(0xffffffffu, s, 1);
     }
     if (active && lead) {
-        double4* R = cur ? D.rec1 : D.rec0;
         if constexpr (!PAIR) {
             check_gather(P, D, i);
             s = P.ell ? gather1_ell<WIDE>(D.slot_th, D.ell + 2 * (size_t)P.ell * i, P.ell, ia, ib)
                       : gather1(D.slot_th, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1));
         }
-        const double T = R[i].w;
+        if constexpr (!HOIST) {
+            T = R[i].w;
+            qr = __ldg(D.qr + i);
+            m = __ldg(D.mask + i);
+        }
         const double c = P.td ? interp1(P.cT, P.cV, P.c_len, T) : P.c_fixed;
         const double C = P.rho * c * V;
-        double Tn = T + P.dt / C * (-s - P.wbcb * V * (T - P.Ta) + P.Qm * V + __ldg(D.qr + i));
-        const uint8_t m = __ldg(D.mask + i);
+        double Tn = T + P.dt / C * (-s - P.wbcb * V * (T - P.Ta) + P.Qm * V + qr);
         if (m & BC_TFIX) Tn = __ldg(D.bc_tfix + __ldg(D.bc_index + i));
         if (!isfinite(Tn)) atomicMin(D.err_inst, pack_inst(D.clock->step, 0, D.node_orig[i]));
         R[i].w = Tn;
@@ -1222,16 +1238,30 @@ __global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T
 // PAIR: two threads per node for long CSR lists (T4, ~24 contributions): each sums one
 // half in canonical order, the first half's sum + the second's is the node's force (a
 // fixed two-leaf tree: deterministic, partition-invariant).
+// [n0, n1): the local node range of this launch (the whole partition, or one of the
+// slices tvegpu_step_io reads back as they complete).
 template <bool PAIR>
 __global__ void NODE_BOUNDS k_mech_node(const DevParams P, const DevPtrs D, int cur, int closes,
-                                                   double* __restrict__ u_out) {
+                                                   double* __restrict__ u_out, int n0, int n1) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    const int i = PAIR ? (t >> 1) : t;
+    const int i = n0 + (PAIR ? (t >> 1) : t);
     const bool lead = !PAIR || !(threadIdx.x & 1);
     int4 ia = make_int4(0, 0, 0, 0), ib = ia;
-    if (!PAIR && i < P.N && P.ell == 1) ia = __ldg(D.ell + 2 * (size_t)i), ib = __ldg(D.ell + 2 * (size_t)i + 1);
+    if (!PAIR && i < n1 && P.ell == 1) ia = __ldg(D.ell + 2 * (size_t)i), ib = __ldg(D.ell + 2 * (size_t)i + 1);
+    const double4* Rc = cur ? D.rec1 : D.rec0;
+    double4* Rn = cur ? D.rec0 : D.rec1;  // holds u^{n-1}; receives u^{n+1}
+    constexpr bool HOIST = (TVEGPU_NODE_HOIST & 2) != 0;
+    double4 u = make_double4(0.0, 0.0, 0.0, 0.0), up = u;
+    double m = 0.0;
+    uint8_t msk = 0;
+    if (HOIST && i < n1 && lead) {  // u^n, T^{n+1}, u^{n-1}: written two or more launches back
+        u = ldg4(Rc + i);
+        up = ld4(Rn + i);
+        m = __ldg(D.mass + i);
+        msk = __ldg(D.mask + i);
+    }
     pdl_wait();
-    const bool active = i < P.N && !D.clock->halted;  // the same for both threads of a pair
+    const bool active = i < n1 && !D.clock->halted;  // the same for both threads of a pair
     double f0 = 0.0, f1 = 0.0, f2 = 0.0;
     if constexpr (PAIR) {
         if (active) {
@@ -1244,16 +1274,17 @@ __global__ void NODE_BOUNDS k_mech_node(const DevParams P, const DevPtrs D, int 
         f2 += __shfl_down_sync(0xffffffffu, f2, 1);
     }
     if (active && lead) {
-        const double4* Rc = cur ? D.rec1 : D.rec0;
-        double4* Rn = cur ? D.rec0 : D.rec1;  // holds u^{n-1}; receives u^{n+1}
         if constexpr (!PAIR) {
             check_gather(P, D, i);
             if (P.ell == 1) gather3_ell(D.slot_m, ia, ib, f0, f1, f2);
             else gather3(D.slot_m, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1), f0, f1, f2);
         }
-        const double4 u = ldg4(Rc + i);  // read-only in this kernel
-        const double4 up = ld4(Rn + i);  // this thread overwrites it below
-        const double m = __ldg(D.mass + i);
+        if constexpr (!HOIST) {
+            u = ldg4(Rc + i);  // read-only in this kernel
+            up = ld4(Rn + i);  // this thread overwrites it below
+            m = __ldg(D.mass + i);
+            msk = __ldg(D.mask + i);
+        }
         const double Dm = P.gamma * m;
         const double a = Dm * P.inv_2dt, b = m * P.inv_dt2;
         const double iab = 1.0 / (a + b);
@@ -1266,7 +1297,6 @@ __global__ void NODE_BOUNDS k_mech_node(const DevParams P, const DevPtrs D, int 
         double x = (R0 - f0 + 2.0 * b * u.x + (a - b) * up.x) * iab;
         double y = (R1 - f1 + 2.0 * b * u.y + (a - b) * up.y) * iab;
         double z = (R2 - f2 + 2.0 * b * u.z + (a - b) * up.z) * iab;
-        const uint8_t msk = __ldg(D.mask + i);
         if (msk & (BC_FIXED | BC_PX | BC_PY | BC_PZ)) {
             if (msk & BC_FIXED) x = y = z = 0.0;
             if (msk & (BC_PX | BC_PY | BC_PZ)) {
