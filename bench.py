@@ -218,12 +218,12 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
     if args.gpus != world:
         raise SystemExit(f"bench.py --gpus {args.gpus} needs {args.gpus} ranks (torchrun --nproc-per-node "
                          f"{args.gpus}); this process group has {world}")
     if world > torch.cuda.device_count():
         raise SystemExit(f"--gpus {world}: only {torch.cuda.device_count()} CUDA device(s) visible")
+    torch.cuda.set_device(local)
     dist = None
     if world > 1:
         # communicator-init lines (rank count) of the halo communicator and torch's

@@ -111,6 +111,11 @@ struct MechBCs {
     std::vector<PrescribedDisplacement> prescribed;
     std::vector<double> external_force;  // 3 per node or empty
     Vec3 body_force{0, 0, 0};
+    // mechanics.hpp:43-46: optional per-node trajectory; a returned value pins the node at
+    // time t (applied last).  A host callback: the GPU engine evaluates it every step for
+    // motion_nodes (empty = every node) and uploads the pins (tvegpu_set_motion_override).
+    std::function<std::optional<Vec3>(int node, double t)> motion_override;
+    std::vector<int> motion_nodes;  // candidate nodes of motion_override (a GPU-side restriction; empty = all)
 };
 
 // ---------------------------------------------------------------- engine.hpp:16-45
@@ -175,8 +180,22 @@ public:
         o.diagnostics = opt.diagnostics ? 1 : 0;
         const tvegpu_status st = tvegpu_create(&p_, &o, &h_);
         if (st != TVEGPU_OK) rethrow(st, tvegpu_create_error(), -1, -1);
+        if (mech_bcs.motion_override) {
+            motion_ = mech_bcs.motion_override;
+            motion_nodes_ = mech_bcs.motion_nodes;
+            check(tvegpu_set_motion_override(h_, &Engine::motion_trampoline, this, (int32_t)motion_nodes_.size(),
+                                             motion_nodes_.empty() ? nullptr : motion_nodes_.data()));
+        }
     }
     ~Engine() { tvegpu_destroy(h_); }
+
+    // C callback -> MechBCs::motion_override
+    static int32_t motion_trampoline(void* self, int32_t node, double t, double* disp) {
+        const std::optional<Vec3> v = static_cast<Engine*>(self)->motion_(node, t);
+        if (!v) return 0;
+        disp[0] = (*v)[0], disp[1] = (*v)[1], disp[2] = (*v)[2];
+        return 1;
+    }
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;
 
@@ -469,6 +488,8 @@ private:
     double dt_, dur_;
     OutputSpec out_;
     tvegpu_engine* h_ = nullptr;
+    std::function<std::optional<Vec3>(int, double)> motion_;  // MechBCs::motion_override (copied, like the reference)
+    std::vector<int32_t> motion_nodes_;
     tvegpu_problem p_{};
     std::vector<double> nodes_, fibers_, axes_, phi_, tau_, cT_, cV_, kT_, kK_, tfixV_, ext_;
     std::vector<int32_t> elems_, fixed_, tfixN_;
