@@ -163,10 +163,10 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_oracle_rate(problem, budget_s, max_steps, warmup=1):
-    """Element-steps/s of the fp64 oracle (OpenMP, all host threads) on the same problem."""
+def cpu_oracle_rate(problem, budget_s, max_steps, warmup=1, threads=None):
+    """Element-steps/s of the fp64 oracle (OpenMP, all host threads unless `threads`) on the same problem."""
     from oracle import oracle as O
-    threads = os.cpu_count() or 1
+    threads = threads or os.cpu_count() or 1
     o = O.OracleEngine(problem, workers=threads)
     o.step(warmup)
     t0 = time.perf_counter()
@@ -178,6 +178,15 @@ def cpu_oracle_rate(problem, budget_s, max_steps, warmup=1):
             break
     dt = time.perf_counter() - t0
     return problem.num_elements * n / dt, n, dt, threads
+
+
+def single_thread_rate(problem, budget_s):
+    """BASELINE.md §3 asks for the CPU baseline at all host threads and also at 1: the
+    same oracle on one thread, a bounded sample (informational beside the main figure)."""
+    if budget_s <= 0:
+        return None
+    rate, n, dt, _ = cpu_oracle_rate(problem, budget_s=budget_s, max_steps=1000, warmup=1, threads=1)
+    return {"value": rate, "unit": METRIC, "cores": 1, "steps": n, "seconds": dt}
 
 
 def cpu_model():
@@ -205,7 +214,8 @@ def run_reference(args):
             "steps": n, "warmup": warm, "ms_per_step": 1e3 * dt / n, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": bench_config(name, label, p, world, args.graph_steps),
-            "cpu_baseline": {"value": rate, "unit": METRIC, "cores": threads, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": rate, "unit": METRIC, "cores": threads, "kind": "port", "sample": sample,
+                             "single_thread": single_thread_rate(p, args.single_budget)},
             "e2e": {"value": rate, "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -372,7 +382,8 @@ def run_ours(args):
         rate, n, dt, threads = cpu_oracle_rate(p, budget_s=args.cpu_budget, max_steps=1000)
         line["cpu_baseline"] = {"value": rate, "unit": METRIC, "cores": threads, "kind": "port",
                                 "sample": f"{n} steps of the full cfg4 mesh in {dt:.1f} s (fp64 oracle, OpenMP "
-                                          f"{threads} threads, {cpu_model()})"}
+                                          f"{threads} threads, {cpu_model()})",
+                                "single_thread": single_thread_rate(p, args.single_budget)}
     if rank == 0 and world == 1 and not args.no_extras:
         # the real-time target: cfg3 liver-shaped T4 (~100k el), ms per step (L2-resident regime)
         p3 = configs.cfg3(steps=100000)
@@ -422,6 +433,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=90.0)
+    ap.add_argument("--single-budget", type=float, default=8.0, help="seconds of the 1-thread CPU sample (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
     args = ap.parse_args()

@@ -96,15 +96,15 @@ typedef struct tvegpu_problem {
     /* ---- HyperelasticParams (materials.hpp:15-19) ---- */
     double mu, kappa, eta_a;
     /* ---- PronySeries::from_terms (materials.hpp:27-36) ---- */
-    int32_t prony_count;
+    int32_t prony_count;            /* any number of terms (PronySeries, materials.hpp:27-35) */
     const double* prony_phi;        /* prony_count */
     const double* prony_tau;        /* prony_count */
     /* ---- ThermalProps (materials.hpp:67-75) ---- */
     double density;
-    int32_t c_table_len;            /* ScalarTable specific_heat (materials.hpp:39-49) */
+    int32_t c_table_len;            /* ScalarTable specific_heat (materials.hpp:39-49), >= 1 entries, any length */
     const double* c_table_T;
     const double* c_table_value;
-    int32_t k_table_len;            /* ConductivityTable (materials.hpp:53-65) */
+    int32_t k_table_len;            /* ConductivityTable (materials.hpp:53-65), >= 1 entries, any length */
     const double* k_table_T;
     const double* k_table_tensor;   /* 9 per entry, row-major (symmetric) */
     double perfusion_rate;          /* w_b */

@@ -919,13 +919,39 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     m.inv_dt2 = 1.0 / (p.dt * p.dt);
     m.c_len = p.c_table_len;
     m.k_len = p.k_table_len;
-    for (int i = 0; i < p.c_table_len; ++i) {
+    for (int i = 0; i < std::min(p.c_table_len, kMaxTable); ++i) {
         m.cT[i] = p.c_table_T[i];
         m.cV[i] = p.c_table_value[i];
     }
-    for (int i = 0; i < p.k_table_len; ++i) {
+    for (int i = 0; i < std::min(p.k_table_len, kMaxTable); ++i) {
         m.kT[i] = p.k_table_T[i];
         for (int q = 0; q < 9; ++q) m.kK[i][q] = p.k_table_tensor[9 * i + q];
+    }
+    // every table and Prony coefficient in one device array (read there when longer than
+    // the launch-parameter copies): cT | cV | kT | kK (9 per entry) | pa | pb
+    std::vector<double> tabs;
+    {
+        auto put = [&](const double* v, size_t n) {
+            const int off = (int)tabs.size();
+            tabs.insert(tabs.end(), v, v + n);
+            return off;
+        };
+        m.tab_cT = put(p.c_table_T, p.c_table_len);
+        m.tab_cV = put(p.c_table_value, p.c_table_len);
+        m.tab_kT = put(p.k_table_T, p.k_table_len);
+        m.tab_kK = put(p.k_table_tensor, (size_t)9 * p.k_table_len);
+        std::vector<double> pa(P), pb(P);
+        for (int i = 0; i < P; ++i) {
+            const double phi = p.prony_phi[i], tau = p.prony_tau[i];
+            pa[i] = p.dt * phi / (p.dt + tau);
+            pb[i] = tau / (p.dt + tau);
+            if (i < kMaxProny) {
+                m.pa[i] = pa[i];
+                m.pb[i] = pb[i];
+            }
+        }
+        m.tab_pa = put(pa.data(), P);
+        m.tab_pb = put(pb.data(), P);
     }
     // fixed-property temperature 37 degC (engine.hpp:141)
     {
@@ -937,11 +963,11 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
             const double w = (T - Ts[j]) / (Ts[j + 1] - Ts[j]);
             return Vs[j] + (Vs[j + 1] - Vs[j]) * w;
         };
-        m.c_fixed = interp(m.cT, m.cV, m.c_len, 37.0);
+        m.c_fixed = interp(p.c_table_T, p.c_table_value, m.c_len, 37.0);
+        std::vector<double> col(m.k_len);
         for (int q = 0; q < 9; ++q) {
-            double col[kMaxTable];
-            for (int i = 0; i < m.k_len; ++i) col[i] = m.kK[i][q];
-            m.k_fixed[q] = interp(m.kT, col, m.k_len, 37.0);
+            for (int i = 0; i < m.k_len; ++i) col[i] = p.k_table_tensor[9 * i + q];
+            m.k_fixed[q] = interp(p.k_table_T, col.data(), m.k_len, 37.0);
         }
     }
     const bool expansion = p.mode == TVEGPU_COUPLED && p.expansion_enabled && p.has_expansion;
@@ -957,11 +983,6 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     }
     m.axes_per_elem = p.expansion_axes ? 1 : 0;
     m.fiber_mode = p.eta_a > 0 ? (p.fiber_dirs ? 2 : 1) : 0;
-    for (int i = 0; i < P; ++i) {
-        const double phi = p.prony_phi[i], tau = p.prony_tau[i];
-        m.pa[i] = p.dt * phi / (p.dt + tau);
-        m.pb[i] = tau / (p.dt + tau);
-    }
     m.diag = o.diagnostics ? 1 : 0;
     // ---- streams
     CU(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
@@ -1053,6 +1074,7 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     h->ptr.elem_orig = dupload(own, pl.elem_orig, s);
     const size_t es = (size_t)m.es;
     h->ptr.theta = dalloc<double>(own, (size_t)6 * P * es);
+    h->ptr.tabs = dupload(own, tabs, h->s);
     CU(cudaMemsetAsync(h->ptr.theta, 0, std::max<size_t>(1, (size_t)6 * P * es) * 8, s));
     if (p.fiber_dirs && m.fiber_mode == 2) {
         fvec<double> f((size_t)3 * es);

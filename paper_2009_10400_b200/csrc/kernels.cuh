@@ -32,8 +32,8 @@
 
 namespace tvegpu {
 
-constexpr int kMaxTable = 16;
-constexpr int kMaxProny = 4;
+constexpr int kMaxTable = 16;  // table entries held in the launch parameters (longer tables: D.tabs)
+constexpr int kMaxProny = 4;   // Prony terms with coefficients in the launch parameters and staged history rows
 #ifndef TVEGPU_CHUNK
 #define TVEGPU_CHUNK 128
 #endif
@@ -95,6 +95,9 @@ struct DevParams {
     double alpha_i, alpha_m, alpha_n, Tref;
     double axis_m[3], axis_n[3];
     double pa[kMaxProny], pb[kMaxProny];
+    // offsets into DevPtrs::tabs (every table and all Prony coefficients, any length); the
+    // kernels read them from there only when c_len / k_len > kMaxTable or P > kMaxProny
+    int tab_cT, tab_cV, tab_kT, tab_kK, tab_pa, tab_pb;
 };
 
 struct DevPtrs {
@@ -138,6 +141,7 @@ struct DevPtrs {
     double* diag_f;            // [N][3] or null
     const int32_t* motion_row;  // [N] row of motion_val for override candidates, else -1 (motion only)
     const double4* motion_val;  // [rows] (x, y, z, pinned) of this step's motion_override(node, t + dt)
+    const double* tabs;         // c(T), k(T) tables and Prony coefficients (DevParams::tab_*)
 };
 
 enum : uint8_t { BC_FIXED = 1, BC_PX = 2, BC_PY = 4, BC_PZ = 8, BC_TFIX = 16 };
@@ -152,23 +156,33 @@ __device__ __forceinline__ double interp1(const double* Ts, const double* Vs, in
     return Vs[j] + (Vs[j + 1] - Vs[j]) * w;
 }
 
-__device__ __forceinline__ void conductivity_at(const DevParams& P, double T, double D[9]) {
-    const int n = P.k_len;
-    if (n == 1 || T <= P.kT[0]) {
+// k(T) at the element-mean temperature from tables (T_j) and (K_j, 9 each)
+__device__ __forceinline__ void conductivity_interp(const double* kT, const double* kK, int n, double T, double D[9]) {
+    if (n == 1 || T <= kT[0]) {
 #pragma unroll
-        for (int q = 0; q < 9; ++q) D[q] = P.kK[0][q];
+        for (int q = 0; q < 9; ++q) D[q] = kK[q];
         return;
     }
-    if (T >= P.kT[n - 1]) {
+    if (T >= kT[n - 1]) {
 #pragma unroll
-        for (int q = 0; q < 9; ++q) D[q] = P.kK[n - 1][q];
+        for (int q = 0; q < 9; ++q) D[q] = kK[9 * (n - 1) + q];
         return;
     }
     int j = 0;
-    while (j + 2 < n && T >= P.kT[j + 1]) ++j;
-    const double w = (T - P.kT[j]) / (P.kT[j + 1] - P.kT[j]);
+    while (j + 2 < n && T >= kT[j + 1]) ++j;
+    const double w = (T - kT[j]) / (kT[j + 1] - kT[j]);
 #pragma unroll
-    for (int q = 0; q < 9; ++q) D[q] = P.kK[j][q] + (P.kK[j + 1][q] - P.kK[j][q]) * w;
+    for (int q = 0; q < 9; ++q) D[q] = kK[9 * j + q] + (kK[9 * (j + 1) + q] - kK[9 * j + q]) * w;
+}
+// ConductivityTable::at / ScalarTable::at (materials.hpp:39-65): short tables from the
+// launch parameters, any longer one from device memory (same arithmetic)
+__device__ __forceinline__ void conductivity_at(const DevParams& P, const DevPtrs& D, double T, double Dk[9]) {
+    if (P.k_len <= kMaxTable) conductivity_interp(P.kT, &P.kK[0][0], P.k_len, T, Dk);
+    else conductivity_interp(D.tabs + P.tab_kT, D.tabs + P.tab_kK, P.k_len, T, Dk);
+}
+__device__ __forceinline__ double heat_capacity_at(const DevParams& P, const DevPtrs& D, double T) {
+    return P.c_len <= kMaxTable ? interp1(P.cT, P.cV, P.c_len, T)
+                                : interp1(D.tabs + P.tab_cT, D.tabs + P.tab_cV, P.c_len, T);
 }
 
 // adjugate (transpose of cofactors) of a row-major 3x3, returns det
@@ -598,7 +612,7 @@ __device__ __forceinline__ void k1_body(const DevParams& P, const DevPtrs& D, co
             F[i * 3 + j] = (i == j ? 1.0 : 0.0) + H[i * 3 + 0] * A[j * 3 + 0] + H[i * 3 + 1] * A[j * 3 + 1] +
                            H[i * 3 + 2] * A[j * 3 + 2];
     double Dk[9];
-    if (P.td) conductivity_at(P, Ts / NN, Dk);
+    if (P.td) conductivity_at(P, D, Ts / NN, Dk);
     else {
 #pragma unroll
         for (int q = 0; q < 9; ++q) Dk[q] = P.k_fixed[q];
@@ -857,7 +871,7 @@ __global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, i
             qr = __ldg(D.qr + i);
             m = __ldg(D.mask + i);
         }
-        const double c = P.td ? interp1(P.cT, P.cV, P.c_len, T) : P.c_fixed;
+        const double c = P.td ? heat_capacity_at(P, D, T) : P.c_fixed;
         const double C = P.rho * c * V;
         double Tn = T + P.dt / C * (-s - P.wbcb * V * (T - P.Ta) + P.Qm * V + qr);
         if (m & BC_TFIX) Tn = __ldg(D.bc_tfix + __ldg(D.bc_index + i));
@@ -1054,7 +1068,7 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
 #pragma unroll
     for (int q = 0; q < 6; ++q) St[q] = S[q];
 #pragma unroll 1
-    for (int p = 0; p < P.P; ++p) {
+    for (int p = 0; p < (P.P < kMaxProny ? P.P : kMaxProny); ++p) {  // staged history rows
         double* th = D.theta + (size_t)p * 6 * es + e;
         double t[6];
 #pragma unroll
@@ -1064,6 +1078,17 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
             t[q] = P.pa[p] * S[q] + P.pb[p] * t[q];
             th[q * es] = t[q];
             St[q] -= t[q];
+        }
+    }
+#pragma unroll 1
+    for (int p = kMaxProny; p < P.P; ++p) {  // further terms: history and coefficients from device memory
+        double* th = D.theta + (size_t)p * 6 * es + e;
+        const double pa = D.tabs[P.tab_pa + p], pb = D.tabs[P.tab_pb + p];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            const double t = pa * S[q] + pb * th[q * es];
+            th[q * es] = t;
+            St[q] -= t;
         }
     }
     // ---- P = V F S~ = V (S~ + Hd S~) ;  Q = P A  (f_a = Q xi_a)
@@ -1225,11 +1250,11 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
     }
 }
 
-// K3 rows: geometry (T4 10, H8 22 with the hourglass vectors), Prony history, and the
-// per-element fibres / expansion axes when the material has them
+// K3 rows: geometry (T4 10, H8 22 with the hourglass vectors), Prony history (the first
+// kMaxProny terms; any further term is read in place), and the per-element fibres / expansion axes when the material has them
 template <int NN, int EXP>
 __host__ __device__ __forceinline__ RowPlan k3_rows(const DevParams& P) {
-    return RowPlan{k3_xstage<NN>() ? 0 : (NN == 8 ? kGeoRows : 10), 6 * P.P, P.fiber_mode == 2 ? 3 : 0,
+    return RowPlan{k3_xstage<NN>() ? 0 : (NN == 8 ? kGeoRows : 10), 6 * (P.P < kMaxProny ? P.P : kMaxProny), P.fiber_mode == 2 ? 3 : 0,
                    (EXP == 2 && P.axes_per_elem) ? 6 : 0};
 }
 

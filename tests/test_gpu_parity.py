@@ -83,6 +83,28 @@ def test_anisotropic_expansion(kind, exp_kind, per_element_axes):
 
 
 @pytest.mark.parametrize("kind", [T4, H8])
+@pytest.mark.parametrize("exp_kind", [EXP_ISOTROPIC, EXP_ORTHOTROPIC])
+def test_long_tables_and_prony_series(kind, exp_kind):
+    """PronySeries / ScalarTable / ConductivityTable have no length limit (materials.hpp:27-65):
+    six Prony terms (two beyond the staged history rows) and 20- / 24-entry c(T), k(T)
+    tables (beyond the launch-parameter copies) whose entries the run's 37.0-37.12 degC
+    range crosses several of."""
+    p = configs.small_problem(kind=kind, n=4, steps=60)
+    p.prony_phi = [0.2, 0.15, 0.1, 0.08, 0.06, 0.05]
+    p.prony_tau = [0.58, 0.058, 0.0058, 5.8, 0.0012, 0.021]
+    Tc = np.linspace(36.99, 37.13, 20)
+    p.c_table = [(float(t), 3600.0 + 700.0 * math.sin(9.0 * i)) for i, t in enumerate(Tc)]
+    Tk = np.linspace(36.995, 37.125, 24)
+    p.k_table = [(float(t), np.array([[0.53 + 0.1 * math.cos(i), 0.01 * i, 0.0], [0.01 * i, 0.6, 0.02],
+                                      [0.0, 0.02, 0.5 + 0.004 * i]])) for i, t in enumerate(Tk)]
+    if exp_kind == EXP_ORTHOTROPIC:
+        p.expansion = dict(kind=EXP_ORTHOTROPIC, alpha_i=1e-4, alpha_m=3e-4, alpha_n=-5e-5,
+                           reference_temperature=37.0)
+        p.axis_m, p.axis_n = (0.0, 0.6, 0.8), (1.0, 0.0, 0.0)
+    compare(p, 60)
+
+
+@pytest.mark.parametrize("kind", [T4, H8])
 @pytest.mark.parametrize("mode", [THERMAL_ONLY, MECHANICAL_ONLY])
 def test_modes(kind, mode):
     p = configs.small_problem(kind=kind, n=4, steps=50)
