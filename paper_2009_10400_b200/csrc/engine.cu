@@ -485,7 +485,13 @@ void launch_step_kernel(tvegpu_engine* h, void (*kern)(KArgs...), int grid, int 
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = h->pdl ? 1 : 0;
-    CU(cudaLaunchKernelEx(&cfg, kern, args...));
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args...);
+    if (e != cudaSuccess) {
+        char buf[160];
+        std::snprintf(buf, sizeof buf, " (grid %d, block %d, dynamic shared memory %zu B, pdl %d)", grid, block, smem,
+                      (int)h->pdl);
+        throw Error(TVEGPU_E_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e) + buf);
+    }
 }
 
 using NodeKernel = void (*)(const DevParams, const DevPtrs, int, int, double*);
@@ -534,7 +540,32 @@ void launch_mech_node(tvegpu_engine* h, double* u_out, int n0 = 0, int n1 = -1, 
 
 void set_smem_limits(tvegpu_engine* h) {
     const int sm = (int)std::max(k1_smem(h), k3_smem(h));
-    if (sm <= 48 * 1024) return;
+    // TVEGPU_CARVEOUT=<percent>: one shared-memory carve-out for all four step kernels
+    // (an SM runs blocks of two kernels side by side only under the same L1/shared split)
+    if (const char* cv = std::getenv("TVEGPU_CARVEOUT")) {
+        const int pct = std::atoi(cv);
+        auto co = [&](const void* f) { CU(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct)); };
+        co((const void*)k_thermal_element<4>);
+        co((const void*)k_thermal_element<8>);
+        co((const void*)k_mech_element<4, 0>);
+        co((const void*)k_mech_element<4, 1>);
+        co((const void*)k_mech_element<4, 2>);
+        co((const void*)k_mech_element<8, 0>);
+        co((const void*)k_mech_element<8, 1>);
+        co((const void*)k_mech_element<8, 2>);
+        co((const void*)k_thermal_node<0>);
+        co((const void*)k_thermal_node<1>);
+        co((const void*)k_thermal_node<2>);
+        co((const void*)k_mech_node<false>);
+        co((const void*)k_mech_node<true>);
+    }
+    // the limit is a per-function attribute shared by every engine of the process: only
+    // ever raise it (a later, smaller engine must not undercut an earlier one's launches)
+    static std::mutex mu;
+    static int set_to = 48 * 1024;
+    std::lock_guard<std::mutex> lock(mu);
+    if (sm <= set_to) return;
+    set_to = sm;
     auto attr = [&](const void* f) { CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); };
     attr((const void*)k_thermal_element<4>);
     attr((const void*)k_thermal_element<8>);
