@@ -103,6 +103,59 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+KERNEL_REGEX = {"thermal_element": "k_thermal_element", "thermal_node": "k_thermal_node",
+                "mech_element": "k_mech_element", "mech_node": "k_mech_node"}
+_UNITS = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "kib": 1024, "mib": 1024 ** 2, "gib": 1024 ** 3}
+
+
+def ncu_traffic_live(args, kernel, timeout_s=300):
+    """DRAM bytes of ONE launch of `kernel`, measured in this bench run: ncu (dram__bytes_read.sum
+    + dram__bytes_write.sum, cache flushed before the launch as in a --set full capture) on a
+    short probe of the same workload (`bench.py --traffic-probe`), after the probe's own warm-up
+    steps.  A byte count, not a time: the bench's timings never run under the profiler.
+    Returns (bytes, note) or (None, why)."""
+    import shutil
+    ncu = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu" if os.path.exists("/usr/local/cuda/bin/ncu") else None)
+    if ncu is None:
+        return None, "ncu not found"
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control", "none",
+           "-k", f"regex:{KERNEL_REGEX[kernel]}", "-s", "6", "-c", "1", "--csv",
+           sys.executable, os.path.join(ROOT, "bench.py"), "--traffic-probe"]
+    if args.workload:
+        cmd += ["--workload", args.workload]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s, cwd=ROOT)
+    except Exception as ex:  # noqa: BLE001
+        return None, f"ncu probe failed: {type(ex).__name__}"
+    import csv
+    import io
+    tot, seen = 0.0, set()
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith('"')]
+    try:
+        rows = list(csv.reader(io.StringIO("\n".join(lines))))
+        h = rows[0]
+        im, iu, iv = h.index("Metric Name"), h.index("Metric Unit"), h.index("Metric Value")
+        for row in rows[1:]:
+            if row[im] in ("dram__bytes_read.sum", "dram__bytes_write.sum") and row[im] not in seen:
+                seen.add(row[im])
+                tot += float(row[iv].replace(",", "")) * _UNITS.get(row[iu].strip().lower(), float("nan"))
+    except Exception:  # noqa: BLE001
+        return None, "ncu probe output not parsed (rc %d): %s" % (r.returncode, (r.stderr or r.stdout)[-200:])
+    if len(seen) != 2 or not math.isfinite(tot):
+        return None, "ncu probe: metrics missing (rc %d)" % r.returncode
+    return tot, "measured in this run: ncu dram__bytes_read.sum + dram__bytes_write.sum of one launch"
+
+
+def traffic_probe(args):
+    """--traffic-probe: the bench workload, a few direct steps (the ncu pass in ncu_traffic_live)."""
+    import paper_2009_10400_b200 as tg
+    _, _, make = workload_for(args, 1)
+    eng = tg.Engine(make(64), steps_per_graph=1)
+    eng.step(8)
+    eng.close()
+    return 0
+
+
 def ncu_traffic(workload_key, kernel):
     """dram bytes per launch from a committed `ncu --set full` capture (profiles/ncu_dram_bytes.json)."""
     try:
@@ -302,11 +355,16 @@ def run_ours(args):
     step_bytes = sum(local_bytes.values())
     step_gbs = step_bytes * args.steps / (ms / 1e3) / 1e9
     wkey = wname if world == 1 else f"{wname}_n{world}"
+    traffic, tsrc = (None, "skipped (--no-ncu-traffic)")
+    if rank == 0 and world == 1 and not args.no_ncu_traffic:
+        traffic, tsrc = ncu_traffic_live(args, dom)
+    if traffic is None:  # fall back to the committed capture, saying so
+        traffic = ncu_traffic(wkey, dom)
+        tsrc = (f"{tsrc}; profiles/ncu_dram_bytes.json (dram__bytes_read.sum + dram__bytes_write.sum of the "
+                f"committed ncu --set full capture of this workload)")
     roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "traffic": ncu_traffic(wkey, dom), "kernel": dom, "kernel_ms": t_dom,
-                "algorithmic_bytes_per_launch": b_dom, "peak_source": peak_src,
-                "traffic_source": "profiles/ncu_dram_bytes.json (dram__bytes_read.sum + dram__bytes_write.sum of "
-                                  "the committed ncu --set full capture of this workload)"}
+                "traffic": traffic, "kernel": dom, "kernel_ms": t_dom,
+                "algorithmic_bytes_per_launch": b_dom, "peak_source": peak_src, "traffic_source": tsrc}
     halo = None
     if world > 1:  # per rank: halo volume and the transfer time on the comm stream
         nb, sb, rb = eng.halo_info()
@@ -436,7 +494,11 @@ def main():
     ap.add_argument("--single-budget", type=float, default=8.0, help="seconds of the 1-thread CPU sample (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-ncu-traffic", action="store_true", help="roofline.traffic from the committed capture")
+    ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.traffic_probe:
+        return traffic_probe(args)
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     return run_reference(args) if args.impl == "reference" else run_ours(args)

@@ -9,7 +9,7 @@ timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_all.log 2>
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/summary.txt
 timeout 900 python bench.py > gpurun_out/bench_${TAG}.log 2>&1; echo "bench rc=$?" >> gpurun_out/summary.txt
 timeout 900 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/bench_ref_${TAG}.log 2>&1; echo "bench ref rc=$?" >> gpurun_out/summary.txt
-CMD="python bench.py --steps 64 --warmup 3 --soak 0 --no-cpu-baseline --no-extras --e2e-steps 3"
+CMD="python bench.py --steps 64 --warmup 3 --soak 0 --no-cpu-baseline --no-extras --e2e-steps 3 --no-ncu-traffic --single-budget 0"
 $CMD > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -s 200 -c 80 --csv --log-file gpurun_out/launches_${TAG}.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 echo "ncu launches rc=$?" >> gpurun_out/summary.txt
