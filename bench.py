@@ -302,6 +302,18 @@ def run_ours(args):
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     eng = tg.Engine(p, device=local, nranks=world, rank=rank, nccl_id=nccl_id, steps_per_graph=args.graph_steps)
+    halo_transport = None
+    if world > 1:
+        # peer-memory halo: all-gather the partitions' descriptors (CUDA IPC handles of the
+        # receive areas + flag inboxes), attach; the boundary element kernels then store the
+        # interface contributions straight into the neighbours' memory over NVLink.
+        # TVEGPU_HALO=nccl keeps the pack + ncclSend/ncclRecv path.
+        halo_transport = "nccl"
+        if os.environ.get("TVEGPU_HALO", "peer") != "nccl":
+            blobs = [None] * world
+            dist.all_gather_object(blobs, eng.peer_export())
+            eng.peer_attach(blobs)
+            halo_transport = "peer" if eng.halo_peer else "nccl"
     stream = torch.cuda.ExternalStream(eng.stream, device=local)
     props = torch.cuda.get_device_properties(local)
     sampler = ClockSampler(getattr(props, "uuid", None) and f"GPU-{props.uuid}" or local)
@@ -435,6 +447,7 @@ def run_ours(args):
             "gpu_launches": eng.kernels_per_step() * args.steps, "clocks": clocks}
     if halo is not None:
         line["halo"] = halo
+        line["halo_transport"] = halo_transport
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, n, dt, threads = cpu_oracle_rate(p, budget_s=args.cpu_budget, max_steps=1000)

@@ -163,6 +163,11 @@ struct DeviceOptions {
     int device = -1;
     int steps_per_graph = 64;
     bool diagnostics = false;
+    // one RCB partition per process and GPU (nranks > 1): NCCL id from tvegpu_nccl_unique_id
+    // on one rank, shared by the caller; then peer_export / all-gather / peer_attach
+    int nranks = 1, rank = 0;
+    std::vector<unsigned char> nccl_unique_id;  // 128 bytes when nranks > 1
+    int halo_transport = TVEGPU_HALO_PEER;
 };
 
 // tve::Engine (engine.hpp:83-143) on a B200.
@@ -178,6 +183,10 @@ public:
         o.device = opt.device;
         o.steps_per_graph = opt.steps_per_graph;
         o.diagnostics = opt.diagnostics ? 1 : 0;
+        o.nranks = opt.nranks;
+        o.rank = opt.rank;
+        o.nccl_unique_id = opt.nccl_unique_id.empty() ? nullptr : opt.nccl_unique_id.data();
+        o.halo_transport = opt.halo_transport;
         const tvegpu_status st = tvegpu_create(&p_, &o, &h_);
         if (st != TVEGPU_OK) rethrow(st, tvegpu_create_error(), -1, -1);
         if (mech_bcs.motion_override) {
@@ -198,6 +207,25 @@ public:
     }
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;
+
+    // Peer-memory halo across processes (tvegpu.h tvegpu_peer_export / tvegpu_peer_attach):
+    // every rank exports, the caller all-gathers the descriptors, every rank attaches.
+    std::vector<unsigned char> peer_export() {
+        size_t n = 0;
+        check(tvegpu_peer_export(h_, nullptr, 0, &n));
+        std::vector<unsigned char> b(n);
+        check(tvegpu_peer_export(h_, b.data(), b.size(), &n));
+        return b;
+    }
+    void peer_attach(const std::vector<std::vector<unsigned char>>& by_rank) {
+        std::vector<const void*> p;
+        std::vector<size_t> n;
+        for (const auto& b : by_rank) {
+            p.push_back(b.data());
+            n.push_back(b.size());
+        }
+        check(tvegpu_peer_attach(h_, p.data(), n.data(), (int32_t)p.size()));
+    }
 
     // engine.hpp:89-90
     void step() { steps(1); }

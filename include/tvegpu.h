@@ -160,7 +160,21 @@ typedef struct tvegpu_options {
     int32_t reorder;                /* 1 (default) = Morton elements + first-touch nodes; 0 = identity */
     int32_t diagnostics;            /* 1 = keep F, S_tilde, assembled forces (engine.hpp:101-105) */
     int32_t steps_per_graph;        /* CUDA-graph chunk length; 0 = default (64) */
+    int32_t halo_transport;         /* partitioned engines and groups: TVEGPU_HALO_* (default PEER) */
 } tvegpu_options;
+
+/* Halo exchange of partitioned steps (interface-node heat fluxes and forces).
+ *   TVEGPU_HALO_PEER  the boundary elements' kernel stores every interface contribution
+ *                     straight into the neighbouring partitions' receive areas (NVLink peer
+ *                     memory of the other GPUs; in a group, the other partitions' buffers) and
+ *                     raises a per-phase flag there; the neighbours' node kernels wait for it
+ *                     on the device.  No pack kernel and no NCCL call on the step path.
+ *                     Across processes it needs tvegpu_peer_export / tvegpu_peer_attach once
+ *                     after tvegpu_create (until then the NCCL transport is used).
+ *   TVEGPU_HALO_NCCL  pack kernel + grouped ncclSend/ncclRecv on a comm stream (a group:
+ *                     device copies of the packed segments instead).
+ * Both deliver the same values to the same receive slots: results are bit-identical. */
+enum { TVEGPU_HALO_PEER = 0, TVEGPU_HALO_NCCL = 1 };
 
 typedef struct tvegpu_engine tvegpu_engine;
 
@@ -362,13 +376,28 @@ void tvegpu_plan_destroy(tvegpu_plan* plan);
 /* ncclGetUniqueId for the multi-GPU halo communicator (128 bytes). */
 tvegpu_status tvegpu_nccl_unique_id(void* out128);
 
+/* Peer-memory halo across processes (one partition per process and GPU, one node).
+ * Every rank exports a descriptor (CUDA IPC handles of its receive areas and flag inbox,
+ * its neighbour list; blob == NULL queries the size into *len), the ranks all-gather the
+ * descriptors (any host channel, e.g. torch.distributed), and every rank attaches with
+ * the nranks descriptors indexed by rank.  Only neighbours' buffers are mapped.  After
+ * the attach, tvegpu_step runs the TVEGPU_HALO_PEER path (options.halo_transport). */
+tvegpu_status tvegpu_peer_export(tvegpu_engine* h, void* blob, size_t cap, size_t* len);
+tvegpu_status tvegpu_peer_attach(tvegpu_engine* h, const void* const* blobs, const size_t* lens, int32_t nranks);
+/* 1 if the engine steps with the peer-memory halo (attached, or a group part), else 0. */
+int32_t tvegpu_halo_peer(const tvegpu_engine* h);
+
 /* ---------------------------------------------------------------------------
  * Partition group: nparts RCB partitions of one problem stepped together on ONE
- * device by the multi-GPU step code (boundary-first elements, halo pack, exchange
- * on a comm stream ordered by events, interior elements, receive-area gathers,
- * CUDA-graph replay, agreement on the first failure, device state gather for
- * checkpoints); the transport is a device copy of each neighbour's packed segment
- * instead of ncclSend/ncclRecv.  Results are bit-identical to a single partition.
+ * device by the multi-GPU step code (boundary-first elements, halo delivery,
+ * interior elements, receive-area gathers, CUDA-graph replay, agreement on the first
+ * failure, device state gather for checkpoints).  options.halo_transport selects the
+ * halo path exactly as for one partition per GPU: TVEGPU_HALO_PEER (default) runs the
+ * peer-memory kernels (the parts' buffers stand in for the other GPUs' memory; node
+ * kernels are also ordered after their neighbours' send kernels by events), and
+ * TVEGPU_HALO_NCCL the pack + exchange path with device copies of each neighbour's
+ * packed segment instead of ncclSend/ncclRecv.  Results are bit-identical to a single
+ * partition either way.
  * The calls mirror the engine's (tvegpu_step, tvegpu_set_state, ...).  After a
  * failure every partition reports the same (step, node); the state is then invalid
  * (the other partitions ran on) until set_state / load_checkpoint — the same rule as
@@ -400,7 +429,8 @@ void* tvegpu_stream(tvegpu_engine* h);
 /* Halo exchange volume of one partition (nranks > 1): neighbours, and bytes sent /
  * received per step (every contribution of a shared node, both coupled phases). */
 tvegpu_status tvegpu_halo_info(const tvegpu_engine* h, int32_t* neighbors, int64_t* send_bytes, int64_t* recv_bytes);
-/* Kernel launches per step (K1..K5, plus halo packs when nranks > 1). */
+/* Kernel launches per step (per coupled phase: element + node kernel; partitioned:
+ * boundary + interior element launches, plus the halo pack with the NCCL transport). */
 int32_t tvegpu_kernels_per_step(const tvegpu_engine* h);
 /* Enqueue nsteps on the stream without waiting or reading back the finite
  * check; tvegpu_sync() waits and applies it.  tvegpu_step == enqueue + sync. */

@@ -271,6 +271,10 @@ struct tvegpu_engine {
     Stepper solo;                           // this engine as a one-part step set (graph cache)
     bool pdl = false;     // programmatic dependent launch of the step kernels (single partition)
     bool pair = false;    // node kernels with two threads per node (long CSR gather lists: T4)
+    // peer-memory halo (kernels.cuh peer_send / peer_signal / peer_wait)
+    int halo_transport = TVEGPU_HALO_PEER;  // tvegpu_options.halo_transport
+    bool peer = false;                      // attached: the boundary element kernels deliver the halo
+    std::vector<void*> ipc_open;            // neighbours' allocations mapped by cudaIpcOpenMemHandle
     // errors
     std::string err;
     long long err_step = -1;
@@ -453,6 +457,96 @@ struct LoopbackTransport final : Transport {
     }
 };
 
+// ---------------------------------------------------------------- peer-memory halo setup
+// What a partition publishes to its neighbours: where its receive areas and inbox are
+// (pointers valid in the attaching process) and its receive segments per neighbour.
+struct PeerDesc {
+    int rank = -1;
+    double* th = nullptr;                    // thermal receive area
+    double* m = nullptr;                     // mechanical receive area (kMW doubles per entry)
+    unsigned long long* inbox = nullptr;     // per neighbour (its order) a flag word, then an ack word
+    std::vector<int32_t> nbr, recv_off;      // its neighbour ranks; receive segment offsets (nbr + 1)
+};
+
+PeerDesc peer_desc(const tvegpu_engine* h) {
+    PeerDesc d;
+    d.rank = h->plan.rank;
+    d.th = recv_area(const_cast<tvegpu_engine*>(h), false);
+    d.m = recv_area(const_cast<tvegpu_engine*>(h), true);
+    d.inbox = h->ptr.inbox;
+    d.nbr = h->plan.neighbors;
+    d.recv_off = h->plan.recv_off;
+    return d;
+}
+
+// Builds this partition's destination table from its neighbours' descriptors: each
+// send-list entry k of neighbour j (a boundary slot, canonical order) goes to index
+// recv_off'[j'] + (k - send_off[j]) of that neighbour's receive area, j' = this
+// partition's position in the neighbour's list — exactly where the NCCL transport's
+// ncclRecv would have put it, so the gathers (and results) are unchanged.
+void peer_attach(tvegpu_engine* h, const std::vector<PeerDesc>& by_rank) {
+    const RankPlan& pl = h->plan;
+    const int np = (int)pl.neighbors.size();
+    if (np > 63) throw Error(TVEGPU_E_ARG, "peer-memory halo: more than 63 neighbouring partitions");
+    const int nb = pl.Eb * pl.nn;
+    std::vector<double*> pth(np), pm(np);
+    std::vector<unsigned long long*> pf(np), pa(np);
+    std::vector<int32_t> start(np), off((size_t)nb + 1, 0);
+    for (int j = 0; j < np; ++j) {
+        const int r = pl.neighbors[j];
+        if (r < 0 || r >= (int)by_rank.size() || by_rank[r].rank != r)
+            throw Error(TVEGPU_E_ARG, "peer-memory halo: no descriptor of partition " + std::to_string(r));
+        const PeerDesc& d = by_rank[r];
+        const auto it = std::find(d.nbr.begin(), d.nbr.end(), pl.rank);
+        if (it == d.nbr.end()) throw Error(TVEGPU_E_ARG, "internal: asymmetric halo");
+        const size_t jj = (size_t)(it - d.nbr.begin());
+        if (d.recv_off.size() != d.nbr.size() + 1 ||
+            d.recv_off[jj + 1] - d.recv_off[jj] != pl.send_off[j + 1] - pl.send_off[j])
+            throw Error(TVEGPU_E_ARG, "internal: halo size");
+        pth[j] = d.th;
+        pm[j] = d.m;
+        pf[j] = d.inbox + jj;
+        pa[j] = d.inbox + d.nbr.size() + jj;
+        start[j] = d.recv_off[jj];
+        for (int k = pl.send_off[j]; k < pl.send_off[j + 1]; ++k) {
+            const int32_t sl = pl.send_slot[k];
+            if (sl < 0 || sl >= nb) throw Error(TVEGPU_E_ARG, "internal: send slot outside the boundary elements");
+            off[(size_t)sl + 1]++;
+        }
+    }
+    for (int k = 0; k < nb; ++k) off[(size_t)k + 1] += off[k];
+    std::vector<uint32_t> ent(off[nb]);
+    std::vector<int32_t> fill(off.begin(), off.end() - 1);
+    for (int j = 0; j < np; ++j)
+        for (int k = pl.send_off[j]; k < pl.send_off[j + 1]; ++k) {
+            const int64_t dst = (int64_t)start[j] + (k - pl.send_off[j]);
+            if (dst >= (1 << 26)) throw Error(TVEGPU_E_ARG, "peer-memory halo: receive area above 2^26 entries");
+            ent[fill[pl.send_slot[k]]++] = (uint32_t)j << 26 | (uint32_t)dst;
+        }
+    cudaStream_t s = h->s;
+    auto& own = h->owned;
+    h->ptr.pd_off = dupload(own, off, s);
+    h->ptr.pd_ent = dupload(own, ent, s);
+    h->ptr.peer_th = dupload(own, pth, s);
+    h->ptr.peer_m = dupload(own, pm, s);
+    h->ptr.peer_flag = dupload(own, pf, s);
+    h->ptr.peer_ack = dupload(own, pa, s);
+    CU(cudaStreamSynchronize(s));
+    h->prm.npeers = np;
+    h->prm.ack = h->mode == TVEGPU_COUPLED ? 0 : 1;
+    h->peer = true;
+}
+
+// Cross-process form of PeerDesc (tvegpu_peer_export / tvegpu_peer_attach): CUDA IPC
+// handles of the two slot buffers and the inbox, then the neighbour ranks and offsets.
+struct PeerBlobHead {
+    uint32_t magic;
+    int32_t rank, nnbr, abi;
+    cudaIpcMemHandle_t th, m, inbox;
+    uint64_t off_th, off_m;
+};
+constexpr uint32_t kPeerMagic = 0x54564550u;  // "PEVT"
+
 // element-kernel dynamic shared memory: mbarrier, the chunk's element rows (TMA),
 // the staged node planes (ux,uy), (uz,T)
 size_t elem_smem(const tvegpu_engine* h, int rows) {
@@ -500,27 +594,31 @@ NodeKernel thermal_node_kernel(const tvegpu_engine* h) {
 }
 
 // Element kernels run one CTA per 128-element chunk over chunk range [c0, c1).
-template <int NN>
+// SEND: the boundary chunks of a peer-memory partitioned step (kernels.cuh peer_send).
+template <int NN, bool SEND>
 void launch_mech_element(tvegpu_engine* h, int c0, int c1) {
     if (c1 <= c0) return;
     const size_t sm = k3_smem(h);
     switch (h->prm.exp_kind < 0 ? 0 : (h->prm.exp_kind == 0 ? 1 : 2)) {
-        case 0: launch_step_kernel(h, k_mech_element<NN, 0>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
-        case 1: launch_step_kernel(h, k_mech_element<NN, 1>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
-        default: launch_step_kernel(h, k_mech_element<NN, 2>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
+        case 0: launch_step_kernel(h, k_mech_element<NN, 0, SEND>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
+        case 1: launch_step_kernel(h, k_mech_element<NN, 1, SEND>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
+        default: launch_step_kernel(h, k_mech_element<NN, 2, SEND>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
     }
 }
 
-template <int NN>
+template <int NN, bool SEND>
 void launch_thermal_element(tvegpu_engine* h, int c0, int c1) {
     if (c1 <= c0) return;
-    launch_step_kernel(h, k_thermal_element<NN>, c1 - c0, kChunkThreads, k1_smem(h), h->prm, h->ptr, h->cur, c0, c1);
+    launch_step_kernel(h, k_thermal_element<NN, SEND>, c1 - c0, kChunkThreads, k1_smem(h), h->prm, h->ptr, h->cur, c0,
+                       c1);
 }
-void launch_thermal_elements(tvegpu_engine* h, int c0, int c1) {
-    h->nn == 4 ? launch_thermal_element<4>(h, c0, c1) : launch_thermal_element<8>(h, c0, c1);
+void launch_thermal_elements(tvegpu_engine* h, int c0, int c1, bool send = false) {
+    if (send) h->nn == 4 ? launch_thermal_element<4, true>(h, c0, c1) : launch_thermal_element<8, true>(h, c0, c1);
+    else h->nn == 4 ? launch_thermal_element<4, false>(h, c0, c1) : launch_thermal_element<8, false>(h, c0, c1);
 }
-void launch_mech_elements(tvegpu_engine* h, int c0, int c1) {
-    h->nn == 4 ? launch_mech_element<4>(h, c0, c1) : launch_mech_element<8>(h, c0, c1);
+void launch_mech_elements(tvegpu_engine* h, int c0, int c1, bool send = false) {
+    if (send) h->nn == 4 ? launch_mech_element<4, true>(h, c0, c1) : launch_mech_element<8, true>(h, c0, c1);
+    else h->nn == 4 ? launch_mech_element<4, false>(h, c0, c1) : launch_mech_element<8, false>(h, c0, c1);
 }
 void launch_thermal_node(tvegpu_engine* h, double* t_out) {
     const int N = h->plan.N;
@@ -538,6 +636,26 @@ void launch_mech_node(tvegpu_engine* h, double* u_out, int n0 = 0, int n1 = -1, 
                            h->ptr, h->cur, closes, u_out, n0, n1);
 }
 
+template <class F>
+void for_each_element_kernel(F&& f) {
+    f((const void*)k_thermal_element<4, false>);
+    f((const void*)k_thermal_element<8, false>);
+    f((const void*)k_thermal_element<4, true>);
+    f((const void*)k_thermal_element<8, true>);
+    f((const void*)k_mech_element<4, 0, false>);
+    f((const void*)k_mech_element<4, 1, false>);
+    f((const void*)k_mech_element<4, 2, false>);
+    f((const void*)k_mech_element<8, 0, false>);
+    f((const void*)k_mech_element<8, 1, false>);
+    f((const void*)k_mech_element<8, 2, false>);
+    f((const void*)k_mech_element<4, 0, true>);
+    f((const void*)k_mech_element<4, 1, true>);
+    f((const void*)k_mech_element<4, 2, true>);
+    f((const void*)k_mech_element<8, 0, true>);
+    f((const void*)k_mech_element<8, 1, true>);
+    f((const void*)k_mech_element<8, 2, true>);
+}
+
 void set_smem_limits(tvegpu_engine* h) {
     const int sm = (int)std::max(k1_smem(h), k3_smem(h));
     // TVEGPU_CARVEOUT=<percent>: one shared-memory carve-out for all four step kernels
@@ -545,14 +663,7 @@ void set_smem_limits(tvegpu_engine* h) {
     if (const char* cv = std::getenv("TVEGPU_CARVEOUT")) {
         const int pct = std::atoi(cv);
         auto co = [&](const void* f) { CU(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct)); };
-        co((const void*)k_thermal_element<4>);
-        co((const void*)k_thermal_element<8>);
-        co((const void*)k_mech_element<4, 0>);
-        co((const void*)k_mech_element<4, 1>);
-        co((const void*)k_mech_element<4, 2>);
-        co((const void*)k_mech_element<8, 0>);
-        co((const void*)k_mech_element<8, 1>);
-        co((const void*)k_mech_element<8, 2>);
+        for_each_element_kernel(co);
         co((const void*)k_thermal_node<0>);
         co((const void*)k_thermal_node<1>);
         co((const void*)k_thermal_node<2>);
@@ -567,14 +678,7 @@ void set_smem_limits(tvegpu_engine* h) {
     if (sm <= set_to) return;
     set_to = sm;
     auto attr = [&](const void* f) { CU(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); };
-    attr((const void*)k_thermal_element<4>);
-    attr((const void*)k_thermal_element<8>);
-    attr((const void*)k_mech_element<4, 0>);
-    attr((const void*)k_mech_element<4, 1>);
-    attr((const void*)k_mech_element<4, 2>);
-    attr((const void*)k_mech_element<8, 0>);
-    attr((const void*)k_mech_element<8, 1>);
-    attr((const void*)k_mech_element<8, 2>);
+    for_each_element_kernel(attr);
 }
 
 // One Engine::step() (engine.hpp:70-82) of a single-partition engine: K1 K2 [K3 K4]
@@ -620,6 +724,57 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr, cudaEvent_t 
     CU(cudaGetLastError());
 }
 
+// Peer-memory form (every part attached, peer_attach): per phase the boundary chunks
+// as a SEND launch (element math + stores into the neighbours' receive areas + flags),
+// the interior chunks, then the node kernel, which waits for the neighbours' flags on
+// the device.  No pack kernel, no comm stream, no NCCL call.  Parts sharing one device
+// (a group) additionally order each node kernel after its neighbours' SEND launches
+// with events, so a waiting kernel never occupies the SMs a sender still needs; in
+// single-physics steps (no other phase in between) each SEND launch also follows its
+// neighbours' previous node kernels (DevParams::ack; a group: events as well).
+// xev (profiling, one-part sets): per phase a (start, end) pair around the SEND launch.
+void enqueue_peer_step(Stepper& S, cudaEvent_t* evs, cudaEvent_t* xev) {
+    const std::vector<tvegpu_engine*>& parts = S.parts;
+    tvegpu_engine* h0 = parts[0];
+    const bool shared_device = parts.size() > 1;
+    int ev = 0;
+    auto mark = [&]() {
+        if (evs) CU(cudaEventRecord(evs[ev++], h0->s));
+    };
+    auto phase = [&](bool mech, cudaEvent_t* x) {
+        for (tvegpu_engine* h : parts) {
+            const int nb = h->plan.nchunks_boundary, nc = (int)h->plan.chunk_start.size() - 1;
+            auto elements = mech ? launch_mech_elements : launch_thermal_elements;
+            if (x && h == h0) CU(cudaEventRecord(x[0], h->s));
+            elements(h, 0, nb, true);
+            if (x && h == h0) CU(cudaEventRecord(x[1], h->s));
+            if (shared_device) CU(cudaEventRecord(h->ev_pack, h->s));
+            elements(h, nb, nc, false);
+        }
+        mark();
+        for (tvegpu_engine* h : parts) {
+            if (shared_device)
+                for (int r : h->plan.neighbors) CU(cudaStreamWaitEvent(h->s, parts.at(r)->ev_pack, 0));
+            if (mech) {
+                launch_mech_node(h, nullptr);
+                h->cur ^= 1;
+            } else {
+                launch_thermal_node(h, nullptr);
+            }
+        }
+        if (shared_device && h0->prm.ack) {  // single physics: next SEND after the neighbours' node kernels
+            for (tvegpu_engine* h : parts) CU(cudaEventRecord(h->ev_comm, h->s));
+            for (tvegpu_engine* h : parts)
+                for (int r : h->plan.neighbors) CU(cudaStreamWaitEvent(h->s, parts.at(r)->ev_comm, 0));
+        }
+        mark();
+    };
+    mark();
+    if (h0->mode != TVEGPU_MECHANICAL_ONLY) phase(false, xev);
+    if (h0->mode != TVEGPU_THERMAL_ONLY) phase(true, xev ? xev + 2 : nullptr);
+    CU(cudaGetLastError());
+}
+
 // One step of a partitioned set (every part an RCB partition), phase by
 // phase over the parts so the transport sees every part's packed segment:
 //   boundary elements + pack (ev_pack) | exchange (ev_comm) | interior elements,
@@ -631,6 +786,10 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr, cudaEvent_t 
 void enqueue_partitioned_step(Stepper& S, cudaEvent_t* evs = nullptr, cudaEvent_t* xev = nullptr) {
     const std::vector<tvegpu_engine*>& parts = S.parts;
     tvegpu_engine* h0 = parts[0];
+    if (h0->peer) {
+        enqueue_peer_step(S, evs, xev);
+        return;
+    }
     int ev = 0;
     auto mark = [&]() {
         if (evs) CU(cudaEventRecord(evs[ev++], h0->s));
@@ -804,7 +963,7 @@ void enqueue_steps(Stepper& S, long long nsteps) {
 
 // Enqueues the 40-byte status read (clock + error words) on the main stream.
 void enqueue_status_read(tvegpu_engine* h) {
-    CU(cudaMemcpyAsync(h->h_words, h->ptr.clock, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->s));
+    CU(cudaMemcpyAsync(h->h_words, h->ptr.clock, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->s));
 }
 
 // Ends a pending window: waits for every part, agrees on the first failure across
@@ -825,18 +984,33 @@ tvegpu_status sync_and_check(Stepper& S, bool status_enqueued = false) {
         std::memcpy(&c, h->h_words, sizeof(Clock));
         any_halt |= c.halted != 0;
     }
-    unsigned long long wi = S.parts[0]->h_words[3], we = S.parts[0]->h_words[4];
+    unsigned long long wi = S.parts[0]->h_words[3], we = S.parts[0]->h_words[4], wh = S.parts[0]->h_words[5];
     if (multi) {
-        // agree on the first failure: min over the partitions of (err_inst, err_elem)
+        // agree on the first failure: min over the partitions of (err_inst, err_elem, err_halo)
         std::vector<unsigned long long*> w;
         for (tvegpu_engine* h : S.parts) w.push_back(reinterpret_cast<unsigned long long*>(h->ptr.err_inst));
-        S.parts[0]->tx->allreduce_u64(S.parts, w, 2, /*max=*/false);
+        S.parts[0]->tx->allreduce_u64(S.parts, w, 3, /*max=*/false);
         for (tvegpu_engine* h : S.parts) {
-            CU(cudaMemcpyAsync(h->h_words + 3, h->ptr.err_inst, 16, cudaMemcpyDeviceToHost, h->s));
+            CU(cudaMemcpyAsync(h->h_words + 3, h->ptr.err_inst, 24, cudaMemcpyDeviceToHost, h->s));
             CU(cudaStreamSynchronize(h->s));
         }
         wi = S.parts[0]->h_words[3];
         we = S.parts[0]->h_words[4];
+        wh = S.parts[0]->h_words[5];
+    }
+    if (wh != ~0ULL) {  // a peer-memory halo wait timed out: no verdict on the physics is possible
+        char buf[200];
+        std::snprintf(buf, sizeof buf,
+                      "halo exchange: a neighbouring partition's contributions did not arrive within 20 s at step %llu",
+                      wh);
+        for (tvegpu_engine* h : S.parts) {
+            h->halted = true;
+            h->err_step = (long long)wh;
+            h->err_node = -1;
+            h->err = buf;
+            h->state_invalid = true;
+        }
+        return TVEGPU_E_NCCL;
     }
     if (!any_halt && wi == ~0ULL && we == ~0ULL) {
         for (tvegpu_engine* h : S.parts) {
@@ -1262,19 +1436,21 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     }
     lap("gather lists, slot buffers");
     // ---- clock and error words
-    // clock + the two error words contiguous: the end-of-call check is one 40-byte read
+    // clock + the three error words contiguous: the end-of-call check is one 48-byte read
     static_assert(sizeof(Clock) == 24, "status block layout");
     {
-        unsigned long long* st = dalloc<unsigned long long>(own, 5);
+        unsigned long long* st = dalloc<unsigned long long>(own, 7);
         h->ptr.clock = reinterpret_cast<Clock*>(st);
         h->ptr.err_inst = st + 3;
         h->ptr.err_elem = st + 4;
+        h->ptr.err_halo = st + 5;
+        h->ptr.epoch = st + 6;  // never reset (peer-memory halo sequence base)
     }
     {
         Clock c{0.0, 0, 0, 0};
         CU(cudaMemcpyAsync(h->ptr.clock, &c, sizeof c, cudaMemcpyHostToDevice, s));
-        CU(cudaMemsetAsync(h->ptr.err_inst, 0xff, 8, s));
-        CU(cudaMemsetAsync(h->ptr.err_elem, 0xff, 8, s));
+        CU(cudaMemsetAsync(h->ptr.err_inst, 0xff, 24, s));
+        CU(cudaMemsetAsync(h->ptr.epoch, 0, 8, s));
         CU(cudaStreamSynchronize(s));
     }
     if (m.diag) {
@@ -1327,6 +1503,15 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
         h->d_send_slot = dupload(own, pl.send_slot, s);
         h->send_th = dalloc<double>(own, ns);
         h->send_m = dalloc<double>(own, kMW * ns);
+        // peer-memory halo: the inbox the neighbours raise their flags in, the send-kernel CTA counters
+        h->halo_transport = o.halo_transport;
+        // [0, np): the neighbours' phase flags; [np, 2 np): their end-of-step acks (single physics)
+        const size_t np = std::max<size_t>(1, pl.neighbors.size());
+        h->ptr.inbox = dalloc<unsigned long long>(own, 2 * np);
+        h->ptr.ack_inbox = h->ptr.inbox + pl.neighbors.size();
+        CU(cudaMemsetAsync(h->ptr.inbox, 0, 2 * np * 8, s));
+        h->ptr.send_cnt = dalloc<unsigned>(own, 2);
+        CU(cudaMemsetAsync(h->ptr.send_cnt, 0, 8, s));
         CU(cudaStreamSynchronize(s));
     }
     CU(cudaStreamSynchronize(s));
@@ -1744,6 +1929,7 @@ void tvegpu_default_options(tvegpu_options* o) {
     o->rank = 0;
     o->reorder = 1;
     o->steps_per_graph = 64;
+    o->halo_transport = TVEGPU_HALO_PEER;
 }
 
 tvegpu_status tvegpu_create(const tvegpu_problem* p, const tvegpu_options* o, tvegpu_engine** out) {
@@ -1779,6 +1965,7 @@ void tvegpu_destroy(tvegpu_engine* h) {
     if (h->s) cudaStreamSynchronize(h->s);
     if (h->sc) cudaStreamSynchronize(h->sc);
     if (h->comm) nccl().CommDestroy(h->comm);
+    for (void* p : h->ipc_open) cudaIpcCloseMemHandle(p);
     for (void* p : h->owned) cudaFree(p);
     if (h->h_words) cudaFreeHost(h->h_words);
     if (h->stage) cudaFreeHost(h->stage);
@@ -1916,8 +2103,7 @@ tvegpu_status tvegpu_set_state(tvegpu_engine* h, const double* T, const double* 
         }
         Clock c{time, (long long)step, 0, 0};
         CU(cudaMemcpyAsync(h->ptr.clock, &c, sizeof c, cudaMemcpyHostToDevice, h->s));
-        CU(cudaMemsetAsync(h->ptr.err_inst, 0xff, 8, h->s));
-        CU(cudaMemsetAsync(h->ptr.err_elem, 0xff, 8, h->s));
+        CU(cudaMemsetAsync(h->ptr.err_inst, 0xff, 24, h->s));
         CU(cudaStreamSynchronize(h->s));
         h->host_time = time;
         h->host_step = step;
@@ -2495,6 +2681,77 @@ tvegpu_status tvegpu_nccl_unique_id(void* out128) {
     return TVEGPU_OK;
 }
 
+tvegpu_status tvegpu_peer_export(tvegpu_engine* h, void* blob, size_t cap, size_t* len) {
+    if (!h || !len) return TVEGPU_E_ARG;
+    return guard(h, [&] {
+        const RankPlan& pl = h->plan;
+        if (pl.nranks < 2) throw Error(TVEGPU_E_ARG, "tvegpu_peer_export: not a partitioned engine (nranks == 1)");
+        const size_t nn = pl.neighbors.size();
+        const size_t need = sizeof(PeerBlobHead) + (2 * nn + 1) * sizeof(int32_t);
+        *len = need;
+        if (!blob) return TVEGPU_OK;  // size query
+        if (cap < need) throw Error(TVEGPU_E_ARG, "tvegpu_peer_export: buffer too small");
+        PeerBlobHead hd{};
+        hd.magic = kPeerMagic;
+        hd.rank = pl.rank;
+        hd.nnbr = (int32_t)nn;
+        hd.abi = TVEGPU_ABI_VERSION;
+        CU(cudaIpcGetMemHandle(&hd.th, h->ptr.slot_th));
+        CU(cudaIpcGetMemHandle(&hd.m, h->ptr.slot_m));
+        CU(cudaIpcGetMemHandle(&hd.inbox, h->ptr.inbox));
+        hd.off_th = (uint64_t)((char*)recv_area(h, false) - (char*)h->ptr.slot_th);
+        hd.off_m = (uint64_t)((char*)recv_area(h, true) - (char*)h->ptr.slot_m);
+        char* b = static_cast<char*>(blob);
+        std::memcpy(b, &hd, sizeof hd);
+        std::memcpy(b + sizeof hd, pl.neighbors.data(), nn * sizeof(int32_t));
+        std::memcpy(b + sizeof hd + nn * sizeof(int32_t), pl.recv_off.data(), (nn + 1) * sizeof(int32_t));
+        return TVEGPU_OK;
+    });
+}
+
+tvegpu_status tvegpu_peer_attach(tvegpu_engine* h, const void* const* blobs, const size_t* lens, int32_t nranks) {
+    if (!h || !blobs || !lens) return TVEGPU_E_ARG;
+    return guard(h, [&] {
+        const RankPlan& pl = h->plan;
+        if (nranks != pl.nranks) throw Error(TVEGPU_E_ARG, "tvegpu_peer_attach: one descriptor per rank expected");
+        if (h->peer) throw Error(TVEGPU_E_ARG, "tvegpu_peer_attach: already attached");
+        if (h->pending) {
+            const tvegpu_status st = sync_and_check(h->solo);
+            if (st != TVEGPU_OK) return st;
+        }
+        std::vector<PeerDesc> by_rank(nranks);
+        for (int r : pl.neighbors) {  // only the neighbours' buffers are mapped
+            if (!blobs[r] || lens[r] < sizeof(PeerBlobHead)) throw Error(TVEGPU_E_ARG, "tvegpu_peer_attach: short descriptor");
+            PeerBlobHead hd;
+            std::memcpy(&hd, blobs[r], sizeof hd);
+            const size_t nn = hd.nnbr < 0 ? 0 : (size_t)hd.nnbr;
+            if (hd.magic != kPeerMagic || hd.rank != r || hd.abi != TVEGPU_ABI_VERSION ||
+                lens[r] < sizeof hd + (2 * nn + 1) * sizeof(int32_t))
+                throw Error(TVEGPU_E_ARG, "tvegpu_peer_attach: bad descriptor of rank " + std::to_string(r));
+            PeerDesc& d = by_rank[r];
+            d.rank = r;
+            const char* b = static_cast<const char*>(blobs[r]);
+            d.nbr.assign(reinterpret_cast<const int32_t*>(b + sizeof hd), reinterpret_cast<const int32_t*>(b + sizeof hd) + nn);
+            const int32_t* ro = reinterpret_cast<const int32_t*>(b + sizeof hd + nn * sizeof(int32_t));
+            d.recv_off.assign(ro, ro + nn + 1);
+            void *pth = nullptr, *pm = nullptr, *pin = nullptr;
+            CU(cudaIpcOpenMemHandle(&pth, hd.th, cudaIpcMemLazyEnablePeerAccess));
+            h->ipc_open.push_back(pth);
+            CU(cudaIpcOpenMemHandle(&pm, hd.m, cudaIpcMemLazyEnablePeerAccess));
+            h->ipc_open.push_back(pm);
+            CU(cudaIpcOpenMemHandle(&pin, hd.inbox, cudaIpcMemLazyEnablePeerAccess));
+            h->ipc_open.push_back(pin);
+            d.th = reinterpret_cast<double*>(static_cast<char*>(pth) + hd.off_th);
+            d.m = reinterpret_cast<double*>(static_cast<char*>(pm) + hd.off_m);
+            d.inbox = static_cast<unsigned long long*>(pin);
+        }
+        peer_attach(h, by_rank);
+        return TVEGPU_OK;
+    });
+}
+
+int32_t tvegpu_halo_peer(const tvegpu_engine* h) { return h && h->peer ? 1 : 0; }
+
 void* tvegpu_stream(tvegpu_engine* h) { return h ? (void*)h->s : nullptr; }
 
 tvegpu_status tvegpu_halo_info(const tvegpu_engine* h, int32_t* neighbors, int64_t* send_bytes, int64_t* recv_bytes) {
@@ -2513,9 +2770,12 @@ tvegpu_status tvegpu_halo_info(const tvegpu_engine* h, int32_t* neighbors, int64
 int32_t tvegpu_kernels_per_step(const tvegpu_engine* h) {
     if (!h) return 0;
     const bool multi = h->plan.nranks > 1;
+    // per phase: element kernel + node kernel; partitioned: boundary and interior element
+    // launches, plus the halo pack with the NCCL transport (peer memory: none)
+    const int per = multi ? (h->peer ? 3 : 4) : 2;
     int k = 0;
-    if (h->mode != TVEGPU_MECHANICAL_ONLY) k += multi ? 4 : 2;  // K1 (x2 + pack) + K2
-    if (h->mode != TVEGPU_THERMAL_ONLY) k += multi ? 4 : 2;
+    if (h->mode != TVEGPU_MECHANICAL_ONLY) k += per;
+    if (h->mode != TVEGPU_THERMAL_ONLY) k += per;
     return k;
 }
 
@@ -2666,6 +2926,11 @@ tvegpu_status tvegpu_group_create(const tvegpu_problem* p, int32_t nparts, const
             G->parts.push_back(h);
             build_engine(h, *p, oo, /*loopback=*/true);
             h->tx = &G->tx;
+        }
+        if (o->halo_transport == TVEGPU_HALO_PEER) {  // the parts' buffers are on this device: plain pointers
+            std::vector<PeerDesc> d;
+            for (tvegpu_engine* h : G->parts) d.push_back(peer_desc(h));
+            for (tvegpu_engine* h : G->parts) peer_attach(h, d);
         }
         G->st.parts = G->parts;
         G->st.steps_per_graph = o->steps_per_graph > 0 ? o->steps_per_graph : 64;

@@ -83,6 +83,8 @@ struct DevParams {
     int stage_stride;     // entries per chunk in stage_ent (max unique nodes of a chunk)
     int ell;              // G > 0: ELL gathers with rows of 8 G slot ids (every node has <= 8 G contributions)
     int motion;           // MechBCs::motion_override active (host-evaluated pins, K4 reads motion_row/val)
+    int npeers;           // peer-memory halo (nranks > 1): neighbours whose inbox flags the node kernels wait for
+    int ack;              // ... single-physics mode: SEND kernels also wait for the neighbours' end-of-step acks
     int es;               // row stride of the per-element SoA arrays (geo, theta, fiber, axes): >= E + 1, 16-aligned
     int xstride;          // doubles per chunk in chunk_x (3 * even max_chunk_nodes)
     double dt, mu, kappa, eta_a, kh, rho, wbcb, Ta, Qm, gamma;
@@ -142,6 +144,18 @@ struct DevPtrs {
     const int32_t* motion_row;  // [N] row of motion_val for override candidates, else -1 (motion only)
     const double4* motion_val;  // [rows] (x, y, z, pinned) of this step's motion_override(node, t + dt)
     const double* tabs;         // c(T), k(T) tables and Prony coefficients (DevParams::tab_*)
+    // peer-memory halo (nranks > 1, DevParams::npeers > 0): see peer_send / peer_signal / peer_wait
+    const int32_t* pd_off;                 // [Eb nn + 1] per boundary slot (e nn + a) its destinations
+    const uint32_t* pd_ent;                // (neighbour << 26) | index in that neighbour's receive area
+    double* const* peer_th;                // [npeers] the neighbours' thermal receive areas
+    double* const* peer_m;                 // [npeers] mechanical receive areas (kMW doubles per entry)
+    unsigned long long* const* peer_flag;  // [npeers] this partition's flag word in each neighbour's inbox
+    unsigned long long* inbox;             // [npeers] flags raised by the neighbours
+    unsigned* send_cnt;                    // [2] boundary CTAs done in the running send kernel (per phase)
+    unsigned long long* epoch;             // steps enqueued since creation (never reset): flag sequence base
+    unsigned long long* err_halo;          // first step whose halo wait timed out, else ~0
+    unsigned long long* ack_inbox;         // [npeers] neighbours' completed steps (DevParams::ack)
+    unsigned long long* const* peer_ack;   // [npeers] this partition's word in each neighbour's ack_inbox
 };
 
 enum : uint8_t { BC_FIXED = 1, BC_PX = 2, BC_PY = 4, BC_PZ = 8, BC_TFIX = 16 };
@@ -584,6 +598,93 @@ __device__ __forceinline__ void check_gather(const DevParams& P, const DevPtrs& 
     }
 }
 
+// ------------------------------------------------------------------ peer-memory halo
+// In a partitioned step the boundary chunks run as their own launch of the element kernel
+// with SEND: every contribution another partition gathers is stored by the thread that
+// computed it straight into that partition's receive area — NVLink peer memory of the
+// other GPU (CUDA IPC mapping), or another partition's buffer in a group — so the
+// element math and the halo transfer are one kernel (no pack kernel, no NCCL call).
+// When the launch's last CTA is done it raises flag = 2 epoch + 1 + phase in each
+// neighbour's inbox (release, system scope); the neighbours' node kernels wait for it
+// (acquire) while the interior chunks still run.  Receive areas are reused safely
+// without a second buffer: a partition's phase-p sends of step n follow its own node
+// kernel of the other phase, which waited for its neighbours' sends that follow their
+// reads of the receive areas (shared nodes make every halo relation symmetric).
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// contribution (e, a) of a boundary element (W doubles) to every partition that gathers it
+template <int W>
+__device__ __forceinline__ void peer_send(const DevPtrs& D, int slot, const double* v) {
+    const int k0 = __ldg(D.pd_off + slot), k1 = __ldg(D.pd_off + slot + 1);
+    for (int k = k0; k < k1; ++k) {
+        const uint32_t en = __ldg(D.pd_ent + k);
+        double* b = (W == 1 ? D.peer_th : D.peer_m)[en >> 26] + (size_t)(en & 0x3ffffffu) * W;
+#pragma unroll
+        for (int q = 0; q < W; ++q) b[q] = v[q];
+    }
+}
+// start of a SEND launch in a single-physics partitioned step (DevParams::ack): the
+// neighbours' node kernels of the previous step are done with the receive areas this
+// launch overwrites.  (In coupled steps the other phase's flags already imply it.)
+__device__ __forceinline__ void peer_wait_ack(const DevParams& P, const DevPtrs& D) {
+    if (threadIdx.x == 0) {
+        const unsigned long long ep = *(volatile unsigned long long*)D.epoch;
+        const unsigned long long t0 = globaltimer_ns();
+        for (int j = 0; j < P.npeers; ++j)
+            while (ld_acquire_sys(D.ack_inbox + j) < ep) {
+                if (globaltimer_ns() - t0 > 20000000000ull) {
+                    atomicMin(D.err_halo, (unsigned long long)D.clock->step);
+                    break;
+                }
+                __nanosleep(100);
+            }
+    }
+    __syncthreads();
+}
+// end of a SEND launch (every thread of every CTA; halted partitions still signal so their
+// neighbours never wait on them): the last CTA raises the phase flag in each neighbour's inbox
+__device__ __forceinline__ void peer_signal(const DevParams& P, const DevPtrs& D, int phase) {
+    __threadfence_system();  // this thread's peer stores before the CTA's arrival
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    const unsigned n = atomicAdd(D.send_cnt + phase, 1u);
+    if (n != gridDim.x - 1) return;
+    D.send_cnt[phase] = 0;
+    __threadfence_system();
+    const unsigned long long seq = 2 * *D.epoch + 1 + phase;
+    for (int j = 0; j < P.npeers; ++j) st_release_sys(D.peer_flag[j], seq);
+}
+// start of a node kernel of a partitioned step: this phase's contributions from every
+// neighbour have landed.  Bounded: after 20 s the wait gives up and records the step in
+// err_halo (the call's verdict reports it, collectively) instead of hanging the device.
+__device__ __forceinline__ void peer_wait(const DevParams& P, const DevPtrs& D, int phase) {
+    if (P.npeers == 0) return;
+    if (threadIdx.x == 0) {
+        const unsigned long long seq = 2 * *(volatile unsigned long long*)D.epoch + 1 + phase;
+        const unsigned long long t0 = globaltimer_ns();
+        for (int j = 0; j < P.npeers; ++j)
+            while (ld_acquire_sys(D.inbox + j) < seq) {
+                if (globaltimer_ns() - t0 > 20000000000ull) {
+                    atomicMin(D.err_halo, (unsigned long long)D.clock->step);
+                    break;
+                }
+                __nanosleep(100);
+            }
+    }
+    __syncthreads();
+}
+
 // ------------------------------------------------------------------ K1: thermal element
 #ifdef TVEGPU_K1_MINBLOCKS
 #define K1_BOUNDS __launch_bounds__(kChunkThreads, TVEGPU_K1_MINBLOCKS)
@@ -591,7 +692,7 @@ __device__ __forceinline__ void check_gather(const DevParams& P, const DevPtrs& 
 #define K1_BOUNDS __launch_bounds__(kChunkThreads)
 #endif
 // K1 element body: element e of the staged chunk S (n = its node slots)
-template <int NN>
+template <int NN, bool SEND>
 __device__ __forceinline__ void k1_body(const DevParams& P, const DevPtrs& D, const NodeStage& S,
                                         const ElemRows<kTmaK1>& rows, const CoordStage& xs, const int e,
                                         const int (&n)[NN]) {
@@ -641,12 +742,20 @@ __device__ __forceinline__ void k1_body(const DevParams& P, const DevPtrs& D, co
         const double f0 = -(r[0] + r[1] + r[2]);
         reinterpret_cast<double2*>(out)[0] = make_double2(f0, r[0]);
         reinterpret_cast<double2*>(out)[1] = make_double2(r[1], r[2]);
+        if constexpr (SEND) {
+            const double f[4] = {f0, r[0], r[1], r[2]};
+#pragma unroll
+            for (int a = 0; a < 4; ++a) peer_send<1>(D, e * NN + a, f + a);
+        }
     } else {
         double f[8];
 #pragma unroll
         for (int a = 0; a < 8; ++a) f[a] = h8s(a, 0) * r[0] + h8s(a, 1) * r[1] + h8s(a, 2) * r[2];
 #pragma unroll
         for (int a = 0; a < 8; a += 2) reinterpret_cast<double2*>(out)[a / 2] = make_double2(f[a], f[a + 1]);
+        if constexpr (SEND)
+#pragma unroll
+            for (int a = 0; a < 8; ++a) peer_send<1>(D, e * NN + a, f + a);
     }
     if (dF == 0.0) atomicMin(D.err_elem, pack_elem(D.clock->step, D.elem_orig[e]));
 }
@@ -655,7 +764,8 @@ __device__ __forceinline__ void k1_body(const DevParams& P, const DevPtrs& D, co
 template <int NN>
 __host__ __device__ __forceinline__ RowPlan k1_rows() { return RowPlan{k1_xstage<NN>() ? 0 : 10, 0, 0, 0}; }
 
-template <int NN>
+// SEND: the boundary chunks of a peer-memory partitioned step (peer_send / peer_signal)
+template <int NN, bool SEND = false>
 __global__ void K1_BOUNDS k_thermal_element(const DevParams P, const DevPtrs D, int cur, int c0, int c1) {
     extern __shared__ __align__(128) unsigned char smem[];
     const RowPlan rp = k1_rows<NN>();
@@ -680,9 +790,18 @@ __global__ void K1_BOUNDS k_thermal_element(const DevParams P, const DevPtrs D, 
     int n[NN];
     const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c, P.stage_stride, S, n);
     wait_elem_rows<kTmaK1>(bar);  // every thread: the CTA must not retire with bulk copies in flight
+    if constexpr (SEND) {  // every thread reaches peer_signal, halted or not
+        if (P.ack) peer_wait_ack(P, D);
+        if (!D.clock->halted && e >= 0) {
+            check_chunk<NN>(P, D, c, e, n);
+            k1_body<NN, true>(P, D, S, ElemRows<kTmaK1>{rows, (int)threadIdx.x}, xs, e, n);
+        }
+        peer_signal(P, D, 0);
+        return;
+    }
     if (D.clock->halted || e < 0) return;  // halted: uniform across the grid (read after the wait)
     check_chunk<NN>(P, D, c, e, n);
-    k1_body<NN>(P, D, S, ElemRows<kTmaK1>{rows, (int)threadIdx.x}, xs, e, n);
+    k1_body<NN, false>(P, D, S, ElemRows<kTmaK1>{rows, (int)threadIdx.x}, xs, e, n);
     pdl_trigger();  // after this block's work: the successor fills in behind the last wave
 }
 
@@ -690,7 +809,7 @@ __global__ void K1_BOUNDS k_thermal_element(const DevParams P, const DevPtrs D, 
 // Applies the finite-check verdict of the step and advances time/step
 // (engine.hpp:89-90: the reference throws before advancing).  Called by every
 // block of the closing node kernel after its body; the last block to arrive acts.
-__device__ __forceinline__ void close_step(const DevPtrs& D, double dt) {
+__device__ __forceinline__ void close_step(const DevParams& P, const DevPtrs& D, double dt) {
     __syncthreads();
     if (threadIdx.x != 0) return;
     __threadfence();
@@ -710,6 +829,15 @@ __device__ __forceinline__ void close_step(const DevPtrs& D, double dt) {
         }
     }
     c->ticket = 0;
+    if (D.epoch) {  // every enqueued step, halted or not: the peers' sequences stay in step
+        const unsigned long long ep = *D.epoch + 1;
+        *D.epoch = ep;
+        if (P.ack) {  // single-physics peer halo: this step's receive areas are consumed
+            __threadfence_system();
+            for (int j = 0; j < P.npeers; ++j)
+                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(D.peer_ack[j]), "l"(ep) : "memory");
+        }
+    }
     __threadfence();
 }
 
@@ -850,6 +978,7 @@ __global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, i
         }
     }
     pdl_wait();
+    peer_wait(P, D, 0);
     const bool active = i < P.N && !D.clock->halted;  // the same for both threads of a pair
     double s = 0.0;
     if constexpr (PAIR) {
@@ -880,7 +1009,7 @@ __global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, i
         if (t_out) t_out[__ldg(D.node_orig + i)] = Tn;
     }
     pdl_trigger();
-    if (closes) close_step(D, P.dt);
+    if (closes) close_step(P, D, P.dt);
 }
 
 // ------------------------------------------------------------------ K3: mechanical element
@@ -895,7 +1024,7 @@ __global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, i
 #define TVEGPU_K3_MINBLOCKS_T4 5  // T4: 102 registers, 20 warps/SM (cfg5 T4 K3 -12 % vs 4)
 #endif
 // K3 element body: element e of the staged chunk st (n = its node slots)
-template <int NN, int EXP>
+template <int NN, int EXP, bool SEND>
 __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, const NodeStage& st,
                                         const ElemRows<kTmaK3>& rows, const RowPlan& rp, const CoordStage& xs,
                                         const int e, const int (&n)[NN]) {
@@ -1115,6 +1244,12 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
         st4(o + 0, make_double4(-(Q[0] + Q[1] + Q[2]), -(Q[3] + Q[4] + Q[5]), -(Q[6] + Q[7] + Q[8]), Q[0]));
         st4(o + 1, make_double4(Q[3], Q[6], Q[1], Q[4]));
         st4(o + 2, make_double4(Q[7], Q[2], Q[5], Q[8]));
+        if constexpr (SEND) {
+            const double f[4][3] = {{-(Q[0] + Q[1] + Q[2]), -(Q[3] + Q[4] + Q[5]), -(Q[6] + Q[7] + Q[8])},
+                                    {Q[0], Q[3], Q[6]}, {Q[1], Q[4], Q[7]}, {Q[2], Q[5], Q[8]}};
+#pragma unroll
+            for (int a = 0; a < 4; ++a) peer_send<3>(D, e * NN + a, f[a]);
+        }
     } else if constexpr (NN == 4) {
         st4(out + 0, make_double4(-(Q[0] + Q[1] + Q[2]), -(Q[3] + Q[4] + Q[5]), -(Q[6] + Q[7] + Q[8]), 0.0));
         st4(out + 1, make_double4(Q[0], Q[3], Q[6], 0.0));
@@ -1241,6 +1376,13 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
                 st4(out + a, make_double4(f[0], f[1], f[2], 0.0));
             }
         }
+        if constexpr (SEND)
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {
+                double f[3];
+                corner(a, f);
+                peer_send<3>(D, e * NN + a, f);
+            }
     }
     if (P.diag) {
 #pragma unroll
@@ -1258,7 +1400,7 @@ __host__ __device__ __forceinline__ RowPlan k3_rows(const DevParams& P) {
                    (EXP == 2 && P.axes_per_elem) ? 6 : 0};
 }
 
-template <int NN, int EXP>
+template <int NN, int EXP, bool SEND = false>
 __global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T4 : TVEGPU_K3_MINBLOCKS)
     k_mech_element(const DevParams P, const DevPtrs D, int cur, int c0, int c1) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -1284,9 +1426,18 @@ __global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T
     int n[NN];
     const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c, P.stage_stride, st, n);
     wait_elem_rows<kTmaK3>(bar);  // every thread: the CTA must not retire with bulk copies in flight
+    if constexpr (SEND) {
+        if (P.ack) peer_wait_ack(P, D);
+        if (!D.clock->halted && e >= 0) {
+            check_chunk<NN>(P, D, c, e, n);
+            k3_body<NN, EXP, true>(P, D, st, ElemRows<kTmaK3>{rows, (int)threadIdx.x}, rp, xs, e, n);
+        }
+        peer_signal(P, D, 1);
+        return;
+    }
     if (D.clock->halted || e < 0) return;
     check_chunk<NN>(P, D, c, e, n);
-    k3_body<NN, EXP>(P, D, st, ElemRows<kTmaK3>{rows, (int)threadIdx.x}, rp, xs, e, n);
+    k3_body<NN, EXP, false>(P, D, st, ElemRows<kTmaK3>{rows, (int)threadIdx.x}, rp, xs, e, n);
     pdl_trigger();
 }
 
@@ -1318,6 +1469,7 @@ __global__ void NODE_BOUNDS k_mech_node(const DevParams P, const DevPtrs D, int 
         msk = __ldg(D.mask + i);
     }
     pdl_wait();
+    peer_wait(P, D, 1);
     const bool active = i < n1 && !D.clock->halted;  // the same for both threads of a pair
     double f0 = 0.0, f1 = 0.0, f2 = 0.0;
     if constexpr (PAIR) {
@@ -1390,7 +1542,7 @@ __global__ void NODE_BOUNDS k_mech_node(const DevParams P, const DevPtrs D, int 
         }
     }
     pdl_trigger();
-    if (closes) close_step(D, P.dt);
+    if (closes) close_step(P, D, P.dt);
 }
 
 // ------------------------------------------------------------------ halo pack / unpack (nranks > 1)

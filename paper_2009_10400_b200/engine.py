@@ -71,7 +71,11 @@ _BY_STATUS = {1: ParseError, 2: ValidationError, 3: InstabilityError, 4: IoError
 
 class COptions(C.Structure):
     _fields_ = [("device", C.c_int32), ("nranks", C.c_int32), ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p),
-                ("reorder", C.c_int32), ("diagnostics", C.c_int32), ("steps_per_graph", C.c_int32)]
+                ("reorder", C.c_int32), ("diagnostics", C.c_int32), ("steps_per_graph", C.c_int32),
+                ("halo_transport", C.c_int32)]
+
+
+HALO_PEER, HALO_NCCL = 0, 1  # tvegpu.h TVEGPU_HALO_*
 
 
 class CPlanView(C.Structure):
@@ -121,6 +125,9 @@ EXPORTS = {
     "tvegpu_plan_get": (C.c_int, [C.c_void_p, C.POINTER(CPlanView)]),
     "tvegpu_plan_destroy": (None, [C.c_void_p]),
     "tvegpu_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "tvegpu_peer_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "tvegpu_peer_attach": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.c_int32]),
+    "tvegpu_halo_peer": (C.c_int32, [C.c_void_p]),
     "tvegpu_stream": (C.c_void_p, [C.c_void_p]),
     "tvegpu_kernels_per_step": (C.c_int32, [C.c_void_p]),
     "tvegpu_halo_info": (C.c_int, [C.c_void_p, _ip, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
@@ -320,10 +327,13 @@ def plan(problem: Problem, nranks=1, rank=0, reorder=True):
 
 class PartitionGroup:
     """nparts RCB partitions of one problem stepped together on one GPU by the
-    multi-GPU step code (tvegpu_group_*; the halo moves by device copies instead of
-    NCCL): the same calls as :class:`Engine`."""
+    multi-GPU step code (tvegpu_group_*): the same calls as :class:`Engine`.
+    halo_transport: HALO_PEER (default; the peer-memory send kernels, with the other
+    partitions' buffers standing in for the other GPUs) or HALO_NCCL (pack + exchange,
+    device copies instead of ncclSend/ncclRecv)."""
 
-    def __init__(self, problem: Problem, nparts: int, *, device: int = -1, steps_per_graph: int = 64):
+    def __init__(self, problem: Problem, nparts: int, *, device: int = -1, steps_per_graph: int = 64,
+                 halo_transport: int = HALO_PEER):
         L = lib()
         self.problem = problem
         self._c, self._keep = problem.to_c()
@@ -331,6 +341,7 @@ class PartitionGroup:
         L.tvegpu_default_options(C.byref(o))
         o.device = device
         o.steps_per_graph = steps_per_graph
+        o.halo_transport = halo_transport
         h = C.c_void_p()
         rc = L.tvegpu_group_create(C.byref(self._c), nparts, C.byref(o), C.byref(h))
         if rc:
@@ -428,7 +439,7 @@ class Engine:
 
     def __init__(self, problem: Problem, *, device: int = -1, nranks: int = 1, rank: int = 0,
                  nccl_id: bytes | None = None, reorder: bool = True, diagnostics: bool = False,
-                 steps_per_graph: int = 64):
+                 steps_per_graph: int = 64, halo_transport: int = HALO_PEER):
         L = lib()
         self.problem = problem
         t0 = time.perf_counter()
@@ -442,6 +453,7 @@ class Engine:
         self._id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         o.nccl_unique_id = C.cast(self._id, C.c_void_p) if self._id is not None else None
         o.reorder, o.diagnostics, o.steps_per_graph = int(reorder), int(diagnostics), steps_per_graph
+        o.halo_transport = halo_transport
         self._opt = o
         h = C.c_void_p()
         t0 = time.perf_counter()
@@ -677,6 +689,33 @@ class Engine:
 
     def kernels_per_step(self) -> int:
         return lib().tvegpu_kernels_per_step(self._h)
+
+    def peer_export(self) -> bytes:
+        """This partition's peer-memory halo descriptor (tvegpu_peer_export): all-gather
+        them over the ranks, then :meth:`peer_attach` on every rank."""
+        n = C.c_size_t()
+        rc = lib().tvegpu_peer_export(self._h, None, 0, C.byref(n))
+        if rc:
+            self._raise(rc)
+        buf = C.create_string_buffer(n.value)
+        rc = lib().tvegpu_peer_export(self._h, buf, n.value, C.byref(n))
+        if rc:
+            self._raise(rc)
+        return buf.raw[:n.value]
+
+    def peer_attach(self, blobs):
+        """Attach the neighbours' descriptors (a list indexed by rank): the halo then moves
+        by peer-memory stores from the boundary element kernels (tvegpu_peer_attach)."""
+        bufs = [C.create_string_buffer(b, len(b)) for b in blobs]
+        ptrs = (C.c_void_p * len(bufs))(*[C.cast(b, C.c_void_p) for b in bufs])
+        lens = (C.c_size_t * len(bufs))(*[len(b) for b in blobs])
+        rc = lib().tvegpu_peer_attach(self._h, ptrs, lens, len(bufs))
+        if rc:
+            self._raise(rc)
+
+    @property
+    def halo_peer(self) -> bool:
+        return bool(lib().tvegpu_halo_peer(self._h))
 
     def halo_info(self):
         """(neighbours, bytes sent, bytes received) per step of this partition's halo exchange."""

@@ -1,11 +1,18 @@
 """The multi-GPU step code on one GPU: RCB partitions stepped by
-enqueue_partitioned_step — boundary-first element launches, halo pack + ev_pack on the
-compute stream, the exchange on each partition's comm stream ending in ev_comm,
-interior elements, the node kernels after ev_comm, CUDA-graph capture of all
-partitions' streams, agreement on the first failure and the device state gather of
-checkpoints.  Only the transport differs from one NCCL rank per GPU: a device copy of
-each neighbour's packed segment instead of ncclSend/ncclRecv (engine.cu
-LoopbackTransport vs NcclTransport).
+enqueue_partitioned_step, CUDA-graph capture of all partitions' streams, agreement on
+the first failure and the device state gather of checkpoints, with both halo paths:
+
+- HALO_PEER (default): the boundary chunks run as SEND launches of the element kernels,
+  which store each interface contribution straight into the neighbours' receive areas
+  and raise per-phase flags there; the node kernels wait for the flags on the device
+  (kernels.cuh peer_send / peer_signal / peer_wait) — the same kernels and tables a
+  partition per GPU runs over NVLink peer memory, here with the other partitions'
+  buffers as the "peer" memory (plus events ordering each node kernel after its
+  neighbours' SEND launches, so no waiting kernel can starve a sender of SMs);
+- HALO_NCCL: halo pack + ev_pack, the exchange on each partition's comm stream ending in
+  ev_comm, the node kernels after ev_comm — with a device copy of each neighbour's
+  packed segment instead of ncclSend/ncclRecv (engine.cu LoopbackTransport vs
+  NcclTransport).
 
 Partition invariance is bit-exact by construction (canonical gather order over
 replicated nodes, node constants built once on the global mesh; engine.hpp:80-82
@@ -29,29 +36,34 @@ def assert_same(a, b, keys=FIELDS):
     assert a["time"] == b["time"] and a["step"] == b["step"]
 
 
+HALOS = [pytest.param(tg.HALO_PEER, id="peer"), pytest.param(tg.HALO_NCCL, id="nccl")]
+
+
 @pytest.mark.parametrize("kind,n", [(H8, 6), (T4, 5)])
 @pytest.mark.parametrize("nparts", [2, 3, 4, 8])
 @pytest.mark.parametrize("spg", [7, 64])
-def test_partitioned_step_bit_identical(kind, n, nparts, spg):
+@pytest.mark.parametrize("halo", HALOS)
+def test_partitioned_step_bit_identical(kind, n, nparts, spg, halo):
     """P partitions (graph chunks of 7 or 64 steps, so several replays plus direct
     remainders) reproduce the single-partition state bit for bit."""
     steps = 150
     p = configs.small_problem(kind=kind, n=n, steps=steps)
     one = tg.Engine(p)
     one.step(steps)
-    grp = PartitionGroup(p, nparts, steps_per_graph=spg)
+    grp = PartitionGroup(p, nparts, steps_per_graph=spg, halo_transport=halo)
     grp.step(3)  # plain steps first, then graph replays
     grp.step(steps - 3)
     assert_same(one.state(), grp.state())
 
 
 @pytest.mark.parametrize("mode", [THERMAL_ONLY, MECHANICAL_ONLY])
-def test_partitioned_modes(mode):
+@pytest.mark.parametrize("halo", HALOS)
+def test_partitioned_modes(mode, halo):
     p = configs.small_problem(kind=H8, n=5, steps=80)
     p.mode = mode
     one = tg.Engine(p)
     one.step(80)
-    grp = PartitionGroup(p, 4, steps_per_graph=16)
+    grp = PartitionGroup(p, 4, steps_per_graph=16, halo_transport=halo)
     grp.step(80)
     assert_same(one.state(), grp.state())
 
@@ -119,7 +131,8 @@ def test_partitioned_checkpoint_round_trip():
 
 
 @pytest.mark.parametrize("kind", [T4, H8])
-def test_partitioned_failure_is_collective(kind):
+@pytest.mark.parametrize("halo", HALOS)
+def test_partitioned_failure_is_collective(kind, halo):
     """A NaN injected into one node (held by one or several partitions): every partition
     reports the same InstabilityError (step, node) as the single engine, the group's
     state is then refused until set_state, and after a reset the group runs on bit-
@@ -128,7 +141,7 @@ def test_partitioned_failure_is_collective(kind):
     p = configs.small_problem(kind=kind, n=5, steps=40)
     p.expansion_enabled = False  # the NaN would reach F_ther and be reported as an element error instead
     one = tg.Engine(p)
-    grp = PartitionGroup(p, 4, steps_per_graph=4)
+    grp = PartitionGroup(p, 4, steps_per_graph=4, halo_transport=halo)
     one.step(5)
     grp.step(5)
     s = one.state()
@@ -156,7 +169,8 @@ def test_partitioned_failure_is_collective(kind):
 
 @pytest.mark.slow
 @pytest.mark.parametrize("nparts", [2, 8])
-def test_cfg4_partitions_bit_identical(nparts):
+@pytest.mark.parametrize("halo", HALOS)
+def test_cfg4_partitions_bit_identical(nparts, halo):
     """cfg4 (1M-element H8, the benchmark workload) at 200 steps: 2 and 8 partitions
     (multi-chunk boundary ordering, 128-element chunks on both sides of each cut)
     bit-identical to one partition."""
@@ -165,6 +179,6 @@ def test_cfg4_partitions_bit_identical(nparts):
     one.step(200)
     a = one.state()
     one.close()
-    grp = PartitionGroup(p, nparts)
+    grp = PartitionGroup(p, nparts, halo_transport=halo)
     grp.step(200)
     assert_same(a, grp.state())

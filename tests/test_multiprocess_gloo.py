@@ -9,6 +9,15 @@ ncclSend/ncclRecv on the GPU), and assembles every local node through its gather
 list (local slots + receive area) in canonical order.  The per-node sums must be
 bit-identical to the single-rank assembly: the precondition for results at P GPUs
 to equal 1 GPU.
+
+transport "peer" plays the peer-memory halo instead (engine.cu peer_attach, kernels.cuh
+peer_send): the ranks all-gather their descriptors (neighbour list, receive segment
+offsets — what tvegpu_peer_export publishes besides the IPC handles), each rank derives
+for every send-list entry the destination index in the neighbour's receive area by the
+same rule as peer_attach (recv_off'[j'] + position in the segment), and "stores" its
+contributions there (here: (index, value) pairs over gloo, scattered by the receiver).
+Every receive slot must be written exactly once and the node sums must again be
+bit-identical to one rank.
 """
 import os
 import socket
@@ -25,7 +34,19 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, result_q):
+def _peer_destinations(pl, descs, rank):
+    """engine.cu peer_attach: per neighbour j, the receive-area index of each send entry."""
+    out = []
+    for j, r in enumerate(pl["neighbors"]):
+        d = descs[int(r)]
+        jj = list(d["neighbors"]).index(rank)
+        a, b = int(pl["send_offsets"][j]), int(pl["send_offsets"][j + 1])
+        assert d["recv_offsets"][jj + 1] - d["recv_offsets"][jj] == b - a, "halo size"
+        out.append(np.arange(b - a, dtype=np.int64) + int(d["recv_offsets"][jj]))
+    return out
+
+
+def _worker(rank, world, port, result_q, transport="sendrecv"):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -47,23 +68,50 @@ def _worker(rank, world, port, result_q):
         fm = d["forces"].reshape(-1, nn, 3)               # (E, nn, 3)
         pl = tg.plan(p, world, rank)
         El = pl["num_elements"]
+        if transport == "peer":
+            mine = {"neighbors": np.asarray(pl["neighbors"]), "recv_offsets": np.asarray(pl["recv_offsets"])}
+            descs = [None] * world
+            dist.all_gather_object(descs, mine)
+            dests = _peer_destinations(pl, descs, rank)
         for width, contrib in ((1, th[..., None]), (3, fm)):
             local = contrib[pl["element_orig"]].reshape(El * nn, width)
             sendbuf = local[pl["send_slots"]]
-            recv = np.zeros((int(pl["recv_offsets"][-1]), width))
-            reqs, bufs = [], []
-            for j, s in enumerate(pl["neighbors"]):
-                a, b = pl["send_offsets"][j], pl["send_offsets"][j + 1]
-                t = torch.from_numpy(np.ascontiguousarray(sendbuf[a:b]))
-                reqs.append(dist.isend(t, int(s)))
-                ra, rb = pl["recv_offsets"][j], pl["recv_offsets"][j + 1]
-                r = torch.zeros((int(rb - ra), width), dtype=torch.float64)
-                bufs.append((ra, rb, r))
-                reqs.append(dist.irecv(r, int(s)))
-            for q in reqs:
-                q.wait()
-            for ra, rb, r in bufs:
-                recv[ra:rb] = r.numpy()
+            nrecv = int(pl["recv_offsets"][-1])
+            recv = np.zeros((nrecv, width))
+            if transport == "peer":
+                # each sender "stores" at the indices it derived; the receiver only scatters
+                reqs, bufs = [], []
+                for j, s in enumerate(pl["neighbors"]):
+                    a, b = pl["send_offsets"][j], pl["send_offsets"][j + 1]
+                    reqs.append(dist.isend(torch.from_numpy(dests[j]), int(s)))
+                    reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(sendbuf[a:b])), int(s)))
+                    n = int(pl["recv_offsets"][j + 1] - pl["recv_offsets"][j])
+                    ri, rv = torch.zeros(n, dtype=torch.int64), torch.zeros((n, width), dtype=torch.float64)
+                    bufs.append((ri, rv))
+                    reqs.append(dist.irecv(ri, int(s)))
+                    reqs.append(dist.irecv(rv, int(s)))
+                for q in reqs:
+                    q.wait()
+                hits = np.zeros(nrecv, np.int64)
+                for ri, rv in bufs:
+                    recv[ri.numpy()] = rv.numpy()
+                    np.add.at(hits, ri.numpy(), 1)
+                if not np.all(hits == 1):
+                    raise AssertionError(f"rank {rank}: receive slots written {hits.min()}..{hits.max()} times")
+            else:
+                reqs, bufs = [], []
+                for j, s in enumerate(pl["neighbors"]):
+                    a, b = pl["send_offsets"][j], pl["send_offsets"][j + 1]
+                    t = torch.from_numpy(np.ascontiguousarray(sendbuf[a:b]))
+                    reqs.append(dist.isend(t, int(s)))
+                    ra, rb = pl["recv_offsets"][j], pl["recv_offsets"][j + 1]
+                    r = torch.zeros((int(rb - ra), width), dtype=torch.float64)
+                    bufs.append((ra, rb, r))
+                    reqs.append(dist.irecv(r, int(s)))
+                for q in reqs:
+                    q.wait()
+                for ra, rb, r in bufs:
+                    recv[ra:rb] = r.numpy()
             slots = np.concatenate([local, recv])
             off, idx = pl["csr_offsets"], pl["csr_slots"]
             sums = np.zeros((pl["num_nodes"], width))
@@ -91,12 +139,13 @@ def _worker(rank, world, port, result_q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("transport", ["sendrecv", "peer"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_halo_protocol_gloo(world):
+def test_halo_protocol_gloo(world, transport):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, transport)) for r in range(world)]
     for pr in procs:
         pr.start()
     results = [q.get(timeout=300) for _ in range(world)]
