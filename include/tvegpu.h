@@ -386,6 +386,10 @@ tvegpu_status tvegpu_peer_export(tvegpu_engine* h, void* blob, size_t cap, size_
 tvegpu_status tvegpu_peer_attach(tvegpu_engine* h, const void* const* blobs, const size_t* lens, int32_t nranks);
 /* 1 if the engine steps with the peer-memory halo (attached, or a group part), else 0. */
 int32_t tvegpu_halo_peer(const tvegpu_engine* h);
+/* Back to the NCCL halo (unmaps the neighbours).  Collective in effect: every rank must
+ * step with the same transport, so callers agree first (e.g. all-reduce the attach status
+ * and detach everywhere if any rank failed to attach). */
+tvegpu_status tvegpu_peer_detach(tvegpu_engine* h);
 
 /* ---------------------------------------------------------------------------
  * Partition group: nparts RCB partitions of one problem stepped together on ONE

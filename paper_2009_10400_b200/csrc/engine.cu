@@ -2752,6 +2752,25 @@ tvegpu_status tvegpu_peer_attach(tvegpu_engine* h, const void* const* blobs, con
 
 int32_t tvegpu_halo_peer(const tvegpu_engine* h) { return h && h->peer ? 1 : 0; }
 
+tvegpu_status tvegpu_peer_detach(tvegpu_engine* h) {
+    if (!h) return TVEGPU_E_ARG;
+    return guard(h, [&] {
+        if (h->pending) {
+            const tvegpu_status st = sync_and_check(h->solo);
+            if (st != TVEGPU_OK) return st;
+        }
+        CU(cudaStreamSynchronize(h->s));
+        for (auto& kv : h->solo.graphs) CU(cudaGraphExecDestroy(kv.second));  // captured with the peer path
+        h->solo.graphs.clear();
+        for (void* p : h->ipc_open) CU(cudaIpcCloseMemHandle(p));
+        h->ipc_open.clear();
+        h->peer = false;
+        h->prm.npeers = 0;
+        h->prm.ack = 0;
+        return TVEGPU_OK;
+    });
+}
+
 void* tvegpu_stream(tvegpu_engine* h) { return h ? (void*)h->s : nullptr; }
 
 tvegpu_status tvegpu_halo_info(const tvegpu_engine* h, int32_t* neighbors, int64_t* send_bytes, int64_t* recv_bytes) {

@@ -128,6 +128,7 @@ EXPORTS = {
     "tvegpu_peer_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "tvegpu_peer_attach": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.c_int32]),
     "tvegpu_halo_peer": (C.c_int32, [C.c_void_p]),
+    "tvegpu_peer_detach": (C.c_int, [C.c_void_p]),
     "tvegpu_stream": (C.c_void_p, [C.c_void_p]),
     "tvegpu_kernels_per_step": (C.c_int32, [C.c_void_p]),
     "tvegpu_halo_info": (C.c_int, [C.c_void_p, _ip, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
@@ -710,6 +711,12 @@ class Engine:
         ptrs = (C.c_void_p * len(bufs))(*[C.cast(b, C.c_void_p) for b in bufs])
         lens = (C.c_size_t * len(bufs))(*[len(b) for b in blobs])
         rc = lib().tvegpu_peer_attach(self._h, ptrs, lens, len(bufs))
+        if rc:
+            self._raise(rc)
+
+    def peer_detach(self):
+        """Back to the NCCL halo (every rank must use the same transport)."""
+        rc = lib().tvegpu_peer_detach(self._h)
         if rc:
             self._raise(rc)
 

@@ -5,7 +5,7 @@ set -u
 mkdir -p gpurun_out
 TAG=${TAG:-r1}
 nvidia-smi > gpurun_out/nvidia_smi.txt 2>&1
-timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_all.log 2>&1; echo "pytest all rc=$?" >> gpurun_out/summary.txt
+timeout 2400 python -m pytest tests -m gpu -q -s -rs --durations=25 > gpurun_out/pytest_gpu_all.log 2>&1; echo "pytest all rc=$?" >> gpurun_out/summary.txt
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/summary.txt
 timeout 900 python bench.py > gpurun_out/bench_${TAG}.log 2>&1; echo "bench rc=$?" >> gpurun_out/summary.txt
 timeout 900 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/bench_ref_${TAG}.log 2>&1; echo "bench ref rc=$?" >> gpurun_out/summary.txt
