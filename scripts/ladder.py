@@ -88,7 +88,7 @@ def main():
                 torch.cuda.empty_cache()
             rows.append(row)
             print(json.dumps(row), flush=True)
-    out = {"rows": rows, "slopes": {}}
+    out = {"rows": rows, "slopes": {}, "steps": args.steps, "warmup": args.warmup}
     for kname in args.kinds.split(","):
         r = [x for x in rows if x["kind"] == kname]
         for mname in MODES:

@@ -7,7 +7,8 @@ d = json.load(open(sys.argv[1]))
 tag = sys.argv[2] if len(sys.argv) > 2 else "r1"
 modes = ["TherMechTI", "TherMechExpanTI", "TherMechExpanTD"]
 print(f"# Size ladder {tag} — one B200 (scripts/ladder.py)\n")
-print("Per-step time [ms] (CUDA events, graph-replayed, 200 steps after 20 warm-up) of the three coupled "
+print(f"Per-step time [ms] (CUDA events, graph-replayed, {d.get('steps', 200)} steps after {d.get('warmup', 20)} "
+      "warm-up) of the three coupled "
       "modes on structured cubes; setup = `tvegpu_create` wall time (plan + upload). Reference API: "
       "`run_bench` / `bench_scaling_slope` (engine.hpp:145-162), SPEC.md criterion 9.\n")
 print("| kind | n | elements | nodes | " + " | ".join(modes) +
