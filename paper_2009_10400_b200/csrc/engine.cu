@@ -534,6 +534,13 @@ void peer_attach(tvegpu_engine* h, const std::vector<PeerDesc>& by_rank) {
     CU(cudaStreamSynchronize(s));
     h->prm.npeers = np;
     h->prm.ack = h->mode == TVEGPU_COUPLED ? 0 : 1;
+    {
+        const char* t = std::getenv("TVEGPU_HALO_TIMEOUT_MS");
+        const double ms = t ? std::atof(t) : 20000.0;
+        h->prm.halo_timeout_ns = (unsigned long long)(std::max(1.0, ms) * 1e6);
+        const char* d = std::getenv("TVEGPU_HALO_DROP_RANK");  // fault injection (tests)
+        h->prm.drop_signal = (d && std::atoi(d) == pl.rank) ? 1 : 0;
+    }
     h->peer = true;
 }
 
@@ -1001,8 +1008,7 @@ tvegpu_status sync_and_check(Stepper& S, bool status_enqueued = false) {
     if (wh != ~0ULL) {  // a peer-memory halo wait timed out: no verdict on the physics is possible
         char buf[200];
         std::snprintf(buf, sizeof buf,
-                      "halo exchange: a neighbouring partition's contributions did not arrive within 20 s at step %llu",
-                      wh);
+                      "halo exchange: a neighbouring partition's contributions did not arrive in time (step %llu)", wh);
         for (tvegpu_engine* h : S.parts) {
             h->halted = true;
             h->err_step = (long long)wh;

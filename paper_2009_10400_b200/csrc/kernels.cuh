@@ -85,6 +85,8 @@ struct DevParams {
     int motion;           // MechBCs::motion_override active (host-evaluated pins, K4 reads motion_row/val)
     int npeers;           // peer-memory halo (nranks > 1): neighbours whose inbox flags the node kernels wait for
     int ack;              // ... single-physics mode: SEND kernels also wait for the neighbours' end-of-step acks
+    int drop_signal;      // fault injection (TVEGPU_HALO_DROP_RANK): this partition's SEND kernels raise no flags
+    unsigned long long halo_timeout_ns;  // bound of every peer-memory wait (TVEGPU_HALO_TIMEOUT_MS, default 20 s)
     int es;               // row stride of the per-element SoA arrays (geo, theta, fiber, axes): >= E + 1, 16-aligned
     int xstride;          // doubles per chunk in chunk_x (3 * even max_chunk_nodes)
     double dt, mu, kappa, eta_a, kh, rho, wbcb, Ta, Qm, gamma;
@@ -643,7 +645,7 @@ __device__ __forceinline__ void peer_wait_ack(const DevParams& P, const DevPtrs&
         const unsigned long long t0 = globaltimer_ns();
         for (int j = 0; j < P.npeers; ++j)
             while (ld_acquire_sys(D.ack_inbox + j) < ep) {
-                if (globaltimer_ns() - t0 > 20000000000ull) {
+                if (globaltimer_ns() - t0 > P.halo_timeout_ns) {
                     atomicMin(D.err_halo, (unsigned long long)D.clock->step);
                     break;
                 }
@@ -663,11 +665,12 @@ __device__ __forceinline__ void peer_signal(const DevParams& P, const DevPtrs& D
     D.send_cnt[phase] = 0;
     __threadfence_system();
     const unsigned long long seq = 2 * *D.epoch + 1 + phase;
+    if (P.drop_signal) return;
     for (int j = 0; j < P.npeers; ++j) st_release_sys(D.peer_flag[j], seq);
 }
 // start of a node kernel of a partitioned step: this phase's contributions from every
-// neighbour have landed.  Bounded: after 20 s the wait gives up and records the step in
-// err_halo (the call's verdict reports it, collectively) instead of hanging the device.
+// neighbour have landed.  Bounded: after P.halo_timeout_ns the wait gives up and records
+// the step in err_halo (the call's verdict reports it, collectively) instead of hanging.
 __device__ __forceinline__ void peer_wait(const DevParams& P, const DevPtrs& D, int phase) {
     if (P.npeers == 0) return;
     if (threadIdx.x == 0) {
@@ -675,7 +678,7 @@ __device__ __forceinline__ void peer_wait(const DevParams& P, const DevPtrs& D, 
         const unsigned long long t0 = globaltimer_ns();
         for (int j = 0; j < P.npeers; ++j)
             while (ld_acquire_sys(D.inbox + j) < seq) {
-                if (globaltimer_ns() - t0 > 20000000000ull) {
+                if (globaltimer_ns() - t0 > P.halo_timeout_ns) {
                     atomicMin(D.err_halo, (unsigned long long)D.clock->step);
                     break;
                 }

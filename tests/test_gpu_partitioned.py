@@ -182,3 +182,23 @@ def test_cfg4_partitions_bit_identical(nparts, halo):
     grp = PartitionGroup(p, nparts, halo_transport=halo)
     grp.step(200)
     assert_same(a, grp.state())
+
+
+def test_peer_halo_timeout_is_reported_not_hung():
+    """Fault injection: partition 1 of 3 never raises its halo flags (TVEGPU_HALO_DROP_RANK).
+    Its neighbours' node kernels give up after TVEGPU_HALO_TIMEOUT_MS instead of spinning
+    forever, and every partition reports the same halo error; the state is then invalid
+    until reset.  (On one device the waiting kernels are launched after the silent sender
+    finished, so nothing ever waits on a kernel that is not running.)"""
+    import os
+    p = configs.small_problem(kind=H8, n=6, steps=10)
+    os.environ["TVEGPU_HALO_DROP_RANK"] = "1"
+    os.environ["TVEGPU_HALO_TIMEOUT_MS"] = "50"
+    try:
+        grp = PartitionGroup(p, 3, steps_per_graph=4)
+    finally:
+        del os.environ["TVEGPU_HALO_DROP_RANK"], os.environ["TVEGPU_HALO_TIMEOUT_MS"]
+    with pytest.raises(tg.NcclError, match="halo exchange"):
+        grp.step(2)
+    with pytest.raises(tg.TveError):
+        grp.state()
