@@ -433,6 +433,12 @@ void* tvegpu_stream(tvegpu_engine* h);
 /* Halo exchange volume of one partition (nranks > 1): neighbours, and bytes sent /
  * received per step (every contribution of a shared node, both coupled phases). */
 tvegpu_status tvegpu_halo_info(const tvegpu_engine* h, int32_t* neighbors, int64_t* send_bytes, int64_t* recv_bytes);
+/* One partition of a P-GPU run stepped ALONE on this device, to time a rank's work
+ * without the other GPUs: create it with nranks = P, rank = r, nccl_unique_id = NULL and
+ * halo_transport = TVEGPU_HALO_PEER, then call this.  Its halo stores go to a scratch
+ * buffer and its waits pass at once, so its numbers are meaningless; its step time is
+ * the rank's step minus the NVLink transfer (scripts/partition_solo.py). */
+tvegpu_status tvegpu_peer_attach_solo(tvegpu_engine* h);
 /* Kernel launches per step (per coupled phase: element + node kernel; partitioned:
  * boundary + interior element launches, plus the halo pack with the NCCL transport). */
 int32_t tvegpu_kernels_per_step(const tvegpu_engine* h);

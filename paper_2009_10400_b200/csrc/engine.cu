@@ -457,6 +457,16 @@ struct LoopbackTransport final : Transport {
     }
 };
 
+// One partition stepped alone (tvegpu_peer_attach_solo: a measurement hook): no peers,
+// no collective — the partition's own error words are the verdict.
+struct SoloTransport final : Transport {
+    void exchange(const std::vector<tvegpu_engine*>&, bool, cudaEvent_t) override {
+        throw Error(TVEGPU_E_ARG, "partition without NCCL: attach the peer-memory halo first");
+    }
+    void allreduce_u64(const std::vector<tvegpu_engine*>&, const std::vector<unsigned long long*>&, size_t,
+                       bool) override {}
+};
+
 // ---------------------------------------------------------------- peer-memory halo setup
 // What a partition publishes to its neighbours: where its receive areas and inbox are
 // (pointers valid in the attaching process) and its receive segments per neighbour.
@@ -534,6 +544,21 @@ void peer_attach(tvegpu_engine* h, const std::vector<PeerDesc>& by_rank) {
     CU(cudaStreamSynchronize(s));
     h->prm.npeers = np;
     h->prm.ack = h->mode == TVEGPU_COUPLED ? 0 : 1;
+    h->prm.nb_chunks = pl.nchunks_boundary;
+    {  // nodes that gather received contributions: boundary elements' nodes, numbered first
+        const int32_t local = pl.E * pl.nn;
+        int hi = 0;
+#pragma omp parallel for schedule(static) reduction(max : hi)
+        for (int i = 0; i < pl.N; ++i)
+            for (int k = pl.csr_off[i]; k < pl.csr_off[i + 1]; ++k)
+                if (pl.csr_slot[k] >= local) hi = std::max(hi, i + 1);
+        h->prm.halo_hi = hi;
+    }
+    // programmatic dependent launch between the step kernels, as for one partition: every
+    // peer-path kernel waits for its predecessor grid before touching its outputs
+    h->pdl = !std::getenv("TVEGPU_NO_PDL");
+    for (auto& kv : h->solo.graphs) CU(cudaGraphExecDestroy(kv.second));
+    h->solo.graphs.clear();
     {
         const char* t = std::getenv("TVEGPU_HALO_TIMEOUT_MS");
         const double ms = t ? std::atof(t) : 20000.0;
@@ -601,31 +626,27 @@ NodeKernel thermal_node_kernel(const tvegpu_engine* h) {
 }
 
 // Element kernels run one CTA per 128-element chunk over chunk range [c0, c1).
-// SEND: the boundary chunks of a peer-memory partitioned step (kernels.cuh peer_send).
-template <int NN, bool SEND>
+template <int NN>
 void launch_mech_element(tvegpu_engine* h, int c0, int c1) {
     if (c1 <= c0) return;
     const size_t sm = k3_smem(h);
     switch (h->prm.exp_kind < 0 ? 0 : (h->prm.exp_kind == 0 ? 1 : 2)) {
-        case 0: launch_step_kernel(h, k_mech_element<NN, 0, SEND>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
-        case 1: launch_step_kernel(h, k_mech_element<NN, 1, SEND>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
-        default: launch_step_kernel(h, k_mech_element<NN, 2, SEND>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
+        case 0: launch_step_kernel(h, k_mech_element<NN, 0>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
+        case 1: launch_step_kernel(h, k_mech_element<NN, 1>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
+        default: launch_step_kernel(h, k_mech_element<NN, 2>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
     }
 }
 
-template <int NN, bool SEND>
+template <int NN>
 void launch_thermal_element(tvegpu_engine* h, int c0, int c1) {
     if (c1 <= c0) return;
-    launch_step_kernel(h, k_thermal_element<NN, SEND>, c1 - c0, kChunkThreads, k1_smem(h), h->prm, h->ptr, h->cur, c0,
-                       c1);
+    launch_step_kernel(h, k_thermal_element<NN>, c1 - c0, kChunkThreads, k1_smem(h), h->prm, h->ptr, h->cur, c0, c1);
 }
-void launch_thermal_elements(tvegpu_engine* h, int c0, int c1, bool send = false) {
-    if (send) h->nn == 4 ? launch_thermal_element<4, true>(h, c0, c1) : launch_thermal_element<8, true>(h, c0, c1);
-    else h->nn == 4 ? launch_thermal_element<4, false>(h, c0, c1) : launch_thermal_element<8, false>(h, c0, c1);
+void launch_thermal_elements(tvegpu_engine* h, int c0, int c1) {
+    h->nn == 4 ? launch_thermal_element<4>(h, c0, c1) : launch_thermal_element<8>(h, c0, c1);
 }
-void launch_mech_elements(tvegpu_engine* h, int c0, int c1, bool send = false) {
-    if (send) h->nn == 4 ? launch_mech_element<4, true>(h, c0, c1) : launch_mech_element<8, true>(h, c0, c1);
-    else h->nn == 4 ? launch_mech_element<4, false>(h, c0, c1) : launch_mech_element<8, false>(h, c0, c1);
+void launch_mech_elements(tvegpu_engine* h, int c0, int c1) {
+    h->nn == 4 ? launch_mech_element<4>(h, c0, c1) : launch_mech_element<8>(h, c0, c1);
 }
 void launch_thermal_node(tvegpu_engine* h, double* t_out) {
     const int N = h->plan.N;
@@ -645,22 +666,14 @@ void launch_mech_node(tvegpu_engine* h, double* u_out, int n0 = 0, int n1 = -1, 
 
 template <class F>
 void for_each_element_kernel(F&& f) {
-    f((const void*)k_thermal_element<4, false>);
-    f((const void*)k_thermal_element<8, false>);
-    f((const void*)k_thermal_element<4, true>);
-    f((const void*)k_thermal_element<8, true>);
-    f((const void*)k_mech_element<4, 0, false>);
-    f((const void*)k_mech_element<4, 1, false>);
-    f((const void*)k_mech_element<4, 2, false>);
-    f((const void*)k_mech_element<8, 0, false>);
-    f((const void*)k_mech_element<8, 1, false>);
-    f((const void*)k_mech_element<8, 2, false>);
-    f((const void*)k_mech_element<4, 0, true>);
-    f((const void*)k_mech_element<4, 1, true>);
-    f((const void*)k_mech_element<4, 2, true>);
-    f((const void*)k_mech_element<8, 0, true>);
-    f((const void*)k_mech_element<8, 1, true>);
-    f((const void*)k_mech_element<8, 2, true>);
+    f((const void*)k_thermal_element<4>);
+    f((const void*)k_thermal_element<8>);
+    f((const void*)k_mech_element<4, 0>);
+    f((const void*)k_mech_element<4, 1>);
+    f((const void*)k_mech_element<4, 2>);
+    f((const void*)k_mech_element<8, 0>);
+    f((const void*)k_mech_element<8, 1>);
+    f((const void*)k_mech_element<8, 2>);
 }
 
 void set_smem_limits(tvegpu_engine* h) {
@@ -731,15 +744,15 @@ void enqueue_one_step(tvegpu_engine* h, cudaEvent_t* evs = nullptr, cudaEvent_t 
     CU(cudaGetLastError());
 }
 
-// Peer-memory form (every part attached, peer_attach): per phase the boundary chunks
-// as a SEND launch (element math + stores into the neighbours' receive areas + flags),
-// the interior chunks, then the node kernel, which waits for the neighbours' flags on
-// the device.  No pack kernel, no comm stream, no NCCL call.  Parts sharing one device
-// (a group) additionally order each node kernel after its neighbours' SEND launches
+// Peer-memory form (every part attached, peer_attach): per phase one launch of the
+// element kernel — the boundary chunks first (element math + stores into the neighbours'
+// receive areas + flags), then the interior chunks — and the node kernel, whose blocks
+// holding interface nodes wait for the neighbours' flags on the device.  No pack kernel, no comm stream, no NCCL call.  Parts sharing one device
+// (a group) additionally order each node kernel after its neighbours' element launches
 // with events, so a waiting kernel never occupies the SMs a sender still needs; in
-// single-physics steps (no other phase in between) each SEND launch also follows its
+// single-physics steps (no other phase in between) each element launch also follows its
 // neighbours' previous node kernels (DevParams::ack; a group: events as well).
-// xev (profiling, one-part sets): per phase a (start, end) pair around the SEND launch.
+// xev (profiling, one-part sets): zero-length (start, end) pairs: the transfer is in-kernel.
 void enqueue_peer_step(Stepper& S, cudaEvent_t* evs, cudaEvent_t* xev) {
     const std::vector<tvegpu_engine*>& parts = S.parts;
     tvegpu_engine* h0 = parts[0];
@@ -750,13 +763,14 @@ void enqueue_peer_step(Stepper& S, cudaEvent_t* evs, cudaEvent_t* xev) {
     };
     auto phase = [&](bool mech, cudaEvent_t* x) {
         for (tvegpu_engine* h : parts) {
-            const int nb = h->plan.nchunks_boundary, nc = (int)h->plan.chunk_start.size() - 1;
-            auto elements = mech ? launch_mech_elements : launch_thermal_elements;
-            if (x && h == h0) CU(cudaEventRecord(x[0], h->s));
-            elements(h, 0, nb, true);
-            if (x && h == h0) CU(cudaEventRecord(x[1], h->s));
+            const int nc = (int)h->plan.chunk_start.size() - 1;
+            // one launch: the boundary chunks first (they forward + signal), then the interior
+            (mech ? launch_mech_elements : launch_thermal_elements)(h, 0, nc);
+            if (x && h == h0) {  // the transfer is inside the element kernel: nothing separate to time
+                CU(cudaEventRecord(x[0], h->s));
+                CU(cudaEventRecord(x[1], h->s));
+            }
             if (shared_device) CU(cudaEventRecord(h->ev_pack, h->s));
-            elements(h, nb, nc, false);
         }
         mark();
         for (tvegpu_engine* h : parts) {
@@ -769,7 +783,7 @@ void enqueue_peer_step(Stepper& S, cudaEvent_t* evs, cudaEvent_t* xev) {
                 launch_thermal_node(h, nullptr);
             }
         }
-        if (shared_device && h0->prm.ack) {  // single physics: next SEND after the neighbours' node kernels
+        if (shared_device && h0->prm.ack) {  // single physics: next element launch after the neighbours' node kernels
             for (tvegpu_engine* h : parts) CU(cudaEventRecord(h->ev_comm, h->s));
             for (tvegpu_engine* h : parts)
                 for (int r : h->plan.neighbors) CU(cudaStreamWaitEvent(h->s, parts.at(r)->ev_comm, 0));
@@ -1495,8 +1509,13 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     }
     // ---- multi-GPU halo
     if (nranks > 1) {
-        if (!loopback) {  // one partition per process and GPU: the NCCL transport
-            if (!o.nccl_unique_id) throw Error(TVEGPU_E_ARG, "nranks > 1 needs options.nccl_unique_id");
+        if (!loopback && !o.nccl_unique_id) {  // only for tvegpu_peer_attach_solo (measurement hook)
+            if (o.halo_transport != TVEGPU_HALO_PEER)
+                throw Error(TVEGPU_E_ARG, "nranks > 1 needs options.nccl_unique_id");
+            auto t = std::make_unique<SoloTransport>();
+            h->tx = t.get();
+            h->own_tx = std::move(t);
+        } else if (!loopback) {  // one partition per process and GPU: the NCCL transport
             ncclUniqueId id;
             std::memcpy(&id, o.nccl_unique_id, sizeof id);
             NC(nccl().CommInitRank(&h->comm, nranks, id, o.rank));
@@ -2758,6 +2777,37 @@ tvegpu_status tvegpu_peer_attach(tvegpu_engine* h, const void* const* blobs, con
 
 int32_t tvegpu_halo_peer(const tvegpu_engine* h) { return h && h->peer ? 1 : 0; }
 
+tvegpu_status tvegpu_peer_attach_solo(tvegpu_engine* h) {
+    if (!h) return TVEGPU_E_ARG;
+    return guard(h, [&] {
+        const RankPlan& pl = h->plan;
+        if (pl.nranks < 2 || h->peer) throw Error(TVEGPU_E_ARG, "tvegpu_peer_attach_solo: unattached partition expected");
+        if (!dynamic_cast<SoloTransport*>(h->tx))
+            throw Error(TVEGPU_E_ARG, "tvegpu_peer_attach_solo: create the partition without an NCCL id");
+        // every neighbour is a scratch area on this device; the partition's own waits pass at once
+        int32_t most = 1;
+        for (size_t j = 0; j + 1 < pl.send_off.size(); ++j) most = std::max(most, pl.send_off[j + 1] - pl.send_off[j]);
+        double* sth = dalloc<double>(h->owned, most);
+        double* sm = dalloc<double>(h->owned, (size_t)kMW * most);
+        unsigned long long* sin = dalloc<unsigned long long>(h->owned, 2);
+        std::vector<PeerDesc> by_rank(pl.nranks);
+        for (size_t j = 0; j < pl.neighbors.size(); ++j) {
+            PeerDesc& d = by_rank[pl.neighbors[j]];
+            d.rank = pl.neighbors[j];
+            d.th = sth;
+            d.m = sm;
+            d.inbox = sin;
+            d.nbr = {pl.rank};
+            d.recv_off = {0, pl.send_off[j + 1] - pl.send_off[j]};
+        }
+        peer_attach(h, by_rank);
+        if (std::getenv("TVEGPU_SOLO_NOFWD")) h->prm.nb_chunks = 0;  // (measurement: the ordering alone)
+        CU(cudaMemsetAsync(h->ptr.inbox, 0xff, 2 * std::max<size_t>(1, pl.neighbors.size()) * 8, h->s));
+        CU(cudaStreamSynchronize(h->s));
+        return TVEGPU_OK;
+    });
+}
+
 tvegpu_status tvegpu_peer_detach(tvegpu_engine* h) {
     if (!h) return TVEGPU_E_ARG;
     return guard(h, [&] {
@@ -2773,6 +2823,8 @@ tvegpu_status tvegpu_peer_detach(tvegpu_engine* h) {
         h->peer = false;
         h->prm.npeers = 0;
         h->prm.ack = 0;
+        h->prm.nb_chunks = 0;
+        h->pdl = false;  // the NCCL path's pack kernel is not PDL-aware
         return TVEGPU_OK;
     });
 }
@@ -2797,7 +2849,7 @@ int32_t tvegpu_kernels_per_step(const tvegpu_engine* h) {
     const bool multi = h->plan.nranks > 1;
     // per phase: element kernel + node kernel; partitioned: boundary and interior element
     // launches, plus the halo pack with the NCCL transport (peer memory: none)
-    const int per = multi ? (h->peer ? 3 : 4) : 2;
+    const int per = multi ? (h->peer ? 2 : 4) : 2;
     int k = 0;
     if (h->mode != TVEGPU_MECHANICAL_ONLY) k += per;
     if (h->mode != TVEGPU_THERMAL_ONLY) k += per;

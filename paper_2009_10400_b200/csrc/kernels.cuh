@@ -84,8 +84,8 @@ struct DevParams {
     int ell;              // G > 0: ELL gathers with rows of 8 G slot ids (every node has <= 8 G contributions)
     int motion;           // MechBCs::motion_override active (host-evaluated pins, K4 reads motion_row/val)
     int npeers;           // peer-memory halo (nranks > 1): neighbours whose inbox flags the node kernels wait for
-    int ack;              // ... single-physics mode: SEND kernels also wait for the neighbours' end-of-step acks
-    int drop_signal;      // fault injection (TVEGPU_HALO_DROP_RANK): this partition's SEND kernels raise no flags
+    int ack;              // ... single-physics mode: element kernels' boundary chunks also wait for the neighbours' end-of-step acks
+    int drop_signal;      // fault injection (TVEGPU_HALO_DROP_RANK): this partition's boundary chunks raise no flags
     unsigned long long halo_timeout_ns;  // bound of every peer-memory wait (TVEGPU_HALO_TIMEOUT_MS, default 20 s)
     int es;               // row stride of the per-element SoA arrays (geo, theta, fiber, axes): >= E + 1, 16-aligned
     int xstride;          // doubles per chunk in chunk_x (3 * even max_chunk_nodes)
@@ -102,6 +102,8 @@ struct DevParams {
     // offsets into DevPtrs::tabs (every table and all Prony coefficients, any length); the
     // kernels read them from there only when c_len / k_len > kMaxTable or P > kMaxProny
     int tab_cT, tab_cV, tab_kT, tab_kK, tab_pa, tab_pb;
+    int nb_chunks;        // boundary chunks [0, nb_chunks): the element-kernel CTAs that forward and signal (0: no peers)
+    int halo_hi;          // local nodes [0, halo_hi) hold every node that gathers received contributions
 };
 
 struct DevPtrs {
@@ -146,7 +148,7 @@ struct DevPtrs {
     const int32_t* motion_row;  // [N] row of motion_val for override candidates, else -1 (motion only)
     const double4* motion_val;  // [rows] (x, y, z, pinned) of this step's motion_override(node, t + dt)
     const double* tabs;         // c(T), k(T) tables and Prony coefficients (DevParams::tab_*)
-    // peer-memory halo (nranks > 1, DevParams::npeers > 0): see peer_send / peer_signal / peer_wait
+    // peer-memory halo (nranks > 1, DevParams::npeers > 0): see peer_forward / peer_signal / peer_wait
     const int32_t* pd_off;                 // [Eb nn + 1] per boundary slot (e nn + a) its destinations
     const uint32_t* pd_ent;                // (neighbour << 26) | index in that neighbour's receive area
     double* const* peer_th;                // [npeers] the neighbours' thermal receive areas
@@ -601,9 +603,9 @@ __device__ __forceinline__ void check_gather(const DevParams& P, const DevPtrs& 
 }
 
 // ------------------------------------------------------------------ peer-memory halo
-// In a partitioned step the boundary chunks run as their own launch of the element kernel
-// with SEND: every contribution another partition gathers is stored by the thread that
-// computed it straight into that partition's receive area — NVLink peer memory of the
+// In a partitioned step the boundary chunks of the element kernel forward every
+// contribution another partition gathers, right after computing it, straight into that
+// partition's receive area — NVLink peer memory of the
 // other GPU (CUDA IPC mapping), or another partition's buffer in a group — so the
 // element math and the halo transfer are one kernel (no pack kernel, no NCCL call).
 // When the launch's last CTA is done it raises flag = 2 epoch + 1 + phase in each
@@ -625,21 +627,34 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-// contribution (e, a) of a boundary element (W doubles) to every partition that gathers it
-template <int W>
-__device__ __forceinline__ void peer_send(const DevPtrs& D, int slot, const double* v) {
-    const int k0 = __ldg(D.pd_off + slot), k1 = __ldg(D.pd_off + slot + 1);
-    for (int k = k0; k < k1; ++k) {
-        const uint32_t en = __ldg(D.pd_ent + k);
-        double* b = (W == 1 ? D.peer_th : D.peer_m)[en >> 26] + (size_t)(en & 0x3ffffffu) * W;
+// the contributions (e, a) of a boundary element (W doubles each) to every partition that
+// gathers them: read back from the thread's own slot stores (program order) and stored into
+// the neighbours' receive areas.  Forwarding the stored bits, instead of sending from the
+// element math, keeps that math — and its FMA contraction — identical to the kernel every
+// other element and every single-GPU run uses: bit-identity across partitions needs it.
+template <int NN, int W>
+__device__ __forceinline__ void peer_forward(const DevPtrs& D, const double* slots, int e) {
+#pragma unroll 1
+    for (int a = 0; a < NN; ++a) {
+        const int slot = e * NN + a;
+        const int k0 = __ldg(D.pd_off + slot), k1 = __ldg(D.pd_off + slot + 1);
+        if (k0 == k1) continue;
+        double v[W];
 #pragma unroll
-        for (int q = 0; q < W; ++q) b[q] = v[q];
+        for (int q = 0; q < W; ++q) v[q] = slots[(size_t)slot * W + q];  // coherent: written just above
+        for (int k = k0; k < k1; ++k) {
+            const uint32_t en = __ldg(D.pd_ent + k);
+            double* b = (W == 1 ? D.peer_th : D.peer_m)[en >> 26] + (size_t)(en & 0x3ffffffu) * W;
+#pragma unroll
+            for (int q = 0; q < W; ++q) b[q] = v[q];
+        }
     }
 }
-// start of a SEND launch in a single-physics partitioned step (DevParams::ack): the
+// start of a boundary CTA in a single-physics partitioned step (DevParams::ack): the
 // neighbours' node kernels of the previous step are done with the receive areas this
 // launch overwrites.  (In coupled steps the other phase's flags already imply it.)
 __device__ __forceinline__ void peer_wait_ack(const DevParams& P, const DevPtrs& D) {
+    pdl_wait();  // the epoch is bumped by the predecessor (the closing node kernel)
     if (threadIdx.x == 0) {
         const unsigned long long ep = *(volatile unsigned long long*)D.epoch;
         const unsigned long long t0 = globaltimer_ns();
@@ -654,14 +669,16 @@ __device__ __forceinline__ void peer_wait_ack(const DevParams& P, const DevPtrs&
     }
     __syncthreads();
 }
-// end of a SEND launch (every thread of every CTA; halted partitions still signal so their
-// neighbours never wait on them): the last CTA raises the phase flag in each neighbour's inbox
-__device__ __forceinline__ void peer_signal(const DevParams& P, const DevPtrs& D, int phase) {
-    __threadfence_system();  // this thread's peer stores before the CTA's arrival
-    __syncthreads();
+// end of a boundary CTA of an element kernel (every thread; halted partitions still signal so
+// their neighbours never wait on them): the last boundary CTA raises the phase flag in each
+// neighbour's inbox.  The interior chunks run in the same launch, after the boundary ones.
+__device__ __forceinline__ void peer_signal(const DevParams& P, const DevPtrs& D, int phase, int c) {
+    if (c >= P.nb_chunks) return;  // interior chunk of the launch (CTA-uniform)
+    __syncthreads();               // the CTA's peer stores happen before thread 0's release
     if (threadIdx.x != 0) return;
+    __threadfence_system();        // cumulative: orders them before the arrival and the flags
     const unsigned n = atomicAdd(D.send_cnt + phase, 1u);
-    if (n != gridDim.x - 1) return;
+    if (n != (unsigned)P.nb_chunks - 1) return;
     D.send_cnt[phase] = 0;
     __threadfence_system();
     const unsigned long long seq = 2 * *D.epoch + 1 + phase;
@@ -671,8 +688,8 @@ __device__ __forceinline__ void peer_signal(const DevParams& P, const DevPtrs& D
 // start of a node kernel of a partitioned step: this phase's contributions from every
 // neighbour have landed.  Bounded: after P.halo_timeout_ns the wait gives up and records
 // the step in err_halo (the call's verdict reports it, collectively) instead of hanging.
-__device__ __forceinline__ void peer_wait(const DevParams& P, const DevPtrs& D, int phase) {
-    if (P.npeers == 0) return;
+__device__ __forceinline__ void peer_wait(const DevParams& P, const DevPtrs& D, int phase, int first_node) {
+    if (P.npeers == 0 || first_node >= P.halo_hi) return;  // no received contributions in this block
     if (threadIdx.x == 0) {
         const unsigned long long seq = 2 * *(volatile unsigned long long*)D.epoch + 1 + phase;
         const unsigned long long t0 = globaltimer_ns();
@@ -695,7 +712,7 @@ __device__ __forceinline__ void peer_wait(const DevParams& P, const DevPtrs& D, 
 #define K1_BOUNDS __launch_bounds__(kChunkThreads)
 #endif
 // K1 element body: element e of the staged chunk S (n = its node slots)
-template <int NN, bool SEND>
+template <int NN>
 __device__ __forceinline__ void k1_body(const DevParams& P, const DevPtrs& D, const NodeStage& S,
                                         const ElemRows<kTmaK1>& rows, const CoordStage& xs, const int e,
                                         const int (&n)[NN]) {
@@ -745,20 +762,12 @@ __device__ __forceinline__ void k1_body(const DevParams& P, const DevPtrs& D, co
         const double f0 = -(r[0] + r[1] + r[2]);
         reinterpret_cast<double2*>(out)[0] = make_double2(f0, r[0]);
         reinterpret_cast<double2*>(out)[1] = make_double2(r[1], r[2]);
-        if constexpr (SEND) {
-            const double f[4] = {f0, r[0], r[1], r[2]};
-#pragma unroll
-            for (int a = 0; a < 4; ++a) peer_send<1>(D, e * NN + a, f + a);
-        }
     } else {
         double f[8];
 #pragma unroll
         for (int a = 0; a < 8; ++a) f[a] = h8s(a, 0) * r[0] + h8s(a, 1) * r[1] + h8s(a, 2) * r[2];
 #pragma unroll
         for (int a = 0; a < 8; a += 2) reinterpret_cast<double2*>(out)[a / 2] = make_double2(f[a], f[a + 1]);
-        if constexpr (SEND)
-#pragma unroll
-            for (int a = 0; a < 8; ++a) peer_send<1>(D, e * NN + a, f + a);
     }
     if (dF == 0.0) atomicMin(D.err_elem, pack_elem(D.clock->step, D.elem_orig[e]));
 }
@@ -767,8 +776,12 @@ __device__ __forceinline__ void k1_body(const DevParams& P, const DevPtrs& D, co
 template <int NN>
 __host__ __device__ __forceinline__ RowPlan k1_rows() { return RowPlan{k1_xstage<NN>() ? 0 : 10, 0, 0, 0}; }
 
-// SEND: the boundary chunks of a peer-memory partitioned step (peer_send / peer_signal)
-template <int NN, bool SEND = false>
+// One kernel for every path: with the peer-memory halo attached (P.npeers > 0) its
+// boundary chunks [0, P.nb_chunks) also forward their contributions and signal
+// (peer_forward / peer_signal).  A separate "send" kernel would be compiled separately,
+// and ptxas may contract its element math into FMAs differently: the partitions would
+// then no longer match one GPU bit for bit (measured: 1e-15 drifts on T4).
+template <int NN>
 __global__ void K1_BOUNDS k_thermal_element(const DevParams P, const DevPtrs D, int cur, int c0, int c1) {
     extern __shared__ __align__(128) unsigned char smem[];
     const RowPlan rp = k1_rows<NN>();
@@ -793,18 +806,14 @@ __global__ void K1_BOUNDS k_thermal_element(const DevParams P, const DevPtrs D, 
     int n[NN];
     const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c, P.stage_stride, S, n);
     wait_elem_rows<kTmaK1>(bar);  // every thread: the CTA must not retire with bulk copies in flight
-    if constexpr (SEND) {  // every thread reaches peer_signal, halted or not
-        if (P.ack) peer_wait_ack(P, D);
-        if (!D.clock->halted && e >= 0) {
-            check_chunk<NN>(P, D, c, e, n);
-            k1_body<NN, true>(P, D, S, ElemRows<kTmaK1>{rows, (int)threadIdx.x}, xs, e, n);
-        }
-        peer_signal(P, D, 0);
-        return;
+    const bool bnd = c < P.nb_chunks;  // a boundary chunk of a peer-memory partition (else false)
+    if (P.ack && bnd) peer_wait_ack(P, D);
+    if (!D.clock->halted && e >= 0) {  // halted: uniform across the grid (read after the wait)
+        check_chunk<NN>(P, D, c, e, n);
+        k1_body<NN>(P, D, S, ElemRows<kTmaK1>{rows, (int)threadIdx.x}, xs, e, n);
+        if (bnd) peer_forward<NN, 1>(D, D.slot_th, e);
     }
-    if (D.clock->halted || e < 0) return;  // halted: uniform across the grid (read after the wait)
-    check_chunk<NN>(P, D, c, e, n);
-    k1_body<NN, false>(P, D, S, ElemRows<kTmaK1>{rows, (int)threadIdx.x}, xs, e, n);
+    if (P.npeers) peer_signal(P, D, 0, c);  // every thread of a boundary CTA, halted or not
     pdl_trigger();  // after this block's work: the successor fills in behind the last wave
 }
 
@@ -981,7 +990,7 @@ __global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, i
         }
     }
     pdl_wait();
-    peer_wait(P, D, 0);
+    peer_wait(P, D, 0, PAIR ? (int)(blockIdx.x * blockDim.x) >> 1 : (int)(blockIdx.x * blockDim.x));
     const bool active = i < P.N && !D.clock->halted;  // the same for both threads of a pair
     double s = 0.0;
     if constexpr (PAIR) {
@@ -1027,7 +1036,7 @@ __global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, i
 #define TVEGPU_K3_MINBLOCKS_T4 5  // T4: 102 registers, 20 warps/SM (cfg5 T4 K3 -12 % vs 4)
 #endif
 // K3 element body: element e of the staged chunk st (n = its node slots)
-template <int NN, int EXP, bool SEND>
+template <int NN, int EXP>
 __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, const NodeStage& st,
                                         const ElemRows<kTmaK3>& rows, const RowPlan& rp, const CoordStage& xs,
                                         const int e, const int (&n)[NN]) {
@@ -1247,12 +1256,6 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
         st4(o + 0, make_double4(-(Q[0] + Q[1] + Q[2]), -(Q[3] + Q[4] + Q[5]), -(Q[6] + Q[7] + Q[8]), Q[0]));
         st4(o + 1, make_double4(Q[3], Q[6], Q[1], Q[4]));
         st4(o + 2, make_double4(Q[7], Q[2], Q[5], Q[8]));
-        if constexpr (SEND) {
-            const double f[4][3] = {{-(Q[0] + Q[1] + Q[2]), -(Q[3] + Q[4] + Q[5]), -(Q[6] + Q[7] + Q[8])},
-                                    {Q[0], Q[3], Q[6]}, {Q[1], Q[4], Q[7]}, {Q[2], Q[5], Q[8]}};
-#pragma unroll
-            for (int a = 0; a < 4; ++a) peer_send<3>(D, e * NN + a, f[a]);
-        }
     } else if constexpr (NN == 4) {
         st4(out + 0, make_double4(-(Q[0] + Q[1] + Q[2]), -(Q[3] + Q[4] + Q[5]), -(Q[6] + Q[7] + Q[8]), 0.0));
         st4(out + 1, make_double4(Q[0], Q[3], Q[6], 0.0));
@@ -1379,13 +1382,6 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
                 st4(out + a, make_double4(f[0], f[1], f[2], 0.0));
             }
         }
-        if constexpr (SEND)
-#pragma unroll
-            for (int a = 0; a < 8; ++a) {
-                double f[3];
-                corner(a, f);
-                peer_send<3>(D, e * NN + a, f);
-            }
     }
     if (P.diag) {
 #pragma unroll
@@ -1403,7 +1399,7 @@ __host__ __device__ __forceinline__ RowPlan k3_rows(const DevParams& P) {
                    (EXP == 2 && P.axes_per_elem) ? 6 : 0};
 }
 
-template <int NN, int EXP, bool SEND = false>
+template <int NN, int EXP>
 __global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T4 : TVEGPU_K3_MINBLOCKS)
     k_mech_element(const DevParams P, const DevPtrs D, int cur, int c0, int c1) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -1429,18 +1425,14 @@ __global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T
     int n[NN];
     const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c, P.stage_stride, st, n);
     wait_elem_rows<kTmaK3>(bar);  // every thread: the CTA must not retire with bulk copies in flight
-    if constexpr (SEND) {
-        if (P.ack) peer_wait_ack(P, D);
-        if (!D.clock->halted && e >= 0) {
-            check_chunk<NN>(P, D, c, e, n);
-            k3_body<NN, EXP, true>(P, D, st, ElemRows<kTmaK3>{rows, (int)threadIdx.x}, rp, xs, e, n);
-        }
-        peer_signal(P, D, 1);
-        return;
+    const bool bnd = c < P.nb_chunks;  // (see k_thermal_element)
+    if (P.ack && bnd) peer_wait_ack(P, D);
+    if (!D.clock->halted && e >= 0) {
+        check_chunk<NN>(P, D, c, e, n);
+        k3_body<NN, EXP>(P, D, st, ElemRows<kTmaK3>{rows, (int)threadIdx.x}, rp, xs, e, n);
+        if (bnd) peer_forward<NN, kMW>(D, D.slot_m, e);
     }
-    if (D.clock->halted || e < 0) return;
-    check_chunk<NN>(P, D, c, e, n);
-    k3_body<NN, EXP, false>(P, D, st, ElemRows<kTmaK3>{rows, (int)threadIdx.x}, rp, xs, e, n);
+    if (P.npeers) peer_signal(P, D, 1, c);
     pdl_trigger();
 }
 
@@ -1472,7 +1464,7 @@ __global__ void NODE_BOUNDS k_mech_node(const DevParams P, const DevPtrs D, int 
         msk = __ldg(D.mask + i);
     }
     pdl_wait();
-    peer_wait(P, D, 1);
+    peer_wait(P, D, 1, n0 + (PAIR ? (int)(blockIdx.x * blockDim.x) >> 1 : (int)(blockIdx.x * blockDim.x)));
     const bool active = i < n1 && !D.clock->halted;  // the same for both threads of a pair
     double f0 = 0.0, f1 = 0.0, f2 = 0.0;
     if constexpr (PAIR) {

@@ -129,6 +129,7 @@ EXPORTS = {
     "tvegpu_peer_attach": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.c_int32]),
     "tvegpu_halo_peer": (C.c_int32, [C.c_void_p]),
     "tvegpu_peer_detach": (C.c_int, [C.c_void_p]),
+    "tvegpu_peer_attach_solo": (C.c_int, [C.c_void_p]),
     "tvegpu_stream": (C.c_void_p, [C.c_void_p]),
     "tvegpu_kernels_per_step": (C.c_int32, [C.c_void_p]),
     "tvegpu_halo_info": (C.c_int, [C.c_void_p, _ip, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
@@ -711,6 +712,13 @@ class Engine:
         ptrs = (C.c_void_p * len(bufs))(*[C.cast(b, C.c_void_p) for b in bufs])
         lens = (C.c_size_t * len(bufs))(*[len(b) for b in blobs])
         rc = lib().tvegpu_peer_attach(self._h, ptrs, lens, len(bufs))
+        if rc:
+            self._raise(rc)
+
+    def peer_attach_solo(self):
+        """Measurement hook (tvegpu_peer_attach_solo): step this partition alone, halo stores
+        into scratch, waits passing — for timing one rank of a P-GPU run on one device."""
+        rc = lib().tvegpu_peer_attach_solo(self._h)
         if rc:
             self._raise(rc)
 
