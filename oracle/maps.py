@@ -108,7 +108,9 @@ def rank_plan(nodes, el, nranks=1, rank=0, reorder=True):
     bnd = mine[shared_other.any(axis=1)]
     inr = mine[~shared_other.any(axis=1)]
     if reorder:
-        keys = morton_keys(c, lo, morton_scale(c, lo, hi, min_edge(nodes, el)))
+        # lattice origin: the partition's own lowest centroid (plan.cpp build_rank_plan)
+        klo = c[mine].min(axis=0) if nranks > 1 and len(mine) else lo
+        keys = morton_keys(c, klo, morton_scale(c, lo, hi, min_edge(nodes, el)))
         bnd = bnd[np.lexsort((bnd, keys[bnd]))]
         inr = inr[np.lexsort((inr, keys[inr]))]
         if len(bnd) % 2 == 1 and len(inr):  # even chunk starts (plan.cpp: aligned element rows)

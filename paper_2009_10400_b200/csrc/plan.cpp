@@ -455,11 +455,27 @@ RankPlan build_rank_plan(const tvegpu_problem& p, const GlobalMesh& g, int nrank
     if (reorder) {
         fvec<uint64_t> key((size_t)E);
         const double mscale = morton_scale(g);
+        // lattice origin: the partition's own lowest centroid (every partition's Morton blocks
+        // start at its corner, not wherever the global lattice happens to cut it)
+        double klo[3] = {g.lo[0], g.lo[1], g.lo[2]};
+        if (nranks > 1) {
+            double l0 = INFINITY, l1 = INFINITY, l2 = INFINITY;
+            auto scan = [&](const std::vector<int32_t>& v) {
+#pragma omp parallel for schedule(static) reduction(min : l0, l1, l2)
+                for (size_t q = 0; q < v.size(); ++q) {
+                    const double* c = &g.centroid[(size_t)3 * v[q]];
+                    l0 = std::min(l0, c[0]), l1 = std::min(l1, c[1]), l2 = std::min(l2, c[2]);
+                }
+            };
+            scan(bnd);
+            scan(inr);
+            if (l0 != INFINITY) klo[0] = l0, klo[1] = l1, klo[2] = l2;
+        }
         auto sort_group = [&](std::vector<int32_t>& v) {
             uint64_t kmax = 0;
 #pragma omp parallel for schedule(static) reduction(max : kmax)
             for (size_t q = 0; q < v.size(); ++q) {
-                key[v[q]] = morton_key(&g.centroid[(size_t)3 * v[q]], g.lo, mscale);
+                key[v[q]] = morton_key(&g.centroid[(size_t)3 * v[q]], klo, mscale);
                 kmax = std::max(kmax, key[v[q]]);
             }
             // total order (key, id): a stable radix sort of the id-ordered list by key
