@@ -169,6 +169,15 @@ __global__ void k_init_nodes(const int32_t* __restrict__ node_orig, const double
     mass[i] = mass_o[o];
     vn[i] = vn_o[o];
 }
+// out[c] = 1 iff flag[e] for every element e of chunk c
+__global__ void k_chunk_all(const int32_t* __restrict__ chunk_start, const uint8_t* __restrict__ flag,
+                            uint8_t* __restrict__ out) {
+    const int c = blockIdx.x;
+    int ok = 1;
+    for (int e = chunk_start[c] + threadIdx.x; e < chunk_start[c + 1]; e += blockDim.x) ok &= flag[e];
+    ok = __syncthreads_and(ok);
+    if (threadIdx.x == 0) out[c] = (uint8_t)ok;
+}
 __global__ void k_stage_entries(const int32_t* __restrict__ off, const int32_t* __restrict__ nodes,
                                 const uint16_t* __restrict__ slot, int st, int2* __restrict__ ent) {
     const int c = blockIdx.x;
@@ -271,6 +280,7 @@ struct tvegpu_engine {
     Stepper solo;                           // this engine as a one-part step set (graph cache)
     bool pdl = false;     // programmatic dependent launch of the step kernels (single partition)
     bool pair = false;    // node kernels with two threads per node (long CSR gather lists: T4)
+    int n_affine_chunks = 0;  // H8 chunks whose elements are all affine (K3 skips their c_al rows)
     // peer-memory halo (kernels.cuh peer_send / peer_signal / peer_wait)
     int halo_transport = TVEGPU_HALO_PEER;  // tvegpu_options.halo_transport
     bool peer = false;                      // attached: the boundary element kernels deliver the halo
@@ -1326,12 +1336,33 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
         const int grows = (nn == 8 && !k3_xstage<8>()) ? kGeoRows : 10;
         double* geo = dalloc<double>(own, (size_t)grows * es);
         CU(cudaMemsetAsync(geo, 0, (size_t)grows * es * 8, s));  // the pad columns feed whole-chunk bulk copies
+        // affine H8 elements (parallelepipeds): k_geometry stores their hourglass geometry as
+        // exact zeros and flags them; per chunk whether all are, and whether the whole
+        // partition is — then K3 stages only the 10 A / V rows (TVEGPU_NO_AFFINE: off)
+        const bool detect = nn == 8 && grows == kGeoRows && pl.E > 0 && !std::getenv("TVEGPU_NO_AFFINE");
+        DeviceScratch tmp;
+        uint8_t* aff = detect ? tmp.get<uint8_t>(pl.E) : nullptr;
         if (pl.E > 0) {
-            if (nn == 8) k_geometry<8><<<blocks(pl.E, 256), 256, 0, s>>>(h->ptr.X, h->d_conn, pl.E, m.es, grows, geo);
-            else k_geometry<4><<<blocks(pl.E, 256), 256, 0, s>>>(h->ptr.X, h->d_conn, pl.E, m.es, grows, geo);
+            if (nn == 8) k_geometry<8><<<blocks(pl.E, 256), 256, 0, s>>>(h->ptr.X, h->d_conn, pl.E, m.es, grows, geo, aff);
+            else k_geometry<4><<<blocks(pl.E, 256), 256, 0, s>>>(h->ptr.X, h->d_conn, pl.E, m.es, grows, geo, nullptr);
             CU(cudaGetLastError());
         }
         h->ptr.geo = geo;
+        if (detect) {
+            const int nc = (int)pl.chunk_start.size() - 1;
+            uint8_t* caff = dalloc<uint8_t>(own, nc);
+            k_chunk_all<<<nc, 128, 0, s>>>(h->ptr.chunk_start, aff, caff);
+            CU(cudaGetLastError());
+            std::vector<uint8_t> hc(nc);
+            CU(cudaMemcpyAsync(hc.data(), caff, nc, cudaMemcpyDeviceToHost, s));
+            CU(cudaStreamSynchronize(s));
+            int all = 1;
+            for (uint8_t v : hc) all &= v;
+            h->ptr.chunk_affine = caff;
+            m.affine_all = all;
+            h->n_affine_chunks = 0;
+            for (uint8_t v : hc) h->n_affine_chunks += v;
+        }
     }
     CU(cudaMallocHost(&h->qr_host, std::max(1, N) * sizeof(double)));
     std::memset(h->qr_host, 0, std::max(1, N) * sizeof(double));

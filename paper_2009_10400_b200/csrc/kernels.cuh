@@ -102,6 +102,7 @@ struct DevParams {
     // offsets into DevPtrs::tabs (every table and all Prony coefficients, any length); the
     // kernels read them from there only when c_len / k_len > kMaxTable or P > kMaxProny
     int tab_cT, tab_cV, tab_kT, tab_kK, tab_pa, tab_pb;
+    int affine_all;       // H8: every element affine (hourglass geometry c_al = 0): K3 stages no c_al rows
     int nb_chunks;        // boundary chunks [0, nb_chunks): the element-kernel CTAs that forward and signal (0: no peers)
     int halo_hi;          // local nodes [0, halo_hi) hold every node that gathers received contributions
 };
@@ -148,6 +149,7 @@ struct DevPtrs {
     const int32_t* motion_row;  // [N] row of motion_val for override candidates, else -1 (motion only)
     const double4* motion_val;  // [rows] (x, y, z, pinned) of this step's motion_override(node, t + dt)
     const double* tabs;         // c(T), k(T) tables and Prony coefficients (DevParams::tab_*)
+    const uint8_t* chunk_affine;  // H8: per chunk 1 if all its elements are affine (c_al rows not staged)
     // peer-memory halo (nranks > 1, DevParams::npeers > 0): see peer_forward / peer_signal / peer_wait
     const int32_t* pd_off;                 // [Eb nn + 1] per boundary slot (e nn + a) its destinations
     const uint32_t* pd_ent;                // (neighbour << 26) | index in that neighbour's receive area
@@ -292,6 +294,7 @@ __device__ __forceinline__ void mbar_wait0(unsigned long long* bar) {
 
 // Rows of one element kernel: [0, ngeo) geometry, then 6 P Prony history, then 3
 // fibre and 6 expansion-axis rows when those are per element.
+constexpr int kGeoRows = 22;  // A (9), V, H8 hourglass geometry c_al = X h_al (12)
 struct RowPlan {
     int ngeo, ntheta, nfib, nax;
     __host__ __device__ __forceinline__ int total() const { return ngeo + ntheta + nfib + nax; }
@@ -314,11 +317,14 @@ struct ElemRows {
 
 // Warp 0: issue the chunk's row copies (or, without TMA, every thread prefetches its
 // rows into L1).  e0 = first element of the chunk, ne = its element count.
+// skip_hg: an affine H8 chunk — its hourglass rows [10, kGeoRows) are zero, not copied.
 template <bool TMA>
 __device__ __forceinline__ void load_elem_rows(const DevParams& P, const DevPtrs& D, const RowPlan& rp, int e0, int ne,
                                                double* rows, unsigned long long* bar, double* blob = nullptr,
-                                               const double* blob_src = nullptr, unsigned blob_bytes = 0) {
+                                               const double* blob_src = nullptr, unsigned blob_bytes = 0,
+                                               bool skip_hg = false) {
     const int R = rp.total();
+    const int hg0 = skip_hg && rp.ngeo == kGeoRows ? 10 : R, hg1 = skip_hg && rp.ngeo == kGeoRows ? kGeoRows : R;
     auto src = [&](int r) -> const double* {
         if (r < rp.theta0()) return D.geo + (size_t)r * P.es;
         if (r < rp.fib0()) return D.theta + (size_t)(r - rp.theta0()) * P.es;
@@ -328,12 +334,14 @@ __device__ __forceinline__ void load_elem_rows(const DevParams& P, const DevPtrs
     if constexpr (TMA) {
         if (threadIdx.x >= 32) return;
         const unsigned bytes = (unsigned)((ne + 1) & ~1) * 8u;  // even: 16-byte multiple (rows are padded)
-        if (threadIdx.x == 0) mbar_init_expect(bar, bytes * (unsigned)R + blob_bytes);
+        if (threadIdx.x == 0) mbar_init_expect(bar, bytes * (unsigned)(R - (hg1 - hg0)) + blob_bytes);
         __syncwarp();
-        for (int r = threadIdx.x; r < R; r += 32) tma_row(rows + r * kChunkThreads, src(r) + e0, bytes, bar);
+        for (int r = threadIdx.x; r < R; r += 32)
+            if (r < hg0 || r >= hg1) tma_row(rows + r * kChunkThreads, src(r) + e0, bytes, bar);
         if (blob_bytes && threadIdx.x == 31) tma_row(blob, blob_src, blob_bytes, bar);
     } else if ((int)threadIdx.x < ne) {
-        for (int r = 0; r < R; ++r) asm volatile("prefetch.global.L1 [%0];" ::"l"(src(r) + e0 + threadIdx.x));
+        for (int r = 0; r < R; ++r)
+            if (r < hg0 || r >= hg1) asm volatile("prefetch.global.L1 [%0];" ::"l"(src(r) + e0 + threadIdx.x));
     }
 }
 template <bool TMA>
@@ -347,10 +355,9 @@ constexpr int kRowsOffset = 128;
 // Reference geometry from the element's corner coordinates, in exactly the
 // arithmetic order of element_pass: J (T4: edge matrix; H8: X Xi^T / 8), A = J^-T
 // (H8: / 8), V; and for H8 the hourglass geometry c_al = X h_al in corner order.
-constexpr int kGeoRows = 22;
 template <int NN>
 __global__ void k_geometry(const double4* __restrict__ X, const int32_t* __restrict__ conn, int E, int es, int rows,
-                           double* geo) {
+                           double* geo, uint8_t* __restrict__ affine) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E) return;
     double J[9];
@@ -389,11 +396,23 @@ __global__ void k_geometry(const double4* __restrict__ X, const int32_t* __restr
         }
 #pragma unroll
         for (int q = 0; q < 9; ++q) J[q] = J[q] / 8.0;
-        if (rows > 10)
+        if (rows > 10) {
+            // affine element (parallelepiped: X h_al = 0 up to the rounding of the corner sums,
+            // |c_al| <= 1e-12 of the element size): exact zeros, so K3 need not stage the rows
+            const double L = cbrt(fabs(8.0 * (J[0] * (J[4] * J[8] - J[5] * J[7]) - J[1] * (J[3] * J[8] - J[5] * J[6]) +
+                                             J[2] * (J[3] * J[7] - J[4] * J[6]))));
+            double cm = 0.0;
 #pragma unroll
             for (int al = 0; al < 4; ++al)
 #pragma unroll
-                for (int i = 0; i < 3; ++i) geo[(size_t)(10 + al * 3 + i) * es + e] = cX[al][i];
+                for (int i = 0; i < 3; ++i) cm = fmax(cm, fabs(cX[al][i]));
+            const bool aff = affine && cm <= 1e-12 * L;  // (affine == nullptr: no detection)
+#pragma unroll
+            for (int al = 0; al < 4; ++al)
+#pragma unroll
+                for (int i = 0; i < 3; ++i) geo[(size_t)(10 + al * 3 + i) * es + e] = aff ? 0.0 : cX[al][i];
+            if (affine) affine[e] = aff ? 1 : 0;
+        }
     }
     double Ad[9];
     const double dJ = adj3(J, Ad);
@@ -1036,10 +1055,11 @@ __global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, i
 #define TVEGPU_K3_MINBLOCKS_T4 5  // T4: 102 registers, 20 warps/SM (cfg5 T4 K3 -12 % vs 4)
 #endif
 // K3 element body: element e of the staged chunk st (n = its node slots)
+// affine: the chunk's elements are all affine (c_al = 0, rows not staged)
 template <int NN, int EXP>
 __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, const NodeStage& st,
                                         const ElemRows<kTmaK3>& rows, const RowPlan& rp, const CoordStage& xs,
-                                        const int e, const int (&n)[NN]) {
+                                        const int e, const int (&n)[NN], bool affine = false) {
     const size_t es = (size_t)P.es;
     double Hd[9], A[9], V, Ts;
     {
@@ -1301,7 +1321,8 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
 #pragma unroll
             for (int al = 0; al < 4; ++al)
 #pragma unroll
-                for (int i = 0; i < 3; ++i) cX[al][i] = rows.get(10 + al * 3 + i, D.geo + (10 + al * 3 + i) * es + e);
+                for (int i = 0; i < 3; ++i)
+                    cX[al][i] = affine ? 0.0 : rows.get(10 + al * 3 + i, D.geo + (10 + al * 3 + i) * es + e);
         }
         const double k = P.kh * cbrt(V);
 #pragma unroll
@@ -1395,7 +1416,7 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
 // kMaxProny terms; any further term is read in place), and the per-element fibres / expansion axes when the material has them
 template <int NN, int EXP>
 __host__ __device__ __forceinline__ RowPlan k3_rows(const DevParams& P) {
-    return RowPlan{k3_xstage<NN>() ? 0 : (NN == 8 ? kGeoRows : 10), 6 * (P.P < kMaxProny ? P.P : kMaxProny), P.fiber_mode == 2 ? 3 : 0,
+    return RowPlan{k3_xstage<NN>() ? 0 : (NN == 8 && !P.affine_all ? kGeoRows : 10), 6 * (P.P < kMaxProny ? P.P : kMaxProny), P.fiber_mode == 2 ? 3 : 0,
                    (EXP == 2 && P.axes_per_elem) ? 6 : 0};
 }
 
@@ -1412,6 +1433,8 @@ __global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T
     const NodeStage st{planes, planes + ms};
     const int c = c0 + blockIdx.x;
     CoordStage xs{nullptr, nullptr, nullptr};
+    // affine H8 chunk: hourglass geometry c_al = 0, its rows neither staged nor read
+    const bool affine = NN == 8 && !k3_xstage<NN>() && (P.affine_all || (D.chunk_affine && __ldg(D.chunk_affine + c)));
     {
         const int e0 = __ldg(D.chunk_start + c), ne = __ldg(D.chunk_start + c + 1) - e0;
         if constexpr (k3_xstage<NN>()) {
@@ -1419,7 +1442,7 @@ __global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T
             xs = CoordStage{xblk, xblk + S, xblk + 2 * S};
             load_elem_rows<kTmaK3>(P, D, rp, e0, ne, rows, bar, xblk, D.chunk_x + (size_t)c * P.xstride, 24u * S);
         } else {
-            load_elem_rows<kTmaK3>(P, D, rp, e0, ne, rows, bar);
+            load_elem_rows<kTmaK3>(P, D, rp, e0, ne, rows, bar, nullptr, nullptr, 0, affine);
         }
     }
     int n[NN];
@@ -1429,7 +1452,7 @@ __global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T
     if (P.ack && bnd) peer_wait_ack(P, D);
     if (!D.clock->halted && e >= 0) {
         check_chunk<NN>(P, D, c, e, n);
-        k3_body<NN, EXP>(P, D, st, ElemRows<kTmaK3>{rows, (int)threadIdx.x}, rp, xs, e, n);
+        k3_body<NN, EXP>(P, D, st, ElemRows<kTmaK3>{rows, (int)threadIdx.x}, rp, xs, e, n, affine);
         if (bnd) peer_forward<NN, kMW>(D, D.slot_m, e);
     }
     if (P.npeers) peer_signal(P, D, 1, c);

@@ -19,3 +19,4 @@ timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_
 echo "ncu full rc=$?" >> gpurun_out/summary.txt
 tail -3 gpurun_out/pytest_gpu_all.log >> gpurun_out/summary.txt
 cat gpurun_out/summary.txt
+timeout 900 python scripts/partition_solo.py --workload cfg4 --out gpurun_out/partition_solo_${TAG}_cfg4.json > gpurun_out/ps_cfg4.log 2>&1; echo "partition solo cfg4 rc=$?" >> gpurun_out/summary.txt

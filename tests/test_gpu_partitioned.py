@@ -202,3 +202,26 @@ def test_peer_halo_timeout_is_reported_not_hung():
         grp.step(2)
     with pytest.raises(tg.TveError):
         grp.state()
+
+
+def test_peer_api_errors_and_solo_partition():
+    """tvegpu_peer_export refuses a single-GPU engine; tvegpu_peer_attach needs one
+    descriptor per rank; a partition created without an NCCL id can be stepped alone with
+    tvegpu_peer_attach_solo (the per-rank timing hook) and then reports the peer path."""
+    p = configs.small_problem(kind=H8, n=6, steps=10)
+    one = tg.Engine(p)
+    with pytest.raises(tg.TveError, match="not a partitioned engine"):
+        one.peer_export()
+    solo = tg.Engine(p, nranks=4, rank=1)
+    blob = solo.peer_export()
+    assert len(blob) > 0 and not solo.halo_peer
+    with pytest.raises(tg.TveError, match="one descriptor per rank"):
+        solo.peer_attach([blob])
+    with pytest.raises(tg.TveError):  # stepping a partition without NCCL needs an attached halo
+        solo.step(1)
+    solo2 = tg.Engine(p, nranks=4, rank=2)
+    solo2.peer_attach_solo()
+    assert solo2.halo_peer and solo2.kernels_per_step() == 4
+    solo2.step(5)  # its halo values are scratch: only that it runs is checked
+    solo2.peer_detach()
+    assert not solo2.halo_peer
