@@ -653,21 +653,24 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // other element and every single-GPU run uses: bit-identity across partitions needs it.
 template <int NN, int W>
 __device__ __forceinline__ void peer_forward(const DevPtrs& D, const double* slots, int e) {
-#pragma unroll 1
-    for (int a = 0; a < NN; ++a) {
-        const int slot = e * NN + a;
-        const int k0 = __ldg(D.pd_off + slot), k1 = __ldg(D.pd_off + slot + 1);
-        if (k0 == k1) continue;
-        double v[W];
+    // every load issued up front (the element's destination offsets and its whole slot
+    // block, just stored: L2 hits), then the destinations: a few dependent round trips
+    // instead of a chain per corner — boundary CTAs must not stretch the launch's first wave
+    int off[NN + 1];
 #pragma unroll
-        for (int q = 0; q < W; ++q) v[q] = slots[(size_t)slot * W + q];  // coherent: written just above
-        for (int k = k0; k < k1; ++k) {
+    for (int a = 0; a <= NN; ++a) off[a] = __ldg(D.pd_off + (size_t)e * NN + a);
+    double v[NN * W];
+#pragma unroll
+    for (int q = 0; q < NN * W; ++q) v[q] = slots[(size_t)e * NN * W + q];  // coherent: written just above
+    double* const* base = W == 1 ? D.peer_th : D.peer_m;
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+        for (int k = off[a]; k < off[a + 1]; ++k) {
             const uint32_t en = __ldg(D.pd_ent + k);
-            double* b = (W == 1 ? D.peer_th : D.peer_m)[en >> 26] + (size_t)(en & 0x3ffffffu) * W;
+            double* b = base[en >> 26] + (size_t)(en & 0x3ffffffu) * W;
 #pragma unroll
-            for (int q = 0; q < W; ++q) b[q] = v[q];
+            for (int q = 0; q < W; ++q) b[q] = v[a * W + q];
         }
-    }
 }
 // start of a boundary CTA in a single-physics partitioned step (DevParams::ack): the
 // neighbours' node kernels of the previous step are done with the receive areas this

@@ -26,9 +26,15 @@ from bench import WORKLOADS, ClockSampler
 NVLINK_GBS = 900.0  # B200 NVLink 5, per direction
 
 
-def time_engine(eng, steps, warmup, sampler):
+def time_engine(eng, steps, warmup, sampler, soak=0.5):
     st = torch.cuda.ExternalStream(eng.stream)
     eng.step(warmup)
+    t0 = time.time()  # keep the GPU busy until clocks settle (the bench's soak)
+    while time.time() - t0 < soak:
+        try:
+            eng.step(32)
+        except tg.TveError:
+            break
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     w0 = time.time()
     a.record(st)
