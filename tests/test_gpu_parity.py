@@ -365,3 +365,40 @@ def test_one_step_from_random_state(kind, mode):
         assert np.array_equal(a["u"], u) and np.array_equal(b["u"], u)
     if mode == MECHANICAL_ONLY:
         assert np.array_equal(a["T"], T) and np.array_equal(b["T"], T)
+
+
+def _jitter(p, frac, seed=9, where=None):
+    """Move nodes by up to frac of the spacing (only those selected by `where`): distorted,
+    non-affine H8 elements whose hourglass geometry c_al = X h_al is genuinely non-zero."""
+    h = (p.nodes[:, 0].max() - p.nodes[:, 0].min()) / round(p.num_elements ** (1 / 3))
+    d = np.random.default_rng(seed).uniform(-frac * h, frac * h, p.nodes.shape)
+    if where is not None:
+        d[~where(p.nodes)] = 0.0
+    p.nodes = p.nodes + d
+    return p
+
+
+@pytest.mark.parametrize("kind", [H8, T4])
+def test_distorted_mesh(kind):
+    """Every node jittered by up to 15 % of the spacing: the general element path (H8: the
+    hourglass geometry rows staged and used; no element is affine) against the oracle."""
+    p = _jitter(configs.small_problem(kind=kind, n=5, steps=60), 0.15)
+    compare(p, 60)
+
+
+def test_mixed_affine_mesh_and_partitions():
+    """Half the block distorted, half regular: affine chunks skip the hourglass rows, the
+    others stage them, per chunk.  Parity with the oracle, and 2 / 3 / 4 partitions (whose
+    chunks mix differently) bit-identical to one engine: the affine decision is per element."""
+    from paper_2009_10400_b200.engine import PartitionGroup
+    p = configs.small_problem(kind=H8, n=6, steps=80)
+    L = p.nodes[:, 0].max()
+    p = _jitter(p, 0.12, where=lambda X: X[:, 0] < 0.5 * L - 1e-9)
+    g, _, _ = compare(p, 80)
+    a = g.state()
+    for nparts in (2, 3, 4):
+        grp = PartitionGroup(p, nparts, steps_per_graph=16)
+        grp.step(80)
+        b = grp.state()
+        for k in ("T", "u", "u_prev", "viscous"):
+            np.testing.assert_array_equal(a[k], b[k], err_msg=f"{nparts} parts {k}")
