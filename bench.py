@@ -289,6 +289,8 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
+        # a halo wait that cannot complete fails the run in seconds instead of stalling it
+        os.environ.setdefault("TVEGPU_HALO_TIMEOUT_MS", "5000")
         # communicator-init lines (rank count) of the halo communicator and torch's
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
