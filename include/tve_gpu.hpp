@@ -168,6 +168,7 @@ struct DeviceOptions {
     int nranks = 1, rank = 0;
     std::vector<unsigned char> nccl_unique_id;  // 128 bytes when nranks > 1
     int halo_transport = TVEGPU_HALO_PEER;
+    bool slot_fp32 = false;  // mixed precision: fp32 contributions between element and node kernels
 };
 
 // tve::Engine (engine.hpp:83-143) on a B200.
@@ -187,6 +188,7 @@ public:
         o.rank = opt.rank;
         o.nccl_unique_id = opt.nccl_unique_id.empty() ? nullptr : opt.nccl_unique_id.data();
         o.halo_transport = opt.halo_transport;
+        o.slot_fp32 = opt.slot_fp32 ? 1 : 0;
         const tvegpu_status st = tvegpu_create(&p_, &o, &h_);
         if (st != TVEGPU_OK) rethrow(st, tvegpu_create_error(), -1, -1);
         if (mech_bcs.motion_override) {

@@ -161,6 +161,11 @@ typedef struct tvegpu_options {
     int32_t diagnostics;            /* 1 = keep F, S_tilde, assembled forces (engine.hpp:101-105) */
     int32_t steps_per_graph;        /* CUDA-graph chunk length; 0 = default (64) */
     int32_t halo_transport;         /* partitioned engines and groups: TVEGPU_HALO_* (default PEER) */
+    int32_t slot_fp32;              /* 0 (default): fp64 everywhere (the parity path, <= 1e-10 vs the
+                                       reference algorithm).  1: mixed precision — element and node math
+                                       in fp64, the per-element contributions between them stored as
+                                       fp32 and summed in fp64 (about a quarter fewer bytes per step;
+                                       deviation bound in DESIGN.md §2) */
 } tvegpu_options;
 
 /* Halo exchange of partitioned steps (interface-node heat fluxes and forces).

@@ -123,7 +123,10 @@ class OracleEngine:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            lib().oracle_destroy(self._h)
+            try:
+                lib().oracle_destroy(self._h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self._h = None
 
     def step(self, n=1):

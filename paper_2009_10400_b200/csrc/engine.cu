@@ -281,6 +281,8 @@ struct tvegpu_engine {
     bool pdl = false;     // programmatic dependent launch of the step kernels (single partition)
     bool pair = false;    // node kernels with two threads per node (long CSR gather lists: T4)
     int n_affine_chunks = 0;  // H8 chunks whose elements are all affine (K3 skips their c_al rows)
+    bool slot32 = false;      // tvegpu_options.slot_fp32: contributions stored as fp32, summed in fp64
+    size_t slot_bytes() const { return slot32 ? sizeof(float) : sizeof(double); }
     // peer-memory halo (kernels.cuh peer_send / peer_signal / peer_wait)
     int halo_transport = TVEGPU_HALO_PEER;  // tvegpu_options.halo_transport
     bool peer = false;                      // attached: the boundary element kernels deliver the halo
@@ -375,15 +377,28 @@ bool sources_stable(tvegpu_engine* h, double t) {
 // interior elements run meanwhile and the node kernel waits on ev_comm.
 void pack_halo(tvegpu_engine* h, bool mech) {
     const int ns = h->plan.send_off.back();
-    if (ns > 0)
-        k_pack<<<blocks(ns, 256), 256, 0, h->s>>>(mech ? h->ptr.slot_m : h->ptr.slot_th, h->d_send_slot, ns,
-                                                  mech ? kMW : 1, mech ? h->send_m : h->send_th);
+    double* slots = mech ? h->ptr.slot_m : h->ptr.slot_th;
+    double* out = mech ? h->send_m : h->send_th;
+    if (ns > 0 && h->slot32)
+        k_pack<float><<<blocks(ns, 256), 256, 0, h->s>>>(reinterpret_cast<const float*>(slots), h->d_send_slot, ns,
+                                                         mech ? kMW : 1, reinterpret_cast<float*>(out));
+    else if (ns > 0)
+        k_pack<double><<<blocks(ns, 256), 256, 0, h->s>>>(slots, h->d_send_slot, ns, mech ? kMW : 1, out);
     CU(cudaEventRecord(h->ev_pack, h->s));
 }
 
-double* recv_area(tvegpu_engine* h, bool mech) {
+// element offset in the slot buffer's own type (fp64 or fp32 slots) -> pointer
+double* slot_ptr(const tvegpu_engine* h, bool mech, size_t entries) {
     const int width = mech ? kMW : 1;
-    return (mech ? h->ptr.slot_m : h->ptr.slot_th) + (size_t)h->plan.E * h->plan.nn * width;
+    return reinterpret_cast<double*>(reinterpret_cast<char*>(mech ? h->ptr.slot_m : h->ptr.slot_th) +
+                                     entries * width * h->slot_bytes());
+}
+double* recv_area(tvegpu_engine* h, bool mech) { return slot_ptr(h, mech, (size_t)h->plan.E * h->plan.nn); }
+// entries of a packed send buffer
+const double* send_ptr(const tvegpu_engine* h, bool mech, size_t entries) {
+    const int width = mech ? kMW : 1;
+    return reinterpret_cast<const double*>(reinterpret_cast<const char*>(mech ? h->send_m : h->send_th) +
+                                           entries * width * h->slot_bytes());
 }
 
 struct NcclTransport final : Transport {
@@ -392,8 +407,7 @@ struct NcclTransport final : Transport {
         tvegpu_engine* h = parts[0];  // one partition per process and GPU
         const RankPlan& pl = h->plan;
         const int width = mech ? kMW : 1;
-        const double* sendbuf = mech ? h->send_m : h->send_th;
-        double* recvbuf = recv_area(h, mech);
+        const ncclDataType_t type = h->slot32 ? ncclFloat32 : ncclFloat64;
         CU(cudaStreamWaitEvent(h->sc, h->ev_pack, 0));
         if (t0) CU(cudaEventRecord(t0, h->sc));
         auto& api = nccl();
@@ -402,8 +416,8 @@ struct NcclTransport final : Transport {
             const int peer = pl.neighbors[j];
             const size_t so = pl.send_off[j], sn = pl.send_off[j + 1] - so;
             const size_t ro = pl.recv_off[j], rn = pl.recv_off[j + 1] - ro;
-            if (sn) NC(api.Send(sendbuf + so * width, sn * width, ncclFloat64, peer, comm, h->sc));
-            if (rn) NC(api.Recv(recvbuf + ro * width, rn * width, ncclFloat64, peer, comm, h->sc));
+            if (sn) NC(api.Send(send_ptr(h, mech, so), sn * width, type, peer, comm, h->sc));
+            if (rn) NC(api.Recv(slot_ptr(h, mech, (size_t)pl.E * pl.nn + ro), rn * width, type, peer, comm, h->sc));
         }
         NC(api.GroupEnd());
         CU(cudaEventRecord(h->ev_comm, h->sc));
@@ -432,7 +446,6 @@ struct LoopbackTransport final : Transport {
             if (t0 && r == parts[0])
                 for (const tvegpu_engine* q : parts) CU(cudaStreamWaitEvent(r->sc, q->ev_pack, 0));
             if (t0 && r == parts[0]) CU(cudaEventRecord(t0, r->sc));
-            double* dst0 = recv_area(r, mech);
             for (size_t j = 0; j < pr.neighbors.size(); ++j) {
                 const tvegpu_engine* q = parts.at(pr.neighbors[j]);
                 const RankPlan& ps = q->plan;
@@ -442,8 +455,8 @@ struct LoopbackTransport final : Transport {
                 if (n != (size_t)(pr.recv_off[j + 1] - pr.recv_off[j])) throw Error(TVEGPU_E_ARG, "internal: halo size");
                 if (!n) continue;
                 CU(cudaStreamWaitEvent(r->sc, q->ev_pack, 0));  // the neighbour's packed segment (ncclRecv)
-                const double* src = (mech ? q->send_m : q->send_th) + (size_t)ps.send_off[jj] * width;
-                CU(cudaMemcpyAsync(dst0 + (size_t)pr.recv_off[j] * width, src, n * width * sizeof(double),
+                CU(cudaMemcpyAsync(slot_ptr(r, mech, (size_t)pr.E * pr.nn + pr.recv_off[j]),
+                                   send_ptr(q, mech, ps.send_off[jj]), n * width * r->slot_bytes(),
                                    cudaMemcpyDeviceToDevice, r->sc));
             }
             CU(cudaEventRecord(r->ev_comm, r->sc));
@@ -632,31 +645,35 @@ void launch_step_kernel(tvegpu_engine* h, void (*kern)(KArgs...), int grid, int 
 
 using NodeKernel = void (*)(const DevParams, const DevPtrs, int, int, double*);
 NodeKernel thermal_node_kernel(const tvegpu_engine* h) {
+    if (h->slot32)
+        return h->pair ? k_thermal_node<2, float> : (h->prm.ell > 1 ? k_thermal_node<1, float> : k_thermal_node<0, float>);
     return h->pair ? k_thermal_node<2> : (h->prm.ell > 1 ? k_thermal_node<1> : k_thermal_node<0>);
 }
 
 // Element kernels run one CTA per 128-element chunk over chunk range [c0, c1).
-template <int NN>
+template <int NN, typename ST>
 void launch_mech_element(tvegpu_engine* h, int c0, int c1) {
     if (c1 <= c0) return;
     const size_t sm = k3_smem(h);
     switch (h->prm.exp_kind < 0 ? 0 : (h->prm.exp_kind == 0 ? 1 : 2)) {
-        case 0: launch_step_kernel(h, k_mech_element<NN, 0>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
-        case 1: launch_step_kernel(h, k_mech_element<NN, 1>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
-        default: launch_step_kernel(h, k_mech_element<NN, 2>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
+        case 0: launch_step_kernel(h, k_mech_element<NN, 0, ST>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
+        case 1: launch_step_kernel(h, k_mech_element<NN, 1, ST>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
+        default: launch_step_kernel(h, k_mech_element<NN, 2, ST>, c1 - c0, kChunkThreads, sm, h->prm, h->ptr, h->cur, c0, c1); break;
     }
 }
 
-template <int NN>
+template <int NN, typename ST>
 void launch_thermal_element(tvegpu_engine* h, int c0, int c1) {
     if (c1 <= c0) return;
-    launch_step_kernel(h, k_thermal_element<NN>, c1 - c0, kChunkThreads, k1_smem(h), h->prm, h->ptr, h->cur, c0, c1);
+    launch_step_kernel(h, k_thermal_element<NN, ST>, c1 - c0, kChunkThreads, k1_smem(h), h->prm, h->ptr, h->cur, c0, c1);
 }
 void launch_thermal_elements(tvegpu_engine* h, int c0, int c1) {
-    h->nn == 4 ? launch_thermal_element<4>(h, c0, c1) : launch_thermal_element<8>(h, c0, c1);
+    if (h->slot32) h->nn == 4 ? launch_thermal_element<4, float>(h, c0, c1) : launch_thermal_element<8, float>(h, c0, c1);
+    else h->nn == 4 ? launch_thermal_element<4, double>(h, c0, c1) : launch_thermal_element<8, double>(h, c0, c1);
 }
 void launch_mech_elements(tvegpu_engine* h, int c0, int c1) {
-    h->nn == 4 ? launch_mech_element<4>(h, c0, c1) : launch_mech_element<8>(h, c0, c1);
+    if (h->slot32) h->nn == 4 ? launch_mech_element<4, float>(h, c0, c1) : launch_mech_element<8, float>(h, c0, c1);
+    else h->nn == 4 ? launch_mech_element<4, double>(h, c0, c1) : launch_mech_element<8, double>(h, c0, c1);
 }
 void launch_thermal_node(tvegpu_engine* h, double* t_out) {
     const int N = h->plan.N;
@@ -666,24 +683,27 @@ void launch_thermal_node(tvegpu_engine* h, double* t_out) {
 void launch_mech_node(tvegpu_engine* h, double* u_out, int n0 = 0, int n1 = -1, int closes = 1) {
     if (n1 < 0) n1 = h->plan.N;
     const int n = std::max(0, n1 - n0);
-    if (h->pair)
-        launch_step_kernel(h, k_mech_node<true>, std::max(1, blocks(2 * n, kNodeThreads)), kNodeThreads, 0, h->prm,
-                           h->ptr, h->cur, closes, u_out, n0, n1);
-    else
-        launch_step_kernel(h, k_mech_node<false>, std::max(1, blocks(n, kNodeThreads)), kNodeThreads, 0, h->prm,
-                           h->ptr, h->cur, closes, u_out, n0, n1);
+    const int nb = std::max(1, blocks(h->pair ? 2 * n : n, kNodeThreads));
+    auto k = h->slot32 ? (h->pair ? k_mech_node<true, float> : k_mech_node<false, float>)
+                       : (h->pair ? k_mech_node<true> : k_mech_node<false>);
+    launch_step_kernel(h, k, nb, kNodeThreads, 0, h->prm, h->ptr, h->cur, closes, u_out, n0, n1);
 }
 
+template <class ST, class F>
+void for_each_element_kernel_t(F&& f) {
+    f((const void*)k_thermal_element<4, ST>);
+    f((const void*)k_thermal_element<8, ST>);
+    f((const void*)k_mech_element<4, 0, ST>);
+    f((const void*)k_mech_element<4, 1, ST>);
+    f((const void*)k_mech_element<4, 2, ST>);
+    f((const void*)k_mech_element<8, 0, ST>);
+    f((const void*)k_mech_element<8, 1, ST>);
+    f((const void*)k_mech_element<8, 2, ST>);
+}
 template <class F>
 void for_each_element_kernel(F&& f) {
-    f((const void*)k_thermal_element<4>);
-    f((const void*)k_thermal_element<8>);
-    f((const void*)k_mech_element<4, 0>);
-    f((const void*)k_mech_element<4, 1>);
-    f((const void*)k_mech_element<4, 2>);
-    f((const void*)k_mech_element<8, 0>);
-    f((const void*)k_mech_element<8, 1>);
-    f((const void*)k_mech_element<8, 2>);
+    for_each_element_kernel_t<double>(f);
+    for_each_element_kernel_t<float>(f);
 }
 
 void set_smem_limits(tvegpu_engine* h) {
@@ -699,6 +719,11 @@ void set_smem_limits(tvegpu_engine* h) {
         co((const void*)k_thermal_node<2>);
         co((const void*)k_mech_node<false>);
         co((const void*)k_mech_node<true>);
+        co((const void*)k_thermal_node<0, float>);
+        co((const void*)k_thermal_node<1, float>);
+        co((const void*)k_thermal_node<2, float>);
+        co((const void*)k_mech_node<false, float>);
+        co((const void*)k_mech_node<true, float>);
     }
     // the limit is a per-function attribute shared by every engine of the process: only
     // ever raise it (a later, smaller engine must not undercut an earlier one's launches)
@@ -1451,10 +1476,12 @@ void build_engine(tvegpu_engine* h, const tvegpu_problem& p, const tvegpu_option
     const size_t nslots = (size_t)nn * E + nrecv;
     m.nslots = (int)nslots;
     // + one sentinel slot (index nslots) that nothing writes: the ELL padding target
-    h->ptr.slot_th = dalloc<double>(own, nslots + 1);
-    h->ptr.slot_m = dalloc<double>(own, kMW * (nslots + 1));
-    CU(cudaMemsetAsync(h->ptr.slot_th, 0, (nslots + 1) * 8, s));
-    CU(cudaMemsetAsync(h->ptr.slot_m, 0, kMW * (nslots + 1) * 8, s));
+    h->slot32 = o.slot_fp32 != 0;
+    const size_t sb = h->slot_bytes();  // (fp32 slots: half the doubles allocated, rounded up)
+    h->ptr.slot_th = dalloc<double>(own, ((nslots + 1) * sb + 7) / 8);
+    h->ptr.slot_m = dalloc<double>(own, (kMW * (nslots + 1) * sb + 7) / 8);
+    CU(cudaMemsetAsync(h->ptr.slot_th, 0, (nslots + 1) * sb, s));
+    CU(cudaMemsetAsync(h->ptr.slot_m, 0, kMW * (nslots + 1) * sb, s));
     {
         StageTimer tm("gather tables (ELL, valence)");
         // Node-kernel summation trees must not depend on the partition (bit-identity at any
@@ -2866,12 +2893,12 @@ tvegpu_status tvegpu_halo_info(const tvegpu_engine* h, int32_t* neighbors, int64
     if (!h) return TVEGPU_E_ARG;
     const RankPlan& pl = h->plan;
     const int64_t ns = pl.send_off.empty() ? 0 : pl.send_off.back(), nr = pl.recv_off.empty() ? 0 : pl.recv_off.back();
-    int64_t per = 0;  // doubles per contribution and step: 1 thermal + kMW mechanical, per coupled phase
+    int64_t per = 0;  // values per contribution and step: 1 thermal + kMW mechanical, per coupled phase
     if (h->mode != TVEGPU_MECHANICAL_ONLY) per += 1;
     if (h->mode != TVEGPU_THERMAL_ONLY) per += kMW;
     if (neighbors) *neighbors = (int32_t)pl.neighbors.size();
-    if (send_bytes) *send_bytes = 8 * per * ns;
-    if (recv_bytes) *recv_bytes = 8 * per * nr;
+    if (send_bytes) *send_bytes = (int64_t)h->slot_bytes() * per * ns;
+    if (recv_bytes) *recv_bytes = (int64_t)h->slot_bytes() * per * nr;
     return TVEGPU_OK;
 }
 

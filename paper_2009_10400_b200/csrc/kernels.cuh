@@ -651,23 +651,23 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // the neighbours' receive areas.  Forwarding the stored bits, instead of sending from the
 // element math, keeps that math — and its FMA contraction — identical to the kernel every
 // other element and every single-GPU run uses: bit-identity across partitions needs it.
-template <int NN, int W>
-__device__ __forceinline__ void peer_forward(const DevPtrs& D, const double* slots, int e) {
+template <int NN, int W, typename ST>
+__device__ __forceinline__ void peer_forward(const DevPtrs& D, const ST* slots, int e) {
     // every load issued up front (the element's destination offsets and its whole slot
     // block, just stored: L2 hits), then the destinations: a few dependent round trips
     // instead of a chain per corner — boundary CTAs must not stretch the launch's first wave
     int off[NN + 1];
 #pragma unroll
     for (int a = 0; a <= NN; ++a) off[a] = __ldg(D.pd_off + (size_t)e * NN + a);
-    double v[NN * W];
+    ST v[NN * W];
 #pragma unroll
     for (int q = 0; q < NN * W; ++q) v[q] = slots[(size_t)e * NN * W + q];  // coherent: written just above
-    double* const* base = W == 1 ? D.peer_th : D.peer_m;
+    ST* const* base = reinterpret_cast<ST* const*>(W == 1 ? D.peer_th : D.peer_m);
 #pragma unroll
     for (int a = 0; a < NN; ++a)
         for (int k = off[a]; k < off[a + 1]; ++k) {
             const uint32_t en = __ldg(D.pd_ent + k);
-            double* b = base[en >> 26] + (size_t)(en & 0x3ffffffu) * W;
+            ST* b = base[en >> 26] + (size_t)(en & 0x3ffffffu) * W;
 #pragma unroll
             for (int q = 0; q < W; ++q) b[q] = v[a * W + q];
         }
@@ -734,7 +734,7 @@ __device__ __forceinline__ void peer_wait(const DevParams& P, const DevPtrs& D, 
 #define K1_BOUNDS __launch_bounds__(kChunkThreads)
 #endif
 // K1 element body: element e of the staged chunk S (n = its node slots)
-template <int NN>
+template <int NN, typename ST>
 __device__ __forceinline__ void k1_body(const DevParams& P, const DevPtrs& D, const NodeStage& S,
                                         const ElemRows<kTmaK1>& rows, const CoordStage& xs, const int e,
                                         const int (&n)[NN]) {
@@ -779,6 +779,20 @@ __device__ __forceinline__ void k1_body(const DevParams& P, const DevPtrs& D, co
     // element-major slots: one contiguous 8*NN-byte write per element.  (A node-major
     // layout written through a position map made the node kernels ~25 % faster but
     // the scattered element writes cost more; measured.)
+    if constexpr (sizeof(ST) == 4) {  // mixed precision: the element's NN contributions as fp32
+        float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(D.slot_th) + (size_t)e * NN);
+        if constexpr (NN == 4) {
+            o[0] = make_float4((float)-(r[0] + r[1] + r[2]), (float)r[0], (float)r[1], (float)r[2]);
+        } else {
+            float f[8];
+#pragma unroll
+            for (int a = 0; a < 8; ++a) f[a] = (float)(h8s(a, 0) * r[0] + h8s(a, 1) * r[1] + h8s(a, 2) * r[2]);
+            o[0] = make_float4(f[0], f[1], f[2], f[3]);
+            o[1] = make_float4(f[4], f[5], f[6], f[7]);
+        }
+        if (dF == 0.0) atomicMin(D.err_elem, pack_elem(D.clock->step, D.elem_orig[e]));
+        return;
+    }
     double* out = D.slot_th + (size_t)e * NN;
     if constexpr (NN == 4) {
         const double f0 = -(r[0] + r[1] + r[2]);
@@ -803,7 +817,7 @@ __host__ __device__ __forceinline__ RowPlan k1_rows() { return RowPlan{k1_xstage
 // (peer_forward / peer_signal).  A separate "send" kernel would be compiled separately,
 // and ptxas may contract its element math into FMAs differently: the partitions would
 // then no longer match one GPU bit for bit (measured: 1e-15 drifts on T4).
-template <int NN>
+template <int NN, typename ST = double>
 __global__ void K1_BOUNDS k_thermal_element(const DevParams P, const DevPtrs D, int cur, int c0, int c1) {
     extern __shared__ __align__(128) unsigned char smem[];
     const RowPlan rp = k1_rows<NN>();
@@ -832,8 +846,8 @@ __global__ void K1_BOUNDS k_thermal_element(const DevParams P, const DevPtrs D, 
     if (P.ack && bnd) peer_wait_ack(P, D);
     if (!D.clock->halted && e >= 0) {  // halted: uniform across the grid (read after the wait)
         check_chunk<NN>(P, D, c, e, n);
-        k1_body<NN>(P, D, S, ElemRows<kTmaK1>{rows, (int)threadIdx.x}, xs, e, n);
-        if (bnd) peer_forward<NN, 1>(D, D.slot_th, e);
+        k1_body<NN, ST>(P, D, S, ElemRows<kTmaK1>{rows, (int)threadIdx.x}, xs, e, n);
+        if (bnd) peer_forward<NN, 1>(D, reinterpret_cast<const ST*>(D.slot_th), e);
     }
     if (P.npeers) peer_signal(P, D, 0, c);  // every thread of a boundary CTA, halted or not
     pdl_trigger();  // after this block's work: the successor fills in behind the last wave
@@ -863,7 +877,7 @@ __device__ __forceinline__ void close_step(const DevParams& P, const DevPtrs& D,
         }
     }
     c->ticket = 0;
-    if (D.epoch) {  // every enqueued step, halted or not: the peers' sequences stay in step
+    if (P.npeers) {  // peer-memory halo: every enqueued step, halted or not, so the ranks' sequences agree
         const unsigned long long ep = *D.epoch + 1;
         *D.epoch = ep;
         if (P.ack) {  // single-physics peer halo: this step's receive areas are consumed
@@ -875,28 +889,42 @@ __device__ __forceinline__ void close_step(const DevParams& P, const DevPtrs& D,
     __threadfence();
 }
 
+// Slot values are fp64 (ST = double, the default and the parity path) or, in the
+// mixed-precision mode (tvegpu_options.slot_fp32), fp32 contributions summed in fp64.
+template <typename ST>
+__device__ __forceinline__ double ldslot(const ST* p) { return (double)__ldg(p); }
+
 // Sum of a node's contributions through its gather list, in canonical
 // (original element, local) order.
-__device__ __forceinline__ double gather1(const double* __restrict__ slots, const int32_t* __restrict__ idx, int k0,
+template <typename ST>
+__device__ __forceinline__ double gather1(const ST* __restrict__ slots, const int32_t* __restrict__ idx, int k0,
                                          int k1) {
     double s = 0.0;
-    for (int k = k0; k < k1; ++k) s += __ldg(slots + __ldg(idx + k));
+    for (int k = k0; k < k1; ++k) s += ldslot(slots + __ldg(idx + k));
     return s;
 }
 
 // Packed 24-byte slot record: the 16-byte-aligned pair is (x, y) for even ids and
-// (y, z) for odd ids; the remaining component is one 8-byte load.
-__device__ __forceinline__ double3 ld_slot3(const double* __restrict__ slots, int id) {
-    const int lo = id & 1;
-    const double* b = slots + 3 * (size_t)id;
-    const double2 v = __ldg(reinterpret_cast<const double2*>(b + lo));
-    const double w = __ldg(b + (lo ? 0 : 2));
-    return lo ? make_double3(w, v.x, v.y) : make_double3(v.x, v.y, w);
+// (y, z) for odd ids; the remaining component is one 8-byte load.  (fp32: 12-byte
+// records, three 4-byte loads from one or two sectors.)
+template <typename ST>
+__device__ __forceinline__ double3 ld_slot3(const ST* __restrict__ slots, int id) {
+    if constexpr (sizeof(ST) == 4) {
+        const ST* b = slots + 3 * (size_t)id;
+        return make_double3((double)__ldg(b), (double)__ldg(b + 1), (double)__ldg(b + 2));
+    } else {
+        const int lo = id & 1;
+        const double* b = slots + 3 * (size_t)id;
+        const double2 v = __ldg(reinterpret_cast<const double2*>(b + lo));
+        const double w = __ldg(b + (lo ? 0 : 2));
+        return lo ? make_double3(w, v.x, v.y) : make_double3(v.x, v.y, w);
+    }
 }
-__device__ __forceinline__ void gather3(const double* __restrict__ slots, const int32_t* __restrict__ idx, int k0,
+template <typename ST>
+__device__ __forceinline__ void gather3(const ST* __restrict__ slots, const int32_t* __restrict__ idx, int k0,
                                         int k1, double& f0, double& f1, double& f2) {
     f0 = f1 = f2 = 0.0;
-    if constexpr (kMW == 3) {
+    if constexpr (kMW == 3 || sizeof(ST) == 4) {
         for (int k = k0; k < k1; ++k) {
             const double3 s = ld_slot3(slots, __ldg(idx + k));
             f0 += s.x;
@@ -919,21 +947,21 @@ __device__ __forceinline__ void gather3(const double* __restrict__ slots, const 
 // order sum is unchanged bit for bit (s + 0.0 == s; s is never -0.0 from a +0.0 start).
 // Rows wider than 8 (T4 meshes: ~24 contributions per node) go in groups of 8: the
 // next group's ids load while the current group's contributions are in flight.
-template <bool WIDE>
-__device__ __forceinline__ double gather1_ell(const double* __restrict__ slots, const int4* __restrict__ row, int G,
+template <bool WIDE, typename ST>
+__device__ __forceinline__ double gather1_ell(const ST* __restrict__ slots, const int4* __restrict__ row, int G,
                                              int4 a, int4 b) {
     double s = 0.0;
     if (!WIDE) {  // one group: straight line (H8 meshes)
-        const double v0 = __ldg(slots + a.x), v1 = __ldg(slots + a.y), v2 = __ldg(slots + a.z), v3 = __ldg(slots + a.w);
-        const double v4 = __ldg(slots + b.x), v5 = __ldg(slots + b.y), v6 = __ldg(slots + b.z), v7 = __ldg(slots + b.w);
+        const double v0 = ldslot(slots + a.x), v1 = ldslot(slots + a.y), v2 = ldslot(slots + a.z), v3 = ldslot(slots + a.w);
+        const double v4 = ldslot(slots + b.x), v5 = ldslot(slots + b.y), v6 = ldslot(slots + b.z), v7 = ldslot(slots + b.w);
         s += v0, s += v1, s += v2, s += v3, s += v4, s += v5, s += v6, s += v7;
         return s;
     }
     for (int g = 0; g < G; ++g) {
         int4 na = a, nb = b;
         if (g + 1 < G) na = __ldg(row + 2 * (g + 1)), nb = __ldg(row + 2 * (g + 1) + 1);
-        const double v0 = __ldg(slots + a.x), v1 = __ldg(slots + a.y), v2 = __ldg(slots + a.z), v3 = __ldg(slots + a.w);
-        const double v4 = __ldg(slots + b.x), v5 = __ldg(slots + b.y), v6 = __ldg(slots + b.z), v7 = __ldg(slots + b.w);
+        const double v0 = ldslot(slots + a.x), v1 = ldslot(slots + a.y), v2 = ldslot(slots + a.z), v3 = ldslot(slots + a.w);
+        const double v4 = ldslot(slots + b.x), v5 = ldslot(slots + b.y), v6 = ldslot(slots + b.z), v7 = ldslot(slots + b.w);
         s += v0, s += v1, s += v2, s += v3, s += v4, s += v5, s += v6, s += v7;
         a = na, b = nb;
     }
@@ -941,11 +969,12 @@ __device__ __forceinline__ double gather1_ell(const double* __restrict__ slots, 
 }
 // (the mechanical gather uses the ELL row only for single-group rows: with 3 groups of
 // eight 32-byte loads the grouped loop measured slower than the CSR loop, T4 K4 +35 %)
-__device__ __forceinline__ void gather3_ell(const double* __restrict__ slots, const int4 a, const int4 b, double& f0,
+template <typename ST>
+__device__ __forceinline__ void gather3_ell(const ST* __restrict__ slots, const int4 a, const int4 b, double& f0,
                                             double& f1, double& f2) {
     const double4* S = reinterpret_cast<const double4*>(slots);
     const int id[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    if constexpr (kMW == 3) {
+    if constexpr (kMW == 3 || sizeof(ST) == 4) {
         double3 v[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[k] = ld_slot3(slots, id[k]);
@@ -990,7 +1019,7 @@ constexpr int kNodeThreads = TVEGPU_NODE_THREADS;
 #endif
 // G: 0 = ELL rows of one group (H8) or CSR, 1 = ELL rows of several groups, 2 = two
 // threads per node over the CSR list (T4; see k_mech_node<PAIR>)
-template <int G>
+template <int G, typename ST = double>
 __global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, int cur, int closes,
                                            double* __restrict__ t_out) {
     constexpr bool PAIR = G == 2, WIDE = G == 1;
@@ -1019,15 +1048,16 @@ __global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, i
         if (active) {
             check_gather(P, D, i);
             const int k0 = __ldg(D.csr_off + i), k1 = __ldg(D.csr_off + i + 1), km = k0 + ((k1 - k0 + 1) >> 1);
-            s = gather1(D.slot_th, D.csr_slot, lead ? k0 : km, lead ? km : k1);
+            s = gather1(reinterpret_cast<const ST*>(D.slot_th), D.csr_slot, lead ? k0 : km, lead ? km : k1);
         }
         s += __shfl_down_sync(0xffffffffu, s, 1);
     }
     if (active && lead) {
         if constexpr (!PAIR) {
             check_gather(P, D, i);
-            s = P.ell ? gather1_ell<WIDE>(D.slot_th, D.ell + 2 * (size_t)P.ell * i, P.ell, ia, ib)
-                      : gather1(D.slot_th, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1));
+            const ST* slot_th = reinterpret_cast<const ST*>(D.slot_th);
+            s = P.ell ? gather1_ell<WIDE>(slot_th, D.ell + 2 * (size_t)P.ell * i, P.ell, ia, ib)
+                      : gather1(slot_th, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1));
         }
         if constexpr (!HOIST) {
             T = R[i].w;
@@ -1059,7 +1089,7 @@ __global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, i
 #endif
 // K3 element body: element e of the staged chunk st (n = its node slots)
 // affine: the chunk's elements are all affine (c_al = 0, rows not staged)
-template <int NN, int EXP>
+template <int NN, int EXP, typename ST>
 __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, const NodeStage& st,
                                         const ElemRows<kTmaK3>& rows, const RowPlan& rp, const CoordStage& xs,
                                         const int e, const int (&n)[NN], bool affine = false) {
@@ -1274,7 +1304,13 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
     }
     double4* out = reinterpret_cast<double4*>(D.slot_m) + (size_t)e * NN;
     double* out3 = D.slot_m + (size_t)e * NN * 3;  // kMW == 3: 32-byte aligned (96 / 192 bytes per element)
-    if constexpr (NN == 4 && kMW == 3) {
+    float4* outf = reinterpret_cast<float4*>(reinterpret_cast<float*>(D.slot_m) + (size_t)e * NN * 3);  // fp32 slots
+    if constexpr (NN == 4 && sizeof(ST) == 4) {
+        outf[0] = make_float4((float)-(Q[0] + Q[1] + Q[2]), (float)-(Q[3] + Q[4] + Q[5]), (float)-(Q[6] + Q[7] + Q[8]),
+                              (float)Q[0]);
+        outf[1] = make_float4((float)Q[3], (float)Q[6], (float)Q[1], (float)Q[4]);
+        outf[2] = make_float4((float)Q[7], (float)Q[2], (float)Q[5], (float)Q[8]);
+    } else if constexpr (NN == 4 && kMW == 3) {
         double4* o = reinterpret_cast<double4*>(out3);
         st4(o + 0, make_double4(-(Q[0] + Q[1] + Q[2]), -(Q[3] + Q[4] + Q[5]), -(Q[6] + Q[7] + Q[8]), Q[0]));
         st4(o + 1, make_double4(Q[3], Q[6], Q[1], Q[4]));
@@ -1382,7 +1418,17 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
             }
         };
 #endif
-        if constexpr (kMW == 3) {
+        if constexpr (sizeof(ST) == 4) {  // fp32 slots: 8 x 12 bytes = six 16-byte stores
+            float f[24];
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {
+                double g[3];
+                corner(a, g);
+                f[3 * a] = (float)g[0], f[3 * a + 1] = (float)g[1], f[3 * a + 2] = (float)g[2];
+            }
+#pragma unroll
+            for (int q = 0; q < 6; ++q) outf[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+        } else if constexpr (kMW == 3) {
             // corner pairs: 48 bytes = one 32-byte and one 16-byte store (pair 2p starts 32-byte aligned)
 #pragma unroll
             for (int a = 0; a < 8; a += 2) {
@@ -1423,7 +1469,7 @@ __host__ __device__ __forceinline__ RowPlan k3_rows(const DevParams& P) {
                    (EXP == 2 && P.axes_per_elem) ? 6 : 0};
 }
 
-template <int NN, int EXP>
+template <int NN, int EXP, typename ST = double>
 __global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T4 : TVEGPU_K3_MINBLOCKS)
     k_mech_element(const DevParams P, const DevPtrs D, int cur, int c0, int c1) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -1455,8 +1501,8 @@ __global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T
     if (P.ack && bnd) peer_wait_ack(P, D);
     if (!D.clock->halted && e >= 0) {
         check_chunk<NN>(P, D, c, e, n);
-        k3_body<NN, EXP>(P, D, st, ElemRows<kTmaK3>{rows, (int)threadIdx.x}, rp, xs, e, n, affine);
-        if (bnd) peer_forward<NN, kMW>(D, D.slot_m, e);
+        k3_body<NN, EXP, ST>(P, D, st, ElemRows<kTmaK3>{rows, (int)threadIdx.x}, rp, xs, e, n, affine);
+        if (bnd) peer_forward<NN, kMW>(D, reinterpret_cast<const ST*>(D.slot_m), e);
     }
     if (P.npeers) peer_signal(P, D, 1, c);
     pdl_trigger();
@@ -1469,9 +1515,10 @@ __global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T
 // fixed two-leaf tree: deterministic, partition-invariant).
 // [n0, n1): the local node range of this launch (the whole partition, or one of the
 // slices tvegpu_step_io reads back as they complete).
-template <bool PAIR>
+template <bool PAIR, typename ST = double>
 __global__ void NODE_BOUNDS k_mech_node(const DevParams P, const DevPtrs D, int cur, int closes,
                                                    double* __restrict__ u_out, int n0, int n1) {
+    const ST* slot_m = reinterpret_cast<const ST*>(D.slot_m);
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int i = n0 + (PAIR ? (t >> 1) : t);
     const bool lead = !PAIR || !(threadIdx.x & 1);
@@ -1497,7 +1544,7 @@ __global__ void NODE_BOUNDS k_mech_node(const DevParams P, const DevPtrs D, int 
         if (active) {
             check_gather(P, D, i);
             const int k0 = __ldg(D.csr_off + i), k1 = __ldg(D.csr_off + i + 1), km = k0 + ((k1 - k0 + 1) >> 1);
-            gather3(D.slot_m, D.csr_slot, lead ? k0 : km, lead ? km : k1, f0, f1, f2);
+            gather3(slot_m, D.csr_slot, lead ? k0 : km, lead ? km : k1, f0, f1, f2);
         }
         f0 += __shfl_down_sync(0xffffffffu, f0, 1);
         f1 += __shfl_down_sync(0xffffffffu, f1, 1);
@@ -1506,8 +1553,8 @@ __global__ void NODE_BOUNDS k_mech_node(const DevParams P, const DevPtrs D, int 
     if (active && lead) {
         if constexpr (!PAIR) {
             check_gather(P, D, i);
-            if (P.ell == 1) gather3_ell(D.slot_m, ia, ib, f0, f1, f2);
-            else gather3(D.slot_m, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1), f0, f1, f2);
+            if (P.ell == 1) gather3_ell(slot_m, ia, ib, f0, f1, f2);
+            else gather3(slot_m, D.csr_slot, __ldg(D.csr_off + i), __ldg(D.csr_off + i + 1), f0, f1, f2);
         }
         if constexpr (!HOIST) {
             u = ldg4(Rc + i);  // read-only in this kernel
@@ -1568,15 +1615,17 @@ __global__ void NODE_BOUNDS k_mech_node(const DevParams P, const DevPtrs D, int 
 
 // ------------------------------------------------------------------ halo pack / unpack (nranks > 1)
 // pack: send buffer k <- node-major slot send_pos[k];  unpack: slot recv_pos[r] <- receive buffer r
-__global__ void k_pack(const double* __restrict__ slots, const int32_t* __restrict__ idx, int n, int width,
-                       double* __restrict__ out) {
+template <typename ST>
+__global__ void k_pack(const ST* __restrict__ slots, const int32_t* __restrict__ idx, int n, int width,
+                       ST* __restrict__ out) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int s = idx[k];
     for (int c = 0; c < width; ++c) out[(size_t)k * width + c] = slots[(size_t)s * width + c];
 }
-__global__ void k_unpack(double* __restrict__ slots, const int32_t* __restrict__ idx, int n, int width,
-                         const double* __restrict__ in) {
+template <typename ST>
+__global__ void k_unpack(ST* __restrict__ slots, const int32_t* __restrict__ idx, int n, int width,
+                         const ST* __restrict__ in) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int s = idx[k];

@@ -72,7 +72,7 @@ _BY_STATUS = {1: ParseError, 2: ValidationError, 3: InstabilityError, 4: IoError
 class COptions(C.Structure):
     _fields_ = [("device", C.c_int32), ("nranks", C.c_int32), ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p),
                 ("reorder", C.c_int32), ("diagnostics", C.c_int32), ("steps_per_graph", C.c_int32),
-                ("halo_transport", C.c_int32)]
+                ("halo_transport", C.c_int32), ("slot_fp32", C.c_int32)]
 
 
 HALO_PEER, HALO_NCCL = 0, 1  # tvegpu.h TVEGPU_HALO_*
@@ -335,7 +335,7 @@ class PartitionGroup:
     device copies instead of ncclSend/ncclRecv)."""
 
     def __init__(self, problem: Problem, nparts: int, *, device: int = -1, steps_per_graph: int = 64,
-                 halo_transport: int = HALO_PEER):
+                 halo_transport: int = HALO_PEER, slot_fp32: bool = False):
         L = lib()
         self.problem = problem
         self._c, self._keep = problem.to_c()
@@ -344,6 +344,7 @@ class PartitionGroup:
         o.device = device
         o.steps_per_graph = steps_per_graph
         o.halo_transport = halo_transport
+        o.slot_fp32 = int(slot_fp32)
         h = C.c_void_p()
         rc = L.tvegpu_group_create(C.byref(self._c), nparts, C.byref(o), C.byref(h))
         if rc:
@@ -441,7 +442,7 @@ class Engine:
 
     def __init__(self, problem: Problem, *, device: int = -1, nranks: int = 1, rank: int = 0,
                  nccl_id: bytes | None = None, reorder: bool = True, diagnostics: bool = False,
-                 steps_per_graph: int = 64, halo_transport: int = HALO_PEER):
+                 steps_per_graph: int = 64, halo_transport: int = HALO_PEER, slot_fp32: bool = False):
         L = lib()
         self.problem = problem
         t0 = time.perf_counter()
@@ -456,6 +457,7 @@ class Engine:
         o.nccl_unique_id = C.cast(self._id, C.c_void_p) if self._id is not None else None
         o.reorder, o.diagnostics, o.steps_per_graph = int(reorder), int(diagnostics), steps_per_graph
         o.halo_transport = halo_transport
+        o.slot_fp32 = int(slot_fp32)
         self._opt = o
         h = C.c_void_p()
         t0 = time.perf_counter()

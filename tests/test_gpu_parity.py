@@ -402,3 +402,39 @@ def test_mixed_affine_mesh_and_partitions():
         b = grp.state()
         for k in ("T", "u", "u_prev", "viscous"):
             np.testing.assert_array_equal(a[k], b[k], err_msg=f"{nparts} parts {k}")
+
+
+# Mixed-precision mode (tvegpu_options.slot_fp32): element and node math in fp64, the
+# per-element contributions between them stored as fp32 and summed in fp64.  Stated bound
+# (measured ~2e-8 for u and ~5e-13 for T after 200 steps):
+FP32_TOL_U, FP32_TOL_T = 1e-6, 1e-9
+
+
+@pytest.mark.parametrize("kind", [T4, H8])
+def test_fp32_slots_within_stated_bound(kind):
+    p = configs.small_problem(kind=kind, n=5, steps=200)
+    g = tg.Engine(p, slot_fp32=True)
+    o = O.OracleEngine(p)
+    g.step(200)
+    o.step(200)
+    a, b = g.state(), o.state()
+    eu = inc_err(a["u"], b["u"], 0.0)
+    eT = inc_err(a["T"], b["T"], p.initial_temperature)
+    assert eu <= FP32_TOL_U and eT <= FP32_TOL_T, (eu, eT)
+    assert eu > 0  # the mode is really in effect (fp32 rounding shows)
+
+
+@pytest.mark.parametrize("halo", [tg.HALO_PEER, tg.HALO_NCCL])
+def test_fp32_slots_partitions_bit_identical(halo):
+    """The mixed mode keeps partition invariance: same kernels, same fp32 roundings, same
+    canonical fp64 sums at any partition count (both halo paths carry fp32 slots)."""
+    from paper_2009_10400_b200.engine import PartitionGroup
+    p = configs.small_problem(kind=H8, n=6, steps=80)
+    one = tg.Engine(p, slot_fp32=True)
+    one.step(80)
+    for nparts in (2, 4):
+        grp = PartitionGroup(p, nparts, steps_per_graph=16, halo_transport=halo, slot_fp32=True)
+        grp.step(80)
+        a, b = one.state(), grp.state()
+        for k in ("T", "u", "u_prev", "viscous"):
+            np.testing.assert_array_equal(a[k], b[k], err_msg=f"{nparts} {k}")
