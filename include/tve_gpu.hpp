@@ -256,11 +256,22 @@ public:
         u.resize(3 * (size_t)N_);
         check(tvegpu_make_snapshot(h_, T.data(), u.data()));
     }
-    // engine.hpp:101-105 (needs DeviceOptions::diagnostics)
+    // engine.hpp:101-105 (needs DeviceOptions::diagnostics): assembled internal force of the
+    // last mechanics phase (3 per node), S~ and F per element (row-major 3x3, original ids)
     std::vector<double> last_internal_forces() {
         std::vector<double> f(3 * (size_t)N_);
         check(tvegpu_get_diagnostics(h_, f.data(), nullptr, nullptr));
         return f;
+    }
+    std::vector<std::array<double, 9>> element_stresses() {
+        std::vector<std::array<double, 9>> S((size_t)E_);
+        check(tvegpu_get_diagnostics(h_, nullptr, nullptr, S.empty() ? nullptr : S[0].data()));
+        return S;
+    }
+    std::vector<std::array<double, 9>> deformation_gradients() {
+        std::vector<std::array<double, 9>> F((size_t)E_);
+        check(tvegpu_get_diagnostics(h_, nullptr, F.empty() ? nullptr : F[0].data(), nullptr));
+        return F;
     }
     // bioheat.hpp:57 nodal source override (power per node [W]); empty restores regions
     void set_nodal_sources(const std::vector<double>& power) {
