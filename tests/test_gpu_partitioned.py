@@ -225,3 +225,34 @@ def test_peer_api_errors_and_solo_partition():
     solo2.step(5)  # its halo values are scratch: only that it runs is checked
     solo2.peer_detach()
     assert not solo2.halo_peer
+
+
+@pytest.mark.parametrize("kind", [T4, H8])
+@pytest.mark.parametrize("mode", [THERMAL_ONLY, MECHANICAL_ONLY])
+def test_fp32_slots_partitioned_modes(kind, mode):
+    """Mixed-precision mode x single-physics steps (the end-of-step acks of the peer path)
+    x both element kinds: partitions stay bit-identical to one engine."""
+    p = configs.small_problem(kind=kind, n=5, steps=60)
+    p.mode = mode
+    one = tg.Engine(p, slot_fp32=True)
+    one.step(60)
+    grp = PartitionGroup(p, 3, steps_per_graph=8, slot_fp32=True)
+    grp.step(60)
+    assert_same(one.state(), grp.state())
+
+
+def test_long_tables_and_prony_partitioned():
+    """Property tables longer than the launch-parameter copies and Prony terms beyond the
+    staged history rows (read from device memory) under partitioning: bit-identical."""
+    import math
+    p = configs.small_problem(kind=H8, n=6, steps=60)
+    p.prony_phi = [0.2, 0.15, 0.1, 0.08, 0.06, 0.05]
+    p.prony_tau = [0.58, 0.058, 0.0058, 5.8, 0.0012, 0.021]
+    Tc = np.linspace(36.99, 37.13, 20)
+    p.c_table = [(float(t), 3600.0 + 700.0 * math.sin(9.0 * i)) for i, t in enumerate(Tc)]
+    one = tg.Engine(p)
+    one.step(60)
+    for halo in (tg.HALO_PEER, tg.HALO_NCCL):
+        grp = PartitionGroup(p, 4, steps_per_graph=16, halo_transport=halo)
+        grp.step(60)
+        assert_same(one.state(), grp.state())
