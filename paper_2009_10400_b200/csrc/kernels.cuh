@@ -1019,8 +1019,9 @@ constexpr int kNodeThreads = TVEGPU_NODE_THREADS;
 #endif
 // G: 0 = ELL rows of one group (H8) or CSR, 1 = ELL rows of several groups, 2 = two
 // threads per node over the CSR list (T4; see k_mech_node<PAIR>)
+// (the pair form is held to 6 blocks/SM: left free, ptxas picks 32 registers and spills)
 template <int G, typename ST = double>
-__global__ void NODE_BOUNDS k_thermal_node(const DevParams P, const DevPtrs D, int cur, int closes,
+__global__ void __launch_bounds__(kNodeThreads, G == 2 ? 6 : 0) k_thermal_node(const DevParams P, const DevPtrs D, int cur, int closes,
                                            double* __restrict__ t_out) {
     constexpr bool PAIR = G == 2, WIDE = G == 1;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
