@@ -532,26 +532,44 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // so every load is issued before any is consumed: the element's own slot indices,
 // then up to kStageBatch node indices per thread, then all their records.
 constexpr int kStageBatch = 3;
+// The chunk's index loads, issued first thing in the kernel (before warp 0 issues the row
+// copies, which wait for the chunk start): the first batch of staging entries — fixed
+// stride, so its address needs no load — and this thread's element node slots.
 template <int NN>
-__device__ __forceinline__ int stage_chunk(const DevPtrs& D, const double4* __restrict__ R, int c, const int st,
-                                           const NodeStage& S, int (&n)[NN]) {
-    // fixed-stride entry list: its address needs no load, so the record gathers
-    // are only one dependent load away from the kernel start
-    const int2* ent = D.stage_ent + (size_t)c * st;
+struct StageHead {
     int2 en[kStageBatch];
+    uint4 w8;
+    uint2 w4;
+    int e;
+};
+template <int NN>
+__device__ __forceinline__ StageHead<NN> stage_head(const DevPtrs& D, int c, const int st, int e0, int ne) {
+    StageHead<NN> h;
+    const int2* ent = D.stage_ent + (size_t)c * st;
 #pragma unroll
     for (int j = 0; j < kStageBatch; ++j) {
         const int k = j * kChunkThreads + threadIdx.x;
-        en[j] = k < st ? __ldg(ent + k) : make_int2(-1, 0);
+        h.en[j] = k < st ? __ldg(ent + k) : make_int2(-1, 0);
     }
-    const int eb = __ldg(D.chunk_start + c), ne = __ldg(D.chunk_start + c + 1) - eb;
-    const int e = (int)threadIdx.x < ne ? eb + (int)threadIdx.x : -1;
-    uint4 w8 = make_uint4(0, 0, 0, 0);
-    uint2 w4 = make_uint2(0, 0);
-    if (e >= 0) {
-        if constexpr (NN == 8) w8 = __ldg(reinterpret_cast<const uint4*>(D.lconn) + e);
-        else w4 = __ldg(reinterpret_cast<const uint2*>(D.lconn) + e);
+    h.e = (int)threadIdx.x < ne ? e0 + (int)threadIdx.x : -1;
+    h.w8 = make_uint4(0, 0, 0, 0);
+    h.w4 = make_uint2(0, 0);
+    if (h.e >= 0) {
+        if constexpr (NN == 8) h.w8 = __ldg(reinterpret_cast<const uint4*>(D.lconn) + h.e);
+        else h.w4 = __ldg(reinterpret_cast<const uint2*>(D.lconn) + h.e);
     }
+    return h;
+}
+template <int NN>
+__device__ __forceinline__ int stage_chunk(const DevPtrs& D, const double4* __restrict__ R, int c, const int st,
+                                           const NodeStage& S, int (&n)[NN], const StageHead<NN>& h) {
+    const int2* ent = D.stage_ent + (size_t)c * st;
+    int2 en[kStageBatch];
+#pragma unroll
+    for (int j = 0; j < kStageBatch; ++j) en[j] = h.en[j];
+    const int e = h.e;
+    const uint4 w8 = h.w8;
+    const uint2 w4 = h.w4;
     for (int k0 = 0; k0 < st; k0 += kStageBatch * kChunkThreads) {  // ascending node ids: coalesced loads
         int g[kStageBatch], s[kStageBatch];
 #pragma unroll
@@ -829,8 +847,12 @@ __global__ void K1_BOUNDS k_thermal_element(const DevParams P, const DevPtrs D, 
     const NodeStage S{planes, planes + ms};
     const int c = c0 + blockIdx.x;
     CoordStage xs{nullptr, nullptr, nullptr};
+    const int e0 = __ldg(D.chunk_start + c), ne = __ldg(D.chunk_start + c + 1) - e0;
+    // H8: the index loads go out before the row copies (K3 104 -> 99 us, K1 54 -> 52 us on
+    // cfg4); T4 chunks are slower that way (K3 305 -> 313 us on cfg5 n=100) and load them after
+    StageHead<NN> hd;
+    if constexpr (NN == 8) hd = stage_head<NN>(D, c, P.stage_stride, e0, ne);
     {
-        const int e0 = __ldg(D.chunk_start + c), ne = __ldg(D.chunk_start + c + 1) - e0;
         if constexpr (k1_xstage<NN>()) {
             const int Sx = __ldg(D.chunk_xs + c);
             xs = CoordStage{xblk, xblk + Sx, xblk + 2 * Sx};
@@ -840,7 +862,8 @@ __global__ void K1_BOUNDS k_thermal_element(const DevParams P, const DevPtrs D, 
         }
     }
     int n[NN];
-    const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c, P.stage_stride, S, n);
+    if constexpr (NN == 4) hd = stage_head<NN>(D, c, P.stage_stride, e0, ne);
+    const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c, P.stage_stride, S, n, hd);
     wait_elem_rows<kTmaK1>(bar);  // every thread: the CTA must not retire with bulk copies in flight
     const bool bnd = c < P.nb_chunks;  // a boundary chunk of a peer-memory partition (else false)
     if (P.ack && bnd) peer_wait_ack(P, D);
@@ -1485,8 +1508,10 @@ __global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T
     CoordStage xs{nullptr, nullptr, nullptr};
     // affine H8 chunk: hourglass geometry c_al = 0, its rows neither staged nor read
     const bool affine = NN == 8 && !k3_xstage<NN>() && (P.affine_all || (D.chunk_affine && __ldg(D.chunk_affine + c)));
+    const int e0 = __ldg(D.chunk_start + c), ne = __ldg(D.chunk_start + c + 1) - e0;
+    StageHead<NN> hd;  // (see k_thermal_element)
+    if constexpr (NN == 8) hd = stage_head<NN>(D, c, P.stage_stride, e0, ne);
     {
-        const int e0 = __ldg(D.chunk_start + c), ne = __ldg(D.chunk_start + c + 1) - e0;
         if constexpr (k3_xstage<NN>()) {
             const int S = __ldg(D.chunk_xs + c);
             xs = CoordStage{xblk, xblk + S, xblk + 2 * S};
@@ -1496,7 +1521,8 @@ __global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T
         }
     }
     int n[NN];
-    const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c, P.stage_stride, st, n);
+    if constexpr (NN == 4) hd = stage_head<NN>(D, c, P.stage_stride, e0, ne);
+    const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c, P.stage_stride, st, n, hd);
     wait_elem_rows<kTmaK3>(bar);  // every thread: the CTA must not retire with bulk copies in flight
     const bool bnd = c < P.nb_chunks;  // (see k_thermal_element)
     if (P.ack && bnd) peer_wait_ack(P, D);
