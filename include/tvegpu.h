@@ -447,6 +447,9 @@ tvegpu_status tvegpu_peer_attach_solo(tvegpu_engine* h);
 /* Kernel launches per step (per coupled phase: element + node kernel; partitioned:
  * boundary + interior element launches, plus the halo pack with the NCCL transport). */
 int32_t tvegpu_kernels_per_step(const tvegpu_engine* h);
+/* H8: chunks of this partition whose elements are all affine (parallelepipeds: hourglass
+ * geometry c_al = 0); K3 skips their c_al rows and terms.  0 for T4. */
+int32_t tvegpu_affine_chunks(const tvegpu_engine* h);
 /* Enqueue nsteps on the stream without waiting or reading back the finite
  * check; tvegpu_sync() waits and applies it.  tvegpu_step == enqueue + sync. */
 tvegpu_status tvegpu_enqueue_steps(tvegpu_engine* h, int64_t nsteps);

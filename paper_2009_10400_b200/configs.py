@@ -91,6 +91,20 @@ def cfg4(steps=200, n=100, prony_terms=1):
     return cube_problem(H8, n, 0.1, 1e-4, steps, 1e-2, 0.01, prony_terms=prony_terms)
 
 
+def cfg4_jittered(steps=200, half=0, seed=6):
+    """cfg4 with its nodes jittered by up to 5 % of the spacing, so its elements are not affine
+    (the general H8 hourglass path); half=1: only the nodes in the upper half in x, a mesh of affine and
+    general elements with mixed chunks along the interface."""
+    p = cfg4(steps=steps)
+    h = 0.1 / 100
+    d = np.random.default_rng(seed).uniform(-0.05 * h, 0.05 * h, p.nodes.shape)
+    if half:
+        x = p.nodes[:, 0]
+        d[x <= 0.5 * (x.min() + x.max()) + 1e-12] = 0.0
+    p.nodes = p.nodes + d
+    return p
+
+
 def cfg5_h8(n, steps=50):
     """Ladder point n in {100,126,159,200,252}: dt = half the mechanical critical step."""
     length = 0.1 * n / 100

@@ -2902,6 +2902,8 @@ tvegpu_status tvegpu_halo_info(const tvegpu_engine* h, int32_t* neighbors, int64
     return TVEGPU_OK;
 }
 
+int32_t tvegpu_affine_chunks(const tvegpu_engine* h) { return h ? h->n_affine_chunks : 0; }
+
 int32_t tvegpu_kernels_per_step(const tvegpu_engine* h) {
     if (!h) return 0;
     const bool multi = h->plan.nranks > 1;

@@ -1118,6 +1118,13 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
                                         const ElemRows<kTmaK3>& rows, const RowPlan& rp, const CoordStage& xs,
                                         const int e, const int (&n)[NN], bool affine = false) {
     const size_t es = (size_t)P.es;
+    // affine chunk: every element is; else the element's own flag (mixed chunks)
+    // affine chunk (all its elements affine; CTA-uniform): K3 takes the short hourglass branch.
+    // An affine element in a mixed chunk takes the general branch, which computes the same
+    // values for c_al = 0 (exact zeros: A^T c_al = Hd c_al = 0, 1/(8 + 0) = 1/8), so the
+    // result does not depend on which chunk — which partitioning — the element lands in.
+    // (A per-element flag instead: +5 us on cfg4 with every node jittered, for its load.)
+    const bool eaff = NN == 8 && affine;
     double Hd[9], A[9], V, Ts;
     {
         double H[9], gT[3];
@@ -1388,6 +1395,14 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
                     cX[al][i] = affine ? 0.0 : rows.get(10 + al * 3 + i, D.geo + (10 + al * 3 + i) * es + e);
         }
         const double k = P.kh * cbrt(V);
+        if (eaff) {
+            // affine element (c_al = 0): gamma_hat_al = h_al, |gamma_hat_al|^2 = 8 — g_al = U h_al / 8,
+            // the general branch's value without its A^T c_al and Hd c_al products (zeros here)
+#pragma unroll
+            for (int al = 0; al < 4; ++al)
+#pragma unroll
+                for (int i = 0; i < 3; ++i) Uh[al][i] *= 0.125;
+        } else {
 #pragma unroll
         for (int al = 0; al < 4; ++al) {
             double atc[3];
@@ -1403,6 +1418,7 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
             for (int i = 0; i < 3; ++i)
 #pragma unroll
                 for (int j = 0; j < 3; ++j) Q[i * 3 + j] -= k * Uh[al][i] * atc[j];
+        }
         }
 #if TVEGPU_K3_WHT
         // corner forces f_a = Q xi_a + sum_al h_al[a] (k g_al): the eight corners are the

@@ -132,6 +132,7 @@ EXPORTS = {
     "tvegpu_peer_attach_solo": (C.c_int, [C.c_void_p]),
     "tvegpu_stream": (C.c_void_p, [C.c_void_p]),
     "tvegpu_kernels_per_step": (C.c_int32, [C.c_void_p]),
+    "tvegpu_affine_chunks": (C.c_int32, [C.c_void_p]),
     "tvegpu_halo_info": (C.c_int, [C.c_void_p, _ip, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "tvegpu_enqueue_steps": (C.c_int, [C.c_void_p, C.c_int64]),
     "tvegpu_sync": (C.c_int, [C.c_void_p]),
@@ -693,6 +694,10 @@ class Engine:
 
     def kernels_per_step(self) -> int:
         return lib().tvegpu_kernels_per_step(self._h)
+
+    def affine_chunks(self) -> int:
+        """H8: chunks whose elements are all affine (K3's short hourglass branch)."""
+        return lib().tvegpu_affine_chunks(self._h)
 
     def peer_export(self) -> bytes:
         """This partition's peer-memory halo descriptor (tvegpu_peer_export): all-gather

@@ -389,7 +389,8 @@ def test_distorted_mesh(kind):
 def test_mixed_affine_mesh_and_partitions():
     """Half the block distorted, half regular: affine chunks skip the hourglass rows, the
     others stage them, per chunk.  Parity with the oracle, and 2 / 3 / 4 partitions (whose
-    chunks mix differently) bit-identical to one engine: the affine decision is per element."""
+    chunks mix differently) bit-identical to one engine: an element's values do not depend on
+    whether its chunk is all affine."""
     from paper_2009_10400_b200.engine import PartitionGroup
     p = configs.small_problem(kind=H8, n=6, steps=80)
     L = p.nodes[:, 0].max()
@@ -402,6 +403,42 @@ def test_mixed_affine_mesh_and_partitions():
         b = grp.state()
         for k in ("T", "u", "u_prev", "viscous"):
             np.testing.assert_array_equal(a[k], b[k], err_msg=f"{nparts} parts {k}")
+
+
+def test_affine_branch_value_identical_to_general_path(monkeypatch):
+    """K3 takes its short hourglass branch per all-affine chunk; an affine element in a mixed
+    chunk goes through the general branch.  Both give the same values for c_al = 0, so (1)
+    an engine with affine detection off (TVEGPU_NO_AFFINE: every element general) matches
+    the default engine, and (2) partitionings that put the interface elements in
+    different chunks match one engine bit for bit.  (1) within 1e-12: without detection the
+    hourglass rows keep the rounding-level c_al of a regular element, which detection snaps
+    to zero.)"""
+    from paper_2009_10400_b200.engine import PartitionGroup
+    p = configs.small_problem(kind=H8, n=16, steps=60)
+    L = p.nodes[:, 0].max()
+    p = _jitter(p, 0.1, where=lambda X: X[:, 0] > 0.75 * L + 1e-9)
+    g = tg.Engine(p)
+    assert g.affine_chunks() > 0  # the short branch is exercised
+    g.step(60)
+    a = g.state()
+    monkeypatch.setenv("TVEGPU_NO_AFFINE", "1")
+    h = tg.Engine(p)
+    assert h.affine_chunks() == 0
+    h.step(60)
+    b = h.state()
+    monkeypatch.delenv("TVEGPU_NO_AFFINE")
+    assert inc_err(b["u"], a["u"], 0.0) <= 1e-12
+    assert inc_err(b["T"], a["T"], p.initial_temperature) <= 1e-12
+    for nparts in (2, 3, 5):
+        grp = PartitionGroup(p, nparts, steps_per_graph=16)
+        grp.step(60)
+        c = grp.state()
+        for k in ("T", "u", "u_prev", "viscous"):
+            np.testing.assert_array_equal(a[k], c[k], err_msg=f"{nparts} parts {k}")
+    o = O.OracleEngine(p)
+    o.step(60)
+    r = o.state()
+    assert inc_err(a["u"], r["u"], 0.0) <= 1e-10
 
 
 # Mixed-precision mode (tvegpu_options.slot_fp32): element and node math in fp64, the
