@@ -532,6 +532,13 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // so every load is issued before any is consumed: the element's own slot indices,
 // then up to kStageBatch node indices per thread, then all their records.
 constexpr int kStageBatch = 3;
+// L2 prefetch of the entry list a CTA about two resident waves later loads first (streamed
+// from DRAM each step, at the head of the staging chain).  The same for the node kernels'
+// ELL rows was slower (K2 +2 us, K4 +1 us on cfg4).
+#ifndef TVEGPU_ENT_PREFETCH
+#define TVEGPU_ENT_PREFETCH 1184  // element kernels: chunks ahead (0: off)
+#endif
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 // The chunk's index loads, issued first thing in the kernel (before warp 0 issues the row
 // copies, which wait for the chunk start): the first batch of staging entries — fixed
 // stride, so its address needs no load — and this thread's element node slots.
@@ -543,9 +550,13 @@ struct StageHead {
     int e;
 };
 template <int NN>
-__device__ __forceinline__ StageHead<NN> stage_head(const DevPtrs& D, int c, const int st, int e0, int ne) {
+__device__ __forceinline__ StageHead<NN> stage_head(const DevPtrs& D, int c, const int st, int e0, int ne, int cend) {
     StageHead<NN> h;
     const int2* ent = D.stage_ent + (size_t)c * st;
+    if constexpr (TVEGPU_ENT_PREFETCH > 0) {  // (cfg4 K3 -1 us, cfg5 T4 K1 / K3 -2 %)
+        const int cn = c + TVEGPU_ENT_PREFETCH;
+        if (cn < cend && (int)threadIdx.x < ((st * 8 + 127) >> 7)) prefetch_l2(D.stage_ent + (size_t)cn * st + threadIdx.x * 16);
+    }
 #pragma unroll
     for (int j = 0; j < kStageBatch; ++j) {
         const int k = j * kChunkThreads + threadIdx.x;
@@ -851,7 +862,7 @@ __global__ void K1_BOUNDS k_thermal_element(const DevParams P, const DevPtrs D, 
     // H8: the index loads go out before the row copies (K3 104 -> 99 us, K1 54 -> 52 us on
     // cfg4); T4 chunks are slower that way (K3 305 -> 313 us on cfg5 n=100) and load them after
     StageHead<NN> hd;
-    if constexpr (NN == 8) hd = stage_head<NN>(D, c, P.stage_stride, e0, ne);
+    if constexpr (NN == 8) hd = stage_head<NN>(D, c, P.stage_stride, e0, ne, c1);
     {
         if constexpr (k1_xstage<NN>()) {
             const int Sx = __ldg(D.chunk_xs + c);
@@ -862,7 +873,7 @@ __global__ void K1_BOUNDS k_thermal_element(const DevParams P, const DevPtrs D, 
         }
     }
     int n[NN];
-    if constexpr (NN == 4) hd = stage_head<NN>(D, c, P.stage_stride, e0, ne);
+    if constexpr (NN == 4) hd = stage_head<NN>(D, c, P.stage_stride, e0, ne, c1);
     const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c, P.stage_stride, S, n, hd);
     wait_elem_rows<kTmaK1>(bar);  // every thread: the CTA must not retire with bulk copies in flight
     const bool bnd = c < P.nb_chunks;  // a boundary chunk of a peer-memory partition (else false)
@@ -1526,7 +1537,7 @@ __global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T
     const bool affine = NN == 8 && !k3_xstage<NN>() && (P.affine_all || (D.chunk_affine && __ldg(D.chunk_affine + c)));
     const int e0 = __ldg(D.chunk_start + c), ne = __ldg(D.chunk_start + c + 1) - e0;
     StageHead<NN> hd;  // (see k_thermal_element)
-    if constexpr (NN == 8) hd = stage_head<NN>(D, c, P.stage_stride, e0, ne);
+    if constexpr (NN == 8) hd = stage_head<NN>(D, c, P.stage_stride, e0, ne, c1);
     {
         if constexpr (k3_xstage<NN>()) {
             const int S = __ldg(D.chunk_xs + c);
@@ -1537,7 +1548,7 @@ __global__ void __launch_bounds__(kChunkThreads, NN == 4 ? TVEGPU_K3_MINBLOCKS_T
         }
     }
     int n[NN];
-    if constexpr (NN == 4) hd = stage_head<NN>(D, c, P.stage_stride, e0, ne);
+    if constexpr (NN == 4) hd = stage_head<NN>(D, c, P.stage_stride, e0, ne, c1);
     const int e = stage_chunk<NN>(D, cur ? D.rec1 : D.rec0, c, P.stage_stride, st, n, hd);
     wait_elem_rows<kTmaK3>(bar);  // every thread: the CTA must not retire with bulk copies in flight
     const bool bnd = c < P.nb_chunks;  // (see k_thermal_element)
