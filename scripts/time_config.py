@@ -1,5 +1,5 @@
 """Graph-replayed ms/step of one configuration (CUDA events on the engine stream), as bench.py
-times it:  python scripts/time_config.py cfg5_h8 252 [steps]"""
+times it:  python scripts/time_config.py cfg5_h8 252 [steps]   (cfg3 - 2000: no size argument)"""
 import os
 import sys
 
@@ -9,7 +9,8 @@ import torch
 import paper_2009_10400_b200 as tg
 from paper_2009_10400_b200 import configs
 
-name, args = sys.argv[1], [int(a) for a in sys.argv[2:3]]
+name = sys.argv[1]
+args = [int(a) for a in sys.argv[2:3] if a != "-"]  # the config's size argument ("-": none)
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 256
 p = getattr(configs, name)(*args, steps=steps + 200) if args else getattr(configs, name)(steps=steps + 200)
 e = tg.Engine(p)
