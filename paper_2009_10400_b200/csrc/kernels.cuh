@@ -1039,6 +1039,14 @@ __device__ __forceinline__ void gather3_ell(const ST* __restrict__ slots, const 
 #define TVEGPU_NODE_THREADS 256
 #endif
 constexpr int kNodeThreads = TVEGPU_NODE_THREADS;
+// Node kernels walk their blocks in reverse: the element kernel before each wrote its
+// contributions in element order, so the last-written ones — still in L2 — belong to the
+// last nodes; taking those first turns part of the slot gather into L2 hits.  (Interface
+// nodes, numbered first, are then also the last to need their neighbours' flags.)
+#ifndef TVEGPU_NODE_REV
+#define TVEGPU_NODE_REV 1
+#endif
+__device__ __forceinline__ int node_block() { return TVEGPU_NODE_REV ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x; }
 // Node kernels issue the loads of data their predecessor does not write (node record,
 // sources, masks, masses) before the PDL wait, so only the slot gathers follow it:
 // bit 0 K2, bit 1 K4.
@@ -1058,7 +1066,8 @@ template <int G, typename ST = double>
 __global__ void __launch_bounds__(kNodeThreads, G == 2 ? 6 : 0) k_thermal_node(const DevParams P, const DevPtrs D, int cur, int closes,
                                            double* __restrict__ t_out) {
     constexpr bool PAIR = G == 2, WIDE = G == 1;
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int b = node_block();
+    const int t = b * blockDim.x + threadIdx.x;
     const int i = PAIR ? (t >> 1) : t;
     const bool lead = !PAIR || !(threadIdx.x & 1);
     int4 ia = make_int4(0, 0, 0, 0), ib = ia;
@@ -1076,7 +1085,7 @@ __global__ void __launch_bounds__(kNodeThreads, G == 2 ? 6 : 0) k_thermal_node(c
         }
     }
     pdl_wait();
-    peer_wait(P, D, 0, PAIR ? (int)(blockIdx.x * blockDim.x) >> 1 : (int)(blockIdx.x * blockDim.x));
+    peer_wait(P, D, 0, PAIR ? (int)(b * blockDim.x) >> 1 : (int)(b * blockDim.x));
     const bool active = i < P.N && !D.clock->halted;  // the same for both threads of a pair
     double s = 0.0;
     if constexpr (PAIR) {
@@ -1573,7 +1582,8 @@ template <bool PAIR, typename ST = double>
 __global__ void NODE_BOUNDS k_mech_node(const DevParams P, const DevPtrs D, int cur, int closes,
                                                    double* __restrict__ u_out, int n0, int n1) {
     const ST* slot_m = reinterpret_cast<const ST*>(D.slot_m);
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int b = node_block();
+    const int t = b * blockDim.x + threadIdx.x;
     const int i = n0 + (PAIR ? (t >> 1) : t);
     const bool lead = !PAIR || !(threadIdx.x & 1);
     int4 ia = make_int4(0, 0, 0, 0), ib = ia;
@@ -1591,7 +1601,7 @@ __global__ void NODE_BOUNDS k_mech_node(const DevParams P, const DevPtrs D, int 
         msk = __ldg(D.mask + i);
     }
     pdl_wait();
-    peer_wait(P, D, 1, n0 + (PAIR ? (int)(blockIdx.x * blockDim.x) >> 1 : (int)(blockIdx.x * blockDim.x)));
+    peer_wait(P, D, 1, n0 + (PAIR ? (int)(b * blockDim.x) >> 1 : (int)(b * blockDim.x)));
     const bool active = i < n1 && !D.clock->halted;  // the same for both threads of a pair
     double f0 = 0.0, f1 = 0.0, f2 = 0.0;
     if constexpr (PAIR) {
