@@ -1138,7 +1138,6 @@ __device__ __forceinline__ void k3_body(const DevParams& P, const DevPtrs& D, co
                                         const ElemRows<kTmaK3>& rows, const RowPlan& rp, const CoordStage& xs,
                                         const int e, const int (&n)[NN], bool affine = false) {
     const size_t es = (size_t)P.es;
-    // affine chunk: every element is; else the element's own flag (mixed chunks)
     // affine chunk (all its elements affine; CTA-uniform): K3 takes the short hourglass branch.
     // An affine element in a mixed chunk takes the general branch, which computes the same
     // values for c_al = 0 (exact zeros: A^T c_al = Hd c_al = 0, 1/(8 + 0) = 1/8), so the
